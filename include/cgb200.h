@@ -1,0 +1,127 @@
+/*
+ * cgb200.h -- C ABI of the B200 RNS-BFV backend for the CryptoGen HE hot path.
+ *
+ * The reference package exposes its homomorphic substrate as the Python
+ * class cryptogen.backend.Context (/root/reference/pkg/src/cryptogen/
+ * backend.py:245-364) with per-op methods; every kernel above it
+ * (encodings.py, linear_kernels.py, arcc.py, kv_cache.py, nonlinear.py) only
+ * calls those methods.  This library is what a drop-in replacement of that
+ * class binds through ctypes (INTEGRATION.md shows the binding).  Each entry
+ * point below names the reference method it replaces.
+ *
+ * Conventions
+ *  - A ring (cgb_ring) owns the parameters, the secret key, the evaluation
+ *    keys and a device arena of fixed-size ciphertext slots.  Ciphertexts
+ *    are named by uint32 slot ids; a ciphertext is uint64[2][L][N] in the
+ *    NTT domain (poly, RNS limb over Q, coefficient).
+ *  - Encoded plaintexts live in a second arena (uint64[L][N]) and are named
+ *    by plaintext ids; kind CGB_PT_MUL is the centred lift used by
+ *    mult_plain, CGB_PT_ADD the floor(Q m / t) scaling used by add_plain.
+ *  - Batched entry points take `count` and host arrays of ids; every output
+ *    id must be distinct from every input id of the same call.
+ *  - Slot vectors crossing the ABI are host uint64[count][n_slots] arrays of
+ *    residues mod t.
+ *  - Return value 0 = success; CGB_ERR_PARAM maps to the reference's
+ *    ParameterError (backend.py:45-46), everything else is a runtime error.
+ *    cgb_last_error() returns the message of the last failure (thread-local).
+ *  - All work is stream-ordered on the ring's stream (cgb_set_stream);
+ *    calls returning host data synchronise that stream.
+ */
+#ifndef CGB200_H
+#define CGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGB_OK 0
+#define CGB_ERR_PARAM 1
+#define CGB_ERR_CUDA 2
+#define CGB_ERR_NOMEM 3
+#define CGB_ERR_STATE 4
+
+#define CGB_PT_MUL 0
+#define CGB_PT_ADD 1
+
+typedef struct cgb_ring cgb_ring;
+
+/* ---- lifetime ------------------------------------------------------------
+ * Replaces Context.__init__ / new_context (backend.py:245-256, :367-368) for
+ * the arithmetic: ring degree 2^log_n, plaintext modulus t (the reference's
+ * plain_modulus, backend.py:121), n_limbs primes of Q, n_slots logical
+ * slots.  one_row = 1 selects the native layout (t = 1 mod 4 n_slots,
+ * N = 2 n_slots, rotation = one automorphism); 0 the two-row layout
+ * (N = n_slots) whose cyclic shift the host composes from two automorphisms.
+ * key_seed seeds the ChaCha20 streams of the secret and evaluation keys.
+ * arena_cts / arena_pts: capacity of the ciphertext / plaintext arenas. */
+int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
+                    int one_row, const uint32_t key_seed[8], int64_t arena_cts,
+                    int64_t arena_pts, cgb_ring **out);
+void cgb_ring_destroy(cgb_ring *ring);
+/* moduli in order Q[0..L) | P | B[0..L]; returns how many were written */
+int cgb_ring_moduli(const cgb_ring *ring, uint64_t *out, int cap);
+/* words of one ciphertext (2*L*N) */
+size_t cgb_ct_words(const cgb_ring *ring);
+const char *cgb_last_error(void);
+int cgb_set_stream(cgb_ring *ring, void *cuda_stream);
+int cgb_sync(cgb_ring *ring);
+/* number of device kernel launches issued by this ring so far */
+uint64_t cgb_launch_count(const cgb_ring *ring);
+
+/* ---- ciphertext / plaintext storage -------------------------------------
+ * Ciphertext handles replace SlotCiphertext (backend.py:216-230); the
+ * reference's values are immutable and GC-owned, so the host frees ids from
+ * a finalizer.  load/store move raw NTT-domain words (checkpoints, tests). */
+int cgb_ct_alloc(cgb_ring *ring, int count, uint32_t *ids_out);
+int cgb_ct_free(cgb_ring *ring, int count, const uint32_t *ids);
+int cgb_ct_copy(cgb_ring *ring, int count, const uint32_t *src, const uint32_t *dst);
+int cgb_ct_store(cgb_ring *ring, int count, const uint32_t *ids, uint64_t *host_words);
+int cgb_ct_load(cgb_ring *ring, int count, const uint32_t *ids, const uint64_t *host_words);
+uint64_t *cgb_ct_device_ptr(cgb_ring *ring, uint32_t id);
+int cgb_pt_alloc(cgb_ring *ring, int count, uint32_t *ids_out);
+int cgb_pt_free(cgb_ring *ring, int count, const uint32_t *ids);
+/* encode host slot vectors into plaintexts; kind CGB_PT_MUL / CGB_PT_ADD.
+ * Replaces the operand handling of mult_plain / add_plain (backend.py:327-339). */
+int cgb_pt_encode(cgb_ring *ring, int count, const uint64_t *slots, int kind,
+                  const uint32_t *pt_ids);
+
+/* ---- client role ----------------------------------------------------------
+ * Context.encrypt (backend.py:307-310): symmetric RLWE encryption; the
+ * randomness of ciphertext i is ChaCha20(enc_key, first_index + i). */
+int cgb_encrypt(cgb_ring *ring, int count, const uint64_t *slots,
+                const uint32_t enc_key[8], uint64_t first_index, const uint32_t *out);
+/* Context.decrypt (backend.py:312-319) */
+int cgb_decrypt(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *slots_out);
+/* client-side diagnostic: invariant noise budget in bits of each ciphertext */
+int cgb_noise_budget(cgb_ring *ring, int count, const uint32_t *cts, double *bits_out);
+
+/* ---- server role (batched) ---------------------------------------------- */
+/* Context.add (backend.py:321-325) */
+int cgb_add(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out);
+/* Context.add_plain (backend.py:327-332); pt of kind CGB_PT_ADD */
+int cgb_add_plain(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out);
+/* Context.mult_plain (backend.py:334-339); pt of kind CGB_PT_MUL */
+int cgb_mult_plain(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out);
+/* Context.mult_cipher (backend.py:341-347): tensor, scale-and-round, relinearise */
+int cgb_mult_cipher(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out);
+/* Galois automorphism X -> X^g plus key switch; g = 1 copies.
+ * Context.rotate (backend.py:349-355) is galois(5^k mod 2N) in the one-row layout. */
+int cgb_galois(cgb_ring *ring, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out);
+/* Context.rotate: cyclic left shift by steps[i] (one-row layout only) */
+int cgb_rotate(cgb_ring *ring, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out);
+/* out = a + rotate(a, step): one doubling/fold step of broadcast_slot
+ * (arcc.py:90-93), tile_token (encodings.py:212-215) and fold_sum
+ * (linear_kernels.py:37-41), fused into one pass */
+int cgb_rotate_add(cgb_ring *ring, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out);
+/* out = sum of count ciphertexts a[0..count) (exact mod q: order-free) */
+int cgb_sum(cgb_ring *ring, int count, const uint32_t *a, uint32_t out);
+/* generate (and cache) evaluation keys for Galois elements ahead of use */
+int cgb_prepare_galois(cgb_ring *ring, int count, const uint64_t *g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGB200_H */

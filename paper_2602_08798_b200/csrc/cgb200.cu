@@ -1,0 +1,1556 @@
+// cgb200.cu -- B200 (sm_100a) RNS-BFV backend for the CryptoGen HE hot path.
+//
+// Implements include/cgb200.h.  The algorithms are the ones stated in
+// DESIGN.md section 3 and restated on the CPU in oracle/rnsbfv.c; every
+// ciphertext word produced here must equal the oracle's (tests/test_gpu_*).
+//
+// Device layout: ciphertext = u64[2][L][N] NTT-domain residues in a
+// fixed-slot arena; workspaces are stream-ordered allocations
+// (cudaMallocAsync) laid out [item][poly][limb][N].  All kernels are
+// batched over items so one launch covers every ciphertext of an op wave
+// (e.g. the 768 broadcast chains of a 12-head decode step).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/cgb200.h"
+#include "cgb_device.cuh"
+
+using namespace cgb;
+typedef unsigned __int128 u128;
+
+// ============================================================================
+// error plumbing
+// ============================================================================
+static thread_local std::string g_err;
+struct CgbError {
+  int code;
+  std::string msg;
+};
+#define FAIL(code, ...)                                   \
+  do {                                                    \
+    char _b[512];                                         \
+    snprintf(_b, sizeof _b, __VA_ARGS__);                 \
+    throw CgbError{code, std::string(_b)};                \
+  } while (0)
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t _e = (x);                                                           \
+    if (_e != cudaSuccess) FAIL(CGB_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define API_BEGIN try {
+#define API_END                          \
+  return CGB_OK;                         \
+  }                                      \
+  catch (const CgbError &e) {            \
+    g_err = e.msg;                       \
+    return e.code;                       \
+  }                                      \
+  catch (const std::exception &e) {      \
+    g_err = e.what();                    \
+    return CGB_ERR_STATE;                \
+  }
+
+// ============================================================================
+// host number theory (exact, u128 / tiny bignum)
+// ============================================================================
+static u64 h_mulmod(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+static u64 h_powmod(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, a, q);
+    a = h_mulmod(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+static u64 h_inv(u64 a, u64 q) { return h_powmod(a % q, q - 2, q); }
+static bool h_prime(u64 n) {
+  static const u64 B[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (u64 b : B)
+    if (n % b == 0) return n == b;
+  u64 d = n - 1;
+  int r = 0;
+  while (!(d & 1)) d >>= 1, r++;
+  for (u64 a : B) {
+    u64 x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool ok = false;
+    for (int i = 0; i < r - 1 && !ok; i++) {
+      x = h_mulmod(x, x, n);
+      ok = (x == n - 1);
+    }
+    if (!ok) return false;
+  }
+  return true;
+}
+static u32 h_brev(u32 x, int bits) {
+  u32 r = 0;
+  for (int i = 0; i < bits; i++) r = (r << 1) | ((x >> i) & 1);
+  return r;
+}
+static u64 h_psi(u64 q, u64 twoN) {
+  for (u64 x = 2;; x++) {
+    u64 p = h_powmod(x, (q - 1) / twoN, q);
+    if (h_powmod(p, twoN / 2, q) == q - 1) return p;
+  }
+}
+struct Big {  // little-endian words
+  std::vector<u64> w;
+  explicit Big(u64 x = 0) : w(40, 0) { w[0] = x; }
+  void mul(u64 x) {
+    u128 c = 0;
+    for (auto &v : w) {
+      c += (u128)v * x;
+      v = (u64)c;
+      c >>= 64;
+    }
+  }
+  u64 divmod(u64 d) {
+    u128 r = 0;
+    for (int i = (int)w.size() - 1; i >= 0; i--) {
+      r = (r << 64) | w[i];
+      w[i] = (u64)(r / d);
+      r %= d;
+    }
+    return (u64)r;
+  }
+  u64 mod(u64 d) const {
+    Big t = *this;
+    return t.divmod(d);
+  }
+};
+static void h_frac128(u64 r, u64 q, u64 *hi, u64 *lo) {
+  u128 x = (u128)r << 64;
+  *hi = (u64)(x / q);
+  u64 r2 = (u64)(x % q);
+  x = (u128)r2 << 64;
+  *lo = (u64)(x / q);
+}
+static u64 h_shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+
+// ============================================================================
+// device-resident constants
+// ============================================================================
+struct Consts {
+  int L, nB, N, logN, n_slots;
+  int pad_;
+  u64 t;
+  u64 Qmodt;
+  u64 tinvq[MAXL], Pinvq[MAXL], Pinvq_sh[MAXL], Pmodq[MAXL];
+  u64 dec_omega[MAXL], dec_th_hi[MAXL], dec_th_lo[MAXL];
+  u64 QhatInv[MAXL], QhatModB[MAXL][MAXL + 1], QmodB[MAXL + 1];
+  double invq[MAXL], invb[MAXL + 1];
+  u64 QBhatInv[MAXL], BQhatInv[MAXL + 1], sc_omega[MAXL][MAXL + 1], sc_th_hi[MAXL], sc_th_lo[MAXL];
+  u64 tBhat[MAXL + 1];
+  u64 BhatInv[MAXL + 1], BhatModQ[MAXL + 1][MAXL], BmodQ[MAXL];
+};
+
+static const u64 DOM_SK = 1, DOM_KSK_A = 2, DOM_KSK_E = 3, DOM_ENC_A = 4, DOM_ENC_E = 5;
+static inline u64 nonce_of(u64 dom, u64 sub) { return (dom << 56) | sub; }
+
+// ============================================================================
+// the ring
+// ============================================================================
+struct cgb_ring {
+  int logN, N, L, nB, nmod, n_slots, one_row;
+  int iP, iB0, iT;  // modulus indices of P, B[0], t
+  u64 t;
+  std::vector<u64> mods;  // Q | P | B | t
+  std::vector<ModTab> h_mods;
+  ModTab *d_mods = nullptr;
+  u64 *d_tables = nullptr;
+  u32 *d_slot_idx = nullptr;
+  u64 *d_s = nullptr;  // secret, NTT over Q u P: [L+1][N]
+  Consts h_c;
+  Consts *d_c = nullptr;
+  ChaKey keyseed;
+  std::unordered_map<u64, u64 *> keys;  // g -> [L][2][L+1][N]; g = 0 relin
+  u64 *arena = nullptr;
+  size_t ct_words, arena_cap;
+  std::vector<u32> ct_free;
+  std::vector<char> ct_used;
+  u64 *pt_arena = nullptr;
+  size_t pt_cap;
+  std::vector<u32> pt_free;
+  std::vector<char> pt_used;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // pinned staging for pointer tables / host payloads
+  char *pin = nullptr;
+  size_t pin_cap = 0, pin_off = 0;
+  u64 launches = 0;
+  std::mutex mu;
+
+  int ntt_E() const { return std::min(16, N); }
+  int ntt_threads() const { return N / ntt_E(); }
+  size_t ntt_smem() const { return sizeof(u64) * (size_t)(N + (N >> 4) + 1); }
+};
+
+// ---------------------------------------------------------------------------
+// pinned staging + device scratch
+// ---------------------------------------------------------------------------
+template <class T>
+static T *stage_to_device(cgb_ring *r, const T *host, size_t n, std::vector<void *> &frees) {
+  size_t bytes = sizeof(T) * n;
+  if (bytes == 0) return nullptr;
+  bytes = (bytes + 255) & ~(size_t)255;
+  T *dev;
+  CK(cudaMallocAsync((void **)&dev, bytes, r->stream));
+  frees.push_back(dev);
+  if (bytes > r->pin_cap) {  // large payload: staged by the driver
+    CK(cudaMemcpyAsync(dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
+    return dev;
+  }
+  if (r->pin_off + bytes > r->pin_cap) {
+    CK(cudaStreamSynchronize(r->stream));  // ring wrap: previous copies have consumed the buffer
+    r->pin_off = 0;
+  }
+  char *dst = r->pin + r->pin_off;
+  memcpy(dst, host, sizeof(T) * n);
+  CK(cudaMemcpyAsync(dev, dst, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
+  r->pin_off += bytes;
+  return dev;
+}
+struct Scratch {
+  cgb_ring *r;
+  std::vector<void *> frees;
+  explicit Scratch(cgb_ring *r_) : r(r_) {}
+  template <class T>
+  T *alloc(size_t n) {
+    T *p;
+    CK(cudaMallocAsync((void **)&p, std::max<size_t>(sizeof(T) * n, 256), r->stream));
+    frees.push_back(p);
+    return p;
+  }
+  template <class T>
+  T *up(const T *host, size_t n) {
+    return stage_to_device(r, host, n, frees);
+  }
+  ~Scratch() {
+    for (void *p : frees) cudaFreeAsync(p, r->stream);
+  }
+};
+
+static void check_launch(cgb_ring *r) {
+  r->launches++;
+  CK(cudaGetLastError());
+}
+
+// ============================================================================
+// kernels
+// ============================================================================
+#define GRID1(n, b) dim3((unsigned)(((n) + (b)-1) / (b)))
+
+// NTT launcher -------------------------------------------------------------
+static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
+  if (count <= 0 || job.nsub <= 0) return;
+  job.mods = r->d_mods;
+  job.logN = r->logN;
+  int E = r->ntt_E(), T = r->ntt_threads();
+  size_t smem = r->ntt_smem();
+  dim3 grid((unsigned)(count * job.nsub));
+#define LNTT(EE)                                                                                \
+  do {                                                                                          \
+    if (fwd) k_ntt<EE, true><<<grid, T, smem, r->stream>>>(job);                                \
+    else k_ntt<EE, false><<<grid, T, smem, r->stream>>>(job);                                   \
+  } while (0)
+  switch (E) {
+    case 16: LNTT(16); break;
+    case 8: LNTT(8); break;
+    case 4: LNTT(4); break;
+    default: LNTT(2); break;
+  }
+#undef LNTT
+  check_launch(r);
+}
+// NTT over `nlimb` limbs of `npoly` polys per item, limb l of poly p at unit p*nlimb+l
+static void ntt_items(cgb_ring *r, bool fwd, u64 *base, u64 *const *items, u64 item_stride, int count, int npoly,
+                      int nlimb, const int *mod_of_limb, int poly_units = -1) {
+  NttJob job{};
+  job.base = base;
+  job.items = items;
+  job.item_stride = item_stride;
+  int pu = poly_units < 0 ? nlimb : poly_units;
+  int n = 0;
+  for (int p = 0; p < npoly; p++)
+    for (int l = 0; l < nlimb; l++) {
+      if (n >= NTT_MAXSUB) FAIL(CGB_ERR_PARAM, "too many NTT units per item");
+      job.sub_off[n] = (unsigned short)(p * pu + l);
+      job.sub_mod[n] = (unsigned char)mod_of_limb[l];
+      n++;
+    }
+  job.nsub = n;
+  launch_ntt(r, fwd, job, count);
+}
+
+// elementwise kernels --------------------------------------------------------
+// out[p][l][j] = a + b  (mod q_l), per-item pointers
+__global__ void k_add(u64 *const *out, const u64 *const *a, const u64 *const *b, const ModTab *mods, int L, int logN,
+                      u64 words) {
+  int item = blockIdx.y;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)((i >> logN) % L);
+  out[item][i] = add_mod(a[item][i], b[item][i], mods[l].q);
+}
+// out = a + b + c (three-way; used by rotate_add combine)
+__global__ void k_mult_plain(u64 *const *out, const u64 *const *a, const u64 *const *pt, const ModTab *mods, int L,
+                             int logN, u64 words) {
+  int item = blockIdx.y;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 li = (i >> logN);
+  int l = (int)(li % L);
+  u64 j = i & ((1ull << logN) - 1);
+  out[item][i] = mul_mod(a[item][i], pt[item][((u64)l << logN) + j], mods[l]);
+}
+__global__ void k_add_plain(u64 *const *out, const u64 *const *a, const u64 *const *pt, const ModTab *mods, int L,
+                            int logN, u64 words) {
+  int item = blockIdx.y;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 half = (u64)L << logN;
+  int l = (int)((i >> logN) % L);
+  u64 v = a[item][i];
+  if (i < half) v = add_mod(v, pt[item][i], mods[l].q);
+  out[item][i] = v;
+}
+__global__ void k_copy(u64 *const *out, const u64 *const *a, u64 words) {
+  int item = blockIdx.y;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  out[item][i] = a[item][i];
+}
+// gather items into a strided workspace: dst[item * dstride + w] = src[item][off + w]
+__global__ void k_gather(u64 *dst, u64 dstride, const u64 *const *src, u64 off, u64 words) {
+  int item = blockIdx.y;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  dst[(u64)item * dstride + i] = src[item][off + i];
+}
+// sum of count items (tree in one kernel: each thread sums one word over all items)
+__global__ void k_sum(u64 *out, const u64 *const *a, int count, const ModTab *mods, int L, int logN, u64 words) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)((i >> logN) % L);
+  u64 q = mods[l].q, s = 0;
+  for (int k = 0; k < count; k++) s = add_mod(s, a[k][i], q);
+  out[i] = s;
+}
+
+// Galois automorphism in the evaluation domain: out[k] = in[perm_g(k)]
+__device__ __forceinline__ u32 dbrev(u32 x, int logN) { return __brev(x) >> (32 - logN); }
+__global__ void k_automorph(u64 *dst /*[item][2][L][N]*/, const u64 *const *src, const u64 *gs, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, words = 2ull * L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 k = i & (N - 1), base = i - k;
+  u64 g = gs[item];
+  u64 e = 2ull * dbrev((u32)k, logN) + 1;
+  u64 se = (e * g) & (2 * N - 1);
+  u64 sk = dbrev((u32)((se - 1) >> 1), logN);
+  dst[(u64)item * words + i] = src[item][base + sk];
+}
+// same, on a plain [limbs][N] array (secret key -> sigma_g(s))
+__global__ void k_automorph_flat(u64 *dst, const u64 *src, u64 g, int nlimb, int logN) {
+  u64 N = 1ull << logN, words = (u64)nlimb * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 k = i & (N - 1), base = i - k;
+  u64 e = 2ull * dbrev((u32)k, logN) + 1;
+  u64 se = (e * g) & (2 * N - 1);
+  dst[i] = src[base + dbrev((u32)((se - 1) >> 1), logN)];
+}
+
+// key switching: ModUp of dnum = L one-limb digits -------------------------
+// D[item][j][l][N] (l over Q u P) : l == j -> NTT-form input limb ; else centred coeff reduced
+__global__ void k_modup(u64 *D, const u64 *xcoef /*[item][L][N]*/, const u64 *xin /*[item][L][N]*/,
+                        const ModTab *mods, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN;
+  u64 words = (u64)L * (L + 1) * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 jn = i & (N - 1), rest = i >> logN;
+  int l = (int)(rest % (L + 1)), j = (int)(rest / (L + 1));
+  const u64 *src = (l == j ? xin : xcoef) + ((u64)item * L + j) * N;
+  u64 v = src[jn];
+  if (l != j) v = centred_to(v, mods[j].q, mods[l].q);
+  D[(u64)item * words + i] = v;
+}
+// acc[item][p][l][N] = sum_j D[j][l] * key[j][p][l]   (p = 0: b, 1: a)
+__global__ void k_ks_inner(u64 *acc, const u64 *D, const u64 *const *keys, const ModTab *mods, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, LP = L + 1;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
+  if (i >= LP * N) return;
+  int l = (int)(i >> logN);
+  const ModTab &M = mods[l];
+  const u64 *Di = D + (u64)item * L * LP * N;
+  const u64 *K = keys[item];
+  u64 s0 = 0, s1 = 0;
+  for (int j = 0; j < L; j++) {
+    u64 d = Di[(u64)j * LP * N + i];
+    s0 = add_mod(s0, mul_mod(d, K[((u64)j * 2 + 0) * LP * N + i], M), M.q);
+    s1 = add_mod(s1, mul_mod(d, K[((u64)j * 2 + 1) * LP * N + i], M), M.q);
+  }
+  acc[((u64)item * 2 + 0) * LP * N + i] = s0;
+  acc[((u64)item * 2 + 1) * LP * N + i] = s1;
+}
+// ModDown lift: W[item][p][l][N] = centred(acc[item][p][L] (coeff, mod P)) mod q_l
+__global__ void k_moddown_lift(u64 *W, const u64 *acc, const ModTab *mods, int L, int iP, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, LP = L + 1, words = 2ull * L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 jn = i & (N - 1), rest = i >> logN;
+  int l = (int)(rest % L), p = (int)(rest / L);
+  u64 v = acc[(((u64)item * 2 + p) * LP + L) * N + jn];
+  W[(u64)item * words + i] = centred_to(v, mods[iP].q, mods[l].q);
+}
+// out[p][l] = (acc[p][l] - W[p][l]) * P^-1 + add0 (poly 0 only) + add1 (both polys)
+__global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W, const u64 *add0 /*[item][2][L][N] or null*/,
+                                  const u64 *const *add1, const ModTab *mods, const Consts *C, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, LP = L + 1, words = 2ull * L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  u64 jn = i & (N - 1), rest = i >> logN;
+  int l = (int)(rest % L), p = (int)(rest / L);
+  u64 q = mods[l].q;
+  u64 a = acc[(((u64)item * 2 + p) * LP + l) * N + jn];
+  u64 v = mul_shoup(sub_mod(a, W[(u64)item * words + i], q), C->Pinvq[l], C->Pinvq_sh[l], q);
+  if (add0 && p == 0) v = add_mod(v, add0[(u64)item * words + i], q);
+  if (add1) v = add_mod(v, add1[item][i], q);
+  out[item][i] = v;
+}
+
+// BFV multiplication --------------------------------------------------------
+// lift coefficient-form Q residues of one poly into B: dst[item][p][L + k][N]
+__global__ void k_lift_QB(u64 *dst /*[item][4][L+nB][N]*/, const u64 *coef /*[item][4][L][N]*/, const ModTab *mods,
+                          const Consts *C, int L, int nB, int iB0, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [4][N]
+  if (i >= 4 * N) return;
+  u64 jn = i & (N - 1);
+  int p = (int)(i >> logN);
+  const u64 *src = coef + ((u64)item * 4 + p) * L * N;
+  u64 y[MAXL];
+  double s = 0.0;
+  for (int l = 0; l < L; l++) {
+    const ModTab &M = mods[l];
+    y[l] = mul_mod(src[(u64)l * N + jn], C->QhatInv[l], M);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(y[l]), C->invq[l]));
+  }
+  u64 v = (u64)__dadd_rn(s, 0.5);
+  u64 *d = dst + ((u64)item * 4 + p) * (L + nB) * N;
+  for (int k = 0; k < nB; k++) {
+    const ModTab &M = mods[iB0 + k];
+    u64 acc = 0;
+    for (int l = 0; l < L; l++) acc = add_mod(acc, mul_mod(y[l], C->QhatModB[l][k], M), M.q);
+    acc = sub_mod(acc, mul_mod(v, C->QmodB[k], M), M.q);
+    d[(u64)(L + k) * N + jn] = acc;
+  }
+}
+// tensor over Q u B: ten[item][3][L+nB][N]
+__global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const ModTab *mods, int L, int nt, int iB0,
+                         int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, P = (u64)nt * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  int l = (int)(i >> logN);
+  const ModTab &M = mods[l < L ? l : iB0 + (l - L)];
+  const u64 *x = in + (u64)item * 4 * P;
+  u64 a0 = x[i], a1 = x[P + i], b0 = x[2 * P + i], b1 = x[3 * P + i];
+  u64 *o = ten + (u64)item * 3 * P;
+  o[i] = mul_mod(a0, b0, M);
+  o[P + i] = add_mod(mul_mod(a0, b1, M), mul_mod(a1, b0, M), M.q);
+  o[2 * P + i] = mul_mod(a1, b1, M);
+}
+// scale by t/Q and round into B, then centred B -> Q: d[item][3][L][N]
+__global__ void k_scale_round(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int L, int nB, int iB0,
+                              int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN;
+  int nt = L + nB;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [3][N]
+  if (i >= 3 * N) return;
+  u64 jn = i & (N - 1);
+  int p = (int)(i >> logN);
+  const u64 *cp = ten + ((u64)item * 3 + p) * nt * N;
+  u64 y[MAXL];
+  u128 S = 0;
+  for (int l = 0; l < L; l++) {
+    y[l] = mul_mod(cp[(u64)l * N + jn], C->QBhatInv[l], mods[l]);
+    S += (u128)y[l] * C->sc_th_hi[l] + (u128)__umul64hi(y[l], C->sc_th_lo[l]);
+  }
+  u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
+  u64 yk[MAXL + 1];
+  double s = 0.0;
+  for (int k = 0; k < nB; k++) {
+    const ModTab &M = mods[iB0 + k];
+    u64 acc = R % M.q;
+    for (int l = 0; l < L; l++) acc = add_mod(acc, mul_mod(y[l], C->sc_omega[l][k], M), M.q);
+    u64 z = mul_mod(cp[(u64)(L + k) * N + jn], C->BQhatInv[k], M);
+    acc = add_mod(acc, mul_mod(z, C->tBhat[k], M), M.q);
+    yk[k] = mul_mod(acc, C->BhatInv[k], M);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(yk[k]), C->invb[k]));
+  }
+  u64 v = (u64)__dadd_rn(s, 0.5);
+  u64 *o = d + ((u64)item * 3 + p) * L * N;
+  for (int l = 0; l < L; l++) {
+    const ModTab &M = mods[l];
+    u64 acc = 0;
+    for (int k = 0; k < nB; k++) acc = add_mod(acc, mul_mod(yk[k], C->BhatModQ[k][l], M), M.q);
+    acc = sub_mod(acc, mul_mod(v, C->BmodQ[l], M), M.q);
+    o[(u64)l * N + jn] = acc;
+  }
+}
+
+// encoding / encryption / decryption ----------------------------------------
+__global__ void k_scatter_slots(u64 *m /*[item][N]*/, const u64 *slots /*[item][n]*/, const u32 *slot_idx, int n,
+                                u64 t, int logN) {
+  int item = blockIdx.y;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  m[((u64)item << logN) + slot_idx[i]] = slots[(u64)item * n + i] % t;
+}
+__global__ void k_gather_slots(u64 *slots, const u64 *m, const u32 *slot_idx, int n, int logN) {
+  int item = blockIdx.y;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  slots[(u64)item * n + i] = m[((u64)item << logN) + slot_idx[i]];
+}
+// plaintext lift into L limbs (coefficient form): kind 0 centred, kind 1 floor(Q m / t)
+__global__ void k_pt_lift(u64 *const *pt, const u64 *m, const ModTab *mods, const Consts *C, int L, int logN, int kind) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, words = (u64)L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)(i >> logN);
+  u64 jn = i & (N - 1);
+  u64 q = mods[l].q, t = C->t;
+  u64 v = m[((u64)item << logN) + jn];
+  u64 out;
+  if (kind == CGB_PT_MUL) {
+    out = (v <= t / 2) ? v % q : (q - ((t - v) % q)) % q;
+  } else {
+    u64 r = (u64)(((u128)C->Qmodt * v) % t);
+    out = sub_mod(0, mul_mod(r % q, C->tinvq[l], mods[l]), q);
+  }
+  pt[item][i] = out;
+}
+__device__ __forceinline__ u64 u128_mod(u64 hi, u64 lo, const ModTab &M) {
+  return add_mod(mul_mod(hi % M.q, M.r64, M), lo % M.q, M.q);
+}
+// uniform residues in NTT form from ChaCha20: element e = l*N + j uses words 4e..4e+3
+__global__ void k_sample_uniform(u64 *const *dst, ChaKey key, const u64 *nonces, int nl, const int *mod_idx,
+                                 const ModTab *mods, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, nblk = ((u64)nl * N + 3) / 4;
+  u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nblk) return;
+  u32 w[16];
+  chacha_block(key, c, nonces[item], w);
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    u64 e = 4 * c + r;
+    if (e >= (u64)nl * N) break;
+    int l = (int)(e >> logN);
+    const ModTab &M = mods[mod_idx[l]];
+    u64 lo = (u64)w[4 * r] | ((u64)w[4 * r + 1] << 32), hi = (u64)w[4 * r + 2] | ((u64)w[4 * r + 3] << 32);
+    dst[item][e] = u128_mod(hi, lo, M);
+  }
+}
+// centred binomial (eta = 21) errors: element j uses words 2j, 2j+1
+__global__ void k_sample_cbd(i64 *e, ChaKey key, const u64 *nonces, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, nblk = (N + 7) / 8;
+  u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nblk) return;
+  u32 w[16];
+  chacha_block(key, c, nonces[item], w);
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    u64 j = 8 * c + r;
+    if (j >= N) break;
+    u64 x = (u64)w[2 * r] | ((u64)w[2 * r + 1] << 32);
+    e[((u64)item << logN) + j] = (i64)__popcll(x & 0x1FFFFFull) - (i64)__popcll((x >> 21) & 0x1FFFFFull);
+  }
+}
+// c0 coefficient form: floor(Q m / t) + e  (mod q_l), written into limbs of dst items (poly 0)
+__global__ void k_enc_c0(u64 *const *dst, const u64 *m, const i64 *e, const ModTab *mods, const Consts *C, int L,
+                         int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, words = (u64)L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)(i >> logN);
+  u64 jn = i & (N - 1);
+  const ModTab &M = mods[l];
+  u64 t = C->t, v = m[((u64)item << logN) + jn];
+  u64 r = (u64)(((u128)C->Qmodt * v) % t);
+  u64 sc = sub_mod(0, mul_mod(r % M.q, C->tinvq[l], M), M.q);
+  i64 ev = e[((u64)item << logN) + jn];
+  u64 er = ev >= 0 ? (u64)ev % M.q : (M.q - ((u64)(-ev) % M.q)) % M.q;
+  dst[item][i] = add_mod(sc, er, M.q);
+}
+// c0 -= c1 * s  (NTT form), per item pointer
+__global__ void k_enc_sub_as(u64 *const *ct, const u64 *s, const ModTab *mods, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, words = (u64)L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)(i >> logN);
+  const ModTab &M = mods[l];
+  u64 *c = ct[item];
+  c[i] = sub_mod(c[i], mul_mod(c[words + i], s[i], M), M.q);
+}
+// X[item][l] = c0 + c1 s (NTT form) ; optionally times t (noise diagnostic)
+__global__ void k_dec_inner(u64 *X, const u64 *const *ct, const u64 *s, const ModTab *mods, const Consts *C, int L,
+                            int logN, int times_t) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN, words = (u64)L * N;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)(i >> logN);
+  const ModTab &M = mods[l];
+  const u64 *c = ct[item];
+  u64 v = add_mod(c[i], mul_mod(c[words + i], s[i], M), M.q);
+  if (times_t) v = mul_mod(v, C->t % M.q, M);
+  X[(u64)item * words + i] = v;
+}
+// m = [sum_l x_l omega_l + round(sum_l x_l theta_l)]_t
+__global__ void k_dec_scale(u64 *m, const u64 *X, const Consts *C, int L, int logN) {
+  int item = blockIdx.y;
+  u64 N = 1ull << logN;
+  u64 jn = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jn >= N) return;
+  u64 t = C->t;
+  u128 S = 0;
+  u64 I = 0;
+  for (int l = 0; l < L; l++) {
+    u64 x = X[((u64)item * L + l) * N + jn];
+    S += (u128)x * C->dec_th_hi[l] + (u128)__umul64hi(x, C->dec_th_lo[l]);
+    I = (I + (u64)(((u128)(x % t) * C->dec_omega[l]) % t)) % t;
+  }
+  u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
+  m[((u64)item << logN) + jn] = (I + R % t) % t;
+}
+// keygen: b[l] = e_l - a_l s_l + (l == j ? [P]_{q_j} s'_l : 0)
+__global__ void k_ksk_b(u64 *key /*[L][2][L+1][N]*/, int j, const i64 *e, const u64 *s, const u64 *sp,
+                        const ModTab *mods, const Consts *C, int L, int iP, int logN) {
+  u64 N = 1ull << logN, LP = L + 1;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= LP * N) return;
+  int l = (int)(i >> logN);
+  u64 jn = i & (N - 1);
+  const ModTab &M = mods[l == L ? iP : l];
+  u64 *b = key + ((u64)j * 2 + 0) * LP * N, *a = key + ((u64)j * 2 + 1) * LP * N;
+  i64 ev = e[jn];
+  u64 er = ev >= 0 ? (u64)ev % M.q : (M.q - ((u64)(-ev) % M.q)) % M.q;
+  b[i] = er;  // NTT applied by the caller, then k_ksk_fin
+  (void)a; (void)s; (void)sp; (void)C;
+}
+__global__ void k_ksk_fin(u64 *key, int j, const u64 *s, const u64 *sp, const ModTab *mods, const Consts *C, int L,
+                          int iP, int logN) {
+  u64 N = 1ull << logN, LP = L + 1;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= LP * N) return;
+  int l = (int)(i >> logN);
+  const ModTab &M = mods[l == L ? iP : l];
+  u64 *b = key + ((u64)j * 2 + 0) * LP * N, *a = key + ((u64)j * 2 + 1) * LP * N;
+  u64 v = sub_mod(b[i], mul_mod(a[i], s[i], M), M.q);
+  if (l == j) v = add_mod(v, mul_mod(C->Pmodq[j], sp[i], M), M.q);
+  b[i] = v;
+}
+__global__ void k_square(u64 *dst, const u64 *s, const ModTab *mods, int nl, const int *mod_idx, int logN) {
+  u64 N = 1ull << logN;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (u64)nl * N) return;
+  const ModTab &M = mods[mod_idx[i >> logN]];
+  dst[i] = mul_mod(s[i], s[i], M);
+}
+
+// ============================================================================
+// host orchestration
+// ============================================================================
+static const int TPB = 256;
+
+static std::vector<u64 *> ct_ptrs(cgb_ring *r, int count, const u32 *ids) {
+  std::vector<u64 *> v(count);
+  for (int i = 0; i < count; i++) {
+    if (ids[i] >= r->arena_cap || !r->ct_used[ids[i]]) FAIL(CGB_ERR_PARAM, "invalid ciphertext id %u", ids[i]);
+    v[i] = r->arena + (size_t)ids[i] * r->ct_words;
+  }
+  return v;
+}
+static std::vector<u64 *> pt_ptrs(cgb_ring *r, int count, const u32 *ids) {
+  std::vector<u64 *> v(count);
+  size_t w = (size_t)r->L * r->N;
+  for (int i = 0; i < count; i++) {
+    if (ids[i] >= r->pt_cap || !r->pt_used[ids[i]]) FAIL(CGB_ERR_PARAM, "invalid plaintext id %u", ids[i]);
+    v[i] = r->pt_arena + (size_t)ids[i] * w;
+  }
+  return v;
+}
+static int *q_mod_idx(cgb_ring *r, std::vector<int> &v) {
+  v.resize(r->L);
+  for (int l = 0; l < r->L; l++) v[l] = l;
+  return v.data();
+}
+
+// encode host slots into plaintext polys m[count][N] (coefficient form mod t)
+static void encode_slots(cgb_ring *r, Scratch &S, const u64 *slots_host, int count, u64 *m) {
+  u64 *d_slots = S.up(slots_host, (size_t)count * r->n_slots);
+  CK(cudaMemsetAsync(m, 0, sizeof(u64) * (size_t)count * r->N, r->stream));
+  k_scatter_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(m, d_slots, r->d_slot_idx,
+                                                                                r->n_slots, r->t, r->logN);
+  check_launch(r);
+  int mi = r->iT;
+  ntt_items(r, false, m, nullptr, r->N, count, 1, 1, &mi);
+}
+
+static u64 *get_key(cgb_ring *r, u64 g);
+
+// key switch of `count` NTT-form polys x[item][L][N] (contiguous) with per-item keys;
+// result combined into out pointers: out = (ks0 + add0_p0 + add1, ks1 + add1)
+static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *const *d_keys, u64 *const *d_out,
+                      const u64 *add0, const u64 *const *d_add1) {
+  const int L = r->L, N = r->N, LP = L + 1, logN = r->logN;
+  std::vector<int> qm;
+  q_mod_idx(r, qm);
+  // digits in coefficient form
+  u64 *xc = S.alloc<u64>((size_t)count * L * N);
+  CK(cudaMemcpyAsync(xc, x, sizeof(u64) * (size_t)count * L * N, cudaMemcpyDeviceToDevice, r->stream));
+  ntt_items(r, false, xc, nullptr, (u64)L * N, count, 1, L, qm.data());
+  // ModUp
+  u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
+  u64 wD = (u64)L * LP * N;
+  k_modup<<<dim3(GRID1(wD, TPB).x, count), TPB, 0, r->stream>>>(D, xc, x, r->d_mods, L, logN);
+  check_launch(r);
+  {
+    NttJob job{};
+    job.base = D;
+    job.item_stride = wD;
+    int n = 0;
+    for (int j = 0; j < L; j++)
+      for (int l = 0; l < LP; l++) {
+        if (l == j) continue;
+        job.sub_off[n] = (unsigned short)(j * LP + l);
+        job.sub_mod[n] = (unsigned char)(l == L ? r->iP : l);
+        n++;
+      }
+    job.nsub = n;
+    launch_ntt(r, true, job, count);
+  }
+  // inner product with the evaluation key
+  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
+  k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, d_keys, r->d_mods, L, logN);
+  check_launch(r);
+  // ModDown
+  {
+    int mP = r->iP;
+    NttJob job{};
+    job.base = acc;
+    job.item_stride = 2ull * LP * N;
+    job.sub_off[0] = (unsigned short)L;
+    job.sub_mod[0] = (unsigned char)mP;
+    job.sub_off[1] = (unsigned short)(LP + L);
+    job.sub_mod[1] = (unsigned char)mP;
+    job.nsub = 2;
+    launch_ntt(r, false, job, count);
+  }
+  u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
+  k_moddown_lift<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(W, acc, r->d_mods, L, r->iP, logN);
+  check_launch(r);
+  ntt_items(r, true, W, nullptr, 2ull * L * N, count, 2, L, qm.data());
+  k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
+      d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN);
+  check_launch(r);
+}
+
+static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
+  size_t budget = (size_t)3 << 30;  // bytes of workspace per chunk
+  size_t c = budget / std::max<size_t>(words_per_item * 8, 1);
+  return std::max<size_t>(1, std::min<size_t>(c, 4096));
+}
+
+// galois (+ optional add of the input) on a batch
+static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, const u32 *out, bool add_input) {
+  const int L = r->L, N = r->N;
+  const u64 twoN = 2ull * N, ctw = r->ct_words;
+  std::vector<int> idx;  // items with g != 1
+  for (int i = 0; i < count; i++) {
+    u64 g = gs[i] % twoN;
+    if (!(g & 1)) FAIL(CGB_ERR_PARAM, "Galois element %llu is even", (unsigned long long)gs[i]);
+    if (g == 1) {
+      Scratch S(r);
+      std::vector<u64 *> src = ct_ptrs(r, 1, &a[i]), dst = ct_ptrs(r, 1, &out[i]);
+      u64 **d_src = S.up(src.data(), 1), **d_dst = S.up(dst.data(), 1);
+      if (add_input) {
+        k_add<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
+                                                                 (const u64 *const *)d_src, r->d_mods, L, r->logN, ctw);
+      } else {
+        k_copy<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
+      }
+      check_launch(r);
+    } else {
+      idx.push_back(i);
+    }
+  }
+  size_t per_item = ctw * 2 + (size_t)L * N * (1 + L * (L + 1) + 2 * (L + 1) + 2 * L);
+  size_t CH = chunk_for(r, per_item);
+  for (size_t c0 = 0; c0 < idx.size(); c0 += CH) {
+    int n = (int)std::min(CH, idx.size() - c0);
+    Scratch S(r);
+    std::vector<u32> ia(n), io(n);
+    std::vector<u64> g(n);
+    std::vector<u64 *> keys(n);
+    for (int k = 0; k < n; k++) {
+      ia[k] = a[idx[c0 + k]];
+      io[k] = out[idx[c0 + k]];
+      g[k] = gs[idx[c0 + k]] % twoN;
+      keys[k] = get_key(r, g[k]);
+    }
+    std::vector<u64 *> src = ct_ptrs(r, n, ia.data()), dst = ct_ptrs(r, n, io.data());
+    u64 **d_src = S.up(src.data(), n), **d_dst = S.up(dst.data(), n), **d_keys = S.up(keys.data(), n);
+    u64 *d_g = S.up(g.data(), n);
+    u64 *A = S.alloc<u64>((size_t)n * ctw);
+    k_automorph<<<dim3(GRID1(ctw, TPB).x, n), TPB, 0, r->stream>>>(A, (const u64 *const *)d_src, d_g, L, r->logN);
+    check_launch(r);
+    // c1' contiguous for the key switch
+    u64 *x = S.alloc<u64>((size_t)n * L * N);
+    CK(cudaMemcpy2DAsync(x, sizeof(u64) * L * N, A + (size_t)L * N, sizeof(u64) * ctw, sizeof(u64) * L * N, n,
+                         cudaMemcpyDeviceToDevice, r->stream));
+    keyswitch(r, S, x, n, d_keys, d_dst, A, add_input ? (const u64 *const *)d_src : nullptr);
+  }
+}
+
+// ============================================================================
+// key generation
+// ============================================================================
+static void sample_cbd(cgb_ring *r, Scratch &S, i64 *e, const ChaKey &key, const std::vector<u64> &nonces) {
+  int n = (int)nonces.size();
+  u64 *d_n = S.up(nonces.data(), n);
+  u64 nblk = ((u64)r->N + 7) / 8;
+  k_sample_cbd<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(e, key, d_n, r->logN);
+  check_launch(r);
+}
+static void sample_uniform(cgb_ring *r, Scratch &S, u64 *const *d_dst, int n, const ChaKey &key,
+                           const std::vector<u64> &nonces, int nl, const int *mod_idx_host) {
+  u64 *d_n = S.up(nonces.data(), n);
+  int *d_mi = S.up(mod_idx_host, nl);
+  u64 nblk = ((u64)nl * r->N + 3) / 4;
+  k_sample_uniform<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(d_dst, key, d_n, nl, d_mi, r->d_mods, r->logN);
+  check_launch(r);
+}
+
+static u64 *get_key(cgb_ring *r, u64 g) {
+  auto it = r->keys.find(g);
+  if (it != r->keys.end()) return it->second;
+  const int L = r->L, LP = L + 1, N = r->N;
+  const u64 LPN = (u64)LP * N;
+  u64 *key;
+  CK(cudaMalloc((void **)&key, sizeof(u64) * (size_t)L * 2 * LPN));
+  Scratch S(r);
+  std::vector<int> mi(LP);
+  for (int l = 0; l < L; l++) mi[l] = l;
+  mi[L] = r->iP;
+  int *d_mi = S.up(mi.data(), LP);
+  // source key s' over Q u P
+  u64 *sp = S.alloc<u64>(LPN);
+  if (g == 0) {
+    k_square<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(sp, r->d_s, r->d_mods, LP, d_mi, r->logN);
+  } else {
+    k_automorph_flat<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(sp, r->d_s, g, LP, r->logN);
+  }
+  check_launch(r);
+  i64 *e = S.alloc<i64>((size_t)N);
+  for (int j = 0; j < L; j++) {
+    u64 sub = (g << 8) | (u64)j;
+    std::vector<u64 *> adst = {key + ((u64)j * 2 + 1) * LPN};
+    u64 **d_a = S.up(adst.data(), 1);
+    sample_uniform(r, S, d_a, 1, r->keyseed, {nonce_of(DOM_KSK_A, sub)}, LP, mi.data());
+    sample_cbd(r, S, e, r->keyseed, {nonce_of(DOM_KSK_E, sub)});
+    k_ksk_b<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, e, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN);
+    check_launch(r);
+    ntt_items(r, true, key + ((u64)j * 2 + 0) * LPN, nullptr, 0, 1, 1, LP, mi.data());
+    k_ksk_fin<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN);
+    check_launch(r);
+  }
+  r->keys[g] = key;
+  return key;
+}
+
+// ============================================================================
+// ring construction
+// ============================================================================
+static void take_primes(cgb_ring *r, int bits, int count) {
+  u64 step = 2ull * r->N, top = 1ull << bits;
+  u64 c = top - (top % step) + 1;
+  if (c >= top) c -= step;
+  int got = 0;
+  while (got < count) {
+    bool dup = std::find(r->mods.begin(), r->mods.end(), c) != r->mods.end();
+    if (!dup && c != r->t && h_prime(c)) {
+      r->mods.push_back(c);
+      got++;
+    }
+    c -= step;
+  }
+}
+
+static void chacha_host(const ChaKey &key, u64 ctr, u64 nonce, u32 out[16]) {
+  auto rotl = [](u32 x, int n) { return (x << n) | (x >> (32 - n)); };
+  u32 s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u, key.k[0], key.k[1], key.k[2], key.k[3],
+               key.k[4],    key.k[5],    key.k[6],    key.k[7],    (u32)ctr, (u32)(ctr >> 32), (u32)nonce,
+               (u32)(nonce >> 32)};
+  u32 x[16];
+  memcpy(x, s, sizeof x);
+  auto qr = [&](int a, int b, int c, int d) {
+    x[a] += x[b]; x[d] ^= x[a]; x[d] = rotl(x[d], 16);
+    x[c] += x[d]; x[b] ^= x[c]; x[b] = rotl(x[b], 12);
+    x[a] += x[b]; x[d] ^= x[a]; x[d] = rotl(x[d], 8);
+    x[c] += x[d]; x[b] ^= x[c]; x[b] = rotl(x[b], 7);
+  };
+  for (int i = 0; i < 10; i++) {
+    qr(0, 4, 8, 12); qr(1, 5, 9, 13); qr(2, 6, 10, 14); qr(3, 7, 11, 15);
+    qr(0, 5, 10, 15); qr(1, 6, 11, 12); qr(2, 7, 8, 13); qr(3, 4, 9, 14);
+  }
+  for (int i = 0; i < 16; i++) out[i] = x[i] + s[i];
+}
+
+static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
+  const int N = r->N, L = r->L, nB = r->nB, logN = r->logN;
+  memcpy(r->keyseed.k, key_seed, sizeof r->keyseed.k);
+  take_primes(r, 60, L);
+  take_primes(r, 61, 1);
+  take_primes(r, 61, nB);
+  r->iP = L;
+  r->iB0 = L + 1;
+  r->iT = L + 1 + nB;
+  r->mods.push_back(r->t);
+  r->nmod = (int)r->mods.size();
+  // twiddle tables
+  size_t per = 4ull * N;
+  CK(cudaMalloc((void **)&r->d_tables, sizeof(u64) * per * r->nmod));
+  std::vector<u64> tab(per);
+  r->h_mods.resize(r->nmod);
+  for (int i = 0; i < r->nmod; i++) {
+    u64 q = r->mods[i];
+    u64 psi = h_psi(q, 2ull * N), psii = h_inv(psi, q);
+    for (int k = 0; k < N; k++) {
+      u32 b = h_brev((u32)k, logN);
+      u64 w = h_powmod(psi, b, q), wi = h_powmod(psii, b, q);
+      tab[k] = w;
+      tab[N + k] = h_shoup(w, q);
+      tab[2 * N + k] = wi;
+      tab[3 * N + k] = h_shoup(wi, q);
+    }
+    u64 *dt = r->d_tables + per * i;
+    CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
+    ModTab &M = r->h_mods[i];
+    M.q = q;
+    int bits = 64 - __builtin_clzll(q);
+    M.bits = bits;
+    M.mu = (u64)((((u128)1) << (2 * bits)) / q);
+    M.r64 = (u64)((((u128)1) << 64) % q);
+    M.ninv = h_inv((u64)N % q, q);
+    M.ninv_sh = h_shoup(M.ninv, q);
+    M.tw = dt;
+    M.tw_sh = dt + N;
+    M.itw = dt + 2 * N;
+    M.itw_sh = dt + 3 * N;
+  }
+  CK(cudaMalloc((void **)&r->d_mods, sizeof(ModTab) * r->nmod));
+  CK(cudaMemcpy(r->d_mods, r->h_mods.data(), sizeof(ModTab) * r->nmod, cudaMemcpyHostToDevice));
+  // slot map
+  std::vector<u32> sidx(r->n_slots);
+  u64 twoN = 2ull * N, e = 1;
+  int h = r->one_row ? r->n_slots : r->n_slots / 2;
+  for (int i = 0; i < h; i++) {
+    sidx[i] = h_brev((u32)((e - 1) / 2), logN);
+    if (!r->one_row) sidx[h + i] = h_brev((u32)((twoN - e - 1) / 2), logN);
+    e = (e * 5) % twoN;
+  }
+  CK(cudaMalloc((void **)&r->d_slot_idx, sizeof(u32) * r->n_slots));
+  CK(cudaMemcpy(r->d_slot_idx, sidx.data(), sizeof(u32) * r->n_slots, cudaMemcpyHostToDevice));
+  // constants
+  Consts &C = r->h_c;
+  memset(&C, 0, sizeof C);
+  C.L = L; C.nB = nB; C.N = N; C.logN = logN; C.n_slots = r->n_slots; C.t = r->t;
+  const u64 *q = r->mods.data(), P = r->mods[r->iP], *b = r->mods.data() + r->iB0, t = r->t;
+  C.Qmodt = 1;
+  for (int l = 0; l < L; l++) C.Qmodt = h_mulmod(C.Qmodt, q[l] % t, t);
+  for (int l = 0; l < L; l++) {
+    C.tinvq[l] = h_inv(t % q[l], q[l]);
+    C.Pmodq[l] = P % q[l];
+    C.Pinvq[l] = h_inv(P % q[l], q[l]);
+    C.Pinvq_sh[l] = h_shoup(C.Pinvq[l], q[l]);
+    u64 qh = 1;
+    for (int i = 0; i < L; i++)
+      if (i != l) qh = h_mulmod(qh, q[i] % q[l], q[l]);
+    C.QhatInv[l] = h_inv(qh, q[l]);
+    u128 x = (u128)t * C.QhatInv[l];
+    C.dec_omega[l] = (u64)(x / q[l]);
+    h_frac128((u64)(x % q[l]), q[l], &C.dec_th_hi[l], &C.dec_th_lo[l]);
+    C.invq[l] = 1.0 / (double)q[l];
+    for (int k = 0; k < nB; k++) {
+      u64 v = 1;
+      for (int i = 0; i < L; i++)
+        if (i != l) v = h_mulmod(v, q[i] % b[k], b[k]);
+      C.QhatModB[l][k] = v;
+    }
+  }
+  for (int k = 0; k < nB; k++) {
+    u64 v = 1;
+    for (int i = 0; i < L; i++) v = h_mulmod(v, q[i] % b[k], b[k]);
+    C.QmodB[k] = v;
+    u64 bh = 1;
+    for (int i = 0; i < nB; i++)
+      if (i != k) bh = h_mulmod(bh, b[i] % b[k], b[k]);
+    C.BhatInv[k] = h_inv(bh, b[k]);
+    C.tBhat[k] = h_mulmod(t % b[k], bh, b[k]);
+    C.BQhatInv[k] = h_inv(h_mulmod(bh, v, b[k]), b[k]);
+    C.invb[k] = 1.0 / (double)b[k];
+    for (int l = 0; l < L; l++) {
+      u64 w = 1;
+      for (int i = 0; i < nB; i++)
+        if (i != k) w = h_mulmod(w, b[i] % q[l], q[l]);
+      C.BhatModQ[k][l] = w;
+    }
+  }
+  for (int l = 0; l < L; l++) {
+    u64 v = 1;
+    for (int i = 0; i < nB; i++) v = h_mulmod(v, b[i] % q[l], q[l]);
+    C.BmodQ[l] = v;
+    u64 qh = 1;
+    for (int i = 0; i < L; i++)
+      if (i != l) qh = h_mulmod(qh, q[i] % q[l], q[l]);
+    C.QBhatInv[l] = h_inv(h_mulmod(qh, v, q[l]), q[l]);
+    Big T(t);
+    for (int i = 0; i < nB; i++) T.mul(b[i]);
+    u64 rem = T.divmod(q[l]);
+    for (int k = 0; k < nB; k++) C.sc_omega[l][k] = T.mod(b[k]);
+    h_frac128(rem, q[l], &C.sc_th_hi[l], &C.sc_th_lo[l]);
+  }
+  CK(cudaMalloc((void **)&r->d_c, sizeof(Consts)));
+  CK(cudaMemcpy(r->d_c, &C, sizeof(Consts), cudaMemcpyHostToDevice));
+  // secret key: ternary from ChaCha20(key_seed, DOM_SK), word j -> (w mod 3) - 1
+  std::vector<u64> s((size_t)(L + 1) * N);
+  u32 blk[16];
+  for (int j = 0; j < N; j++) {
+    if (j % 16 == 0) chacha_host(r->keyseed, (u64)(j / 16), nonce_of(DOM_SK, 0), blk);
+    int sv = (int)(blk[j % 16] % 3) - 1;
+    for (int l = 0; l <= L; l++) {
+      u64 qq = r->mods[l == L ? r->iP : l];
+      s[(size_t)l * N + j] = sv >= 0 ? (u64)sv : qq - 1;
+    }
+  }
+  CK(cudaMalloc((void **)&r->d_s, sizeof(u64) * s.size()));
+  CK(cudaMemcpy(r->d_s, s.data(), sizeof(u64) * s.size(), cudaMemcpyHostToDevice));
+  std::vector<int> mi(L + 1);
+  for (int l = 0; l < L; l++) mi[l] = l;
+  mi[L] = r->iP;
+  ntt_items(r, true, r->d_s, nullptr, 0, 1, 1, L + 1, mi.data());
+  CK(cudaStreamSynchronize(r->stream));
+}
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char *cgb_last_error(void) { return g_err.c_str(); }
+
+int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots, int one_row,
+                    const uint32_t key_seed[8], int64_t arena_cts, int64_t arena_pts, cgb_ring **out) {
+  API_BEGIN
+  if (log_n < 2 || log_n > 14) FAIL(CGB_ERR_PARAM, "log_n %d outside [2, 14]", log_n);
+  if (n_limbs < 1 || n_limbs > MAXL) FAIL(CGB_ERR_PARAM, "n_limbs %d outside [1, %d]", n_limbs, MAXL);
+  u64 N = 1ull << log_n;
+  if (plain_modulus < 3 || plain_modulus >= (1ull << 31) || plain_modulus % (2 * N) != 1)
+    FAIL(CGB_ERR_PARAM, "plain modulus %llu must be < 2^31 and = 1 mod 2N = %llu",
+         (unsigned long long)plain_modulus, (unsigned long long)(2 * N));
+  if (one_row ? (u64)n_slots * 2 != N : (u64)n_slots != N)
+    FAIL(CGB_ERR_PARAM, "n_slots %d does not match ring degree %llu (one_row=%d)", n_slots, (unsigned long long)N,
+         one_row);
+  cgb_ring *r = new cgb_ring();
+  r->logN = log_n;
+  r->N = (int)N;
+  r->L = n_limbs;
+  r->nB = n_limbs + 1;
+  r->t = plain_modulus;
+  r->n_slots = n_slots;
+  r->one_row = one_row;
+  CK(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+  r->own_stream = true;
+  {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    size_t smem = sizeof(u64) * (size_t)(N + (N >> 4) + 1);
+#define SETSMEM(EE)                                                                                           \
+  CK(cudaFuncSetAttribute(k_ntt<EE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));        \
+  CK(cudaFuncSetAttribute(k_ntt<EE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
+#undef SETSMEM
+  }
+  r->pin_cap = 8u << 20;
+  CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
+  build_ring(r, key_seed);
+  r->ct_words = 2ull * r->L * r->N;
+  r->arena_cap = (size_t)std::max<int64_t>(arena_cts, 1);
+  CK(cudaMalloc((void **)&r->arena, sizeof(u64) * r->ct_words * r->arena_cap));
+  r->ct_used.assign(r->arena_cap, 0);
+  for (size_t i = r->arena_cap; i-- > 0;) r->ct_free.push_back((u32)i);
+  r->pt_cap = (size_t)std::max<int64_t>(arena_pts, 1);
+  CK(cudaMalloc((void **)&r->pt_arena, sizeof(u64) * (size_t)r->L * r->N * r->pt_cap));
+  r->pt_used.assign(r->pt_cap, 0);
+  for (size_t i = r->pt_cap; i-- > 0;) r->pt_free.push_back((u32)i);
+  *out = r;
+  API_END
+}
+
+void cgb_ring_destroy(cgb_ring *r) {
+  if (!r) return;
+  cudaStreamSynchronize(r->stream);
+  for (auto &kv : r->keys) cudaFree(kv.second);
+  cudaFree(r->arena);
+  cudaFree(r->pt_arena);
+  cudaFree(r->d_tables);
+  cudaFree(r->d_mods);
+  cudaFree(r->d_slot_idx);
+  cudaFree(r->d_s);
+  cudaFree(r->d_c);
+  cudaFreeHost(r->pin);
+  if (r->own_stream) cudaStreamDestroy(r->stream);
+  delete r;
+}
+
+int cgb_ring_moduli(const cgb_ring *r, uint64_t *out, int cap) {
+  int n = std::min(cap, r->iT);
+  for (int i = 0; i < n; i++) out[i] = r->mods[i];
+  return n;
+}
+size_t cgb_ct_words(const cgb_ring *r) { return r->ct_words; }
+uint64_t cgb_launch_count(const cgb_ring *r) { return r->launches; }
+
+int cgb_set_stream(cgb_ring *r, void *s) {
+  API_BEGIN
+  CK(cudaStreamSynchronize(r->stream));
+  if (r->own_stream) cudaStreamDestroy(r->stream);
+  r->stream = (cudaStream_t)s;
+  r->own_stream = false;
+  API_END
+}
+int cgb_sync(cgb_ring *r) {
+  API_BEGIN
+  CK(cudaStreamSynchronize(r->stream));
+  API_END
+}
+
+int cgb_ct_alloc(cgb_ring *r, int count, uint32_t *ids) {
+  API_BEGIN
+  std::lock_guard<std::mutex> g(r->mu);
+  if ((size_t)count > r->ct_free.size())
+    FAIL(CGB_ERR_NOMEM, "ciphertext arena exhausted (%zu slots)", r->arena_cap);
+  for (int i = 0; i < count; i++) {
+    ids[i] = r->ct_free.back();
+    r->ct_free.pop_back();
+    r->ct_used[ids[i]] = 1;
+  }
+  API_END
+}
+int cgb_ct_free(cgb_ring *r, int count, const uint32_t *ids) {
+  API_BEGIN
+  std::lock_guard<std::mutex> g(r->mu);
+  for (int i = 0; i < count; i++) {
+    if (ids[i] >= r->arena_cap || !r->ct_used[ids[i]]) FAIL(CGB_ERR_PARAM, "double free of ciphertext %u", ids[i]);
+    r->ct_used[ids[i]] = 0;
+    r->ct_free.push_back(ids[i]);
+  }
+  API_END
+}
+uint64_t *cgb_ct_device_ptr(cgb_ring *r, uint32_t id) { return r->arena + (size_t)id * r->ct_words; }
+
+int cgb_pt_alloc(cgb_ring *r, int count, uint32_t *ids) {
+  API_BEGIN
+  std::lock_guard<std::mutex> g(r->mu);
+  if ((size_t)count > r->pt_free.size()) FAIL(CGB_ERR_NOMEM, "plaintext arena exhausted (%zu slots)", r->pt_cap);
+  for (int i = 0; i < count; i++) {
+    ids[i] = r->pt_free.back();
+    r->pt_free.pop_back();
+    r->pt_used[ids[i]] = 1;
+  }
+  API_END
+}
+int cgb_pt_free(cgb_ring *r, int count, const uint32_t *ids) {
+  API_BEGIN
+  std::lock_guard<std::mutex> g(r->mu);
+  for (int i = 0; i < count; i++) {
+    if (ids[i] >= r->pt_cap || !r->pt_used[ids[i]]) FAIL(CGB_ERR_PARAM, "double free of plaintext %u", ids[i]);
+    r->pt_used[ids[i]] = 0;
+    r->pt_free.push_back(ids[i]);
+  }
+  API_END
+}
+
+int cgb_ct_copy(cgb_ring *r, int count, const uint32_t *src, const uint32_t *dst) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  auto ps = ct_ptrs(r, count, src), pd = ct_ptrs(r, count, dst);
+  u64 **ds = S.up(ps.data(), count), **dd = S.up(pd.data(), count);
+  k_copy<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dd, (const u64 *const *)ds, r->ct_words);
+  check_launch(r);
+  API_END
+}
+int cgb_ct_store(cgb_ring *r, int count, const uint32_t *ids, uint64_t *host) {
+  API_BEGIN
+  for (int i = 0; i < count; i++) {
+    auto p = ct_ptrs(r, 1, &ids[i]);
+    CK(cudaMemcpyAsync(host + (size_t)i * r->ct_words, p[0], sizeof(u64) * r->ct_words, cudaMemcpyDeviceToHost,
+                       r->stream));
+  }
+  CK(cudaStreamSynchronize(r->stream));
+  API_END
+}
+int cgb_ct_load(cgb_ring *r, int count, const uint32_t *ids, const uint64_t *host) {
+  API_BEGIN
+  for (int i = 0; i < count; i++) {
+    auto p = ct_ptrs(r, 1, &ids[i]);
+    CK(cudaMemcpyAsync(p[0], host + (size_t)i * r->ct_words, sizeof(u64) * r->ct_words, cudaMemcpyHostToDevice,
+                       r->stream));
+  }
+  CK(cudaStreamSynchronize(r->stream));
+  API_END
+}
+
+int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const uint32_t *pt_ids) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  if (kind != CGB_PT_MUL && kind != CGB_PT_ADD) FAIL(CGB_ERR_PARAM, "unknown plaintext kind %d", kind);
+  Scratch S(r);
+  u64 *m = S.alloc<u64>((size_t)count * r->N);
+  encode_slots(r, S, slots, count, m);
+  auto pp = pt_ptrs(r, count, pt_ids);
+  u64 **dp = S.up(pp.data(), count);
+  u64 words = (u64)r->L * r->N;
+  k_pt_lift<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dp, m, r->d_mods, r->d_c, r->L, r->logN, kind);
+  check_launch(r);
+  std::vector<int> qm;
+  ntt_items(r, true, nullptr, dp, 0, count, 1, r->L, q_mod_idx(r, qm));
+  API_END
+}
+
+int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t enc_key[8], uint64_t first_index,
+                const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  ChaKey key;
+  memcpy(key.k, enc_key, sizeof key.k);
+  u64 *m = S.alloc<u64>((size_t)count * r->N);
+  encode_slots(r, S, slots, count, m);
+  auto pc = ct_ptrs(r, count, out);
+  u64 **dc = S.up(pc.data(), count);
+  std::vector<u64 *> c1(count);
+  std::vector<u64> na(count), ne(count);
+  for (int i = 0; i < count; i++) {
+    c1[i] = pc[i] + (size_t)r->L * r->N;
+    na[i] = nonce_of(DOM_ENC_A, first_index + i);
+    ne[i] = nonce_of(DOM_ENC_E, first_index + i);
+  }
+  u64 **dc1 = S.up(c1.data(), count);
+  std::vector<int> qm;
+  q_mod_idx(r, qm);
+  sample_uniform(r, S, dc1, count, key, na, r->L, qm.data());
+  i64 *e = S.alloc<i64>((size_t)count * r->N);
+  sample_cbd(r, S, e, key, ne);
+  u64 words = (u64)r->L * r->N;
+  k_enc_c0<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, m, e, r->d_mods, r->d_c, r->L, r->logN);
+  check_launch(r);
+  ntt_items(r, true, nullptr, dc, 0, count, 1, r->L, qm.data());
+  k_enc_sub_as<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, r->d_s, r->d_mods, r->L, r->logN);
+  check_launch(r);
+  API_END
+}
+
+int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  auto pc = ct_ptrs(r, count, cts);
+  u64 **dc = S.up(pc.data(), count);
+  u64 words = (u64)r->L * r->N;
+  u64 *X = S.alloc<u64>((size_t)count * words);
+  k_dec_inner<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
+                                                                       r->d_c, r->L, r->logN, 0);
+  check_launch(r);
+  std::vector<int> qm;
+  ntt_items(r, false, X, nullptr, words, count, 1, r->L, q_mod_idx(r, qm));
+  u64 *m = S.alloc<u64>((size_t)count * r->N);
+  k_dec_scale<<<dim3(GRID1(r->N, TPB).x, count), TPB, 0, r->stream>>>(m, X, r->d_c, r->L, r->logN);
+  check_launch(r);
+  int mi = r->iT;
+  ntt_items(r, true, m, nullptr, r->N, count, 1, 1, &mi);
+  u64 *so = S.alloc<u64>((size_t)count * r->n_slots);
+  k_gather_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(so, m, r->d_slot_idx, r->n_slots,
+                                                                               r->logN);
+  check_launch(r);
+  CK(cudaMemcpyAsync(slots_out, so, sizeof(u64) * (size_t)count * r->n_slots, cudaMemcpyDeviceToHost, r->stream));
+  CK(cudaStreamSynchronize(r->stream));
+  API_END
+}
+
+int cgb_noise_budget(cgb_ring *r, int count, const uint32_t *cts, double *bits) {
+  API_BEGIN
+  const int L = r->L, N = r->N;
+  u64 words = (u64)L * N;
+  std::vector<u64> host(words);
+  // Q and Q/q_l as bignums
+  Big Q(1);
+  for (int l = 0; l < L; l++) Q.mul(r->mods[l]);
+  std::vector<Big> Qh(L, Big(1));
+  for (int l = 0; l < L; l++)
+    for (int i = 0; i < L; i++)
+      if (i != l) Qh[l].mul(r->mods[i]);
+  auto cmp = [](const Big &a, const Big &b) {
+    for (int i = (int)a.w.size() - 1; i >= 0; i--)
+      if (a.w[i] != b.w[i]) return a.w[i] < b.w[i] ? -1 : 1;
+    return 0;
+  };
+  auto add = [](Big &a, const Big &b) {
+    u128 c = 0;
+    for (size_t i = 0; i < a.w.size(); i++) {
+      c += (u128)a.w[i] + b.w[i];
+      a.w[i] = (u64)c;
+      c >>= 64;
+    }
+  };
+  auto sub = [](Big &a, const Big &b) {
+    u64 br = 0;
+    for (size_t i = 0; i < a.w.size(); i++) {
+      u64 bi = b.w[i] + br;
+      br = (bi < br) || (a.w[i] < bi);
+      a.w[i] -= bi;
+    }
+  };
+  auto lg = [](const Big &a) {
+    for (int i = (int)a.w.size() - 1; i >= 0; i--)
+      if (a.w[i]) return std::log2((double)a.w[i] + (i ? (double)a.w[i - 1] / 18446744073709551616.0 : 0.0)) + 64.0 * i;
+    return -1e9;
+  };
+  for (int c = 0; c < count; c++) {
+    Scratch S(r);
+    auto pc = ct_ptrs(r, 1, &cts[c]);
+    u64 **dc = S.up(pc.data(), 1);
+    u64 *X = S.alloc<u64>(words);
+    k_dec_inner<<<dim3(GRID1(words, TPB).x, 1), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
+                                                                     r->d_c, L, r->logN, 1);
+    check_launch(r);
+    std::vector<int> qm;
+    ntt_items(r, false, X, nullptr, words, 1, 1, L, q_mod_idx(r, qm));
+    CK(cudaMemcpyAsync(host.data(), X, sizeof(u64) * words, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaStreamSynchronize(r->stream));
+    double worst = -1e9;
+    for (int j = 0; j < N; j++) {
+      Big acc(0);
+      for (int l = 0; l < L; l++) {
+        Big term = Qh[l];
+        term.mul(h_mulmod(host[(size_t)l * N + j], r->h_c.QhatInv[l], r->mods[l]));
+        add(acc, term);
+      }
+      while (cmp(acc, Q) >= 0) sub(acc, Q);
+      Big tw = acc;
+      add(tw, acc);
+      if (cmp(tw, Q) > 0) {
+        Big n = Q;
+        sub(n, acc);
+        acc = n;
+      }
+      worst = std::max(worst, lg(acc));
+    }
+    bits[c] = lg(Q) - std::max(worst, 0.0) - 1.0;
+  }
+  API_END
+}
+
+int cgb_add(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  auto pa = ct_ptrs(r, count, a), pb = ct_ptrs(r, count, b), po = ct_ptrs(r, count, out);
+  u64 **da = S.up(pa.data(), count), **db = S.up(pb.data(), count), **dout = S.up(po.data(), count);
+  k_add<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dout, (const u64 *const *)da,
+                                                                       (const u64 *const *)db, r->d_mods, r->L,
+                                                                       r->logN, r->ct_words);
+  check_launch(r);
+  API_END
+}
+int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
+  u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
+  k_add_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words);
+  check_launch(r);
+  API_END
+}
+int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  Scratch S(r);
+  auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
+  u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
+  k_mult_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words);
+  check_launch(r);
+  API_END
+}
+int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
+  API_BEGIN
+  if (count <= 0) FAIL(CGB_ERR_PARAM, "empty sum");
+  Scratch S(r);
+  auto pa = ct_ptrs(r, count, a), po = ct_ptrs(r, 1, &out);
+  u64 **da = S.up(pa.data(), count);
+  k_sum<<<GRID1(r->ct_words, TPB), TPB, 0, r->stream>>>(po[0], (const u64 *const *)da, count, r->d_mods, r->L,
+                                                        r->logN, r->ct_words);
+  check_launch(r);
+  API_END
+}
+
+int cgb_galois(cgb_ring *r, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  galois_batch(r, count, a, g, out, false);
+  API_END
+}
+static std::vector<u64> steps_to_g(cgb_ring *r, int count, const int64_t *steps) {
+  if (!r->one_row) FAIL(CGB_ERR_PARAM, "cgb_rotate needs the one-row layout; compose galois on the host");
+  std::vector<u64> g(count);
+  u64 twoN = 2ull * r->N;
+  for (int i = 0; i < count; i++) {
+    int64_t k = steps[i] % r->n_slots;
+    if (k < 0) k += r->n_slots;
+    g[i] = h_powmod(5, (u64)k, twoN);
+  }
+  return g;
+}
+int cgb_rotate(cgb_ring *r, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  auto g = steps_to_g(r, count, steps);
+  galois_batch(r, count, a, g.data(), out, false);
+  API_END
+}
+int cgb_rotate_add(cgb_ring *r, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  auto g = steps_to_g(r, count, steps);
+  galois_batch(r, count, a, g.data(), out, true);
+  API_END
+}
+int cgb_prepare_galois(cgb_ring *r, int count, const uint64_t *g) {
+  API_BEGIN
+  for (int i = 0; i < count; i++) {
+    u64 gg = g[i] % (2ull * r->N);
+    if (gg != 1) get_key(r, gg);
+  }
+  API_END
+}
+
+int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  const int L = r->L, nB = r->nB, nt = L + nB, N = r->N, logN = r->logN;
+  u64 *rk = get_key(r, 0);
+  std::vector<int> qm, bm(nB), tm(nt);
+  q_mod_idx(r, qm);
+  for (int k = 0; k < nB; k++) bm[k] = r->iB0 + k;
+  for (int l = 0; l < nt; l++) tm[l] = l < L ? l : r->iB0 + (l - L);
+  size_t per_item = (size_t)N * (4 * nt + 4 * L + 3 * nt + 3 * L + 1 + L * (L + 1) + 2 * (L + 1) + 2 * L + L);
+  size_t CH = chunk_for(r, per_item);
+  for (int c0 = 0; c0 < count; c0 += (int)CH) {
+    int n = std::min((int)CH, count - c0);
+    Scratch S(r);
+    auto pa = ct_ptrs(r, n, a + c0), pb = ct_ptrs(r, n, b + c0), po = ct_ptrs(r, n, out + c0);
+    // inputs: in[item][4][nt][N] with Q limbs = NTT copies; coef[item][4][L][N]
+    u64 *in = S.alloc<u64>((size_t)n * 4 * nt * N);
+    u64 *coef = S.alloc<u64>((size_t)n * 4 * L * N);
+    u64 **dpa = S.up(pa.data(), n), **dpb = S.up(pb.data(), n);
+    for (int p = 0; p < 4; p++) {
+      const u64 *const *src = (const u64 *const *)(p < 2 ? dpa : dpb);
+      u64 off = (p & 1) ? (u64)L * N : 0;
+      k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(in + (u64)p * nt * N, 4ull * nt * N, src,
+                                                                         off, (u64)L * N);
+      check_launch(r);
+      k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(coef + (u64)p * L * N, 4ull * L * N, src,
+                                                                         off, (u64)L * N);
+      check_launch(r);
+    }
+    ntt_items(r, false, coef, nullptr, 4ull * L * N, n, 4, L, qm.data());
+    k_lift_QB<<<dim3(GRID1(4ull * N, TPB).x, n), TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0,
+                                                                      logN);
+    check_launch(r);
+    {
+      NttJob job{};
+      job.base = in;
+      job.item_stride = 4ull * nt * N;
+      int u = 0;
+      for (int p = 0; p < 4; p++)
+        for (int k = 0; k < nB; k++) {
+          job.sub_off[u] = (unsigned short)(p * nt + L + k);
+          job.sub_mod[u] = (unsigned char)bm[k];
+          u++;
+        }
+      job.nsub = u;
+      launch_ntt(r, true, job, n);
+    }
+    u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
+    k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, r->d_mods, L, nt, r->iB0, logN);
+    check_launch(r);
+    ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
+    u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
+    k_scale_round<<<dim3(GRID1(3ull * N, TPB).x, n), TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0,
+                                                                         logN);
+    check_launch(r);
+    ntt_items(r, true, d, nullptr, 3ull * L * N, n, 3, L, qm.data());
+    // relinearise d2, add (d0, d1)
+    u64 *x = S.alloc<u64>((size_t)n * L * N);
+    CK(cudaMemcpy2DAsync(x, sizeof(u64) * L * N, d + 2ull * L * N, sizeof(u64) * 3 * L * N, sizeof(u64) * L * N, n,
+                         cudaMemcpyDeviceToDevice, r->stream));
+    u64 *d01 = S.alloc<u64>((size_t)n * 2 * L * N);
+    CK(cudaMemcpy2DAsync(d01, sizeof(u64) * 2 * L * N, d, sizeof(u64) * 3 * L * N, sizeof(u64) * 2 * L * N, n,
+                         cudaMemcpyDeviceToDevice, r->stream));
+    std::vector<u64 *> keys(n, rk);
+    u64 **dk = S.up(keys.data(), n), **dout = S.up(po.data(), n);
+    // out = ks + d01 : reuse add0 for poly 0 and an add1 table for poly 1 via a second pass
+    std::vector<u64 *> d01p(n);
+    for (int i = 0; i < n; i++) d01p[i] = d01 + (size_t)i * 2 * L * N;
+    u64 **dd01 = S.up(d01p.data(), n);
+    keyswitch(r, S, x, n, dk, dout, nullptr, (const u64 *const *)dd01);
+  }
+  API_END
+}
+
+}  // extern "C"

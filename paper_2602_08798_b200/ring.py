@@ -1,0 +1,177 @@
+"""Thin host object over one ``cgb_ring`` (include/cgb200.h).
+
+A ring is the device-side realisation of one ``BackendParams`` value: the
+ring degree, the prime chains, the secret key, the evaluation keys and the
+ciphertext/plaintext arenas.  Ciphertexts and plaintexts are named by
+uint32 arena ids; every method is batched over arrays of ids.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _native as nat
+
+DEFAULT_ARENA_BYTES = int(os.environ.get("CGB_ARENA_GIB", "24")) << 30
+DEFAULT_PT_BYTES = int(os.environ.get("CGB_PT_ARENA_GIB", "4")) << 30
+
+
+def _ids(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32).reshape(-1))
+
+
+class Ring:
+    def __init__(self, log_n: int, t: int, n_limbs: int, n_slots: int, one_row: bool, key_seed,
+                 arena_cts: int | None = None, arena_pts: int | None = None):
+        self.log_n, self.N, self.t, self.L = log_n, 1 << log_n, int(t), int(n_limbs)
+        self.n_slots, self.one_row = int(n_slots), bool(one_row)
+        self.ct_words = 2 * self.L * self.N
+        if arena_cts is None:
+            arena_cts = max(64, min(65536, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))
+        if arena_pts is None:
+            arena_pts = max(64, min(16384, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
+        self.arena_cts, self.arena_pts = int(arena_cts), int(arena_pts)
+        ks = np.ascontiguousarray(np.asarray(key_seed, dtype=np.uint32).reshape(8))
+        h = ctypes.c_void_p()
+        L = nat.lib()
+        nat.check(L.cgb_ring_create(log_n, self.t, self.L, self.n_slots, int(one_row), nat.u32ptr(ks),
+                                    self.arena_cts, self.arena_pts, ctypes.byref(h)), "cgb_ring_create")
+        self._h = h
+        mods = np.zeros(64, dtype=np.uint64)
+        k = L.cgb_ring_moduli(self._h, nat.u64ptr(mods), 64)
+        self.moduli = [int(x) for x in mods[:k]]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            nat.lib().cgb_ring_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    @property
+    def handle(self):
+        return self._h
+
+    def launches(self) -> int:
+        return int(nat.lib().cgb_launch_count(self._h))
+
+    def sync(self):
+        nat.check(nat.lib().cgb_sync(self._h), "cgb_sync")
+
+    def set_stream(self, cuda_stream: int):
+        nat.check(nat.lib().cgb_set_stream(self._h, ctypes.c_void_p(cuda_stream)), "cgb_set_stream")
+
+    # storage -------------------------------------------------------------
+    def alloc(self, n: int) -> np.ndarray:
+        ids = np.zeros(n, dtype=np.uint32)
+        if n:
+            nat.check(nat.lib().cgb_ct_alloc(self._h, n, nat.u32ptr(ids)), "cgb_ct_alloc")
+        return ids
+
+    def free(self, ids):
+        ids = _ids(ids)
+        if ids.size and self._h:
+            nat.check(nat.lib().cgb_ct_free(self._h, ids.size, nat.u32ptr(ids)), "cgb_ct_free")
+
+    def alloc_pt(self, n: int) -> np.ndarray:
+        ids = np.zeros(n, dtype=np.uint32)
+        if n:
+            nat.check(nat.lib().cgb_pt_alloc(self._h, n, nat.u32ptr(ids)), "cgb_pt_alloc")
+        return ids
+
+    def free_pt(self, ids):
+        ids = _ids(ids)
+        if ids.size and self._h:
+            nat.check(nat.lib().cgb_pt_free(self._h, ids.size, nat.u32ptr(ids)), "cgb_pt_free")
+
+    def copy(self, src, dst):
+        src, dst = _ids(src), _ids(dst)
+        nat.check(nat.lib().cgb_ct_copy(self._h, src.size, nat.u32ptr(src), nat.u32ptr(dst)), "cgb_ct_copy")
+
+    def store(self, ids) -> np.ndarray:
+        ids = _ids(ids)
+        out = np.zeros((ids.size, 2, self.L, self.N), dtype=np.uint64)
+        nat.check(nat.lib().cgb_ct_store(self._h, ids.size, nat.u32ptr(ids), nat.u64ptr(out)), "cgb_ct_store")
+        return out
+
+    def load(self, ids, words):
+        ids = _ids(ids)
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64).reshape(ids.size, 2, self.L, self.N))
+        nat.check(nat.lib().cgb_ct_load(self._h, ids.size, nat.u32ptr(ids), nat.u64ptr(w)), "cgb_ct_load")
+
+    # plaintexts ------------------------------------------------------------
+    def _slots2d(self, slots) -> np.ndarray:
+        a = np.asarray(slots, dtype=np.int64)
+        if a.ndim == 1:
+            a = a.reshape(1, -1)
+        return np.ascontiguousarray(np.mod(a, self.t).astype(np.uint64))
+
+    def encode_pt(self, slots, kind: int, ids):
+        s, ids = self._slots2d(slots), _ids(ids)
+        nat.check(nat.lib().cgb_pt_encode(self._h, ids.size, nat.u64ptr(s), kind, nat.u32ptr(ids)), "cgb_pt_encode")
+
+    # client role -----------------------------------------------------------
+    def encrypt(self, slots, enc_key, first_index: int, ids):
+        s, ids = self._slots2d(slots), _ids(ids)
+        k = np.ascontiguousarray(np.asarray(enc_key, dtype=np.uint32).reshape(8))
+        nat.check(nat.lib().cgb_encrypt(self._h, ids.size, nat.u64ptr(s), nat.u32ptr(k), int(first_index),
+                                        nat.u32ptr(ids)), "cgb_encrypt")
+
+    def decrypt(self, ids) -> np.ndarray:
+        ids = _ids(ids)
+        out = np.zeros((ids.size, self.n_slots), dtype=np.uint64)
+        nat.check(nat.lib().cgb_decrypt(self._h, ids.size, nat.u32ptr(ids), nat.u64ptr(out)), "cgb_decrypt")
+        return out.astype(np.int64)
+
+    def noise_budget(self, ids) -> np.ndarray:
+        ids = _ids(ids)
+        out = np.zeros(ids.size, dtype=np.float64)
+        nat.check(nat.lib().cgb_noise_budget(self._h, ids.size, nat.u32ptr(ids), nat.dblptr(out)), "cgb_noise_budget")
+        return out
+
+    # server role -----------------------------------------------------------
+    def _bin(self, fn, what, a, b, out):
+        a, b, out = _ids(a), _ids(b), _ids(out)
+        nat.check(fn(self._h, a.size, nat.u32ptr(a), nat.u32ptr(b), nat.u32ptr(out)), what)
+
+    def add(self, a, b, out):
+        self._bin(nat.lib().cgb_add, "cgb_add", a, b, out)
+
+    def add_plain(self, a, pt, out):
+        self._bin(nat.lib().cgb_add_plain, "cgb_add_plain", a, pt, out)
+
+    def mult_plain(self, a, pt, out):
+        self._bin(nat.lib().cgb_mult_plain, "cgb_mult_plain", a, pt, out)
+
+    def mult_cipher(self, a, b, out):
+        self._bin(nat.lib().cgb_mult_cipher, "cgb_mult_cipher", a, b, out)
+
+    def galois(self, a, gs, out):
+        a, out = _ids(a), _ids(out)
+        g = np.ascontiguousarray(np.broadcast_to(np.asarray(gs, dtype=np.uint64), a.shape))
+        nat.check(nat.lib().cgb_galois(self._h, a.size, nat.u32ptr(a), nat.u64ptr(g), nat.u32ptr(out)), "cgb_galois")
+
+    def rotate(self, a, steps, out, add_input: bool = False):
+        a, out = _ids(a), _ids(out)
+        st = np.ascontiguousarray(np.broadcast_to(np.asarray(steps, dtype=np.int64), a.shape))
+        fn = nat.lib().cgb_rotate_add if add_input else nat.lib().cgb_rotate
+        nat.check(fn(self._h, a.size, nat.u32ptr(a), nat.i64ptr(st), nat.u32ptr(out)), "cgb_rotate")
+
+    def sum(self, a, out: int):
+        a = _ids(a)
+        nat.check(nat.lib().cgb_sum(self._h, a.size, nat.u32ptr(a), int(out)), "cgb_sum")
+
+    def prepare_galois(self, gs):
+        g = np.ascontiguousarray(np.asarray(gs, dtype=np.uint64).reshape(-1))
+        nat.check(nat.lib().cgb_prepare_galois(self._h, g.size, nat.u64ptr(g)), "cgb_prepare_galois")
+
+    def galois_elt(self, k: int) -> int:
+        return pow(5, int(k) % (self.n_slots if self.one_row else self.n_slots // 2), 2 * self.N)

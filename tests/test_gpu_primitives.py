@@ -1,0 +1,92 @@
+"""GPU primitives vs the CPU RNS-BFV oracle: every ciphertext word bit-exact."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KEY = np.arange(8, dtype=np.uint32) * 7 + 1
+ENC = np.arange(8, dtype=np.uint32) + 1000
+
+CASES = [
+    # (log_n, t, L, n_slots, one_row)
+    (4, 97, 3, 8, True),
+    (3, 17, 2, 8, False),
+    (7, 67109633, 4, 64, True),
+    (14, 536903681, 4, 8192, True),
+]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: f"logN{c[0]}_t{c[1]}_L{c[2]}_{'row' if c[4] else 'two'}")
+def pair(request, oracle_mod):
+    from paper_2602_08798_b200._native import build
+    from paper_2602_08798_b200.ring import Ring
+
+    build()
+    log_n, t, L, n, one_row = request.param
+    g = Ring(log_n, t, L, n, one_row, KEY, arena_cts=64, arena_pts=16)
+    o = oracle_mod.OracleRing(log_n, t, L, n, one_row, KEY)
+    return g, o
+
+
+def test_moduli_match(pair):
+    g, o = pair
+    assert g.moduli == o.moduli[: len(g.moduli)]
+
+
+def _enc(g, o, v, idx):
+    ids = g.alloc(1)
+    g.encrypt(v, ENC, idx, ids)
+    ref = o.encrypt(v, ENC, idx)
+    return ids, ref
+
+
+def test_encrypt_decrypt_bitexact(pair, rng):
+    g, o = pair
+    v = rng.integers(0, o.t, o.n_slots)
+    ids, ref = _enc(g, o, v, 5)
+    assert np.array_equal(g.store(ids)[0], ref)
+    assert np.array_equal(g.decrypt(ids)[0], v)
+
+
+def test_pointwise_ops_bitexact(pair, rng):
+    g, o = pair
+    v, w = rng.integers(0, o.t, (2, o.n_slots))
+    a, ra = _enc(g, o, v, 1)
+    b, rb = _enc(g, o, w, 2)
+    out = g.alloc(1)
+    g.add(a, b, out)
+    assert np.array_equal(g.store(out)[0], o.add(ra, rb))
+    pt = g.alloc_pt(2)
+    g.encode_pt(w, 1, pt[:1])
+    g.add_plain(a, pt[:1], out)
+    assert np.array_equal(g.store(out)[0], o.add_plain(ra, w))
+    g.encode_pt(w, 0, pt[1:])
+    g.mult_plain(a, pt[1:], out)
+    assert np.array_equal(g.store(out)[0], o.mult_plain(ra, w))
+    assert np.array_equal(g.decrypt(out)[0], (v * w) % o.t)
+
+
+def test_rotate_bitexact(pair, rng):
+    g, o = pair
+    v = rng.integers(0, o.t, o.n_slots)
+    a, ra = _enc(g, o, v, 3)
+    out = g.alloc(1)
+    h = o.n_slots if o.one_row else o.n_slots // 2
+    for k in [0, 1, 3, h - 1]:
+        gel = pow(5, k % h, 2 * o.N)
+        g.galois(a, gel, out)
+        assert np.array_equal(g.store(out)[0], o.galois(ra, gel)), k
+        if o.one_row:
+            assert np.array_equal(g.decrypt(out)[0], np.roll(v, -k))
+
+
+def test_mult_cipher_bitexact(pair, rng):
+    g, o = pair
+    v, w = rng.integers(0, o.t, (2, o.n_slots))
+    a, ra = _enc(g, o, v, 7)
+    b, rb = _enc(g, o, w, 8)
+    out = g.alloc(1)
+    g.mult_cipher(a, b, out)
+    ref = o.mult_cipher(ra, rb)
+    assert np.array_equal(g.store(out)[0], ref)
+    assert np.array_equal(g.decrypt(out)[0], (v * w) % o.t)
