@@ -1,0 +1,828 @@
+"""Drop-in HE substrate: the reference ``Context`` API over the B200 ring.
+
+Reference boundary: ``cryptogen.backend`` (/root/reference/pkg/src/
+cryptogen/backend.py).  The reference realises a ciphertext as an n-slot
+vector over Z_p with a bit ledger (backend.py:216-230, :295-301) and op
+counters (:173-213); this module keeps the ledger and counters byte-for-byte
+and replaces the arithmetic with real RNS-BFV ciphertexts that live in the
+device arena of ``libcgb200.so``:
+
+  reference                      here
+  ---------------------------    ----------------------------------------
+  BackendParams / NoiseCosts     same dataclasses, same validation
+  OpCounter                      same fields, merge/snapshot/delta/to_json
+  SlotCiphertext (:216)          GpuCiphertext: arena id + budget + id
+  Context (:245)                 GpuContext: same methods, plus the
+                                 batched "wave" API (``Wave``) the fused
+                                 hot path in arcc/kv_cache/linear_kernels uses
+  new_context (:367)             new_context -> GpuContext (no CPU path)
+
+Layouts: when p = 1 (mod 4n) the ring degree is
+N = 2n and the n logical slots are one hypercube row, so a cyclic shift by
+k is the single automorphism X -> X^(5^k); otherwise (small test
+parameters with p = 1 mod 2n only) N = n and the shift is composed from the
+two row automorphisms and two 0/1 masks.
+
+Keys are shared by every context with equal parameters (contexts in the
+reference interoperate whenever ``params`` compare equal, backend.py:290);
+encryption randomness is per context: ChaCha20 keyed from the context's
+SeedSequence, one nonce per encryption in call order.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import itertools
+import json
+import os
+import threading
+import weakref
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as nat
+
+__all__ = [
+    "BackendParams", "Context", "DecryptionFailure", "GpuCiphertext", "GpuContext", "NoiseBudgetExhausted",
+    "NoiseCosts", "OpCounter", "ParameterError", "PlainVector", "SlotCiphertext", "Wave", "default_plain_modulus",
+    "is_prime", "new_context", "ring_for",
+]
+
+PlainVector = np.ndarray
+MAX_PLAIN_MODULUS = 1 << 31
+
+
+# ----------------------------------------------------------------------------
+# errors and parameters (restating backend.py:45-170)
+# ----------------------------------------------------------------------------
+class ParameterError(ValueError):
+    """Parameters, shapes or ciphertext ownership are invalid (backend.py:45)."""
+
+
+class NoiseBudgetExhausted(RuntimeError):
+    """The ledger would go negative (backend.py:49, :295-301)."""
+
+
+class DecryptionFailure(RuntimeError):
+    """Decryption of a ciphertext whose ledger is at zero (backend.py:53, :312)."""
+
+
+def is_prime(n: int) -> bool:
+    """Deterministic Miller-Rabin for n < 3.3e24 (same contract as backend.py:60)."""
+    if n < 2:
+        return False
+    small = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+    for b in small:
+        if n % b == 0:
+            return n == b
+    d, r = n - 1, 0
+    while not d & 1:
+        d >>= 1
+        r += 1
+    for a in small:
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def default_plain_modulus(n_slots: int, min_bits: int = 29) -> int:
+    """Smallest prime >= 2^min_bits that is 1 mod 2*n_slots (backend.py:84-93)."""
+    step = 2 * n_slots
+    c = (1 << min_bits) + (-(1 << min_bits) + 1) % step
+    while not is_prime(c):
+        c += step
+    return c
+
+
+@dataclass(frozen=True)
+class NoiseCosts:
+    """Ledger cost in bits of each operation (backend.py:96-113)."""
+
+    mult_plain: int = 20
+    mult_cipher: int = 40
+    rotate: int = 2
+    add: int = 0
+    add_plain: int = 0
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("mult_plain", "mult_cipher", "rotate", "add", "add_plain")}
+
+
+@dataclass(frozen=True)
+class BackendParams:
+    """Slot count, plaintext modulus and ledger (backend.py:116-170)."""
+
+    n_slots: int = 8192
+    plain_modulus: int = 536903681
+    initial_noise_budget: int = 190
+    noise_costs: NoiseCosts = field(default_factory=NoiseCosts)
+    refresh_threshold: int = 60
+
+    def __post_init__(self):
+        n, p = self.n_slots, self.plain_modulus
+        if n < 2 or n & (n - 1):
+            raise ParameterError(f"n_slots must be a power of two >= 2, got {n}")
+        if not is_prime(p):
+            raise ParameterError(f"plain_modulus {p} is not prime")
+        if p % (2 * n) != 1:
+            raise ParameterError(f"plain_modulus {p} must be 1 mod 2*n_slots (= {2 * n})")
+        if p >= MAX_PLAIN_MODULUS:
+            raise ParameterError(f"plain_modulus {p} exceeds 2^31")
+        if any(v < 0 for v in self.noise_costs.as_dict().values()):
+            raise ParameterError(f"noise costs must be >= 0, got {self.noise_costs.as_dict()}")
+        if not 0 <= self.refresh_threshold < self.initial_noise_budget:
+            raise ParameterError("refresh_threshold must lie in [0, initial_noise_budget)")
+
+    @property
+    def modulus_bits(self) -> int:
+        return self.plain_modulus.bit_length()
+
+    def ciphertext_bytes(self) -> int:
+        """Modelled wire size of one ciphertext transfer (backend.py:152-154)."""
+        return self.n_slots * self.modulus_bits // 8
+
+    def to_json(self) -> str:
+        d = {"n_slots": self.n_slots, "plain_modulus": self.plain_modulus,
+             "initial_noise_budget": self.initial_noise_budget, "noise_costs": self.noise_costs.as_dict(),
+             "refresh_threshold": self.refresh_threshold}
+        return json.dumps(d, indent=2, sort_keys=True)
+
+    @classmethod
+    def from_json(cls, text: str) -> "BackendParams":
+        d = json.loads(text)
+        return cls(noise_costs=NoiseCosts(**d.pop("noise_costs", {})), **d)
+
+
+_COUNTER_FIELDS = ("mult_plain", "mult_cipher", "rotate", "add", "add_plain", "encrypt", "decrypt",
+                   "refresh_events", "mpc_bytes")
+
+
+@dataclass
+class OpCounter:
+    """Monotone per-op tallies (backend.py:173-213)."""
+
+    mult_plain: int = 0
+    mult_cipher: int = 0
+    rotate: int = 0
+    add: int = 0
+    add_plain: int = 0
+    encrypt: int = 0
+    decrypt: int = 0
+    refresh_events: int = 0
+    mpc_bytes: int = 0
+
+    _FIELDS = _COUNTER_FIELDS
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k in _COUNTER_FIELDS}
+
+    def merge(self, other: "OpCounter") -> None:
+        for k in _COUNTER_FIELDS:
+            setattr(self, k, getattr(self, k) + getattr(other, k))
+
+    def snapshot(self) -> "OpCounter":
+        return OpCounter(**self.as_dict())
+
+    def delta(self, since: "OpCounter") -> dict:
+        return {k: getattr(self, k) - getattr(since, k) for k in _COUNTER_FIELDS}
+
+    def to_json(self) -> str:
+        return json.dumps(self.as_dict(), indent=2, sort_keys=True)
+
+
+def _params_key(params) -> tuple:
+    c = params.noise_costs
+    return (params.n_slots, params.plain_modulus)
+
+
+# ----------------------------------------------------------------------------
+# rings: one per (n_slots, p, limbs, key seed), shared by all contexts
+# ----------------------------------------------------------------------------
+_KEY_SEED = int(os.environ.get("CGB_KEY_SEED", "0"))
+_rings: dict = {}
+_rings_lock = threading.Lock()
+
+
+def default_limbs(ring_degree: int) -> int:
+    """Q limbs of 60 bits: 4 (240 bits) at production sizes -- the paper's
+    q ~ 2^220 class -- and 8 for toy rings, whose composite two-row
+    rotations spend more real noise per logical op."""
+    env = os.environ.get("CGB_LIMBS")
+    if env:
+        return int(env)
+    return 4 if ring_degree >= 2048 else 8
+
+
+def ring_layout(n_slots: int, p: int) -> tuple[int, bool]:
+    """(log2 N, one_row) for a parameter set."""
+    if p % (4 * n_slots) == 1:
+        return (2 * n_slots).bit_length() - 1, True
+    return n_slots.bit_length() - 1, False
+
+
+def ring_for(params, n_limbs: int | None = None, key_seed: int | None = None):
+    from .ring import Ring
+
+    log_n, one_row = ring_layout(params.n_slots, params.plain_modulus)
+    L = n_limbs or default_limbs(1 << log_n)
+    ks = _KEY_SEED if key_seed is None else key_seed
+    key = (params.n_slots, params.plain_modulus, L, ks)
+    with _rings_lock:
+        r = _rings.get(key)
+        if r is None:
+            seed = np.random.SeedSequence([0xB200_4B45, ks]).generate_state(8, dtype=np.uint32)
+            r = Ring(log_n, params.plain_modulus, L, params.n_slots, one_row, seed)
+            _rings[key] = r
+        return r
+
+
+# ----------------------------------------------------------------------------
+# ciphertext storage ownership
+# ----------------------------------------------------------------------------
+class _Block:
+    """Owns a set of arena ids; frees them when the last reference dies."""
+
+    __slots__ = ("ids", "__weakref__")
+
+    def __init__(self, ring, ids: np.ndarray):
+        self.ids = ids
+        weakref.finalize(self, ring.free, ids)
+
+
+class GpuCiphertext:
+    """Immutable ciphertext handle (replaces SlotCiphertext, backend.py:216-230).
+
+    ``slots`` is a client-side diagnostic: it decrypts on first access with
+    the ring's secret key and is read-only, like the reference's array."""
+
+    __slots__ = ("_block", "_aid", "noise_budget", "id", "params", "_ring", "_slots")
+
+    def __init__(self, block: _Block, aid: int, budget: int, cid: int, params, ring):
+        self._block, self._aid = block, int(aid)
+        self.noise_budget, self.id, self.params, self._ring = int(budget), int(cid), params, ring
+        self._slots = None
+
+    def __setattr__(self, name, value):
+        if hasattr(self, "_slots") and name != "_slots":
+            raise AttributeError("GpuCiphertext is immutable")
+        object.__setattr__(self, name, value)
+
+    @property
+    def n_slots(self) -> int:
+        return self.params.n_slots
+
+    @property
+    def slots(self) -> np.ndarray:
+        if self._slots is None:
+            s = self._ring.decrypt([self._aid])[0]
+            s.setflags(write=False)
+            object.__setattr__(self, "_slots", s)
+        return self._slots
+
+    def words(self) -> np.ndarray:
+        """The raw NTT-domain ciphertext words, uint64[2][L][N]."""
+        return self._ring.store([self._aid])[0]
+
+    def __repr__(self):
+        return f"GpuCiphertext(id={self.id}, budget={self.noise_budget}, slot={self._aid})"
+
+
+SlotCiphertext = GpuCiphertext
+
+
+# ----------------------------------------------------------------------------
+# waves: batches of ciphertexts processed by one launch sequence
+# ----------------------------------------------------------------------------
+class Wave:
+    """A batch of ciphertexts (arena ids + ledger budgets + owning contexts).
+
+    The fused hot path works on waves so that, e.g., all 64 x 12 broadcast
+    chains of a decode step rotate in one batched key switch.  ``owner``
+    maps each item to an index into ``ctxs``; counters and ciphertext ids
+    (``cids``) are charged to the owning context exactly as the per-op
+    path would charge them."""
+
+    __slots__ = ("ctxs", "owner", "aids", "budgets", "blocks", "cids")
+
+    def __init__(self, ctxs, owner, aids, budgets, blocks, cids=None):
+        self.ctxs, self.owner, self.aids, self.budgets, self.blocks = ctxs, owner, aids, budgets, blocks
+        self.cids = np.zeros(len(aids), np.int64) if cids is None else cids
+
+    def __len__(self):
+        return int(self.aids.size)
+
+    def take(self, idx) -> "Wave":
+        idx = np.asarray(idx, dtype=np.int64).reshape(-1)
+        return Wave(self.ctxs, self.owner[idx], self.aids[idx], self.budgets[idx], self.blocks, self.cids[idx])
+
+    @staticmethod
+    def concat(waves: Sequence["Wave"]) -> "Wave":
+        ctxs, owners = [], []
+        for w in waves:
+            base = len(ctxs)
+            ctxs.extend(w.ctxs)
+            owners.append(w.owner + base)
+        blocks = [b for w in waves for b in w.blocks]
+        return Wave(ctxs, np.concatenate(owners), np.concatenate([w.aids for w in waves]),
+                    np.concatenate([w.budgets for w in waves]), blocks, np.concatenate([w.cids for w in waves]))
+
+    def handles(self) -> list:
+        keep = self.blocks[0] if len(self.blocks) == 1 else _Keep(self.blocks)
+        out = []
+        for i in range(len(self)):
+            c = self.ctxs[self.owner[i]]
+            out.append(GpuCiphertext(keep, self.aids[i], self.budgets[i], self.cids[i], c.params, c._ring))
+        return out
+
+
+# ----------------------------------------------------------------------------
+# the context
+# ----------------------------------------------------------------------------
+_context_uid = itertools.count()
+
+
+def _as_slots(values, params) -> np.ndarray:
+    arr = np.asarray(values, dtype=np.int64)
+    if arr.ndim != 1 or arr.shape[0] != params.n_slots:
+        raise ParameterError(f"expected a vector of length {params.n_slots}, got shape {arr.shape}")
+    return np.mod(arr, params.plain_modulus)
+
+
+class GpuContext:
+    """``Context`` (backend.py:245-364) over the B200 RNS-BFV ring."""
+
+    def __init__(self, params, seed=0, n_limbs: int | None = None):
+        self.params = params
+        self.counter = OpCounter()
+        self._seed_seq = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+        self.rng = np.random.default_rng(self._seed_seq)
+        self._next_id = next(_context_uid) * 1_000_000_000
+        self._ring = ring_for(params, n_limbs)
+        ss = self._seed_seq
+        self._enc_key = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (0xB200,)).generate_state(
+            8, dtype=np.uint32)
+        self._hook_key = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (0xB201,)).generate_state(
+            8, dtype=np.uint32)
+        self._enc_index = 0
+        self._hook_index = 0
+        self._n_limbs = n_limbs
+
+    # -- helpers (backend.py:262-288) ---------------------------------------
+    @property
+    def ring(self):
+        return self._ring
+
+    def plain_vector(self, values) -> PlainVector:
+        return _as_slots(values, self.params)
+
+    def plain_from_dense(self, values) -> PlainVector:
+        arr = np.asarray(values, dtype=np.int64)
+        if arr.shape[0] > self.params.n_slots:
+            raise ParameterError("vector longer than slot count")
+        out = np.zeros(self.params.n_slots, dtype=np.int64)
+        out[: arr.shape[0]] = arr
+        return np.mod(out, self.params.plain_modulus)
+
+    def zeros(self) -> PlainVector:
+        return np.zeros(self.params.n_slots, dtype=np.int64)
+
+    def fork(self) -> "GpuContext":
+        return GpuContext(self.params, self._seed_seq.spawn(1)[0], self._n_limbs)
+
+    def join(self, child) -> None:
+        self.counter.merge(child.counter)
+
+    def _take_ids(self, n: int) -> int:
+        base = self._next_id
+        self._next_id += n
+        return base
+
+    def _new(self, n: int):
+        ids = self._ring.alloc(n)
+        return _Block(self._ring, ids), ids
+
+    def _check(self, *cts) -> None:
+        for ct in cts:
+            if not isinstance(ct, GpuCiphertext) or ct.params != self.params:
+                raise ParameterError("ciphertext belongs to an incompatible context")
+
+    def _spend(self, budget: int, cost: int) -> int:
+        left = budget - cost
+        if left < 0:
+            raise NoiseBudgetExhausted(f"operation needs {cost} bits but only {budget} remain")
+        return left
+
+    def _emit(self, block, aid, budget) -> GpuCiphertext:
+        return GpuCiphertext(block, aid, budget, self._take_ids(1), self.params, self._ring)
+
+    # -- plaintext operands ------------------------------------------------------
+    def _plaintexts(self, vecs: np.ndarray, kind: int):
+        """Encode a batch of slot vectors; returns (owner, ids)."""
+        return _pt_cache(self._ring).get(vecs, kind)
+
+    # -- client role ---------------------------------------------------------------
+    def _encrypt_slots(self, vecs: np.ndarray, hook: bool = False):
+        n = vecs.shape[0]
+        blk, ids = self._new(n)
+        if hook:
+            self._ring.encrypt(vecs, self._hook_key, self._hook_index, ids)
+            self._hook_index += n
+        else:
+            self._ring.encrypt(vecs, self._enc_key, self._enc_index, ids)
+            self._enc_index += n
+        return blk, ids
+
+    def encrypt(self, v) -> GpuCiphertext:
+        slots = _as_slots(v, self.params)
+        blk, ids = self._encrypt_slots(slots.reshape(1, -1))
+        self.counter.encrypt += 1
+        return self._emit(blk, ids[0], self.params.initial_noise_budget)
+
+    def decrypt(self, ct) -> PlainVector:
+        self._check(ct)
+        if ct.noise_budget <= 0:
+            raise DecryptionFailure("noise budget exhausted: decryption would be incorrect")
+        self.counter.decrypt += 1
+        return self._ring.decrypt([ct._aid])[0]
+
+    # -- server role ---------------------------------------------------------------
+    def add(self, a, b) -> GpuCiphertext:
+        self._check(a, b)
+        budget = self._spend(min(a.noise_budget, b.noise_budget), self.params.noise_costs.add)
+        blk, ids = self._new(1)
+        self._ring.add([a._aid], [b._aid], ids)
+        self.counter.add += 1
+        return self._emit(blk, ids[0], budget)
+
+    def add_plain(self, a, v) -> GpuCiphertext:
+        self._check(a)
+        slots = _as_slots(v, self.params)
+        budget = self._spend(a.noise_budget, self.params.noise_costs.add_plain)
+        keep, pts = self._plaintexts(slots.reshape(1, -1), nat.CGB_PT_ADD)
+        blk, ids = self._new(1)
+        self._ring.add_plain([a._aid], pts, ids)
+        self.counter.add_plain += 1
+        return self._emit(blk, ids[0], budget)
+
+    def mult_plain(self, a, v) -> GpuCiphertext:
+        self._check(a)
+        slots = _as_slots(v, self.params)
+        budget = self._spend(a.noise_budget, self.params.noise_costs.mult_plain)
+        keep, pts = self._plaintexts(slots.reshape(1, -1), nat.CGB_PT_MUL)
+        blk, ids = self._new(1)
+        self._ring.mult_plain([a._aid], pts, ids)
+        self.counter.mult_plain += 1
+        return self._emit(blk, ids[0], budget)
+
+    def mult_cipher(self, a, b) -> GpuCiphertext:
+        self._check(a, b)
+        budget = self._spend(min(a.noise_budget, b.noise_budget), self.params.noise_costs.mult_cipher)
+        blk, ids = self._new(1)
+        self._ring.mult_cipher([a._aid], [b._aid], ids)
+        self.counter.mult_cipher += 1
+        return self._emit(blk, ids[0], budget)
+
+    def rotate(self, a, k: int) -> GpuCiphertext:
+        """Cyclic left shift by k slots (backend.py:349-355)."""
+        self._check(a)
+        budget = self._spend(a.noise_budget, self.params.noise_costs.rotate)
+        blk, ids = self._new(1)
+        _rotate_ids(self._ring, self.params, np.array([a._aid], np.uint32), np.array([int(k)], np.int64), ids, False)
+        self.counter.rotate += 1
+        return self._emit(blk, ids[0], budget)
+
+    def with_budget(self, ct, budget: int):
+        """Test hook (backend.py:357-360): same values, explicit budget.
+
+        Raising the ledger above the ciphertext's own budget re-encrypts the
+        payload (client role, separate nonce stream, not counted) so that the
+        real noise matches the fresh ledger; lowering it is ledger-only."""
+        self._check(ct)
+        if budget > ct.noise_budget:
+            vals = self._ring.decrypt([ct._aid])
+            blk, ids = self._encrypt_slots(vals, hook=True)
+            return GpuCiphertext(blk, ids[0], budget, ct.id, self.params, self._ring)
+        return GpuCiphertext(ct._block, ct._aid, budget, ct.id, self.params, self._ring)
+
+    def load_ciphertext(self, values, budget: int) -> GpuCiphertext:
+        """Rehydrate a serialized (decrypted) part; not counted (backend.py:362)."""
+        slots = _as_slots(values, self.params)
+        blk, ids = self._encrypt_slots(slots.reshape(1, -1), hook=True)
+        return self._emit(blk, ids[0], budget)
+
+    # -- diagnostics -------------------------------------------------------------------
+    def noise_budget_bits(self, ct) -> float:
+        """Real invariant noise budget (bits) of a ciphertext; client-side."""
+        return float(self._ring.noise_budget([ct._aid])[0])
+
+    # =============================================================================
+    # wave API (batched; used by the fused hot path)
+    # =============================================================================
+    @staticmethod
+    def wave_of(cts: Sequence[GpuCiphertext], ctxs=None) -> Wave:
+        cts = list(cts)
+        if ctxs is None:
+            ctxs = [None]
+            owner = np.zeros(len(cts), dtype=np.int64)
+        else:
+            ctxs, owner = _owners(ctxs)
+        aids = np.array([c._aid for c in cts], dtype=np.uint32)
+        budgets = np.array([c.noise_budget for c in cts], dtype=np.int64)
+        cids = np.array([c.id for c in cts], dtype=np.int64)
+        return Wave(ctxs, owner, aids, budgets, [c._block for c in cts], cids)
+
+    @staticmethod
+    def bind(wave: Wave, ctx) -> Wave:
+        return Wave([ctx], np.zeros(len(wave), np.int64), wave.aids, wave.budgets, wave.blocks, wave.cids)
+
+    # -- wave primitives: each charges counters/ids to the owning contexts exactly
+    # -- as the equivalent sequence of per-op calls would
+    @staticmethod
+    def _charge(wave: Wave, field_name: str, n_emit: int = 1, counts=None) -> np.ndarray:
+        """Bump the owners' counters; returns the ids the emitted items get
+        (item order within each owner, n_emit ids per item, last one kept)."""
+        counts = np.bincount(wave.owner, minlength=len(wave.ctxs)) if counts is None else counts
+        for c, k in zip(wave.ctxs, counts):
+            if k:
+                setattr(c.counter, field_name, getattr(c.counter, field_name) + int(k))
+        if n_emit == 0:
+            return wave.cids
+        cids = np.empty(len(wave), np.int64)
+        for o, c in enumerate(wave.ctxs):
+            sel = np.nonzero(wave.owner == o)[0]
+            if sel.size:
+                cids[sel] = c._next_id + n_emit * np.arange(sel.size) + (n_emit - 1)
+                c._next_id += n_emit * sel.size
+        return cids
+
+    @staticmethod
+    def _spend_all(budgets: np.ndarray, cost: int) -> np.ndarray:
+        left = budgets - cost
+        if left.size and left.min() < 0:
+            i = int(np.argmin(left))
+            raise NoiseBudgetExhausted(f"operation needs {cost} bits but only {int(budgets[i])} remain")
+        return left
+
+    @staticmethod
+    def _derive(wave: Wave, aids, budgets, block) -> Wave:
+        return Wave(wave.ctxs, wave.owner, aids, budgets, [block])
+
+    @staticmethod
+    def w_encrypt(ctxs, vecs) -> Wave:
+        """Encrypt rows of ``vecs`` (item i by ctxs[i]); one nonce per item in order."""
+        uniq, owner = _owners(ctxs)
+        vecs = np.ascontiguousarray(np.mod(np.asarray(vecs, dtype=np.int64), uniq[0].params.plain_modulus))
+        ring = uniq[0]._ring
+        ids = ring.alloc(len(owner))
+        blk = _Block(ring, ids)
+        for k, c in enumerate(uniq):
+            sel = np.nonzero(owner == k)[0]
+            if sel.size == 0:
+                continue
+            ring.encrypt(vecs[sel], c._enc_key, c._enc_index, ids[sel])
+            c._enc_index += sel.size
+        w = Wave(uniq, owner, ids, np.full(len(owner), uniq[0].params.initial_noise_budget, np.int64), [blk])
+        w.cids = GpuContext._charge(w, "encrypt")
+        return w
+
+    @staticmethod
+    def w_decrypt(wave: Wave) -> np.ndarray:
+        if len(wave) == 0:
+            return np.zeros((0, wave.ctxs[0].params.n_slots), np.int64)
+        if wave.budgets.min() <= 0:
+            raise DecryptionFailure("noise budget exhausted: decryption would be incorrect")
+        GpuContext._charge(wave, "decrypt", n_emit=0)
+        return wave.ctxs[0]._ring.decrypt(wave.aids)
+
+    @staticmethod
+    def w_add(wa: Wave, wb: Wave) -> Wave:
+        c0 = wa.ctxs[0]
+        b = GpuContext._spend_all(np.minimum(wa.budgets, wb.budgets), c0.params.noise_costs.add)
+        blk, ids = c0._new(len(wa))
+        c0._ring.add(wa.aids, wb.aids, ids)
+        return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "add"))
+
+    @staticmethod
+    def _plain_op(wave: Wave, vecs, kind, field_name):
+        c0 = wave.ctxs[0]
+        cost = getattr(c0.params.noise_costs, field_name)
+        b = GpuContext._spend_all(wave.budgets, cost)
+        vecs = np.mod(np.asarray(vecs, dtype=np.int64), c0.params.plain_modulus)
+        if vecs.ndim == 1:
+            vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
+        _, pts = c0._plaintexts(vecs, kind)
+        blk, ids = c0._new(len(wave))
+        fn = c0._ring.add_plain if kind == nat.CGB_PT_ADD else c0._ring.mult_plain
+        fn(wave.aids, pts, ids)
+        return Wave(wave.ctxs, wave.owner, ids, b, [blk], GpuContext._charge(wave, field_name))
+
+    @staticmethod
+    def w_add_plain(wave: Wave, vecs) -> Wave:
+        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain")
+
+    @staticmethod
+    def w_mult_plain(wave: Wave, vecs) -> Wave:
+        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_MUL, "mult_plain")
+
+    @staticmethod
+    def w_mult_cipher(wa: Wave, wb: Wave) -> Wave:
+        c0 = wa.ctxs[0]
+        b = GpuContext._spend_all(np.minimum(wa.budgets, wb.budgets), c0.params.noise_costs.mult_cipher)
+        blk, ids = c0._new(len(wa))
+        c0._ring.mult_cipher(wa.aids, wb.aids, ids)
+        return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "mult_cipher"))
+
+    @staticmethod
+    def w_rotate(wave: Wave, steps, add_input: bool = False) -> Wave:
+        """rotate(a, k) per item; with add_input, add(a, rotate(a, k)) (the
+        doubling / folding step), fused into the key-switch epilogue."""
+        c0 = wave.ctxs[0]
+        costs = c0.params.noise_costs
+        st = np.ascontiguousarray(np.broadcast_to(np.asarray(steps, dtype=np.int64), (len(wave),)))
+        rb = GpuContext._spend_all(wave.budgets, costs.rotate)
+        b = GpuContext._spend_all(np.minimum(wave.budgets, rb), costs.add) if add_input else rb
+        blk, ids = c0._new(len(wave))
+        _rotate_ids(c0._ring, c0.params, wave.aids, st, ids, add_input)
+        if add_input:
+            GpuContext._charge(wave, "rotate", n_emit=0)
+            cids = GpuContext._charge(wave, "add", n_emit=2)
+        else:
+            cids = GpuContext._charge(wave, "rotate")
+        return Wave(wave.ctxs, wave.owner, ids, b, [blk], cids)
+
+    @staticmethod
+    def w_sum(wave: Wave, groups) -> Wave:
+        """Left-fold sum of each index group (len-1 adds per group, exact mod q
+        so one batched reduction gives the sequential fold's words)."""
+        c0 = wave.ctxs[0]
+        cost = c0.params.noise_costs.add
+        groups = [np.asarray(g, dtype=np.int64) for g in groups]
+        blk, ids = c0._new(len(groups))
+        budgets = np.empty(len(groups), np.int64)
+        owner = np.empty(len(groups), np.int64)
+        cids = np.empty(len(groups), np.int64)
+        for gi, g in enumerate(groups):
+            if g.size == 0:
+                raise ParameterError("empty sum")
+            acc = int(wave.budgets[g[0]])
+            for j in g[1:]:
+                acc = min(acc, int(wave.budgets[j])) - cost
+                if acc < 0:
+                    raise NoiseBudgetExhausted(f"operation needs {cost} bits but only {acc + cost} remain")
+            budgets[gi] = acc
+            o = owner[gi] = wave.owner[g[0]]
+            c = wave.ctxs[o]
+            if g.size == 1:
+                c0._ring.copy(wave.aids[g], ids[gi:gi + 1])
+                cids[gi] = wave.cids[g[0]]
+            else:
+                c0._ring.sum(wave.aids[g], int(ids[gi]))
+                c.counter.add += int(g.size - 1)
+                c._next_id += int(g.size - 1)
+                cids[gi] = c._next_id - 1
+        return Wave(wave.ctxs, owner, ids, budgets, [blk], cids)
+
+
+class _Keep:
+    """Keeps a list of blocks alive for a handle carved from a wave."""
+
+    __slots__ = ("blocks",)
+
+    def __init__(self, blocks):
+        self.blocks = blocks
+
+
+def _owners(ctxs):
+    uniq, owner, seen = [], [], {}
+    for c in ctxs:
+        k = id(c)
+        if k not in seen:
+            seen[k] = len(uniq)
+            uniq.append(c)
+        owner.append(seen[k])
+    return uniq, np.asarray(owner, dtype=np.int64)
+
+
+Context = GpuContext
+
+
+def new_context(params, seed=0) -> GpuContext:
+    """backend.py:367-368 -- always the GPU context; fails loudly without CUDA."""
+    return GpuContext(params, seed)
+
+
+# ----------------------------------------------------------------------------
+# rotation (one-row native, two-row composed)
+# ----------------------------------------------------------------------------
+def _rotate_ids(ring, params, a: np.ndarray, steps: np.ndarray, out: np.ndarray, add_input: bool):
+    if ring.one_row:
+        ring.rotate(a, steps, out, add_input=add_input)
+        return
+    n = params.n_slots
+    h = n // 2
+    two_n = 2 * ring.N
+    cnt = a.size
+    ga = ring.alloc(cnt)
+    gb = ring.alloc(cnt)
+    try:
+        kk = np.mod(steps, n)
+        g_plain = np.empty(cnt, np.uint64)
+        g_swap = np.empty(cnt, np.uint64)
+        masks = np.zeros((cnt, n), dtype=np.int64)
+        col = np.arange(n) % h
+        for i, k in enumerate(kk):
+            kr = int(k) % h
+            e = pow(5, kr, two_n)
+            g_plain[i], g_swap[i] = e, two_n - e
+            keep = col < h - kr
+            # k < h: plain rotation where the column does not wrap, row swap where it does
+            masks[i] = keep if k < h else ~keep
+        ring.galois(a, g_plain, ga)
+        ring.galois(a, g_swap, gb)
+        cache = _pt_cache(ring)
+        kp, pm = cache.get(masks, nat.CGB_PT_MUL)
+        kq, pq = cache.get(1 - masks, nat.CGB_PT_MUL)
+        ring.mult_plain(ga, pm, ga)
+        ring.mult_plain(gb, pq, gb)
+        if add_input:
+            ring.add(ga, gb, gb)
+            ring.add(gb, a, out)
+        else:
+            ring.add(ga, gb, out)
+    finally:
+        ring.free(ga)
+        ring.free(gb)
+
+
+# ----------------------------------------------------------------------------
+# device plaintext cache (content-addressed)
+# ----------------------------------------------------------------------------
+class _PtCache:
+    """Content-hashed cache of encoded plaintexts (one-hot masks, append masks
+    and block masks recur every step).  Entries are evicted LRU."""
+
+    def __init__(self, ring, capacity: int):
+        self.ring, self.capacity = ring, capacity
+        self.map: dict = {}
+        self.lock = threading.Lock()
+        self.tick = 0
+
+    def get(self, vecs: np.ndarray, kind: int):
+        vecs = np.ascontiguousarray(np.asarray(vecs, dtype=np.int64))
+        n = vecs.shape[0]
+        keys = [(kind, hashlib.blake2b(row.tobytes(), digest_size=16).digest()) for row in vecs]
+        out = np.empty(n, dtype=np.uint32)
+        with self.lock:
+            missing = []
+            for i, k in enumerate(keys):
+                ent = self.map.get(k)
+                if ent is None:
+                    missing.append(i)
+                else:
+                    self.tick += 1
+                    ent[1] = self.tick
+                    out[i] = ent[0]
+            if missing:
+                uniq = {}
+                for i in missing:
+                    uniq.setdefault(keys[i], []).append(i)
+                self._evict(len(uniq))
+                ids = self.ring.alloc_pt(len(uniq))
+                rows = np.stack([vecs[v[0]] for v in uniq.values()])
+                self.ring.encode_pt(rows, kind, ids)
+                for pid, (k, idxs) in zip(ids, uniq.items()):
+                    self.tick += 1
+                    self.map[k] = [int(pid), self.tick]
+                    out[idxs] = pid
+        return None, out
+
+    def _evict(self, need: int):
+        free = self.ring.arena_pts - len(self.map)
+        if free >= need:
+            return
+        victims = sorted(self.map.items(), key=lambda kv: kv[1][1])[: need - free + 64]
+        # pending launches may still read these plaintexts: order after them
+        self.ring.sync()
+        self.ring.free_pt([v[1][0] for v in victims])
+        for k, _ in victims:
+            del self.map[k]
+
+
+_pt_caches: dict = {}
+
+
+def _pt_cache(ring) -> _PtCache:
+    c = _pt_caches.get(id(ring))
+    if c is None or c.ring is not ring:
+        c = _PtCache(ring, ring.arena_pts)
+        _pt_caches[id(ring)] = c
+    return c

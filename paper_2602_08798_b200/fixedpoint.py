@@ -1,0 +1,114 @@
+"""Signed fixed-point helpers the attention path calls on the client side.
+
+Out of the B200 scope proper (the MPC non-linear protocols stay host code),
+but ``attention_step`` / ``prefill_attention`` need the reference's integer
+softmax between the score and value phases, so the pieces on that path are
+restated here from /root/reference/pkg/src/cryptogen/fixedpoint.py:
+embedding and truncation (:86-106), Newton reciprocal (:131-145), softmax
+(:148-175) and the attention-weight wrappers (:204-221).  The polynomial
+constants are the reference's frozen fit (fixedpoint.py:51-53).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .backend import ParameterError
+
+# exp(r) on (-ln2, 0] as c2 r^2 + c1 r + c0 (reference fit, fixedpoint.py:51-53)
+EXP_COEFFS = (0.3558034634, 0.9634474169, 0.9982613301)
+SHIFT_CAP = 48
+CAUSAL_MASK_EXPONENT = 6
+
+
+@dataclass(frozen=True)
+class FixedPointParams:
+    f: int
+    p: int
+    reciprocal_iters: int = 4
+
+    def __post_init__(self):
+        if self.f < 1:
+            raise ParameterError("fraction bits must be positive")
+        if (1 << (2 * self.f + 6)) >= self.p:
+            raise ParameterError(f"need 2^(2f+6) < p for product headroom; f={self.f} p={self.p}")
+        if self.reciprocal_iters < 1:
+            raise ParameterError("reciprocal needs at least one iteration")
+
+    @property
+    def scale(self) -> int:
+        return 1 << self.f
+
+    def quantize(self, v: float) -> int:
+        return int(round(v * self.scale))
+
+
+def to_signed(v, p: int):
+    v = np.asarray(v, dtype=np.int64)
+    return np.where(v > p // 2, v - p, v)
+
+
+def from_signed(v, p: int):
+    return np.mod(np.asarray(v, dtype=np.int64), p)
+
+
+def fp_encode(x, fp: FixedPointParams) -> np.ndarray:
+    return np.round(np.asarray(x, dtype=np.float64) * fp.scale).astype(np.int64)
+
+
+def fp_decode(v, fp: FixedPointParams) -> np.ndarray:
+    return np.asarray(v, dtype=np.float64) / fp.scale
+
+
+def fp_truncate(v, f: int):
+    return np.asarray(v, dtype=np.int64) >> f
+
+
+def fp_reciprocal(s: int, fp: FixedPointParams, work_bits: int | None = None):
+    """Newton iteration y <- y (2 - s y) from the bit-length lower bound."""
+    if s <= 0:
+        raise ParameterError("reciprocal needs a positive input")
+    q = 2 * fp.f if work_bits is None else work_bits
+    y = 1 << max(0, fp.f + q - int(s).bit_length())
+    two = 1 << (q + 1)
+    for _ in range(fp.reciprocal_iters):
+        y = (y * (two - ((s * y) >> fp.f))) >> q
+    return y, q
+
+
+def fp_softmax(s, fp: FixedPointParams) -> np.ndarray:
+    """Integer softmax: x = s - max = -ln2 z + r, e = poly(r) >> z, normalise."""
+    f = fp.f
+    s = np.asarray(s, dtype=np.int64)
+    if s.shape[0] == 0:
+        raise ParameterError("softmax needs at least one score")
+    if s.shape[0] == 1:
+        return np.array([fp.scale], dtype=np.int64)
+    c2, c1, c0 = (fp.quantize(c) for c in EXP_COEFFS)
+    x = s - s.max()
+    z = ((-x) * fp.quantize(1.0 / math.log(2.0))) >> (2 * f)
+    r = x + z * fp.quantize(math.log(2.0))
+    poly = np.maximum(((c2 * ((r * r) >> f)) >> f) + ((c1 * r) >> f) + c0, 0)
+    e = poly >> np.minimum(z, SHIFT_CAP)
+    rec, q = fp_reciprocal(int(e.sum()), fp)
+    return (e * rec + (1 << (q - 1))) >> q
+
+
+def _scaled_scores(scores_2f, d2: int, fp: FixedPointParams) -> np.ndarray:
+    s1 = fp_truncate(np.asarray(scores_2f, dtype=np.int64), fp.f)
+    return (s1 * fp.quantize(1.0 / math.sqrt(d2))) >> fp.f
+
+
+def attention_weights(scores_2f, d2: int, fp: FixedPointParams) -> np.ndarray:
+    """scale-2f scores -> softmax(s / sqrt(d2)) at scale f (fixedpoint.py:204-209)."""
+    return fp_softmax(_scaled_scores(scores_2f, d2, fp), fp)
+
+
+def causal_attention_weights(row_2f, row_index: int, d2: int, fp: FixedPointParams) -> np.ndarray:
+    """Prefill row with the additive causal mask -2^(f+6) (fixedpoint.py:212-221)."""
+    s2 = _scaled_scores(row_2f, d2, fp)
+    s2[row_index + 1:] -= 1 << (fp.f + CAUSAL_MASK_EXPONENT)
+    return fp_softmax(s2, fp)

@@ -1,0 +1,135 @@
+"""HE <-> additive-share conversion on the hot path (server-side masking).
+
+Restates the conversion half of /root/reference/pkg/src/cryptogen/
+nonlinear.py: the channel's byte/round ledger and mask RNG (:63-93),
+``share_vector`` (:101-106), ``he_to_shares`` (:112-125), ``shares_to_he``
+(:128-137) and ``truncate`` (:140-144).  The MPC protocols themselves
+(GELU / softmax / layernorm over shares) are host code outside this tier.
+
+Parity-critical: masks are drawn from ``MpcChannel.rng`` with exactly the
+reference's lengths and order (he_to_shares always draws n words, even for
+shorter shares).  The batched forms below take one channel per item and
+draw item by item, which is the order the per-op code would draw in.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from .backend import ParameterError
+from .fixedpoint import FixedPointParams, fp_truncate, from_signed, to_signed
+
+__all__ = ["MpcChannel", "SharePair", "he_to_shares", "he_to_shares_wave", "reconstruct", "share_vector",
+           "shares_to_he", "shares_to_he_wave", "truncate"]
+
+
+@dataclass
+class SharePair:
+    client: np.ndarray
+    server: np.ndarray
+    p: int
+    length: int
+
+    def __post_init__(self):
+        if self.client.shape != (self.length,) or self.server.shape != (self.length,):
+            raise ParameterError("share arrays must match the declared length")
+
+
+class MpcChannel:
+    """Bytes/rounds tally plus the mask RNG of one serial conversation."""
+
+    def __init__(self, p: int, seed=0):
+        self.p = p
+        self.word_bits = p.bit_length()
+        self.bytes_sent = 0
+        self.rounds = 0
+        ss = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+        self.rng = np.random.default_rng(ss)
+        self.transcript: list = []
+
+    def vector_bytes(self, elements: int) -> int:
+        return elements * self.word_bits // 8
+
+    def transfer(self, op: str, elements: int, trips: int = 1) -> None:
+        nbytes = trips * self.vector_bytes(elements)
+        self.bytes_sent += nbytes
+        self.rounds += trips
+        self.transcript.append({"op": op, "elements": elements, "trips": trips, "bytes": nbytes})
+
+    def sample_mask(self, length: int) -> np.ndarray:
+        return self.rng.integers(0, self.p, size=length, dtype=np.int64)
+
+    def transcript_json(self) -> str:
+        return json.dumps({"bytes_sent": self.bytes_sent, "rounds": self.rounds, "log": self.transcript}, indent=2)
+
+
+def reconstruct(s: SharePair) -> np.ndarray:
+    return to_signed((s.client + s.server) % s.p, s.p)
+
+
+def share_vector(values, ch: MpcChannel) -> SharePair:
+    secret = from_signed(values, ch.p)
+    r = ch.sample_mask(secret.shape[0])
+    return SharePair((secret - r) % ch.p, r, ch.p, secret.shape[0])
+
+
+def truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel) -> SharePair:
+    """Floor-divide the reconstruction by 2^f and re-share (nonlinear.py:140-144)."""
+    out = fp_truncate(reconstruct(s), fp.f)
+    ch.transfer("truncate", s.length, trips=3)
+    return share_vector(out, ch)
+
+
+# ----------------------------------------------------------------------------
+# batched conversions: one wave of ciphertexts, one channel per item
+# ----------------------------------------------------------------------------
+def he_to_shares_wave(wave, chans, lengths) -> list:
+    """Server masks each ciphertext with a fresh r (n words from its channel),
+    the client decrypts; returns one SharePair per item."""
+    C = type(wave.ctxs[0])
+    params = wave.ctxs[0].params
+    n, p = params.n_slots, params.plain_modulus
+    lengths = list(lengths)
+    for L in lengths:
+        if not 0 < L <= n:
+            raise ParameterError(f"share length {L} out of range")
+    r = np.stack([ch.sample_mask(n) for ch in chans]) if len(chans) else np.zeros((0, n), np.int64)
+    masked = C.w_add_plain(wave, (p - r) % p)
+    client = C.w_decrypt(masked)
+    out = []
+    for i, ch in enumerate(chans):
+        ch.transfer("he_to_shares", n)
+        L = lengths[i]
+        out.append(SharePair(client[i, :L].copy(), r[i, :L].copy(), p, L))
+    return out
+
+
+def shares_to_he_wave(shares, ctxs, chans, record: bool = True):
+    """Client encrypts its share, server adds its own; returns a wave.
+    ``record=False`` leaves the transcript entries to the caller."""
+    c0 = ctxs[0]
+    C = type(c0)
+    n = c0.params.n_slots
+    client = np.stack([c.plain_from_dense(s.client) for c, s in zip(ctxs, shares)])
+    server = np.stack([c.plain_from_dense(s.server) for c, s in zip(ctxs, shares)])
+    enc = C.w_encrypt(ctxs, client)
+    out = C.w_add_plain(enc, server)
+    if record:
+        for ch in chans:
+            ch.transfer("shares_to_he", n)
+    return out
+
+
+def he_to_shares(ct, ctx, ch: MpcChannel, length: int | None = None) -> SharePair:
+    """nonlinear.py:112-125 (one item of the batched form)."""
+    n = ctx.params.n_slots
+    C = type(ctx)
+    return he_to_shares_wave(C.wave_of([ct], [ctx]), [ch], [n if length is None else length])[0]
+
+
+def shares_to_he(s: SharePair, ctx, ch: MpcChannel):
+    """nonlinear.py:128-137 (one item of the batched form)."""
+    return shares_to_he_wave([s], [ctx], [ch]).handles()[0]

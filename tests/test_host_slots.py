@@ -1,0 +1,44 @@
+"""Host code of the hot path over the slot oracle vs golden vectors recorded
+from the reference (tests/golden/make_golden.py).  CPU only."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+import harness  # noqa: E402
+from hostapi import compare, repo_api  # noqa: E402
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def api():
+    return repo_api()
+
+
+def slot_ctx(params, seed):
+    from oracle.slots import SlotContext
+
+    return SlotContext(params, seed)
+
+
+@pytest.mark.parametrize("name", list(harness.SMALL))
+def test_small_scenarios_match_reference(api, name):
+    fn, kw = harness.SMALL[name]
+    rec, _ = fn(api, slot_ctx, **kw)
+    compare(rec, np.load(GOLD / f"{name}.npz"))
+
+
+@pytest.mark.parametrize("name", ["full_attn_m128", "full_attn_m96_t32", "full_attn_m0_t130"])
+def test_full_size_decode_matches_reference(api, name):
+    fn, kw = harness.FULL[name]
+    rec, _ = fn(api, slot_ctx, **kw)
+    compare(rec, np.load(GOLD / f"{name}.npz"))
+
+
+def test_full_size_prefill_matches_reference(api):
+    fn, kw = harness.FULL["full_prefill_m128"]
+    rec, _ = fn(api, slot_ctx, **kw)
+    compare(rec, np.load(GOLD / "full_prefill_m128.npz"))
