@@ -1,0 +1,349 @@
+"""Encrypted-KV attention decode on one B200: ms/token (BASELINE.json metric).
+
+Workload ("decode_attention_12h_L{L}"): one decode token of a GPT-2-small
+attention layer under RNS-BFV -- 12 heads, d_head = 64, n = 8192 slots,
+p = 536903681 (the reference's default parameter set), a cached prefill of
+L tokens per head (outer-packed K/V), then per step:
+lazy refresh check, append of the new K/V token into the compacted
+generated segment, and the heterogeneous attention step of all 12 heads
+(arcc.attention_step_heads).  Synthetic fixed-point inputs, uniform in
+[-1, 1] at f = 8, seeded.
+
+value: device-resident step (encrypted q/k/v tokens already in HBM).
+e2e:   same step through the public API from HOST plaintext tokens: client
+       encryption of q/k/v (H2D) ... decryption of the 12 head outputs (D2H).
+Both include the MPC client round trips of the attention step itself
+(masked decrypts / re-encryptions), which are part of the reference path.
+
+--impl reference: the reference's CPU path (sequential per-op restatement
+of the emulation, oracle/reference_path.py over oracle/slots.py) on the
+same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+P = 536903681
+N_SLOTS = 8192
+D2 = 64
+HEADS = 12
+F = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=128, help="cached prefill length per head")
+    ap.add_argument("--heads", type=int, default=HEADS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def metric_name(L):
+    return f"HE attention decode ms/token at L={L} (12 heads, d_head=64, n=8192)"
+
+
+def workload(args):
+    return {"workload": f"decode_attention_{args.heads}h_L{args.L}", "heads": args.heads, "d_head": D2,
+            "n_slots": N_SLOTS, "plain_modulus": P, "cached_len": args.L, "steps_appended": 1,
+            "ring": "RNS-BFV N=16384, Q=4x60b, P=61b, dnum=4", "l2": "working set >1.5 GB per step (> 126 MB L2)"}
+
+
+# ----------------------------------------------------------------------------
+# inputs (shared by all arms)
+# ----------------------------------------------------------------------------
+def fp_tokens(rng, rows, d):
+    return np.mod(np.round(rng.uniform(-1.0, 1.0, (rows, d)) * (1 << F)).astype(np.int64), P)
+
+
+def build_state(api, new_ctx, L, heads, seed=0):
+    params = api.BackendParams()
+    root = new_ctx(params, seed)
+    fp = api.FixedPointParams(F, P)
+    rng = np.random.default_rng(seed)
+    ctxs = [root.fork() for _ in range(heads)]
+    caches = []
+    for c in ctxs:
+        K = api.encode(fp_tokens(rng, L, D2), api.EncodingKind.OUTER, c)
+        V = api.encode(fp_tokens(rng, L, D2), api.EncodingKind.OUTER, c)
+        caches.append(api.init_cache(K, V, c))
+    chans = [api.MpcChannel(P, seed=1000 + h) for h in range(heads)]
+    return root, fp, ctxs, caches, chans, rng
+
+
+def step_tokens(rng, heads):
+    """Host plaintext q, k, v (slot vectors) of one step, per head."""
+    return [np.concatenate([fp_tokens(rng, 1, D2)[0], np.zeros(N_SLOTS - D2, np.int64)]) for _ in range(3 * heads)]
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_08798_b200 as api
+    from paper_2602_08798_b200 import _native
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    _native.build()
+    from paper_2602_08798_b200.backend import GpuContext
+
+    root, fp, ctxs, caches, chans, rng = build_state(api, GpuContext, args.L, args.heads, seed=rank)
+    ring = root.ring
+    stream = torch.cuda.current_stream()
+    ring.set_stream(stream.cuda_stream)
+    C = GpuContext
+    W = args.warmup + args.steps
+    host_tokens = [step_tokens(rng, args.heads) for _ in range(W)]
+    # device-resident inputs for the `value` leg
+    dev_tokens = []
+    for toks in host_tokens:
+        w = C.w_encrypt([c for c in ctxs for _ in range(3)], np.stack(toks)).handles()
+        dev_tokens.append(w)
+
+    def one_step(tok_handles):
+        qs, ks, vs = tok_handles[0::3], tok_handles[1::3], tok_handles[2::3]
+        cs = api.maybe_refresh_heads(caches, ctxs, chans)
+        cs = api.append_token_heads(cs, ks, vs, ctxs)
+        return api.attention_step_heads(qs, cs, fp, ctxs, chans)
+
+    def one_step_e2e(toks):
+        wave = C.w_encrypt([c for c in ctxs for _ in range(3)], np.stack(toks))
+        outs = one_step(wave.handles())
+        return C.w_decrypt(C.wave_of(outs, ctxs))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        one_step(dev_tokens[i])
+    one_step_e2e(host_tokens[0])
+    barrier()
+    launches0 = ring.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            one_step(dev_tokens[args.warmup + i])
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ring.launches() - launches0
+    # e2e leg: host plaintext in, host plaintext out
+    h0, d0 = ring.h2d_bytes, ring.d2h_bytes
+    barrier()
+    ev0.record(stream)
+    for i in range(args.steps):
+        one_step_e2e(host_tokens[args.warmup + i])
+    ev1.record(stream)
+    barrier()
+    ms_e2e = ev0.elapsed_time(ev1)
+    h2d = (ring.h2d_bytes - h0) / args.steps
+    d2h = (ring.d2h_bytes - d0) / args.steps
+    # per-kernel live timing pass (CUDA events around every launch)
+    ring.timing(True)
+    one_step(dev_tokens[args.warmup])
+    rep = ring.timing_report()
+    ring.timing(False)
+    peak_mm = ring.modmul_peak()
+
+    def maxall(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms, ms_e2e = maxall(ms), maxall(ms_e2e)
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    ms_step = ms / args.steps
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    step_kernel_ms = sum(v[1] for v in rep.values())
+    top = max(rep.items(), key=lambda kv: kv[1][1])
+    name, (nl, kms, kbytes) = top
+    achieved = kbytes / (kms * 1e-3) / 1e9
+    # NTT integer-pipe utilisation: N/2 log N Shoup modmuls per limb-poly transform
+    ntt = [v for k, v in rep.items() if k.startswith("ntt")]
+    ntt_ms = sum(v[1] for v in ntt)
+    ntt_polys = sum(v[2] for v in ntt) / (16.0 * 2 * N_SLOTS)
+    ntt_mm = ntt_polys * (N_SLOTS) * 14  # (N/2) log2 N with N = 2 n_slots
+    line = {
+        "metric": metric_name(args.L), "value": ms_step / world, "unit": "ms/token", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform [-1,1], f=8)",
+        "config": dict(workload(args), parallelism=f"replicas{world}"),
+        "e2e": {"value": ms_e2e / args.steps / world, "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "launches_per_step": nl,
+                     "share_of_step": kms / step_kernel_ms if step_kernel_ms else None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "int_pipe": {"kernel": "ntt_fwd+ntt_inv", "modmuls_per_s": ntt_mm / (ntt_ms * 1e-3) if ntt_ms else None,
+                     "peak_modmuls_per_s": peak_mm,
+                     "frac": (ntt_mm / (ntt_ms * 1e-3)) / peak_mm if ntt_ms else None,
+                     "share_of_step": ntt_ms / step_kernel_ms if step_kernel_ms else None},
+        "kernels": {k: {"launches": v[0], "ms": round(v[1], 4), "GBps": round(v[2] / (v[1] * 1e-3) / 1e9, 1)
+                        if v[1] else None} for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, samples=1)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the reference's CPU path (sequential per-op, slot emulation)
+# ----------------------------------------------------------------------------
+def reference_step_fn(args):
+    from oracle import reference_path as ref
+    from oracle.slots import SlotContext
+    import paper_2602_08798_b200 as api
+
+    root, fp, ctxs, caches, chans, rng = build_state(api, SlotContext, args.L, args.heads, seed=0)
+
+    def step():
+        toks = step_tokens(rng, args.heads)
+        outs = []
+        for h in range(args.heads):
+            c = ctxs[h]
+            q, k, v = (c.encrypt(toks[3 * h + j]) for j in range(3))
+            cache = ref.maybe_refresh(caches[h], c, chans[h])
+            cache = ref.append_token(cache, k, v, c)
+            outs.append(c.decrypt(ref.attention_step(q, cache, fp, c, chans[h])))
+        return outs
+
+    return step
+
+
+def cpu_baseline(args, samples=1):
+    step = reference_step_fn(args)
+    step()  # warm
+    ts = []
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    return {"value": min(ts) * 1e3, "unit": "ms/token", "cores": 1, "kind": "port",
+            "sample": f"{args.heads}-head decode step at L={args.L}, sequential per-op slot emulation "
+                      f"(oracle/reference_path.py + oracle/slots.py), best of {samples}",
+            "host": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    step = reference_step_fn(args)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    line = {"impl": "reference", "metric": metric_name(args.L), "value": ms, "unit": "ms/token", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64 (Z_p slot emulation)", "data": "synthetic",
+            "config": dict(workload(args), parallelism="cpu"),
+            "cpu_baseline": {"value": ms, "unit": "ms/token", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} decode steps x {args.heads} heads at L={args.L}",
+                             "host": _cpu_model()},
+            "e2e": {"value": ms, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -70,6 +70,14 @@ int cgb_set_stream(cgb_ring *ring, void *cuda_stream);
 int cgb_sync(cgb_ring *ring);
 /* number of device kernel launches issued by this ring so far */
 uint64_t cgb_launch_count(const cgb_ring *ring);
+/* per-launch CUDA-event timing: enable (clears earlier records) / disable */
+int cgb_timing_enable(cgb_ring *ring, int on);
+/* aggregate of the recorded launches, one line per kernel:
+ * "<name> <launches> <total ms> <algorithmic bytes>\n" */
+int cgb_timing_report(cgb_ring *ring, char *buf, size_t cap);
+/* measured integer-pipe peak of the NTT's 64-bit Shoup modular multiply
+ * (register-resident independent chains over the whole GPU), per second */
+int cgb_modmul_peak(cgb_ring *ring, double *modmuls_per_s);
 
 /* ---- ciphertext / plaintext storage -------------------------------------
  * Ciphertext handles replace SlotCiphertext (backend.py:216-230); the

@@ -68,6 +68,9 @@ SIGNATURES = {
     "cgb_set_stream": (ctypes.c_int, [_vp, _vp]),
     "cgb_sync": (ctypes.c_int, [_vp]),
     "cgb_launch_count": (ctypes.c_uint64, [_vp]),
+    "cgb_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "cgb_timing_report": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_size_t]),
+    "cgb_modmul_peak": (ctypes.c_int, [_vp, _dblp]),
     "cgb_ct_alloc": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_ct_free": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_ct_copy": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p]),

@@ -189,6 +189,16 @@ struct cgb_ring {
   size_t pin_cap = 0, pin_off = 0;
   u64 launches = 0;
   std::mutex mu;
+  // per-launch timing (cgb_timing_enable): events around every kernel
+  bool timing = false;
+  struct Rec {
+    const char *name;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t pending = nullptr;
 
   int ntt_E() const { return std::min(16, N); }
   int ntt_threads() const { return N / ntt_E(); }
@@ -240,10 +250,61 @@ struct Scratch {
   }
 };
 
-static void check_launch(cgb_ring *r) {
+static cudaEvent_t take_event(cgb_ring *r) {
+  if (!r->event_pool.empty()) {
+    cudaEvent_t e = r->event_pool.back();
+    r->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+static void launch_begin(cgb_ring *r) {
+  if (!r->timing) return;
+  r->pending = take_event(r);
+  CK(cudaEventRecord(r->pending, r->stream));
+}
+static void launch_end(cgb_ring *r, const char *name, double bytes) {
   r->launches++;
   CK(cudaGetLastError());
+  if (!r->timing) return;
+  cudaEvent_t b = take_event(r);
+  CK(cudaEventRecord(b, r->stream));
+  r->recs.push_back({name, bytes, r->pending, b});
 }
+// algorithmic bytes per launch (read + write once; shared key / table reads once)
+#define BYTES_add (24.0 * count * r->ct_words)
+#define BYTES_add_plain (8.0 * count * (2.0 * r->ct_words + (double)r->L * r->N))
+#define BYTES_mult_plain BYTES_add_plain
+#define BYTES_copy (16.0 * count * r->ct_words)
+#define BYTES_sum (8.0 * (count + 1.0) * r->ct_words)
+#define BYTES_automorph (16.0 * n * ctw)
+#define BYTES_gather (16.0 * n * (double)L * N)
+#define BYTES_modup (8.0 * (double)count * ((double)L * N + (double)L * LP * N))
+#define BYTES_ks_inner (8.0 * (double)count * LP * N * (L + 2.0) + 16.0 * L * (double)LP * N)
+#define BYTES_moddown_lift (8.0 * (double)count * (2.0 * N + 2.0 * L * N))
+#define BYTES_moddown_combine (8.0 * (double)count * 2.0 * L * N * (3 + (add0 ? 1 : 0) + (d_add1 ? 1 : 0)))
+#define BYTES_lift_QB (8.0 * n * 4.0 * (L + nB) * (double)N)
+#define BYTES_tensor (8.0 * n * 7.0 * nt * (double)N)
+#define BYTES_scale_round (8.0 * n * 3.0 * (nt + L) * (double)N)
+#define BYTES_scatter_slots (16.0 * count * r->n_slots)
+#define BYTES_gather_slots (16.0 * count * r->n_slots)
+#define BYTES_pt_lift (8.0 * count * ((double)words + r->N))
+#define BYTES_enc_c0 (8.0 * count * ((double)words + 2.0 * r->N))
+#define BYTES_enc_sub_as (24.0 * count * (double)words)
+#define BYTES_dec_inner (24.0 * count * (double)words)
+#define BYTES_dec_scale (8.0 * count * (r->L + 1.0) * r->N)
+#define BYTES_sample_uniform (8.0 * n * nl * (double)r->N)
+#define BYTES_sample_cbd (8.0 * n * (double)r->N)
+#define BYTES_ksk_b (0.0)
+#define BYTES_ksk_fin (0.0)
+#define LAUNCH(name, bytes, ...)          \
+  do {                                    \
+    launch_begin(r);                      \
+    __VA_ARGS__;                          \
+    launch_end(r, name, (double)(bytes)); \
+  } while (0)
 
 // ============================================================================
 // kernels
@@ -258,11 +319,12 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   int E = r->ntt_E(), T = r->ntt_threads();
   size_t smem = r->ntt_smem();
   dim3 grid((unsigned)(count * job.nsub));
-#define LNTT(EE)                                                                                \
-  do {                                                                                          \
-    if (fwd) k_ntt<EE, true><<<grid, T, smem, r->stream>>>(job);                                \
-    else k_ntt<EE, false><<<grid, T, smem, r->stream>>>(job);                                   \
+#define LNTT(EE)                                                     \
+  do {                                                               \
+    if (fwd) k_ntt<EE, true><<<grid, T, smem, r->stream>>>(job);     \
+    else k_ntt<EE, false><<<grid, T, smem, r->stream>>>(job);        \
   } while (0)
+  launch_begin(r);
   switch (E) {
     case 16: LNTT(16); break;
     case 8: LNTT(8); break;
@@ -270,7 +332,7 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
     default: LNTT(2); break;
   }
 #undef LNTT
-  check_launch(r);
+  launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 16.0 * (double)count * job.nsub * r->N);
 }
 // NTT over `nlimb` limbs of `npoly` polys per item, limb l of poly p at unit p*nlimb+l
 static void ntt_items(cgb_ring *r, bool fwd, u64 *base, u64 *const *items, u64 item_stride, int count, int npoly,
@@ -684,6 +746,22 @@ __global__ void k_square(u64 *dst, const u64 *s, const ModTab *mods, int nl, con
   dst[i] = mul_mod(s[i], s[i], M);
 }
 
+// integer-pipe peak: independent chains of the NTT's 64-bit Shoup modmul,
+// register resident (8 chains per thread, no memory traffic in the loop)
+__global__ void k_modmul_peak(u64 *sink, u64 q, u64 w, u64 wsh, int iters) {
+  u64 x[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = (threadIdx.x * 8 + k + 1) % q;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = mul_shoup(x[k], w, wsh, q);
+  }
+  u64 acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) acc ^= x[k];
+  if (acc == 0x1234567) sink[0] = acc;
+}
+
 // ============================================================================
 // host orchestration
 // ============================================================================
@@ -716,9 +794,8 @@ static int *q_mod_idx(cgb_ring *r, std::vector<int> &v) {
 static void encode_slots(cgb_ring *r, Scratch &S, const u64 *slots_host, int count, u64 *m) {
   u64 *d_slots = S.up(slots_host, (size_t)count * r->n_slots);
   CK(cudaMemsetAsync(m, 0, sizeof(u64) * (size_t)count * r->N, r->stream));
-  k_scatter_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(m, d_slots, r->d_slot_idx,
-                                                                                r->n_slots, r->t, r->logN);
-  check_launch(r);
+  LAUNCH("scatter_slots", BYTES_scatter_slots, k_scatter_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(m, d_slots, r->d_slot_idx,
+                                                                                r->n_slots, r->t, r->logN));
   int mi = r->iT;
   ntt_items(r, false, m, nullptr, r->N, count, 1, 1, &mi);
 }
@@ -739,8 +816,7 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
   // ModUp
   u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
   u64 wD = (u64)L * LP * N;
-  k_modup<<<dim3(GRID1(wD, TPB).x, count), TPB, 0, r->stream>>>(D, xc, x, r->d_mods, L, logN);
-  check_launch(r);
+  LAUNCH("modup", BYTES_modup, k_modup<<<dim3(GRID1(wD, TPB).x, count), TPB, 0, r->stream>>>(D, xc, x, r->d_mods, L, logN));
   {
     NttJob job{};
     job.base = D;
@@ -758,8 +834,7 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
   }
   // inner product with the evaluation key
   u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
-  k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, d_keys, r->d_mods, L, logN);
-  check_launch(r);
+  LAUNCH("ks_inner", BYTES_ks_inner, k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, d_keys, r->d_mods, L, logN));
   // ModDown
   {
     int mP = r->iP;
@@ -774,12 +849,10 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
     launch_ntt(r, false, job, count);
   }
   u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
-  k_moddown_lift<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(W, acc, r->d_mods, L, r->iP, logN);
-  check_launch(r);
+  LAUNCH("moddown_lift", BYTES_moddown_lift, k_moddown_lift<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(W, acc, r->d_mods, L, r->iP, logN));
   ntt_items(r, true, W, nullptr, 2ull * L * N, count, 2, L, qm.data());
-  k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
-      d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN);
-  check_launch(r);
+  LAUNCH("moddown_combine", BYTES_moddown_combine, k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
+      d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
 }
 
 static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
@@ -800,13 +873,14 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
       Scratch S(r);
       std::vector<u64 *> src = ct_ptrs(r, 1, &a[i]), dst = ct_ptrs(r, 1, &out[i]);
       u64 **d_src = S.up(src.data(), 1), **d_dst = S.up(dst.data(), 1);
+      launch_begin(r);
       if (add_input) {
         k_add<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
                                                                  (const u64 *const *)d_src, r->d_mods, L, r->logN, ctw);
       } else {
         k_copy<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
       }
-      check_launch(r);
+      launch_end(r, add_input ? "add" : "copy", (add_input ? 24.0 : 16.0) * ctw);
     } else {
       idx.push_back(i);
     }
@@ -829,8 +903,7 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
     u64 **d_src = S.up(src.data(), n), **d_dst = S.up(dst.data(), n), **d_keys = S.up(keys.data(), n);
     u64 *d_g = S.up(g.data(), n);
     u64 *A = S.alloc<u64>((size_t)n * ctw);
-    k_automorph<<<dim3(GRID1(ctw, TPB).x, n), TPB, 0, r->stream>>>(A, (const u64 *const *)d_src, d_g, L, r->logN);
-    check_launch(r);
+    LAUNCH("automorph", BYTES_automorph, k_automorph<<<dim3(GRID1(ctw, TPB).x, n), TPB, 0, r->stream>>>(A, (const u64 *const *)d_src, d_g, L, r->logN));
     // c1' contiguous for the key switch
     u64 *x = S.alloc<u64>((size_t)n * L * N);
     CK(cudaMemcpy2DAsync(x, sizeof(u64) * L * N, A + (size_t)L * N, sizeof(u64) * ctw, sizeof(u64) * L * N, n,
@@ -846,16 +919,14 @@ static void sample_cbd(cgb_ring *r, Scratch &S, i64 *e, const ChaKey &key, const
   int n = (int)nonces.size();
   u64 *d_n = S.up(nonces.data(), n);
   u64 nblk = ((u64)r->N + 7) / 8;
-  k_sample_cbd<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(e, key, d_n, r->logN);
-  check_launch(r);
+  LAUNCH("sample_cbd", BYTES_sample_cbd, k_sample_cbd<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(e, key, d_n, r->logN));
 }
 static void sample_uniform(cgb_ring *r, Scratch &S, u64 *const *d_dst, int n, const ChaKey &key,
                            const std::vector<u64> &nonces, int nl, const int *mod_idx_host) {
   u64 *d_n = S.up(nonces.data(), n);
   int *d_mi = S.up(mod_idx_host, nl);
   u64 nblk = ((u64)nl * r->N + 3) / 4;
-  k_sample_uniform<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(d_dst, key, d_n, nl, d_mi, r->d_mods, r->logN);
-  check_launch(r);
+  LAUNCH("sample_uniform", BYTES_sample_uniform, k_sample_uniform<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(d_dst, key, d_n, nl, d_mi, r->d_mods, r->logN));
 }
 
 static u64 *get_key(cgb_ring *r, u64 g) {
@@ -872,12 +943,13 @@ static u64 *get_key(cgb_ring *r, u64 g) {
   int *d_mi = S.up(mi.data(), LP);
   // source key s' over Q u P
   u64 *sp = S.alloc<u64>(LPN);
+  launch_begin(r);
   if (g == 0) {
     k_square<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(sp, r->d_s, r->d_mods, LP, d_mi, r->logN);
   } else {
     k_automorph_flat<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(sp, r->d_s, g, LP, r->logN);
   }
-  check_launch(r);
+  launch_end(r, "keygen", 16.0 * LPN);
   i64 *e = S.alloc<i64>((size_t)N);
   for (int j = 0; j < L; j++) {
     u64 sub = (g << 8) | (u64)j;
@@ -885,11 +957,9 @@ static u64 *get_key(cgb_ring *r, u64 g) {
     u64 **d_a = S.up(adst.data(), 1);
     sample_uniform(r, S, d_a, 1, r->keyseed, {nonce_of(DOM_KSK_A, sub)}, LP, mi.data());
     sample_cbd(r, S, e, r->keyseed, {nonce_of(DOM_KSK_E, sub)});
-    k_ksk_b<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, e, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN);
-    check_launch(r);
+    LAUNCH("ksk_b", BYTES_ksk_b, k_ksk_b<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, e, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
     ntt_items(r, true, key + ((u64)j * 2 + 0) * LPN, nullptr, 0, 1, 1, LP, mi.data());
-    k_ksk_fin<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN);
-    check_launch(r);
+    LAUNCH("ksk_fin", BYTES_ksk_fin, k_ksk_fin<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
   }
   r->keys[g] = key;
   return key;
@@ -1152,6 +1222,75 @@ int cgb_ring_moduli(const cgb_ring *r, uint64_t *out, int cap) {
 size_t cgb_ct_words(const cgb_ring *r) { return r->ct_words; }
 uint64_t cgb_launch_count(const cgb_ring *r) { return r->launches; }
 
+int cgb_modmul_peak(cgb_ring *r, double *modmuls_per_s) {
+  API_BEGIN
+  u64 q = r->mods[0], w = r->mods[0] / 3 + 7, wsh = h_shoup(w, q);
+  u64 *sink;
+  CK(cudaMallocAsync((void **)&sink, 8, r->stream));
+  int dev, sms;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  k_modmul_peak<<<blocks, threads, 0, r->stream>>>(sink, q, w, wsh, 64);  // warm-up
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, r->stream));
+  k_modmul_peak<<<blocks, threads, 0, r->stream>>>(sink, q, w, wsh, iters);
+  CK(cudaEventRecord(b, r->stream));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  CK(cudaFreeAsync(sink, r->stream));
+  *modmuls_per_s = (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+  API_END
+}
+
+int cgb_timing_enable(cgb_ring *r, int on) {
+  API_BEGIN
+  CK(cudaStreamSynchronize(r->stream));
+  for (auto &rc : r->recs) {
+    r->event_pool.push_back(rc.a);
+    r->event_pool.push_back(rc.b);
+  }
+  r->recs.clear();
+  r->timing = on != 0;
+  API_END
+}
+
+int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
+  API_BEGIN
+  CK(cudaStreamSynchronize(r->stream));
+  struct Agg {
+    long n = 0;
+    double ms = 0, bytes = 0;
+  };
+  std::vector<std::pair<std::string, Agg>> agg;
+  for (auto &rc : r->recs) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, rc.a, rc.b));
+    auto it = std::find_if(agg.begin(), agg.end(), [&](auto &kv) { return kv.first == rc.name; });
+    if (it == agg.end()) {
+      agg.push_back({rc.name, Agg{}});
+      it = agg.end() - 1;
+    }
+    it->second.n++;
+    it->second.ms += ms;
+    it->second.bytes += rc.bytes;
+  }
+  std::string out;
+  for (auto &kv : agg) {
+    char line[256];
+    snprintf(line, sizeof line, "%s %ld %.6f %.0f\n", kv.first.c_str(), kv.second.n, kv.second.ms, kv.second.bytes);
+    out += line;
+  }
+  if (out.size() + 1 > cap) FAIL(CGB_ERR_PARAM, "timing report needs %zu bytes", out.size() + 1);
+  memcpy(buf, out.c_str(), out.size() + 1);
+  API_END
+}
+
 int cgb_set_stream(cgb_ring *r, void *s) {
   API_BEGIN
   CK(cudaStreamSynchronize(r->stream));
@@ -1218,8 +1357,7 @@ int cgb_ct_copy(cgb_ring *r, int count, const uint32_t *src, const uint32_t *dst
   Scratch S(r);
   auto ps = ct_ptrs(r, count, src), pd = ct_ptrs(r, count, dst);
   u64 **ds = S.up(ps.data(), count), **dd = S.up(pd.data(), count);
-  k_copy<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dd, (const u64 *const *)ds, r->ct_words);
-  check_launch(r);
+  LAUNCH("copy", BYTES_copy, k_copy<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dd, (const u64 *const *)ds, r->ct_words));
   API_END
 }
 int cgb_ct_store(cgb_ring *r, int count, const uint32_t *ids, uint64_t *host) {
@@ -1253,8 +1391,7 @@ int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const
   auto pp = pt_ptrs(r, count, pt_ids);
   u64 **dp = S.up(pp.data(), count);
   u64 words = (u64)r->L * r->N;
-  k_pt_lift<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dp, m, r->d_mods, r->d_c, r->L, r->logN, kind);
-  check_launch(r);
+  LAUNCH("pt_lift", BYTES_pt_lift, k_pt_lift<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dp, m, r->d_mods, r->d_c, r->L, r->logN, kind));
   std::vector<int> qm;
   ntt_items(r, true, nullptr, dp, 0, count, 1, r->L, q_mod_idx(r, qm));
   API_END
@@ -1285,11 +1422,9 @@ int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t en
   i64 *e = S.alloc<i64>((size_t)count * r->N);
   sample_cbd(r, S, e, key, ne);
   u64 words = (u64)r->L * r->N;
-  k_enc_c0<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, m, e, r->d_mods, r->d_c, r->L, r->logN);
-  check_launch(r);
+  LAUNCH("enc_c0", BYTES_enc_c0, k_enc_c0<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, m, e, r->d_mods, r->d_c, r->L, r->logN));
   ntt_items(r, true, nullptr, dc, 0, count, 1, r->L, qm.data());
-  k_enc_sub_as<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, r->d_s, r->d_mods, r->L, r->logN);
-  check_launch(r);
+  LAUNCH("enc_sub_as", BYTES_enc_sub_as, k_enc_sub_as<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, r->d_s, r->d_mods, r->L, r->logN));
   API_END
 }
 
@@ -1301,20 +1436,17 @@ int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out
   u64 **dc = S.up(pc.data(), count);
   u64 words = (u64)r->L * r->N;
   u64 *X = S.alloc<u64>((size_t)count * words);
-  k_dec_inner<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
-                                                                       r->d_c, r->L, r->logN, 0);
-  check_launch(r);
+  LAUNCH("dec_inner", BYTES_dec_inner, k_dec_inner<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
+                                                                       r->d_c, r->L, r->logN, 0));
   std::vector<int> qm;
   ntt_items(r, false, X, nullptr, words, count, 1, r->L, q_mod_idx(r, qm));
   u64 *m = S.alloc<u64>((size_t)count * r->N);
-  k_dec_scale<<<dim3(GRID1(r->N, TPB).x, count), TPB, 0, r->stream>>>(m, X, r->d_c, r->L, r->logN);
-  check_launch(r);
+  LAUNCH("dec_scale", BYTES_dec_scale, k_dec_scale<<<dim3(GRID1(r->N, TPB).x, count), TPB, 0, r->stream>>>(m, X, r->d_c, r->L, r->logN));
   int mi = r->iT;
   ntt_items(r, true, m, nullptr, r->N, count, 1, 1, &mi);
   u64 *so = S.alloc<u64>((size_t)count * r->n_slots);
-  k_gather_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(so, m, r->d_slot_idx, r->n_slots,
-                                                                               r->logN);
-  check_launch(r);
+  LAUNCH("gather_slots", BYTES_gather_slots, k_gather_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(so, m, r->d_slot_idx, r->n_slots,
+                                                                               r->logN));
   CK(cudaMemcpyAsync(slots_out, so, sizeof(u64) * (size_t)count * r->n_slots, cudaMemcpyDeviceToHost, r->stream));
   CK(cudaStreamSynchronize(r->stream));
   API_END
@@ -1363,9 +1495,8 @@ int cgb_noise_budget(cgb_ring *r, int count, const uint32_t *cts, double *bits) 
     auto pc = ct_ptrs(r, 1, &cts[c]);
     u64 **dc = S.up(pc.data(), 1);
     u64 *X = S.alloc<u64>(words);
-    k_dec_inner<<<dim3(GRID1(words, TPB).x, 1), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
-                                                                     r->d_c, L, r->logN, 1);
-    check_launch(r);
+    LAUNCH("dec_inner", BYTES_dec_inner, k_dec_inner<<<dim3(GRID1(words, TPB).x, 1), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
+                                                                     r->d_c, L, r->logN, 1));
     std::vector<int> qm;
     ntt_items(r, false, X, nullptr, words, 1, 1, L, q_mod_idx(r, qm));
     CK(cudaMemcpyAsync(host.data(), X, sizeof(u64) * words, cudaMemcpyDeviceToHost, r->stream));
@@ -1399,10 +1530,9 @@ int cgb_add(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const 
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pb = ct_ptrs(r, count, b), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **db = S.up(pb.data(), count), **dout = S.up(po.data(), count);
-  k_add<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dout, (const u64 *const *)da,
+  LAUNCH("add", BYTES_add, k_add<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dout, (const u64 *const *)da,
                                                                        (const u64 *const *)db, r->d_mods, r->L,
-                                                                       r->logN, r->ct_words);
-  check_launch(r);
+                                                                       r->logN, r->ct_words));
   API_END
 }
 int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
@@ -1411,9 +1541,8 @@ int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt,
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
-  k_add_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
-      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words);
-  check_launch(r);
+  LAUNCH("add_plain", BYTES_add_plain, k_add_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words));
   API_END
 }
 int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
@@ -1422,9 +1551,8 @@ int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
-  k_mult_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
-      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words);
-  check_launch(r);
+  LAUNCH("mult_plain", BYTES_mult_plain, k_mult_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words));
   API_END
 }
 int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
@@ -1433,9 +1561,8 @@ int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), po = ct_ptrs(r, 1, &out);
   u64 **da = S.up(pa.data(), count);
-  k_sum<<<GRID1(r->ct_words, TPB), TPB, 0, r->stream>>>(po[0], (const u64 *const *)da, count, r->d_mods, r->L,
-                                                        r->logN, r->ct_words);
-  check_launch(r);
+  LAUNCH("sum", BYTES_sum, k_sum<<<GRID1(r->ct_words, TPB), TPB, 0, r->stream>>>(po[0], (const u64 *const *)da, count, r->d_mods, r->L,
+                                                        r->logN, r->ct_words));
   API_END
 }
 
@@ -1501,17 +1628,14 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     for (int p = 0; p < 4; p++) {
       const u64 *const *src = (const u64 *const *)(p < 2 ? dpa : dpb);
       u64 off = (p & 1) ? (u64)L * N : 0;
-      k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(in + (u64)p * nt * N, 4ull * nt * N, src,
-                                                                         off, (u64)L * N);
-      check_launch(r);
-      k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(coef + (u64)p * L * N, 4ull * L * N, src,
-                                                                         off, (u64)L * N);
-      check_launch(r);
+      LAUNCH("gather", BYTES_gather, k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(in + (u64)p * nt * N, 4ull * nt * N, src,
+                                                                         off, (u64)L * N));
+      LAUNCH("gather", BYTES_gather, k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(coef + (u64)p * L * N, 4ull * L * N, src,
+                                                                         off, (u64)L * N));
     }
     ntt_items(r, false, coef, nullptr, 4ull * L * N, n, 4, L, qm.data());
-    k_lift_QB<<<dim3(GRID1(4ull * N, TPB).x, n), TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0,
-                                                                      logN);
-    check_launch(r);
+    LAUNCH("lift_QB", BYTES_lift_QB, k_lift_QB<<<dim3(GRID1(4ull * N, TPB).x, n), TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0,
+                                                                      logN));
     {
       NttJob job{};
       job.base = in;
@@ -1527,13 +1651,11 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       launch_ntt(r, true, job, n);
     }
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
-    k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, r->d_mods, L, nt, r->iB0, logN);
-    check_launch(r);
+    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, r->d_mods, L, nt, r->iB0, logN));
     ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
-    k_scale_round<<<dim3(GRID1(3ull * N, TPB).x, n), TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0,
-                                                                         logN);
-    check_launch(r);
+    LAUNCH("scale_round", BYTES_scale_round, k_scale_round<<<dim3(GRID1(3ull * N, TPB).x, n), TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0,
+                                                                         logN));
     ntt_items(r, true, d, nullptr, 3ull * L * N, n, 3, L, qm.data());
     // relinearise d2, add (d0, d1)
     u64 *x = S.alloc<u64>((size_t)n * L * N);

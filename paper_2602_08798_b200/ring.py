@@ -34,6 +34,8 @@ class Ring:
         if arena_pts is None:
             arena_pts = max(64, min(16384, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
         self.arena_cts, self.arena_pts = int(arena_cts), int(arena_pts)
+        self.h2d_bytes = 0  # host payload bytes moved to / from the device (slot vectors, raw words)
+        self.d2h_bytes = 0
         ks = np.ascontiguousarray(np.asarray(key_seed, dtype=np.uint32).reshape(8))
         h = ctypes.c_void_p()
         L = nat.lib()
@@ -62,6 +64,24 @@ class Ring:
 
     def launches(self) -> int:
         return int(nat.lib().cgb_launch_count(self._h))
+
+    def timing(self, on: bool):
+        nat.check(nat.lib().cgb_timing_enable(self._h, int(on)), "cgb_timing_enable")
+
+    def timing_report(self) -> dict:
+        """{kernel: (launches, total_ms, algorithmic_bytes)} of the recorded launches."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        nat.check(nat.lib().cgb_timing_report(self._h, buf, len(buf)), "cgb_timing_report")
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, k, ms, b = line.split()
+            out[name] = (int(k), float(ms), float(b))
+        return out
+
+    def modmul_peak(self) -> float:
+        out = np.zeros(1, dtype=np.float64)
+        nat.check(nat.lib().cgb_modmul_peak(self._h, nat.dblptr(out)), "cgb_modmul_peak")
+        return float(out[0])
 
     def sync(self):
         nat.check(nat.lib().cgb_sync(self._h), "cgb_sync")
@@ -117,6 +137,7 @@ class Ring:
     def encode_pt(self, slots, kind: int, ids):
         s, ids = self._slots2d(slots), _ids(ids)
         nat.check(nat.lib().cgb_pt_encode(self._h, ids.size, nat.u64ptr(s), kind, nat.u32ptr(ids)), "cgb_pt_encode")
+        self.h2d_bytes += s.nbytes
 
     # client role -----------------------------------------------------------
     def encrypt(self, slots, enc_key, first_index: int, ids):
@@ -124,11 +145,13 @@ class Ring:
         k = np.ascontiguousarray(np.asarray(enc_key, dtype=np.uint32).reshape(8))
         nat.check(nat.lib().cgb_encrypt(self._h, ids.size, nat.u64ptr(s), nat.u32ptr(k), int(first_index),
                                         nat.u32ptr(ids)), "cgb_encrypt")
+        self.h2d_bytes += s.nbytes
 
     def decrypt(self, ids) -> np.ndarray:
         ids = _ids(ids)
         out = np.zeros((ids.size, self.n_slots), dtype=np.uint64)
         nat.check(nat.lib().cgb_decrypt(self._h, ids.size, nat.u32ptr(ids), nat.u64ptr(out)), "cgb_decrypt")
+        self.d2h_bytes += out.nbytes
         return out.astype(np.int64)
 
     def noise_budget(self, ids) -> np.ndarray:

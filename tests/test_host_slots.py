@@ -42,3 +42,18 @@ def test_full_size_prefill_matches_reference(api):
     fn, kw = harness.FULL["full_prefill_m128"]
     rec, _ = fn(api, slot_ctx, **kw)
     compare(rec, np.load(GOLD / "full_prefill_m128.npz"))
+
+
+def test_reference_path_restatement_matches_goldens(api):
+    """oracle/reference_path.py (the sequential per-op restatement used as the
+    CPU baseline and as the per-op GPU path) reproduces the reference."""
+    from types import SimpleNamespace
+
+    from oracle import reference_path as ref
+
+    ns = SimpleNamespace(**vars(api))
+    ns.attention_step, ns.append_token, ns.maybe_refresh = ref.attention_step, ref.append_token, ref.maybe_refresh
+    for name in ("attn_m5_t19", "attn_m16_t40_refresh"):
+        fn, kw = harness.SMALL[name]
+        rec, _ = fn(ns, slot_ctx, **kw)
+        compare(rec, np.load(GOLD / f"{name}.npz"))
