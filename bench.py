@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--L", type=int, default=128, help="cached prefill length per head")
     ap.add_argument("--heads", type=int, default=HEADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="warm up, run ONE step inside NVTX range 'timed_step', exit (for ncu)")
     return ap.parse_args()
 
 
@@ -190,6 +192,14 @@ def run_ours(args):
 
     for i in range(args.warmup):
         one_step(dev_tokens[i])
+    if args.profile_step:
+        barrier()
+        torch.cuda.nvtx.range_push("timed_step")
+        one_step(dev_tokens[args.warmup])
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+        print(json.dumps({"profile_step": "done", "launches": ring.launches()}))
+        return
     one_step_e2e(host_tokens[0])
     barrier()
     launches0 = ring.launches()
