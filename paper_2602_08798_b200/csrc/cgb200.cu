@@ -200,7 +200,7 @@ struct cgb_ring {
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t pending = nullptr;
 
-  int ntt_E() const { return std::min(16, N); }
+  int ntt_E() const { return std::min(32, N); }
   int ntt_threads() const { return N / ntt_E(); }
   size_t ntt_smem() const { return sizeof(u64) * (size_t)(N + (N >> 4) + 1); }
 };
@@ -312,10 +312,37 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 #define GRID1(n, b) dim3((unsigned)(((n) + (b)-1) / (b)))
 
 // NTT launcher -------------------------------------------------------------
+static const int NTT2_E = 8;
+static size_t ntt2_smem(int lm) {
+  int M = 1 << lm, G = NTT2_TILE / M, padM = M + (M >> 4);
+  return sizeof(u64) * (size_t)(((G * padM + 1) & ~1)) + sizeof(ulonglong2) * (size_t)NTT2_TILE;
+}
 static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   if (count <= 0 || job.nsub <= 0) return;
   job.mods = r->d_mods;
   job.logN = r->logN;
+  const double bytes = 16.0 * (double)count * job.nsub * r->N;
+  if (r->logN >= 12) {  // two passes over 2048-word tiles, twiddles staged in shared memory
+    const int la = r->logN / 2, lb = r->logN - la;
+    auto grid_for = [&](int lm) {
+      int nsubs = 1 << (r->logN - lm), G = NTT2_TILE / (1 << lm);
+      return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
+    };
+    const int T = NTT2_TILE / NTT2_E;
+    NttJob second = job;
+    second.src_base = nullptr;  // the fused lift happens in the first pass only
+    launch_begin(r);
+    if (fwd) {
+      k_ntt2<NTT2_E, true, 0><<<grid_for(la), T, ntt2_smem(la), r->stream>>>(job, la);
+      k_ntt2<NTT2_E, true, 1><<<grid_for(lb), T, ntt2_smem(lb), r->stream>>>(second, la);
+    } else {
+      k_ntt2<NTT2_E, false, 1><<<grid_for(lb), T, ntt2_smem(lb), r->stream>>>(job, la);
+      k_ntt2<NTT2_E, false, 0><<<grid_for(la), T, ntt2_smem(la), r->stream>>>(second, la);
+    }
+    r->launches++;  // two kernels, counted as one NTT launch pair below
+    launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes);
+    return;
+  }
   int E = r->ntt_E(), T = r->ntt_threads();
   size_t smem = r->ntt_smem();
   dim3 grid((unsigned)(count * job.nsub));
@@ -326,13 +353,14 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   } while (0)
   launch_begin(r);
   switch (E) {
+    case 32: LNTT(32); break;
     case 16: LNTT(16); break;
     case 8: LNTT(8); break;
     case 4: LNTT(4); break;
     default: LNTT(2); break;
   }
 #undef LNTT
-  launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 16.0 * (double)count * job.nsub * r->N);
+  launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", bytes);
 }
 // NTT over `nlimb` limbs of `npoly` polys per item, limb l of poly p at unit p*nlimb+l
 static void ntt_items(cgb_ring *r, bool fwd, u64 *base, u64 *const *items, u64 item_stride, int count, int npoly,
@@ -451,7 +479,8 @@ __global__ void k_modup(u64 *D, const u64 *xcoef /*[item][L][N]*/, const u64 *xi
   D[(u64)item * words + i] = v;
 }
 // acc[item][p][l][N] = sum_j D[j][l] * key[j][p][l]   (p = 0: b, 1: a)
-__global__ void k_ks_inner(u64 *acc, const u64 *D, const u64 *const *keys, const ModTab *mods, int L, int logN) {
+__global__ void k_ks_inner(u64 *acc, const u64 *D, const u64 *xin, const u64 *const *keys, const ModTab *mods, int L,
+                           int logN) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, LP = L + 1;
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
@@ -461,8 +490,9 @@ __global__ void k_ks_inner(u64 *acc, const u64 *D, const u64 *const *keys, const
   const u64 *Di = D + (u64)item * L * LP * N;
   const u64 *K = keys[item];
   u64 s0 = 0, s1 = 0;
+  const u64 N1 = N - 1;
   for (int j = 0; j < L; j++) {
-    u64 d = Di[(u64)j * LP * N + i];
+    u64 d = (l == j) ? xin[((u64)item * L + j) * N + (i & N1)] : Di[(u64)j * LP * N + i];
     s0 = add_mod(s0, mul_mod(d, K[((u64)j * 2 + 0) * LP * N + i], M), M.q);
     s1 = add_mod(s1, mul_mod(d, K[((u64)j * 2 + 1) * LP * N + i], M), M.q);
   }
@@ -813,20 +843,23 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
   u64 *xc = S.alloc<u64>((size_t)count * L * N);
   CK(cudaMemcpyAsync(xc, x, sizeof(u64) * (size_t)count * L * N, cudaMemcpyDeviceToDevice, r->stream));
   ntt_items(r, false, xc, nullptr, (u64)L * N, count, 1, L, qm.data());
-  // ModUp
+  // ModUp: digit j centre-lifted into every other limb of Q u P, fused into the NTT load
   u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
   u64 wD = (u64)L * LP * N;
-  LAUNCH("modup", BYTES_modup, k_modup<<<dim3(GRID1(wD, TPB).x, count), TPB, 0, r->stream>>>(D, xc, x, r->d_mods, L, logN));
   {
     NttJob job{};
     job.base = D;
     job.item_stride = wD;
+    job.src_base = xc;
+    job.src_stride = (u64)L * N;
     int n = 0;
     for (int j = 0; j < L; j++)
       for (int l = 0; l < LP; l++) {
-        if (l == j) continue;
+        if (l == j) continue;  // the digit's own limb is the NTT-form input itself
         job.sub_off[n] = (unsigned short)(j * LP + l);
         job.sub_mod[n] = (unsigned char)(l == L ? r->iP : l);
+        job.src_off[n] = (unsigned short)j;
+        job.src_mod[n] = (unsigned char)j;
         n++;
       }
     job.nsub = n;
@@ -834,7 +867,7 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
   }
   // inner product with the evaluation key
   u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
-  LAUNCH("ks_inner", BYTES_ks_inner, k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, d_keys, r->d_mods, L, logN));
+  LAUNCH("ks_inner", BYTES_ks_inner, k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, x, d_keys, r->d_mods, L, logN));
   // ModDown
   {
     int mP = r->iP;
@@ -848,9 +881,26 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
     job.nsub = 2;
     launch_ntt(r, false, job, count);
   }
+  // ModDown: centre-lift the P limb into Q, fused into the NTT load
   u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
-  LAUNCH("moddown_lift", BYTES_moddown_lift, k_moddown_lift<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(W, acc, r->d_mods, L, r->iP, logN));
-  ntt_items(r, true, W, nullptr, 2ull * L * N, count, 2, L, qm.data());
+  {
+    NttJob job{};
+    job.base = W;
+    job.item_stride = 2ull * L * N;
+    job.src_base = acc;
+    job.src_stride = 2ull * LP * N;
+    int n = 0;
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        job.sub_off[n] = (unsigned short)(pp * L + l);
+        job.sub_mod[n] = (unsigned char)l;
+        job.src_off[n] = (unsigned short)(pp * LP + L);
+        job.src_mod[n] = (unsigned char)r->iP;
+        n++;
+      }
+    job.nsub = n;
+    launch_ntt(r, true, job, count);
+  }
   LAUNCH("moddown_combine", BYTES_moddown_combine, k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
       d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
 }
@@ -1025,10 +1075,10 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     for (int k = 0; k < N; k++) {
       u32 b = h_brev((u32)k, logN);
       u64 w = h_powmod(psi, b, q), wi = h_powmod(psii, b, q);
-      tab[k] = w;
-      tab[N + k] = h_shoup(w, q);
-      tab[2 * N + k] = wi;
-      tab[3 * N + k] = h_shoup(wi, q);
+      tab[2 * k] = w;  // (w, w') pairs: one 16-byte load per twiddle
+      tab[2 * k + 1] = h_shoup(w, q);
+      tab[2 * N + 2 * k] = wi;
+      tab[2 * N + 2 * k + 1] = h_shoup(wi, q);
     }
     u64 *dt = r->d_tables + per * i;
     CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
@@ -1041,9 +1091,9 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.ninv = h_inv((u64)N % q, q);
     M.ninv_sh = h_shoup(M.ninv, q);
     M.tw = dt;
-    M.tw_sh = dt + N;
+    M.tw_sh = nullptr;
     M.itw = dt + 2 * N;
-    M.itw_sh = dt + 3 * N;
+    M.itw_sh = nullptr;
   }
   CK(cudaMalloc((void **)&r->d_mods, sizeof(ModTab) * r->nmod));
   CK(cudaMemcpy(r->d_mods, r->h_mods.data(), sizeof(ModTab) * r->nmod, cudaMemcpyHostToDevice));
@@ -1179,8 +1229,13 @@ int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
 #define SETSMEM(EE)                                                                                           \
   CK(cudaFuncSetAttribute(k_ntt<EE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));        \
   CK(cudaFuncSetAttribute(k_ntt<EE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
+    SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
 #undef SETSMEM
+    size_t s2 = std::max(ntt2_smem(log_n / 2), ntt2_smem(log_n - log_n / 2));
+    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
   }
   r->pin_cap = 8u << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));

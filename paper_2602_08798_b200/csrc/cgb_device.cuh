@@ -105,120 +105,282 @@ __device__ __forceinline__ void chacha_block(const ChaKey &key, u64 ctr, u64 non
 // negacyclic NTT, one CTA per (poly, limb), whole vector in shared memory.
 // Forward: Cooley-Tukey, natural in -> bit-reversed out (a[k] = A(psi^(2brev(k)+1))).
 // Inverse: Gentleman-Sande, bit-reversed in -> natural out, times N^-1.
-// Each thread keeps E = 2^R words in registers and runs R radix-2 stages on
-// them between shared-memory exchanges (logN/R exchanges in total).
+// Harvey lazy butterflies: forward values live in [0, 4q), inverse in [0, 2q)
+// (q < 2^62); outputs are reduced to [0, q) on the final store.
+// Each thread keeps E words in registers as E/16 rows of 16 and runs up to
+// 4 radix-2 stages on them between shared-memory exchanges.  Twiddles are
+// (w, w') pairs read with one 16-byte load, one load per distinct twiddle.
+// Optional fused load: a unit may read its input from another buffer and
+// centre-lift it from a source modulus (ModUp / ModDown base conversion).
 // ---------------------------------------------------------------------------
 constexpr int NTT_MAXSUB = 160;
 
 struct NttJob {
-  u64 *base;                 // contiguous items: base + item * item_stride
-  u64 *const *items;         // or per-item pointers (device array), if non-null
+  u64 *base;                 // destination items: base + item * item_stride
+  u64 *const *items;         // or per-item destination pointers (device array), if non-null
   u64 item_stride;           // words
+  const u64 *src_base;       // fused-load source items (null: in place)
+  u64 src_stride;
   const ModTab *mods;
   int logN;
-  int nsub;                  // (poly, limb) units per item
-  unsigned short sub_off[NTT_MAXSUB];  // unit offset inside the item, in units of N words
-  unsigned char sub_mod[NTT_MAXSUB];   // modulus index of the unit
+  int nsub;                                // (poly, limb) units per item
+  unsigned short sub_off[NTT_MAXSUB];      // unit offset inside the item, in units of N words
+  unsigned short src_off[NTT_MAXSUB];      // source unit offset (fused load)
+  unsigned char sub_mod[NTT_MAXSUB];       // modulus index of the unit
+  unsigned char src_mod[NTT_MAXSUB];       // source modulus of the centred lift (fused load)
 };
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
 
+// lazy Shoup: a * w mod q in [0, 2q) for any a < 2^64
+__device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
+  return a * w - __umul64hi(a, wsh) * q;
+}
+
 template <int E, int RP, bool FWD>
-__device__ __forceinline__ void ntt_phase(u64 *sm, int s0, int logN, int tid, u64 q, const u64 *__restrict__ tw,
-                                          const u64 *__restrict__ twsh) {
-  constexpr int K = 1 << RP;          // words per row
-  constexpr int R = E / K;            // rows per thread
-  const int N = 1 << logN;
-  const int S = N >> s0, st = S >> RP;
-  u64 x[E];
-#pragma unroll
+__device__ __forceinline__ void ntt_phase(u64 *sm, int s0, int logN, int tid, u64 q, u64 q2,
+                                          const ulonglong2 *__restrict__ tw) {
+  constexpr int K = 1 << RP;   // words per row
+  constexpr int R = E / K;     // rows per thread, processed one after another
+  const int S = (1 << logN) >> s0, st = S >> RP;
+#pragma unroll 1
   for (int u = 0; u < R; u++) {
-    int row = tid * R + u, blk = row / st, off = row - blk * st;
+    const int row = tid * R + u, blk = row / st;
+    const int base = blk * S + (row - blk * st);
+    u64 x[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) x[u * K + k] = sm[spad(blk * S + off + k * st)];
-  }
-  if (FWD) {
+    for (int k = 0; k < K; k++) x[k] = sm[spad(base + k * st)];
 #pragma unroll
-    for (int l = 0; l < RP; l++) {
+    for (int ll = 0; ll < RP; ll++) {
+      const int l = FWD ? ll : RP - 1 - ll;
       const int half = K >> (l + 1);
+      ulonglong2 W;
 #pragma unroll
-      for (int u = 0; u < R; u++) {
-        int row = tid * R + u, blk = row / st;
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-          if (k & half) continue;
-          int ti = (1 << (s0 + l)) + (blk << l) + (k >> (RP - l));
-          u64 W = __ldg(tw + ti), Ws = __ldg(twsh + ti);
-          u64 U = x[u * K + k], V = mul_shoup(x[u * K + k + half], W, Ws, q);
-          x[u * K + k] = add_mod(U, V, q);
-          x[u * K + k + half] = sub_mod(U, V, q);
+      for (int k = 0; k < K; k++) {
+        if (k & half) continue;
+        // butterflies sharing twiddle group k >> (RP - l) are consecutive: one 16-byte load per group
+        if ((k & ((1 << (RP - l)) - 1)) == 0) W = __ldg(tw + (1 << (s0 + l)) + (blk << l) + (k >> (RP - l)));
+        u64 &X = x[k], &Y = x[k + half];
+        if (FWD) {
+          u64 a = X >= q2 ? X - q2 : X;
+          u64 t = mul_shoup_lazy(Y, W.x, W.y, q);
+          X = a + t;
+          Y = a - t + q2;
+        } else {
+          u64 a = X + Y;
+          u64 d = X - Y + q2;
+          X = a >= q2 ? a - q2 : a;
+          Y = mul_shoup_lazy(d, W.x, W.y, q);
         }
       }
     }
-  } else {
 #pragma unroll
-    for (int l = RP - 1; l >= 0; l--) {
-      const int half = K >> (l + 1);
-#pragma unroll
-      for (int u = 0; u < R; u++) {
-        int row = tid * R + u, blk = row / st;
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-          if (k & half) continue;
-          int ti = (1 << (s0 + l)) + (blk << l) + (k >> (RP - l));
-          u64 W = __ldg(tw + ti), Ws = __ldg(twsh + ti);
-          u64 U = x[u * K + k], V = x[u * K + k + half];
-          x[u * K + k] = add_mod(U, V, q);
-          x[u * K + k + half] = mul_shoup(sub_mod(U, V, q), W, Ws, q);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < R; u++) {
-    int row = tid * R + u, blk = row / st, off = row - blk * st;
-#pragma unroll
-    for (int k = 0; k < K; k++) sm[spad(blk * S + off + k * st)] = x[u * K + k];
+    for (int k = 0; k < K; k++) sm[spad(base + k * st)] = x[k];
   }
 }
 
 template <int E, bool FWD>
-__device__ __forceinline__ void ntt_phase_dispatch(int rp, u64 *sm, int s0, int logN, int tid, u64 q, const u64 *tw,
-                                                   const u64 *twsh) {
-  if (E >= 16 && rp == 4) { ntt_phase<E, (E >= 16 ? 4 : 1), FWD>(sm, s0, logN, tid, q, tw, twsh); return; }
-  if (E >= 8 && rp == 3) { ntt_phase<E, (E >= 8 ? 3 : 1), FWD>(sm, s0, logN, tid, q, tw, twsh); return; }
-  if (E >= 4 && rp == 2) { ntt_phase<E, (E >= 4 ? 2 : 1), FWD>(sm, s0, logN, tid, q, tw, twsh); return; }
-  ntt_phase<E, 1, FWD>(sm, s0, logN, tid, q, tw, twsh);
+__device__ __forceinline__ void ntt_phase_dispatch(int rp, u64 *sm, int s0, int logN, int tid, u64 q, u64 q2,
+                                                   const ulonglong2 *tw) {
+  switch (rp) {
+    case 4: if constexpr (E >= 16) { ntt_phase<E, 4, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    case 3: if constexpr (E >= 8) { ntt_phase<E, 3, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    case 2: if constexpr (E >= 4) { ntt_phase<E, 2, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    default: break;
+  }
+  ntt_phase<E, 1, FWD>(sm, s0, logN, tid, q, q2, tw);
 }
 
+// E words per thread; phases of RMAX = min(4, log2 E) stages
 template <int E, bool FWD>
-__global__ void __launch_bounds__(1024) k_ntt(NttJob job) {
+__global__ void __launch_bounds__(512) k_ntt(NttJob job) {
   extern __shared__ u64 sm[];
-  constexpr int R = (E == 16) ? 4 : (E == 8) ? 3 : (E == 4) ? 2 : 1;
+  constexpr int RMAX = (E >= 16) ? 4 : (E == 8) ? 3 : (E == 4) ? 2 : 1;
   const int item = blockIdx.x / job.nsub, sub = blockIdx.x - item * job.nsub;
-  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) +
-           ((u64)job.sub_off[sub] << job.logN);
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << job.logN);
   const ModTab &M = job.mods[job.sub_mod[sub]];
-  const u64 q = M.q;
+  const u64 q = M.q, q2 = 2 * q;
   const int logN = job.logN, N = 1 << logN, tid = threadIdx.x, T = blockDim.x;
-  for (int i = tid; i < N; i += T) sm[spad(i)] = p[i];
-  __syncthreads();
-  if (FWD) {
-    for (int s0 = 0; s0 < logN; s0 += R) {
-      int rp = min(R, logN - s0);
-      ntt_phase_dispatch<E, true>(rp, sm, s0, logN, tid, q, M.tw, M.tw_sh);
-      __syncthreads();
-    }
-    for (int i = tid; i < N; i += T) p[i] = sm[spad(i)];
+  if (job.src_base) {  // fused centred lift from the source modulus
+    const u64 *src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << logN);
+    const u64 qs = job.mods[job.src_mod[sub]].q;
+    for (int i = tid; i < N; i += T) sm[spad(i)] = centred_to(src[i], qs, q);
   } else {
-    int nph = (logN + R - 1) / R;
-    for (int ph = nph - 1; ph >= 0; ph--) {
-      int s0 = ph * R, rp = min(R, logN - s0);
-      ntt_phase_dispatch<E, false>(rp, sm, s0, logN, tid, q, M.itw, M.itw_sh);
-      __syncthreads();
+    for (int i = tid; i < N; i += T) sm[spad(i)] = p[i];
+  }
+  __syncthreads();
+  const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(FWD ? M.tw : M.itw);
+  const int nph = (logN + RMAX - 1) / RMAX;
+  for (int ph = 0; ph < nph; ph++) {
+    const int pi = FWD ? ph : nph - 1 - ph;
+    const int s0 = pi * RMAX, rp = min(RMAX, logN - s0);
+    ntt_phase_dispatch<E, FWD>(rp, sm, s0, logN, tid, q, q2, tw);
+    __syncthreads();
+  }
+  if (FWD) {
+    for (int i = tid; i < N; i += T) {
+      u64 v = sm[spad(i)];
+      v = v >= q2 ? v - q2 : v;
+      p[i] = v >= q ? v - q : v;
     }
+  } else {
     const u64 ni = M.ninv, nis = M.ninv_sh;
     for (int i = tid; i < N; i += T) p[i] = mul_shoup(sm[spad(i)], ni, nis, q);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// two-pass NTT for large N = 2^a * 2^b (a = logN / 2):
+//   pass 0: 2^b strided "column" sub-NTTs of 2^a points (stages 0..a-1),
+//   pass 1: 2^a contiguous "row" sub-NTTs of 2^b points (stages a..logN-1).
+// Forward runs pass 0 then 1; inverse runs pass 1 then 0 (GS order).  Every
+// stage-s twiddle of the full transform restricted to one sub-NTT is the
+// sub-NTT's own stage table, so each CTA stages exactly the (w, w') pairs
+// its G sub-NTTs use in shared memory (pass 0: 2^a - 1 pairs shared by all
+// columns; pass 1: 2^b - 1 pairs per row block) and works from there.
+// ---------------------------------------------------------------------------
+constexpr int NTT2_TILE = 2048;  // words per CTA
+
+template <int E, int RP, bool FWD>
+__device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int s0, int lm, int tl, u64 q, u64 q2) {
+  constexpr int K = 1 << RP;
+  constexpr int R = E / K;  // rows per thread (more than one in a short last phase)
+  const int S = (1 << lm) >> s0, st = S >> RP;
+#pragma unroll
+  for (int u = 0; u < R; u++) {
+    const int row = tl * R + u;
+    const int blk = row / st, base = blk * S + (row - blk * st);
+    u64 x[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) x[k] = sub[spad(base + k * st)];
+#pragma unroll
+    for (int ll = 0; ll < RP; ll++) {
+      const int l = FWD ? ll : RP - 1 - ll;
+      const int half = K >> (l + 1);
+      ulonglong2 W;
+#pragma unroll
+      for (int k = 0; k < K; k++) {
+        if (k & half) continue;
+        if ((k & ((1 << (RP - l)) - 1)) == 0) W = tws[(1 << (s0 + l)) + (blk << l) + (k >> (RP - l))];
+        u64 &X = x[k], &Y = x[k + half];
+        if (FWD) {
+          u64 a = X >= q2 ? X - q2 : X;
+          u64 t = mul_shoup_lazy(Y, W.x, W.y, q);
+          X = a + t;
+          Y = a - t + q2;
+        } else {
+          u64 a = X + Y;
+          u64 d = X - Y + q2;
+          X = a >= q2 ? a - q2 : a;
+          Y = mul_shoup_lazy(d, W.x, W.y, q);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) sub[spad(base + k * st)] = x[k];
+  }
+}
+
+// E words per thread (one row of E = 2^RMAX per phase); PASS 0 columns / 1 rows
+template <int E, bool FWD, int PASS>
+__global__ void __launch_bounds__(256) k_ntt2(NttJob job, int la) {
+  extern __shared__ u64 sm2[];
+  constexpr int RMAX = (E == 16) ? 4 : (E == 8) ? 3 : (E == 4) ? 2 : 1;
+  const int logN = job.logN, N = 1 << logN, lb = logN - la;
+  const int lm = PASS == 0 ? la : lb, M = 1 << lm;            // sub-NTT size
+  const int nsubs = PASS == 0 ? (1 << lb) : (1 << la);         // sub-NTTs per unit
+  const int G = NTT2_TILE / M;                                 // sub-NTTs per CTA
+  const int tiles = nsubs / G;
+  const int unit = blockIdx.x / tiles, tile = blockIdx.x - unit * tiles;
+  const int item = unit / job.nsub, sub = unit - item * job.nsub;
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << logN);
+  const ModTab &Md = job.mods[job.sub_mod[sub]];
+  const u64 q = Md.q, q2 = 2 * q;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int padM = M + (M >> 4);
+  u64 *data = sm2;
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm2 + ((G * padM + 1) & ~1));  // 16-byte aligned
+  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(FWD ? Md.tw : Md.itw);
+  const int first = tile * G;  // first sub-NTT of this CTA
+  // stage twiddles
+  if (PASS == 0) {
+    for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
+  } else {
+    for (int e = tid; e < G * M; e += T) {
+      int g = e / M, i = e - g * M;           // i in [1, M): local (stage s', group) -> 2^s' + idx
+      if (i == 0) continue;
+      int sp = 31 - __clz(i), gi = i - (1 << sp);
+      tws[g * M + i] = __ldg(gtw + (1 << (la + sp)) + ((first + g) << sp) + gi);
+    }
+  }
+  // load the tile (optionally centred-lifted from another buffer / modulus)
+  const u64 *src = p;
+  u64 qs = 0;
+  const bool lift = job.src_base != nullptr;
+  if (lift) {
+    src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << logN);
+    qs = job.mods[job.src_mod[sub]].q;
+  }
+  for (int e = tid; e < G * M; e += T) {
+    int g, k;
+    u64 gidx;
+    if (PASS == 0) {  // element (k, column first+g) at k * 2^lb + column
+      g = e % G;
+      k = e / G;
+      gidx = ((u64)k << lb) + first + g;
+    } else {
+      g = e / M;
+      k = e - g * M;
+      gidx = ((u64)(first + g) << lm) + k;
+    }
+    u64 v = src[gidx];
+    if (lift) v = centred_to(v, qs, q);
+    data[g * padM + spad(k)] = v;
+  }
+  __syncthreads();
+  const int tps = M / E;  // threads per sub-NTT
+  const int g = tid / tps, tl = tid - g * tps;
+  const int nph = (lm + RMAX - 1) / RMAX;
+  for (int ph = 0; ph < nph; ph++) {
+    const int pi = FWD ? ph : nph - 1 - ph;
+    const int s0 = pi * RMAX, rp = min(RMAX, lm - s0);
+    if (g < G) {
+      u64 *sub_d = data + g * padM;
+      const ulonglong2 *tw_g = PASS == 0 ? tws : tws + g * M;
+      switch (rp) {
+        case 4: if constexpr (E >= 16) { ntt2_phase<E, 4, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
+        case 3: if constexpr (E >= 8) { ntt2_phase<E, 3, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
+        case 2: if constexpr (E >= 4) { ntt2_phase<E, 2, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
+        default: ntt2_phase<E, 1, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break;
+      }
+    }
+    __syncthreads();
+  }
+  // store (final pass reduces to [0, q); the inverse's final pass is pass 0 and scales by N^-1)
+  const bool last = FWD ? (PASS == 1) : (PASS == 0);
+  const u64 ni = Md.ninv, nis = Md.ninv_sh;
+  for (int e = tid; e < G * M; e += T) {
+    int gg, k;
+    u64 gidx;
+    if (PASS == 0) {
+      gg = e % G;
+      k = e / G;
+      gidx = ((u64)k << lb) + first + gg;
+    } else {
+      gg = e / M;
+      k = e - gg * M;
+      gidx = ((u64)(first + gg) << lm) + k;
+    }
+    u64 v = data[gg * padM + spad(k)];
+    if (last) {
+      if (FWD) {
+        v = v >= q2 ? v - q2 : v;
+        v = v >= q ? v - q : v;
+      } else {
+        v = mul_shoup(v, ni, nis, q);
+      }
+    }
+    p[gidx] = v;
   }
 }
 
