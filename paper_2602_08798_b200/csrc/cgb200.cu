@@ -312,10 +312,30 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 #define GRID1(n, b) dim3((unsigned)(((n) + (b)-1) / (b)))
 
 // NTT launcher -------------------------------------------------------------
-static const int NTT2_E = 8;
-static size_t ntt2_smem(int lm) {
-  int M = 1 << lm, G = NTT2_TILE / M, padM = M + (M >> 4);
-  return sizeof(u64) * (size_t)(((G * padM + 1) & ~1)) + sizeof(ulonglong2) * (size_t)NTT2_TILE;
+template <int LA, int LB>
+static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
+  NttJob second = job;
+  second.src_base = nullptr;  // the fused lift happens in the first pass only
+  auto grid = [&](int lm) {
+    int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
+    return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
+  };
+  const size_t s0 = ntt2_smem_bytes<LA, LB>(0), s1 = ntt2_smem_bytes<LA, LB>(1);
+  if (fwd) {
+    k_ntt2<LA, LB, true, 0><<<grid(LA), NTT2_T, s0, r->stream>>>(job);
+    k_ntt2<LA, LB, true, 1><<<grid(LB), NTT2_T, s1, r->stream>>>(second);
+  } else {
+    k_ntt2<LA, LB, false, 1><<<grid(LB), NTT2_T, s1, r->stream>>>(job);
+    k_ntt2<LA, LB, false, 0><<<grid(LA), NTT2_T, s0, r->stream>>>(second);
+  }
+}
+template <int LA, int LB>
+static void ntt2_attrs() {
+  const int s = (int)std::max(ntt2_smem_bytes<LA, LB>(0), ntt2_smem_bytes<LA, LB>(1));
+  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
 }
 static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   if (count <= 0 || job.nsub <= 0) return;
@@ -323,23 +343,15 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   job.logN = r->logN;
   const double bytes = 16.0 * (double)count * job.nsub * r->N;
   if (r->logN >= 12) {  // two passes over 2048-word tiles, twiddles staged in shared memory
-    const int la = r->logN / 2, lb = r->logN - la;
-    auto grid_for = [&](int lm) {
-      int nsubs = 1 << (r->logN - lm), G = NTT2_TILE / (1 << lm);
-      return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
-    };
-    const int T = NTT2_TILE / NTT2_E;
-    NttJob second = job;
-    second.src_base = nullptr;  // the fused lift happens in the first pass only
     launch_begin(r);
-    if (fwd) {
-      k_ntt2<NTT2_E, true, 0><<<grid_for(la), T, ntt2_smem(la), r->stream>>>(job, la);
-      k_ntt2<NTT2_E, true, 1><<<grid_for(lb), T, ntt2_smem(lb), r->stream>>>(second, la);
-    } else {
-      k_ntt2<NTT2_E, false, 1><<<grid_for(lb), T, ntt2_smem(lb), r->stream>>>(job, la);
-      k_ntt2<NTT2_E, false, 0><<<grid_for(la), T, ntt2_smem(la), r->stream>>>(second, la);
+    switch (r->logN) {
+      case 12: launch_ntt2<6, 6>(r, fwd, job, count); break;
+      case 13: launch_ntt2<6, 7>(r, fwd, job, count); break;
+      case 14: launch_ntt2<7, 7>(r, fwd, job, count); break;
+      case 15: launch_ntt2<7, 8>(r, fwd, job, count); break;
+      default: launch_ntt2<8, 8>(r, fwd, job, count); break;
     }
-    r->launches++;  // two kernels, counted as one NTT launch pair below
+    r->launches++;  // two kernels per transform (launch_end counts the other)
     launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes);
     return;
   }
@@ -1199,7 +1211,7 @@ const char *cgb_last_error(void) { return g_err.c_str(); }
 int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots, int one_row,
                     const uint32_t key_seed[8], int64_t arena_cts, int64_t arena_pts, cgb_ring **out) {
   API_BEGIN
-  if (log_n < 2 || log_n > 14) FAIL(CGB_ERR_PARAM, "log_n %d outside [2, 14]", log_n);
+  if (log_n < 2 || log_n > 16) FAIL(CGB_ERR_PARAM, "log_n %d outside [2, 16]", log_n);
   if (n_limbs < 1 || n_limbs > MAXL) FAIL(CGB_ERR_PARAM, "n_limbs %d outside [1, %d]", n_limbs, MAXL);
   u64 N = 1ull << log_n;
   if (plain_modulus < 3 || plain_modulus >= (1ull << 31) || plain_modulus % (2 * N) != 1)
@@ -1231,11 +1243,14 @@ int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
   CK(cudaFuncSetAttribute(k_ntt<EE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
 #undef SETSMEM
-    size_t s2 = std::max(ntt2_smem(log_n / 2), ntt2_smem(log_n - log_n / 2));
-    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-    CK(cudaFuncSetAttribute(k_ntt2<NTT2_E, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    switch (log_n) {
+      case 12: ntt2_attrs<6, 6>(); break;
+      case 13: ntt2_attrs<6, 7>(); break;
+      case 14: ntt2_attrs<7, 7>(); break;
+      case 15: ntt2_attrs<7, 8>(); break;
+      case 16: ntt2_attrs<8, 8>(); break;
+      default: break;
+    }
   }
   r->pin_cap = 8u << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));

@@ -240,19 +240,21 @@ __global__ void __launch_bounds__(512) k_ntt(NttJob job) {
 // columns; pass 1: 2^b - 1 pairs per row block) and works from there.
 // ---------------------------------------------------------------------------
 constexpr int NTT2_TILE = 2048;  // words per CTA
+constexpr int NTT2_T = 256;      // threads per CTA (8 words each)
 
-template <int E, int RP, bool FWD>
-__device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int s0, int lm, int tl, u64 q, u64 q2) {
-  constexpr int K = 1 << RP;
-  constexpr int R = E / K;  // rows per thread (more than one in a short last phase)
-  const int S = (1 << lm) >> s0, st = S >> RP;
+// one register phase of RP radix-2 stages starting at local stage S0 of an
+// M = 2^LM point sub-NTT; each thread owns 8 words = 8/2^RP rows of 2^RP
+template <int LM, int S0, int RP, bool FWD>
+__device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
+  constexpr int K = 1 << RP, R = 8 / K;
+  constexpr int S = (1 << LM) >> S0, ST = S >> RP;
 #pragma unroll
   for (int u = 0; u < R; u++) {
     const int row = tl * R + u;
-    const int blk = row / st, base = blk * S + (row - blk * st);
+    const int blk = row / ST, base = blk * S + (row & (ST - 1));
     u64 x[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) x[k] = sub[spad(base + k * st)];
+    for (int k = 0; k < K; k++) x[k] = sub[spad(base + k * ST)];
 #pragma unroll
     for (int ll = 0; ll < RP; ll++) {
       const int l = FWD ? ll : RP - 1 - ll;
@@ -261,7 +263,7 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
 #pragma unroll
       for (int k = 0; k < K; k++) {
         if (k & half) continue;
-        if ((k & ((1 << (RP - l)) - 1)) == 0) W = tws[(1 << (s0 + l)) + (blk << l) + (k >> (RP - l))];
+        if ((k & ((1 << (RP - l)) - 1)) == 0) W = tws[(1 << (S0 + l)) + (blk << l) + (k >> (RP - l))];
         u64 &X = x[k], &Y = x[k + half];
         if (FWD) {
           u64 a = X >= q2 ? X - q2 : X;
@@ -277,111 +279,131 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
       }
     }
 #pragma unroll
-    for (int k = 0; k < K; k++) sub[spad(base + k * st)] = x[k];
+    for (int k = 0; k < K; k++) sub[spad(base + k * ST)] = x[k];
   }
 }
 
-// E words per thread (one row of E = 2^RMAX per phase); PASS 0 columns / 1 rows
-template <int E, bool FWD, int PASS>
-__global__ void __launch_bounds__(256) k_ntt2(NttJob job, int la) {
-  extern __shared__ u64 sm2[];
-  constexpr int RMAX = (E == 16) ? 4 : (E == 8) ? 3 : (E == 4) ? 2 : 1;
-  const int logN = job.logN, N = 1 << logN, lb = logN - la;
-  const int lm = PASS == 0 ? la : lb, M = 1 << lm;            // sub-NTT size
-  const int nsubs = PASS == 0 ? (1 << lb) : (1 << la);         // sub-NTTs per unit
-  const int G = NTT2_TILE / M;                                 // sub-NTTs per CTA
-  const int tiles = nsubs / G;
-  const int unit = blockIdx.x / tiles, tile = blockIdx.x - unit * tiles;
-  const int item = unit / job.nsub, sub = unit - item * job.nsub;
-  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << logN);
-  const ModTab &Md = job.mods[job.sub_mod[sub]];
-  const u64 q = Md.q, q2 = 2 * q;
-  const int tid = threadIdx.x, T = blockDim.x;
-  const int padM = M + (M >> 4);
-  u64 *data = sm2;
-  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm2 + ((G * padM + 1) & ~1));  // 16-byte aligned
-  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(FWD ? Md.tw : Md.itw);
-  const int first = tile * G;  // first sub-NTT of this CTA
-  // stage twiddles
-  if (PASS == 0) {
-    for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
+// all phases of one sub-NTT, phases of 3 stages (the last one shorter)
+template <int LM, bool FWD>
+__device__ __forceinline__ void ntt2_sub(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
+  constexpr int NPH = (LM + 2) / 3;
+  if (FWD) {
+    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), true>(sub, tws, tl, q, q2);
+    __syncthreads();
+    if constexpr (NPH > 1) {
+      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), true>(sub, tws, tl, q, q2);
+      __syncthreads();
+    }
+    if constexpr (NPH > 2) {
+      ntt2_phase<LM, 6, LM - 6, true>(sub, tws, tl, q, q2);
+      __syncthreads();
+    }
   } else {
-    for (int e = tid; e < G * M; e += T) {
-      int g = e / M, i = e - g * M;           // i in [1, M): local (stage s', group) -> 2^s' + idx
-      if (i == 0) continue;
-      int sp = 31 - __clz(i), gi = i - (1 << sp);
-      tws[g * M + i] = __ldg(gtw + (1 << (la + sp)) + ((first + g) << sp) + gi);
+    if constexpr (NPH > 2) {
+      ntt2_phase<LM, 6, LM - 6, false>(sub, tws, tl, q, q2);
+      __syncthreads();
     }
-  }
-  // load the tile (optionally centred-lifted from another buffer / modulus)
-  const u64 *src = p;
-  u64 qs = 0;
-  const bool lift = job.src_base != nullptr;
-  if (lift) {
-    src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << logN);
-    qs = job.mods[job.src_mod[sub]].q;
-  }
-  for (int e = tid; e < G * M; e += T) {
-    int g, k;
-    u64 gidx;
-    if (PASS == 0) {  // element (k, column first+g) at k * 2^lb + column
-      g = e % G;
-      k = e / G;
-      gidx = ((u64)k << lb) + first + g;
-    } else {
-      g = e / M;
-      k = e - g * M;
-      gidx = ((u64)(first + g) << lm) + k;
+    if constexpr (NPH > 1) {
+      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), false>(sub, tws, tl, q, q2);
+      __syncthreads();
     }
-    u64 v = src[gidx];
-    if (lift) v = centred_to(v, qs, q);
-    data[g * padM + spad(k)] = v;
-  }
-  __syncthreads();
-  const int tps = M / E;  // threads per sub-NTT
-  const int g = tid / tps, tl = tid - g * tps;
-  const int nph = (lm + RMAX - 1) / RMAX;
-  for (int ph = 0; ph < nph; ph++) {
-    const int pi = FWD ? ph : nph - 1 - ph;
-    const int s0 = pi * RMAX, rp = min(RMAX, lm - s0);
-    if (g < G) {
-      u64 *sub_d = data + g * padM;
-      const ulonglong2 *tw_g = PASS == 0 ? tws : tws + g * M;
-      switch (rp) {
-        case 4: if constexpr (E >= 16) { ntt2_phase<E, 4, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
-        case 3: if constexpr (E >= 8) { ntt2_phase<E, 3, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
-        case 2: if constexpr (E >= 4) { ntt2_phase<E, 2, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break; }
-        default: ntt2_phase<E, 1, FWD>(sub_d, tw_g, s0, lm, tl, q, q2); break;
-      }
-    }
+    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), false>(sub, tws, tl, q, q2);
     __syncthreads();
   }
-  // store (final pass reduces to [0, q); the inverse's final pass is pass 0 and scales by N^-1)
-  const bool last = FWD ? (PASS == 1) : (PASS == 0);
-  const u64 ni = Md.ninv, nis = Md.ninv_sh;
-  for (int e = tid; e < G * M; e += T) {
-    int gg, k;
-    u64 gidx;
+}
+
+// PASS 0: 2^LB strided columns of 2^LA points; PASS 1: 2^LA contiguous rows of 2^LB points
+template <int LA, int LB, bool FWD, int PASS>
+__global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
+  extern __shared__ u64 sm2[];
+  constexpr int LOGN = LA + LB;
+  constexpr int LM = PASS == 0 ? LA : LB, M = 1 << LM;
+  constexpr int G = NTT2_TILE / M, LG = 11 - LM;
+  constexpr int NSUBS = 1 << (PASS == 0 ? LB : LA), TILES = NSUBS / G;
+  constexpr int PADM = M + (M >> 4) + 1, TPS = M / 8;  // odd row pitch: conflict-free column writes
+  static_assert(G * M == NTT2_TILE && (1 << LG) == G, "tile shape");
+  const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
+  const int item = unit / job.nsub, sub = unit - item * job.nsub;
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << LOGN);
+  const ModTab &Md = job.mods[job.sub_mod[sub]];
+  const u64 q = Md.q, q2 = 2 * q;
+  const int tid = threadIdx.x;
+  u64 *data = sm2;
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm2 + ((G * PADM + 1) & ~1));
+  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(FWD ? Md.tw : Md.itw);
+  const int first = tile * G;
+  // element e = tid + i*T of the tile -> (sub-NTT g, index k) and global word
+  auto gidx = [&](int e, int &g, int &k) -> u64 {
     if (PASS == 0) {
-      gg = e % G;
-      k = e / G;
-      gidx = ((u64)k << lb) + first + gg;
+      g = e & (G - 1);
+      k = e >> LG;
+      return ((u64)k << LB) + first + g;
     } else {
-      gg = e / M;
-      k = e - gg * M;
-      gidx = ((u64)(first + gg) << lm) + k;
+      g = e >> LM;
+      k = e & (M - 1);
+      return ((u64)first << LM) + e;
     }
-    u64 v = data[gg * padM + spad(k)];
-    if (last) {
-      if (FWD) {
-        v = v >= q2 ? v - q2 : v;
-        v = v >= q ? v - q : v;
-      } else {
-        v = mul_shoup(v, ni, nis, q);
+  };
+  const u64 *src = p;
+  const bool lift = job.src_base != nullptr;
+  u64 qs = 0;
+  if (lift) {
+    src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << LOGN);
+    qs = job.mods[job.src_mod[sub]].q;
+  }
+  u64 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    int g, k;
+    v[i] = __ldcs(src + gidx(tid + i * NTT2_T, g, k));
+  }
+  // stage twiddles while the tile loads are in flight
+  if (PASS == 0) {
+    for (int i = tid; i < M; i += NTT2_T) tws[i] = __ldg(gtw + i);
+  } else {
+#pragma unroll
+    for (int j = 0; j < NTT2_TILE / NTT2_T; j++) {
+      const int e = tid + j * NTT2_T, g = e >> LM, i = e & (M - 1);
+      if (i) {
+        const int sp = 31 - __clz(i), gi = i - (1 << sp);
+        tws[e] = __ldg(gtw + (1 << (LA + sp)) + ((first + g) << sp) + gi);
       }
     }
-    p[gidx] = v;
   }
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    int g, k;
+    gidx(tid + i * NTT2_T, g, k);
+    data[g * PADM + spad(k)] = lift ? centred_to(v[i], qs, q) : v[i];
+  }
+  __syncthreads();
+  {
+    const int g = tid / TPS, tl = tid & (TPS - 1);
+    ntt2_sub<LM, FWD>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, q, q2);
+  }
+  const bool last = FWD ? (PASS == 1) : (PASS == 0);
+  const u64 ni = Md.ninv, nis = Md.ninv_sh;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    int g, k;
+    const u64 w = gidx(tid + i * NTT2_T, g, k);
+    u64 x = data[g * PADM + spad(k)];
+    if (last) {
+      if (FWD) {
+        x = x >= q2 ? x - q2 : x;
+        x = x >= q ? x - q : x;
+      } else {
+        x = mul_shoup(x, ni, nis, q);
+      }
+    }
+    p[w] = x;
+  }
+}
+
+template <int LA, int LB>
+__host__ size_t ntt2_smem_bytes(int pass) {
+  const int M = 1 << (pass == 0 ? LA : LB), G = NTT2_TILE / M, PADM = M + (M >> 4) + 1;
+  return sizeof(u64) * (size_t)((G * PADM + 1) & ~1) + 16 * (size_t)(pass == 0 ? M : NTT2_TILE);
 }
 
 }  // namespace cgb
