@@ -248,6 +248,8 @@ class SlotContext:
 
     @staticmethod
     def w_add_plain(wave, vecs):
+        if hasattr(vecs, "build"):
+            vecs = vecs.build(vecs.keys)
         c = wave.ctxs[0]
         p = c.params.plain_modulus
         b = SlotContext._spend(wave.budgets, c.params.noise_costs.add_plain)
@@ -256,6 +258,8 @@ class SlotContext:
 
     @staticmethod
     def w_mult_plain(wave, vecs):
+        if hasattr(vecs, "build"):  # PlainBatch (symbolic rows)
+            vecs = vecs.build(vecs.keys)
         c = wave.ctxs[0]
         p = c.params.plain_modulus
         b = SlotContext._spend(wave.budgets, c.params.noise_costs.mult_plain)

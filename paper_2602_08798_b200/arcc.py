@@ -34,7 +34,7 @@ from enum import Enum
 
 import numpy as np
 
-from .backend import ParameterError
+from .backend import ParameterError, onehot_batch
 from .encodings import EncodingKind, PackedMatrix, next_pow2, tile_wave
 from .fixedpoint import FixedPointParams, attention_weights, causal_attention_weights, fp_truncate
 from .linear_kernels import fold_wave
@@ -62,11 +62,9 @@ class ScoreVector:
         return self.parts[0]
 
 
-def _onehots(n: int, slots) -> np.ndarray:
-    slots = np.asarray(slots, dtype=np.int64)
-    v = np.zeros((slots.size, n), dtype=np.int64)
-    v[np.arange(slots.size), slots] = 1
-    return v
+def _onehots(n: int, slots):
+    """One-hot plaintext masks as a symbolic batch (cached on the device by key)."""
+    return onehot_batch(n, slots)
 
 
 def _C(ctx):

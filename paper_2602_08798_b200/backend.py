@@ -46,7 +46,7 @@ from . import _native as nat
 
 __all__ = [
     "BackendParams", "Context", "DecryptionFailure", "GpuCiphertext", "GpuContext", "NoiseBudgetExhausted",
-    "NoiseCosts", "OpCounter", "ParameterError", "PlainVector", "SlotCiphertext", "Wave", "default_plain_modulus",
+    "NoiseCosts", "OpCounter", "ParameterError", "PlainVector", "SlotCiphertext", "PlainBatch", "Wave", "default_plain_modulus", "onehot_batch",
     "is_prime", "new_context", "ring_for",
 ]
 
@@ -344,6 +344,32 @@ class Wave:
         return out
 
 
+class PlainBatch:
+    """A batch of structured plaintext slot vectors named by hashable keys
+    (e.g. one-hot masks), so encoded plaintexts are found in the device
+    cache without building or hashing the vectors; ``build(keys)`` makes
+    the rows only on a cache miss."""
+
+    __slots__ = ("keys", "build")
+
+    def __init__(self, keys, build):
+        self.keys, self.build = list(keys), build
+
+    def __len__(self):
+        return len(self.keys)
+
+
+def onehot_batch(n: int, slots) -> PlainBatch:
+    slots = [int(j) for j in np.asarray(slots).reshape(-1)]
+
+    def build(ks):
+        v = np.zeros((len(ks), n), dtype=np.int64)
+        v[np.arange(len(ks)), [k[2] for k in ks]] = 1
+        return v
+
+    return PlainBatch([("onehot", n, j) for j in slots], build)
+
+
 # ----------------------------------------------------------------------------
 # the context
 # ----------------------------------------------------------------------------
@@ -616,9 +642,10 @@ class GpuContext:
         c0 = wave.ctxs[0]
         cost = getattr(c0.params.noise_costs, field_name)
         b = GpuContext._spend_all(wave.budgets, cost)
-        vecs = np.mod(np.asarray(vecs, dtype=np.int64), c0.params.plain_modulus)
-        if vecs.ndim == 1:
-            vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
+        if not isinstance(vecs, PlainBatch):
+            vecs = np.mod(np.asarray(vecs, dtype=np.int64), c0.params.plain_modulus)
+            if vecs.ndim == 1:
+                vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
         _, pts = c0._plaintexts(vecs, kind)
         blk, ids = c0._new(len(wave))
         fn = c0._ring.add_plain if kind == nat.CGB_PT_ADD else c0._ring.mult_plain
@@ -776,10 +803,15 @@ class _PtCache:
         self.lock = threading.Lock()
         self.tick = 0
 
-    def get(self, vecs: np.ndarray, kind: int):
-        vecs = np.ascontiguousarray(np.asarray(vecs, dtype=np.int64))
-        n = vecs.shape[0]
-        keys = [(kind, hashlib.blake2b(row.tobytes(), digest_size=16).digest()) for row in vecs]
+    def get(self, vecs, kind: int):
+        if isinstance(vecs, PlainBatch):
+            keys = [(kind,) + tuple(k) for k in vecs.keys]
+            build = vecs.build
+        else:
+            vecs = np.ascontiguousarray(np.asarray(vecs, dtype=np.int64))
+            keys = [(kind, hashlib.blake2b(row.tobytes(), digest_size=16).digest()) for row in vecs]
+            build = None
+        n = len(keys)
         out = np.empty(n, dtype=np.uint32)
         with self.lock:
             missing = []
@@ -797,7 +829,10 @@ class _PtCache:
                     uniq.setdefault(keys[i], []).append(i)
                 self._evict(len(uniq))
                 ids = self.ring.alloc_pt(len(uniq))
-                rows = np.stack([vecs[v[0]] for v in uniq.values()])
+                if build is not None:
+                    rows = build([k[1:] for k in uniq])
+                else:
+                    rows = np.stack([vecs[v[0]] for v in uniq.values()])
                 self.ring.encode_pt(rows, kind, ids)
                 for pid, (k, idxs) in zip(ids, uniq.items()):
                     self.tick += 1

@@ -25,7 +25,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .backend import ParameterError
+from .backend import ParameterError, PlainBatch
 from .encodings import Encoding, EncodingKind, PackedMatrix, block_capacity, load_matrix, save_matrix
 from .nonlinear import MpcChannel
 
@@ -45,6 +45,17 @@ def _chain_ids(ctxs, ops, start: dict) -> list:
         nxt[id(c)] += k
         out.append(nxt[id(c)] - 1)
     return out
+
+
+def _block_masks(n: int, pos, widths) -> PlainBatch:
+    """Append masks (ones on [pos, pos + d2)) as a symbolic plaintext batch."""
+    def build(keys):
+        v = np.zeros((len(keys), n), dtype=np.int64)
+        for i, (_, _, p0, w) in enumerate(keys):
+            v[i, p0: p0 + w] = 1
+        return v
+
+    return PlainBatch([("block", n, int(p0), int(w)) for p0, w in zip(pos, widths)], build)
 
 
 def _retag(handles, cids):
@@ -139,10 +150,7 @@ def append_token_heads(caches, ks, vs, ctxs) -> list:
         still = np.nonzero(pos == 0)[0]
         rot = C.w_rotate(w.take(moved), -pos[moved])
         w = type(w).concat([w.take(still), rot]).take(np.argsort(np.concatenate([still, moved])))
-    masks = np.zeros((len(toks), n), dtype=np.int64)
-    for i, (pp, h) in enumerate(zip(pos, np.repeat(np.arange(H), 2))):
-        masks[i, pp: pp + caches[h].d2] = 1
-    new = C.w_mult_plain(w, masks)
+    new = C.w_mult_plain(w, _block_masks(n, pos, [caches[h].d2 for h in np.repeat(np.arange(H), 2)]))
     # fresh blocks add onto encrypt(0); others onto the segment's last part
     fi = np.nonzero(fresh)[0]
     oi = np.nonzero(~fresh)[0]
