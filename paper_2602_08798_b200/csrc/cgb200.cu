@@ -284,7 +284,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 #define BYTES_modup (8.0 * (double)count * ((double)L * N + (double)L * LP * N))
 #define BYTES_ks_inner (8.0 * (double)count * LP * N * (L + 2.0) + 16.0 * L * (double)LP * N)
 #define BYTES_moddown_lift (8.0 * (double)count * (2.0 * N + 2.0 * L * N))
-#define BYTES_moddown_combine (8.0 * (double)count * 2.0 * L * N * (3 + (add0 ? 1 : 0) + (d_add1 ? 1 : 0)))
+#define BYTES_moddown_combine (8.0 * (double)count * 2.0 * L * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)))
 #define BYTES_lift_QB (8.0 * n * 4.0 * (L + nB) * (double)N)
 #define BYTES_tensor (8.0 * n * 7.0 * nt * (double)N)
 #define BYTES_scale_round (8.0 * n * 3.0 * (nt + L) * (double)N)
@@ -315,7 +315,10 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 template <int LA, int LB>
 static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
-  second.src_base = nullptr;  // the fused lift happens in the first pass only
+  second.src_base = nullptr;  // fused loads (lift / permutation) happen in the first pass only
+  second.src_items = nullptr;
+  second.galois = nullptr;
+  second.lift = 0;
   auto grid = [&](int lm) {
     int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
     return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
@@ -491,25 +494,76 @@ __global__ void k_modup(u64 *D, const u64 *xcoef /*[item][L][N]*/, const u64 *xi
   D[(u64)item * words + i] = v;
 }
 // acc[item][p][l][N] = sum_j D[j][l] * key[j][p][l]   (p = 0: b, 1: a)
-__global__ void k_ks_inner(u64 *acc, const u64 *D, const u64 *xin, const u64 *const *keys, const ModTab *mods, int L,
-                           int logN) {
-  int item = blockIdx.y;
-  u64 N = 1ull << logN, LP = L + 1;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
-  if (i >= LP * N) return;
-  int l = (int)(i >> logN);
-  const ModTab &M = mods[l];
-  const u64 *Di = D + (u64)item * L * LP * N;
-  const u64 *K = keys[item];
-  u64 s0 = 0, s1 = 0;
-  const u64 N1 = N - 1;
-  for (int j = 0; j < L; j++) {
-    u64 d = (l == j) ? xin[((u64)item * L + j) * N + (i & N1)] : Di[(u64)j * LP * N + i];
-    s0 = add_mod(s0, mul_mod(d, K[((u64)j * 2 + 0) * LP * N + i], M), M.q);
-    s1 = add_mod(s1, mul_mod(d, K[((u64)j * 2 + 1) * LP * N + i], M), M.q);
+// acc[item][p][l][N] = sum_j D[j][l] * key[j][p][l]  (p = 0: b, 1: a); the digit's own
+// limb comes from the NTT-form input.  Keys carry Shoup companions (key + kw)
+// and are held in registers while consecutive items share them (every item of
+// a doubling / folding wave does); lazy sums in [0, 2Lq) are reduced once.
+struct KsSrc {            // the polynomial to key-switch (NTT form over Q)
+  const u64 *base;        // contiguous items at base + item * stride
+  u64 stride;
+  u64 *const *items;      // or per-item pointers + word offset
+  u64 off;
+  const u64 *g;           // per-item Galois element: read word perm_g(k)
+};
+__device__ __forceinline__ u64 ks_src_word(const KsSrc &x, int item, int limb, u32 k, int logN) {
+  if (x.items) {
+    const u32 kk = x.g ? perm_g(k, x.g[item], logN) : k;
+    return x.items[item][x.off + ((u64)limb << logN) + kk];
   }
-  acc[((u64)item * 2 + 0) * LP * N + i] = s0;
-  acc[((u64)item * 2 + 1) * LP * N + i] = s1;
+  return x.base[(u64)item * x.stride + ((u64)limb << logN) + k];
+}
+template <int L>
+__global__ void k_ks_inner(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *keys, u64 kw,
+                           const ModTab *mods, int logN, int count, int per_block) {
+  constexpr int LP = L + 1;
+  const u64 N = 1ull << logN;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
+  if (i >= LP * N) return;
+  const int l = (int)(i >> logN);
+  const u64 q = mods[l].q;
+  const u64 jn = i & (N - 1);
+  const int it0 = blockIdx.y * per_block, it1 = min(count, it0 + per_block);
+  const u64 *kprev = nullptr;
+  u64 kv[2][L], ks[2][L];
+  for (int item = it0; item < it1; item++) {
+    const u64 *K = keys[item];
+    if (K != kprev) {
+#pragma unroll
+      for (int j = 0; j < L; j++)
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+          const u64 off = ((u64)j * 2 + p) * LP * N + i;
+          kv[p][j] = __ldg(K + off);
+          ks[p][j] = __ldg(K + kw + off);
+        }
+      kprev = K;
+    }
+    const u64 *Di = D + (u64)item * L * LP * N;
+    u64 s0 = 0, s1 = 0;
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+      const u64 d = (l == j) ? ks_src_word(xin, item, j, (u32)jn, logN) : Di[(u64)j * LP * N + i];
+      s0 += mul_shoup_lazy(d, kv[0][j], ks[0][j], q);
+      s1 += mul_shoup_lazy(d, kv[1][j], ks[1][j], q);
+      if ((j & 3) == 3 || j == L - 1) {  // keep lazy sums below 8q < 2^64
+        const u64 q4 = 4 * q, q2 = 2 * q;
+        s0 = s0 >= q4 ? s0 - q4 : s0;
+        s0 = s0 >= q2 ? s0 - q2 : s0;
+        s1 = s1 >= q4 ? s1 - q4 : s1;
+        s1 = s1 >= q2 ? s1 - q2 : s1;
+      }
+    }
+    acc[((u64)item * 2 + 0) * LP * N + i] = s0 >= q ? s0 - q : s0;
+    acc[((u64)item * 2 + 1) * LP * N + i] = s1 >= q ? s1 - q : s1;
+  }
+}
+// Shoup companions of a key: dst[i] = floor(src[i] * 2^64 / q_limb)
+__global__ void k_key_shoup(u64 *dst, const u64 *src, const ModTab *mods, int L, int iP, int logN, u64 words) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  int l = (int)((i >> logN) % (L + 1));
+  u64 q = mods[l == L ? iP : l].q;
+  dst[i] = (u64)((((unsigned __int128)src[i]) << 64) / q);
 }
 // ModDown lift: W[item][p][l][N] = centred(acc[item][p][L] (coeff, mod P)) mod q_l
 __global__ void k_moddown_lift(u64 *W, const u64 *acc, const ModTab *mods, int L, int iP, int logN) {
@@ -522,8 +576,9 @@ __global__ void k_moddown_lift(u64 *W, const u64 *acc, const ModTab *mods, int L
   u64 v = acc[(((u64)item * 2 + p) * LP + L) * N + jn];
   W[(u64)item * words + i] = centred_to(v, mods[iP].q, mods[l].q);
 }
-// out[p][l] = (acc[p][l] - W[p][l]) * P^-1 + add0 (poly 0 only) + add1 (both polys)
-__global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W, const u64 *add0 /*[item][2][L][N] or null*/,
+// out[p][l] = (acc[p][l] - W[p][l]) * P^-1 + add0 (poly 0 only, optionally read through the
+// automorphism) + add1 (both polys)
+__global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W, KsSrc add0,
                                   const u64 *const *add1, const ModTab *mods, const Consts *C, int L, int logN) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, LP = L + 1, words = 2ull * L * N;
@@ -534,7 +589,7 @@ __global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W,
   u64 q = mods[l].q;
   u64 a = acc[(((u64)item * 2 + p) * LP + l) * N + jn];
   u64 v = mul_shoup(sub_mod(a, W[(u64)item * words + i], q), C->Pinvq[l], C->Pinvq_sh[l], q);
-  if (add0 && p == 0) v = add_mod(v, add0[(u64)item * words + i], q);
+  if (p == 0 && (add0.items || add0.base)) v = add_mod(v, ks_src_word(add0, item, l, (u32)jn, logN), q);
   if (add1) v = add_mod(v, add1[item][i], q);
   out[item][i] = v;
 }
@@ -844,26 +899,40 @@ static void encode_slots(cgb_ring *r, Scratch &S, const u64 *slots_host, int cou
 
 static u64 *get_key(cgb_ring *r, u64 g);
 
-// key switch of `count` NTT-form polys x[item][L][N] (contiguous) with per-item keys;
-// result combined into out pointers: out = (ks0 + add0_p0 + add1, ks1 + add1)
-static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *const *d_keys, u64 *const *d_out,
-                      const u64 *add0, const u64 *const *d_add1) {
+// key switch of `count` NTT-form polys (descriptor x: contiguous, or arena items read
+// through an automorphism) with per-item keys; result combined into out pointers:
+// out = (ks0 + add0 + add1, ks1 + add1)
+static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
+                      const KsSrc &add0, const u64 *const *d_add1) {
   const int L = r->L, N = r->N, LP = L + 1, logN = r->logN;
-  std::vector<int> qm;
-  q_mod_idx(r, qm);
-  // digits in coefficient form
+  // digits in coefficient form (automorphism fused into the inverse NTT's load)
   u64 *xc = S.alloc<u64>((size_t)count * L * N);
-  CK(cudaMemcpyAsync(xc, x, sizeof(u64) * (size_t)count * L * N, cudaMemcpyDeviceToDevice, r->stream));
-  ntt_items(r, false, xc, nullptr, (u64)L * N, count, 1, L, qm.data());
+  {
+    NttJob job{};
+    job.base = xc;
+    job.item_stride = (u64)L * N;
+    job.src_items = x.items;
+    job.src_base = x.items ? nullptr : x.base;
+    job.src_stride = x.stride;
+    job.galois = x.g;
+    const int off = (int)(x.items ? x.off / (u64)N : 0);
+    for (int l = 0; l < L; l++) {
+      job.sub_off[l] = (unsigned short)l;
+      job.sub_mod[l] = (unsigned char)l;
+      job.src_off[l] = (unsigned short)(off + l);
+    }
+    job.nsub = L;
+    launch_ntt(r, false, job, count);
+  }
   // ModUp: digit j centre-lifted into every other limb of Q u P, fused into the NTT load
   u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
-  u64 wD = (u64)L * LP * N;
   {
     NttJob job{};
     job.base = D;
-    job.item_stride = wD;
+    job.item_stride = (u64)L * LP * N;
     job.src_base = xc;
     job.src_stride = (u64)L * N;
+    job.lift = 1;
     int n = 0;
     for (int j = 0; j < L; j++)
       for (int l = 0; l < LP; l++) {
@@ -879,21 +948,31 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
   }
   // inner product with the evaluation key
   u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
-  LAUNCH("ks_inner", BYTES_ks_inner, k_ks_inner<<<dim3(GRID1((u64)LP * N, TPB).x, count), TPB, 0, r->stream>>>(acc, D, x, d_keys, r->d_mods, L, logN));
-  // ModDown
   {
-    int mP = r->iP;
+    const int per_block = 16;
+    const dim3 grid(GRID1((u64)LP * N, TPB).x, (count + per_block - 1) / per_block);
+    const u64 kw = (u64)L * 2 * LP * N;
+    launch_begin(r);
+    switch (L) {
+#define KSI(LL) case LL: k_ks_inner<LL><<<grid, TPB, 0, r->stream>>>(acc, D, x, d_keys, kw, r->d_mods, logN, count, per_block); break;
+      KSI(1) KSI(2) KSI(3) KSI(4) KSI(5) KSI(6) KSI(7) KSI(8) KSI(9) KSI(10) KSI(11) KSI(12) KSI(13) KSI(14) KSI(15) KSI(16)
+#undef KSI
+      default: FAIL(CGB_ERR_PARAM, "unsupported limb count %d", L);
+    }
+    launch_end(r, "ks_inner", BYTES_ks_inner);
+  }
+  // ModDown: INTT the P limbs, centre-lift into Q (fused into the NTT load)
+  {
     NttJob job{};
     job.base = acc;
     job.item_stride = 2ull * LP * N;
     job.sub_off[0] = (unsigned short)L;
-    job.sub_mod[0] = (unsigned char)mP;
+    job.sub_mod[0] = (unsigned char)r->iP;
     job.sub_off[1] = (unsigned short)(LP + L);
-    job.sub_mod[1] = (unsigned char)mP;
+    job.sub_mod[1] = (unsigned char)r->iP;
     job.nsub = 2;
     launch_ntt(r, false, job, count);
   }
-  // ModDown: centre-lift the P limb into Q, fused into the NTT load
   u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
   {
     NttJob job{};
@@ -901,6 +980,7 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
     job.item_stride = 2ull * L * N;
     job.src_base = acc;
     job.src_stride = 2ull * LP * N;
+    job.lift = 1;
     int n = 0;
     for (int pp = 0; pp < 2; pp++)
       for (int l = 0; l < L; l++) {
@@ -913,8 +993,9 @@ static void keyswitch(cgb_ring *r, Scratch &S, const u64 *x, int count, u64 *con
     job.nsub = n;
     launch_ntt(r, true, job, count);
   }
-  LAUNCH("moddown_combine", BYTES_moddown_combine, k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
-      d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
+  LAUNCH("moddown_combine", BYTES_moddown_combine,
+         k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
+             d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
 }
 
 static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
@@ -964,13 +1045,10 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
     std::vector<u64 *> src = ct_ptrs(r, n, ia.data()), dst = ct_ptrs(r, n, io.data());
     u64 **d_src = S.up(src.data(), n), **d_dst = S.up(dst.data(), n), **d_keys = S.up(keys.data(), n);
     u64 *d_g = S.up(g.data(), n);
-    u64 *A = S.alloc<u64>((size_t)n * ctw);
-    LAUNCH("automorph", BYTES_automorph, k_automorph<<<dim3(GRID1(ctw, TPB).x, n), TPB, 0, r->stream>>>(A, (const u64 *const *)d_src, d_g, L, r->logN));
-    // c1' contiguous for the key switch
-    u64 *x = S.alloc<u64>((size_t)n * L * N);
-    CK(cudaMemcpy2DAsync(x, sizeof(u64) * L * N, A + (size_t)L * N, sizeof(u64) * ctw, sizeof(u64) * L * N, n,
-                         cudaMemcpyDeviceToDevice, r->stream));
-    keyswitch(r, S, x, n, d_keys, d_dst, A, add_input ? (const u64 *const *)d_src : nullptr);
+    // c1' = sigma_g(c1) is read through the automorphism by the key switch; c0' by its epilogue
+    KsSrc xin{nullptr, 0, d_src, (u64)L * N, d_g};
+    KsSrc c0p{nullptr, 0, d_src, 0, d_g};
+    keyswitch(r, S, xin, n, d_keys, d_dst, c0p, add_input ? (const u64 *const *)d_src : nullptr);
   }
 }
 
@@ -997,7 +1075,7 @@ static u64 *get_key(cgb_ring *r, u64 g) {
   const int L = r->L, LP = L + 1, N = r->N;
   const u64 LPN = (u64)LP * N;
   u64 *key;
-  CK(cudaMalloc((void **)&key, sizeof(u64) * (size_t)L * 2 * LPN));
+  CK(cudaMalloc((void **)&key, 2 * sizeof(u64) * (size_t)L * 2 * LPN));  // values | Shoup companions
   Scratch S(r);
   std::vector<int> mi(LP);
   for (int l = 0; l < L; l++) mi[l] = l;
@@ -1022,6 +1100,10 @@ static u64 *get_key(cgb_ring *r, u64 g) {
     LAUNCH("ksk_b", BYTES_ksk_b, k_ksk_b<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, e, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
     ntt_items(r, true, key + ((u64)j * 2 + 0) * LPN, nullptr, 0, 1, 1, LP, mi.data());
     LAUNCH("ksk_fin", BYTES_ksk_fin, k_ksk_fin<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
+  }
+  {
+    const u64 words = (u64)L * 2 * LPN;
+    LAUNCH("keygen", 0, k_key_shoup<<<GRID1(words, TPB), TPB, 0, r->stream>>>(key + words, key, r->d_mods, L, r->iP, r->logN, words));
   }
   r->keys[g] = key;
   return key;
@@ -1740,7 +1822,9 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     std::vector<u64 *> d01p(n);
     for (int i = 0; i < n; i++) d01p[i] = d01 + (size_t)i * 2 * L * N;
     u64 **dd01 = S.up(d01p.data(), n);
-    keyswitch(r, S, x, n, dk, dout, nullptr, (const u64 *const *)dd01);
+    KsSrc xin{x, (u64)L * N, nullptr, 0, nullptr};
+    KsSrc none{nullptr, 0, nullptr, 0, nullptr};
+    keyswitch(r, S, xin, n, dk, dout, none, (const u64 *const *)dd01);
   }
   API_END
 }

@@ -121,6 +121,9 @@ struct NttJob {
   u64 item_stride;           // words
   const u64 *src_base;       // fused-load source items (null: in place)
   u64 src_stride;
+  u64 *const *src_items;     // or per-item source pointers
+  const u64 *galois;         // per-item Galois element: load src[perm_g(k)] (evaluation-domain automorphism)
+  int lift;                  // centre-lift from src_mod on load
   const ModTab *mods;
   int logN;
   int nsub;                                // (poly, limb) units per item
@@ -131,6 +134,19 @@ struct NttJob {
 };
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+
+// evaluation-domain automorphism X -> X^g: output word k reads input word perm_g(k)
+__device__ __forceinline__ u32 perm_g(u32 k, u64 g, int logN) {
+  const u32 e = 2u * (__brev(k) >> (32 - logN)) + 1u;
+  const u32 se = (u32)((e * g) & ((2ull << logN) - 1));
+  return __brev((se - 1) >> 1) >> (32 - logN);
+}
+// source pointer of unit `sub` of `item` for a fused load (null: in place)
+__device__ __forceinline__ const u64 *job_src(const NttJob &job, int item, int sub, int logN) {
+  if (job.src_items) return job.src_items[item] + ((u64)job.src_off[sub] << logN);
+  if (job.src_base) return job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << logN);
+  return nullptr;
+}
 
 // lazy Shoup: a * w mod q in [0, 2q) for any a < 2^64
 __device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
@@ -201,12 +217,15 @@ __global__ void __launch_bounds__(512) k_ntt(NttJob job) {
   const ModTab &M = job.mods[job.sub_mod[sub]];
   const u64 q = M.q, q2 = 2 * q;
   const int logN = job.logN, N = 1 << logN, tid = threadIdx.x, T = blockDim.x;
-  if (job.src_base) {  // fused centred lift from the source modulus
-    const u64 *src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << logN);
-    const u64 qs = job.mods[job.src_mod[sub]].q;
-    for (int i = tid; i < N; i += T) sm[spad(i)] = centred_to(src[i], qs, q);
-  } else {
-    for (int i = tid; i < N; i += T) sm[spad(i)] = p[i];
+  {
+    const u64 *src = job_src(job, item, sub, logN);
+    if (!src) src = p;
+    const u64 qs = job.lift ? job.mods[job.src_mod[sub]].q : 0;
+    const u64 g = job.galois ? job.galois[item] : 1;
+    for (int i = tid; i < N; i += T) {
+      u64 v = src[g == 1 ? i : perm_g(i, g, logN)];
+      sm[spad(i)] = job.lift ? centred_to(v, qs, q) : v;
+    }
   }
   __syncthreads();
   const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(FWD ? M.tw : M.itw);
@@ -344,18 +363,24 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
       return ((u64)first << LM) + e;
     }
   };
-  const u64 *src = p;
-  const bool lift = job.src_base != nullptr;
-  u64 qs = 0;
-  if (lift) {
-    src = job.src_base + (u64)item * job.src_stride + ((u64)job.src_off[sub] << LOGN);
-    qs = job.mods[job.src_mod[sub]].q;
-  }
+  const u64 *src = job_src(job, item, sub, LOGN);
+  if (!src) src = p;
+  const bool lift = job.lift != 0;
+  const u64 qs = lift ? job.mods[job.src_mod[sub]].q : 0;
+  const u64 gal = job.galois ? job.galois[item] : 1;
   u64 v[8];
+  if (gal == 1) {
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
-    int g, k;
-    v[i] = __ldcs(src + gidx(tid + i * NTT2_T, g, k));
+    for (int i = 0; i < 8; i++) {
+      int g, k;
+      v[i] = __ldcs(src + gidx(tid + i * NTT2_T, g, k));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      int g, k;
+      v[i] = __ldg(src + perm_g((u32)gidx(tid + i * NTT2_T, g, k), gal, LOGN));
+    }
   }
   // stage twiddles while the tile loads are in flight
   if (PASS == 0) {
