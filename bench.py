@@ -65,7 +65,8 @@ def metric_name(L):
 def workload(args):
     return {"workload": f"decode_attention_{args.heads}h_L{args.L}", "heads": args.heads, "d_head": D2,
             "n_slots": N_SLOTS, "plain_modulus": P, "cached_len": args.L, "steps_appended": 1,
-            "ring": "RNS-BFV N=16384, Q=4x60b, P=61b, dnum=4", "l2": "working set >1.5 GB per step (> 126 MB L2)"}
+            "ring": "RNS-BFV N=16384, Q=%dx60b, P=61b, dnum=L" % __import__("paper_2602_08798_b200.backend",
+                                                                         fromlist=["x"]).default_limbs(16384), "l2": "working set >1.5 GB per step (> 126 MB L2)"}
 
 
 # ----------------------------------------------------------------------------

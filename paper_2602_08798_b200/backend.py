@@ -213,12 +213,20 @@ _rings_lock = threading.Lock()
 
 
 def default_limbs(ring_degree: int) -> int:
-    """Q limbs of 60 bits: 4 (240 bits) at production sizes -- the paper's
-    q ~ 2^220 class -- and 8 for toy rings, whose composite two-row
-    rotations spend more real noise per logical op."""
+    """Q limbs of 60 bits.
+
+    N >= 16384 (the production n = 8192 ring): 3 limbs, Q = 180 bits.  The
+    deepest intermediates of the hot path (decode scores/values after one-hot
+    mult_plain + 14 rotations + mult_cipher + 64-term sums; prefill P.V
+    columns) keep >= 60 bits of real noise budget (profiles/r01/
+    noise_probe.jsonl; tests/test_gpu_hotpath.py asserts >= 40).  Smaller
+    production-size rings get 4 limbs, toy rings 8 (their composite two-row
+    rotations spend more real noise per logical op).  CGB_LIMBS overrides."""
     env = os.environ.get("CGB_LIMBS")
     if env:
         return int(env)
+    if ring_degree >= 16384:
+        return 3
     return 4 if ring_degree >= 2048 else 8
 
 

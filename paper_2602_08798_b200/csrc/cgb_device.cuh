@@ -67,6 +67,7 @@ __device__ __forceinline__ u64 reduce4(u64 v, u64 q) {
 }
 // residue in limb q of the centred representative of v in [0, qs)
 __device__ __forceinline__ u64 centred_to(u64 v, u64 qs, u64 q) {
+  if (q > (qs >> 1)) return v > (qs >> 1) ? v + (q - qs) : v;  // both halves already in [0, q)
   if (v <= (qs >> 1)) return reduce4(v, q);
   u64 n = reduce4(qs - v, q);
   return n ? q - n : 0;
@@ -267,13 +268,18 @@ template <int LM, int S0, int RP, bool FWD>
 __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
   constexpr int K = 1 << RP, R = 8 / K;
   constexpr int S = (1 << LM) >> S0, ST = S >> RP;
+  // word k of a row sits at spad(base) + off(k) with a compile-time off(k) when
+  // the stride is a multiple of 16 or the row lies inside one 16-word block
+  constexpr bool CONST_OFF = (ST % 16 == 0) || (S <= 16);
 #pragma unroll
   for (int u = 0; u < R; u++) {
     const int row = tl * R + u;
     const int blk = row / ST, base = blk * S + (row & (ST - 1));
+    const int pb = spad(base);
+    auto addr = [&](int k) { return CONST_OFF ? pb + k * ST + ((ST % 16 == 0) ? (k * ST) >> 4 : 0) : spad(base + k * ST); };
     u64 x[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) x[k] = sub[spad(base + k * ST)];
+    for (int k = 0; k < K; k++) x[k] = sub[addr(k)];
 #pragma unroll
     for (int ll = 0; ll < RP; ll++) {
       const int l = FWD ? ll : RP - 1 - ll;
@@ -298,7 +304,7 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
       }
     }
 #pragma unroll
-    for (int k = 0; k < K; k++) sub[spad(base + k * ST)] = x[k];
+    for (int k = 0; k < K; k++) sub[addr(k)] = x[k];
   }
 }
 

@@ -44,6 +44,18 @@ def test_full_size_decode(api, name):
     assert ctx.noise_budget_bits(out) > 20
 
 
+def test_hot_path_noise_margins(api):
+    """Deepest intermediates of decode and prefill keep >= 40 bits of real noise."""
+    import json
+    import subprocess
+
+    res = subprocess.run([sys.executable, str(Path(__file__).resolve().parent.parent / "scripts" / "noise_probe.py")],
+                         capture_output=True, text=True, check=True)
+    probe = json.loads(res.stdout.strip().splitlines()[-1])
+    for k in ("decode_scores", "decode_values", "prefill_diag", "prefill_pv"):
+        assert probe[k] >= 40, (k, probe)
+
+
 def test_full_size_prefill(api):
     fn, kw = harness.FULL["full_prefill_m128"]
     rec, _ = fn(api, gpu_ctx, **kw)
