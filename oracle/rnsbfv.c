@@ -18,7 +18,7 @@
  * GPU library must reproduce every ciphertext word of it bit-exactly.
  *
  *   ring      R = Z[X]/(X^N + 1), N = 2*n_slots (one-row layout) or n_slots
- *   Q         L primes < 2^60, = 1 mod 2N (largest first)
+ *   Q         L primes < 2^60, = 1 mod 2^32 (so = 1 mod 2N), largest first
  *   P         one special prime < 2^61 (hybrid key switching, dnum = L)
  *   B         L+1 auxiliary primes < 2^61 (BFV tensor base, HPS-style)
  *   slots     slot i <-> evaluation at psi_t^(5^i) (row 0 of the hypercube)
@@ -219,9 +219,11 @@ static void make_tables(int N, int logN, u64 q, u64 **tw, u64 **itw, u64 *ninv) 
     *ninv = invmod((u64)N % q, q);
 }
 
-/* largest primes below 2^bits, = 1 mod 2N, skipping ones already taken */
+/* largest primes below 2^bits with q = 1 mod 2^32 (hence mod 2N), skipping ones
+ * already taken; the low word 1 makes q-hat * q one 32-bit multiply on the GPU */
 static int take_primes(ora_ctx *c, int bits, int count, int at) {
-    u64 step = 2 * (u64)c->N, top = 1ull << bits;
+    u64 step = 1ull << 32, top = 1ull << bits;
+    if (2 * (u64)c->N > step) step = 2 * (u64)c->N;
     u64 cand = top - (top % step) + 1;
     if (cand >= top) cand -= step;
     int got = 0;

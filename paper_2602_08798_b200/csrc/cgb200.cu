@@ -312,7 +312,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 #define GRID1(n, b) dim3((unsigned)(((n) + (b)-1) / (b)))
 
 // NTT launcher -------------------------------------------------------------
-template <int LA, int LB>
+template <int LA, int LB, bool QS>
 static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
   second.src_base = nullptr;  // fused loads (lift / permutation) happen in the first pass only
@@ -325,20 +325,20 @@ static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   };
   const size_t s0 = ntt2_smem_bytes<LA, LB>(0), s1 = ntt2_smem_bytes<LA, LB>(1);
   if (fwd) {
-    k_ntt2<LA, LB, true, 0><<<grid(LA), NTT2_T, s0, r->stream>>>(job);
-    k_ntt2<LA, LB, true, 1><<<grid(LB), NTT2_T, s1, r->stream>>>(second);
+    k_ntt2<LA, LB, true, 0, QS><<<grid(LA), NTT2_T, s0, r->stream>>>(job);
+    k_ntt2<LA, LB, true, 1, QS><<<grid(LB), NTT2_T, s1, r->stream>>>(second);
   } else {
-    k_ntt2<LA, LB, false, 1><<<grid(LB), NTT2_T, s1, r->stream>>>(job);
-    k_ntt2<LA, LB, false, 0><<<grid(LA), NTT2_T, s0, r->stream>>>(second);
+    k_ntt2<LA, LB, false, 1, QS><<<grid(LB), NTT2_T, s1, r->stream>>>(job);
+    k_ntt2<LA, LB, false, 0, QS><<<grid(LA), NTT2_T, s0, r->stream>>>(second);
   }
 }
 template <int LA, int LB>
 static void ntt2_attrs() {
   const int s = (int)std::max(ntt2_smem_bytes<LA, LB>(0), ntt2_smem_bytes<LA, LB>(1));
-  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
-  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
-  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
-  CK(cudaFuncSetAttribute(k_ntt2<LA, LB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+#define NTT2A(F, P, Q) CK(cudaFuncSetAttribute(k_ntt2<LA, LB, F, P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  NTT2A(true, 0, true) NTT2A(true, 1, true) NTT2A(false, 0, true) NTT2A(false, 1, true)
+  NTT2A(true, 0, false) NTT2A(true, 1, false) NTT2A(false, 0, false) NTT2A(false, 1, false)
+#undef NTT2A
 }
 static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   if (count <= 0 || job.nsub <= 0) return;
@@ -347,13 +347,17 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   const double bytes = 16.0 * (double)count * job.nsub * r->N;
   if (r->logN >= 12) {  // two passes over 2048-word tiles, twiddles staged in shared memory
     launch_begin(r);
+    bool qs = true;  // every unit's modulus = 1 mod 2^32 (all but the plaintext modulus)
+    for (int u = 0; u < job.nsub; u++) qs = qs && job.sub_mod[u] != r->iT;
+#define LN2(A, B) (qs ? launch_ntt2<A, B, true>(r, fwd, job, count) : launch_ntt2<A, B, false>(r, fwd, job, count))
     switch (r->logN) {
-      case 12: launch_ntt2<6, 6>(r, fwd, job, count); break;
-      case 13: launch_ntt2<6, 7>(r, fwd, job, count); break;
-      case 14: launch_ntt2<7, 7>(r, fwd, job, count); break;
-      case 15: launch_ntt2<7, 8>(r, fwd, job, count); break;
-      default: launch_ntt2<8, 8>(r, fwd, job, count); break;
+      case 12: LN2(6, 6); break;
+      case 13: LN2(6, 7); break;
+      case 14: LN2(7, 7); break;
+      case 15: LN2(7, 8); break;
+      default: LN2(8, 8); break;
     }
+#undef LN2
     r->launches++;  // two kernels per transform (launch_end counts the other)
     launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes);
     return;
@@ -361,10 +365,17 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   int E = r->ntt_E(), T = r->ntt_threads();
   size_t smem = r->ntt_smem();
   dim3 grid((unsigned)(count * job.nsub));
-#define LNTT(EE)                                                     \
-  do {                                                               \
-    if (fwd) k_ntt<EE, true><<<grid, T, smem, r->stream>>>(job);     \
-    else k_ntt<EE, false><<<grid, T, smem, r->stream>>>(job);        \
+  bool qs = true;
+  for (int u = 0; u < job.nsub; u++) qs = qs && job.sub_mod[u] != r->iT;
+#define LNTT(EE)                                                                        \
+  do {                                                                                  \
+    if (qs) {                                                                           \
+      if (fwd) k_ntt<EE, true, true><<<grid, T, smem, r->stream>>>(job);                \
+      else k_ntt<EE, false, true><<<grid, T, smem, r->stream>>>(job);                   \
+    } else {                                                                            \
+      if (fwd) k_ntt<EE, true, false><<<grid, T, smem, r->stream>>>(job);               \
+      else k_ntt<EE, false, false><<<grid, T, smem, r->stream>>>(job);                  \
+    }                                                                                   \
   } while (0)
   launch_begin(r);
   switch (E) {
@@ -1112,8 +1123,10 @@ static u64 *get_key(cgb_ring *r, u64 g) {
 // ============================================================================
 // ring construction
 // ============================================================================
+// largest primes below 2^bits with q = 1 mod 2^32 (hence mod 2N): the low word 1
+// turns q-hat * q into one 32-bit multiply in every Shoup / Barrett reduction
 static void take_primes(cgb_ring *r, int bits, int count) {
-  u64 step = 2ull * r->N, top = 1ull << bits;
+  u64 step = std::max<u64>(1ull << 32, 2ull * r->N), top = 1ull << bits;
   u64 c = top - (top % step) + 1;
   if (c >= top) c -= step;
   int got = 0;
@@ -1156,10 +1169,12 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
   r->iP = L;
   r->iB0 = L + 1;
   r->iT = L + 1 + nB;
+  for (u64 m : r->mods)
+    if ((m & 0xffffffffull) != 1) FAIL(CGB_ERR_STATE, "modulus %llu is not 1 mod 2^32", (unsigned long long)m);
   r->mods.push_back(r->t);
   r->nmod = (int)r->mods.size();
   // twiddle tables
-  size_t per = 4ull * N;
+  size_t per = 8ull * N;  // tw | itw | row-tile ordered tw1 | itw1 : N (w, w') pairs = 2N words each
   CK(cudaMalloc((void **)&r->d_tables, sizeof(u64) * per * r->nmod));
   std::vector<u64> tab(per);
   r->h_mods.resize(r->nmod);
@@ -1173,6 +1188,22 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
       tab[2 * k + 1] = h_shoup(w, q);
       tab[2 * N + 2 * k] = wi;
       tab[2 * N + 2 * k + 1] = h_shoup(wi, q);
+    }
+    // two-pass row-tile order: entry blk*M + i (i = 2^sp + g) = pair 2^(a+sp) + blk 2^sp + g
+    if (logN >= 12) {
+      const int a = logN / 2, b = logN - a, M = 1 << b;
+      for (int blk = 0; blk < (1 << a); blk++)
+        for (int ii = 0; ii < M; ii++) {
+          size_t dst = (size_t)blk * M + ii, src = 0;
+          if (ii) {
+            int sp = 31 - __builtin_clz((unsigned)ii), gi = ii - (1 << sp);
+            src = ((size_t)1 << (a + sp)) + ((size_t)blk << sp) + gi;
+          }
+          tab[4 * N + 2 * dst] = tab[2 * src];
+          tab[4 * N + 2 * dst + 1] = tab[2 * src + 1];
+          tab[6 * N + 2 * dst] = tab[2 * N + 2 * src];
+          tab[6 * N + 2 * dst + 1] = tab[2 * N + 2 * src + 1];
+        }
     }
     u64 *dt = r->d_tables + per * i;
     CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
@@ -1188,6 +1219,8 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.tw_sh = nullptr;
     M.itw = dt + 2 * N;
     M.itw_sh = nullptr;
+    M.tw1 = dt + 4 * N;
+    M.itw1 = dt + 6 * N;
   }
   CK(cudaMalloc((void **)&r->d_mods, sizeof(ModTab) * r->nmod));
   CK(cudaMemcpy(r->d_mods, r->h_mods.data(), sizeof(ModTab) * r->nmod, cudaMemcpyHostToDevice));
@@ -1321,8 +1354,10 @@ int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     size_t smem = sizeof(u64) * (size_t)(N + (N >> 4) + 1);
 #define SETSMEM(EE)                                                                                           \
-  CK(cudaFuncSetAttribute(k_ntt<EE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));        \
-  CK(cudaFuncSetAttribute(k_ntt<EE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_ntt<EE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+  CK(cudaFuncSetAttribute(k_ntt<EE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  CK(cudaFuncSetAttribute(k_ntt<EE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+  CK(cudaFuncSetAttribute(k_ntt<EE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
 #undef SETSMEM
     switch (log_n) {

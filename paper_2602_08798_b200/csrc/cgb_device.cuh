@@ -24,6 +24,7 @@ struct ModTab {
   u64 r64;      // 2^64 mod q
   u64 ninv, ninv_sh;
   const u64 *tw, *tw_sh, *itw, *itw_sh;  // bit-reversed psi powers + Shoup companions
+  const u64 *tw1, *itw1;                 // the same pairs in two-pass row-tile order (see k_ntt2)
   int bits;
   int pad_;
 };
@@ -37,10 +38,18 @@ __device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) {
 }
 __device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 
+// x * q mod 2^64.  QS: q = k 2^32 + 1 (every ciphertext modulus of this
+// backend) -> one 32-bit multiply; the plaintext modulus t takes the generic path.
+template <bool QS = true>
+__device__ __forceinline__ u64 mul_q(u64 x, u64 q) {
+  if (QS) return x + ((u64)((u32)x * (u32)(q >> 32)) << 32);
+  return x * q;
+}
 // a * w mod q with w' = floor(w 2^64 / q); any a < 2^64, result in [0, q)
+template <bool QS = true>
 __device__ __forceinline__ u64 mul_shoup(u64 a, u64 w, u64 wsh, u64 q) {
   u64 hi = __umul64hi(a, wsh);
-  u64 r = a * w - hi * q;
+  u64 r = a * w - mul_q<QS>(hi, q);
   return r >= q ? r - q : r;
 }
 
@@ -51,7 +60,7 @@ __device__ __forceinline__ u64 mul_mod(u64 a, u64 b, u64 q, u64 mu, int bits) {
   u64 xs = (hi << (64 - s)) | (lo >> s);
   u64 ph = __umul64hi(xs, mu), pl = xs * mu;
   u64 qh = (ph << (64 - s2)) | (pl >> s2);
-  u64 r = lo - qh * q;
+  u64 r = lo - mul_q(qh, q);
   if (r >= q) r -= q;
   if (r >= q) r -= q;
   return r;
@@ -150,11 +159,12 @@ __device__ __forceinline__ const u64 *job_src(const NttJob &job, int item, int s
 }
 
 // lazy Shoup: a * w mod q in [0, 2q) for any a < 2^64
+template <bool QS = true>
 __device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
-  return a * w - __umul64hi(a, wsh) * q;
+  return a * w - mul_q<QS>(__umul64hi(a, wsh), q);
 }
 
-template <int E, int RP, bool FWD>
+template <int E, int RP, bool FWD, bool QS>
 __device__ __forceinline__ void ntt_phase(u64 *sm, int s0, int logN, int tid, u64 q, u64 q2,
                                           const ulonglong2 *__restrict__ tw) {
   constexpr int K = 1 << RP;   // words per row
@@ -180,14 +190,14 @@ __device__ __forceinline__ void ntt_phase(u64 *sm, int s0, int logN, int tid, u6
         u64 &X = x[k], &Y = x[k + half];
         if (FWD) {
           u64 a = X >= q2 ? X - q2 : X;
-          u64 t = mul_shoup_lazy(Y, W.x, W.y, q);
+          u64 t = mul_shoup_lazy<QS>(Y, W.x, W.y, q);
           X = a + t;
           Y = a - t + q2;
         } else {
           u64 a = X + Y;
           u64 d = X - Y + q2;
           X = a >= q2 ? a - q2 : a;
-          Y = mul_shoup_lazy(d, W.x, W.y, q);
+          Y = mul_shoup_lazy<QS>(d, W.x, W.y, q);
         }
       }
     }
@@ -196,20 +206,20 @@ __device__ __forceinline__ void ntt_phase(u64 *sm, int s0, int logN, int tid, u6
   }
 }
 
-template <int E, bool FWD>
+template <int E, bool FWD, bool QS>
 __device__ __forceinline__ void ntt_phase_dispatch(int rp, u64 *sm, int s0, int logN, int tid, u64 q, u64 q2,
                                                    const ulonglong2 *tw) {
   switch (rp) {
-    case 4: if constexpr (E >= 16) { ntt_phase<E, 4, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
-    case 3: if constexpr (E >= 8) { ntt_phase<E, 3, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
-    case 2: if constexpr (E >= 4) { ntt_phase<E, 2, FWD>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    case 4: if constexpr (E >= 16) { ntt_phase<E, 4, FWD, QS>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    case 3: if constexpr (E >= 8) { ntt_phase<E, 3, FWD, QS>(sm, s0, logN, tid, q, q2, tw); return; } break;
+    case 2: if constexpr (E >= 4) { ntt_phase<E, 2, FWD, QS>(sm, s0, logN, tid, q, q2, tw); return; } break;
     default: break;
   }
-  ntt_phase<E, 1, FWD>(sm, s0, logN, tid, q, q2, tw);
+  ntt_phase<E, 1, FWD, QS>(sm, s0, logN, tid, q, q2, tw);
 }
 
 // E words per thread; phases of RMAX = min(4, log2 E) stages
-template <int E, bool FWD>
+template <int E, bool FWD, bool QS>
 __global__ void __launch_bounds__(512) k_ntt(NttJob job) {
   extern __shared__ u64 sm[];
   constexpr int RMAX = (E >= 16) ? 4 : (E == 8) ? 3 : (E == 4) ? 2 : 1;
@@ -234,7 +244,7 @@ __global__ void __launch_bounds__(512) k_ntt(NttJob job) {
   for (int ph = 0; ph < nph; ph++) {
     const int pi = FWD ? ph : nph - 1 - ph;
     const int s0 = pi * RMAX, rp = min(RMAX, logN - s0);
-    ntt_phase_dispatch<E, FWD>(rp, sm, s0, logN, tid, q, q2, tw);
+    ntt_phase_dispatch<E, FWD, QS>(rp, sm, s0, logN, tid, q, q2, tw);
     __syncthreads();
   }
   if (FWD) {
@@ -245,7 +255,7 @@ __global__ void __launch_bounds__(512) k_ntt(NttJob job) {
     }
   } else {
     const u64 ni = M.ninv, nis = M.ninv_sh;
-    for (int i = tid; i < N; i += T) p[i] = mul_shoup(sm[spad(i)], ni, nis, q);
+    for (int i = tid; i < N; i += T) p[i] = mul_shoup<QS>(sm[spad(i)], ni, nis, q);
   }
 }
 
@@ -264,7 +274,7 @@ constexpr int NTT2_T = 256;      // threads per CTA (8 words each)
 
 // one register phase of RP radix-2 stages starting at local stage S0 of an
 // M = 2^LM point sub-NTT; each thread owns 8 words = 8/2^RP rows of 2^RP
-template <int LM, int S0, int RP, bool FWD>
+template <int LM, int S0, int RP, bool FWD, bool QS>
 __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
   constexpr int K = 1 << RP, R = 8 / K;
   constexpr int S = (1 << LM) >> S0, ST = S >> RP;
@@ -292,14 +302,14 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
         u64 &X = x[k], &Y = x[k + half];
         if (FWD) {
           u64 a = X >= q2 ? X - q2 : X;
-          u64 t = mul_shoup_lazy(Y, W.x, W.y, q);
+          u64 t = mul_shoup_lazy<QS>(Y, W.x, W.y, q);
           X = a + t;
           Y = a - t + q2;
         } else {
           u64 a = X + Y;
           u64 d = X - Y + q2;
           X = a >= q2 ? a - q2 : a;
-          Y = mul_shoup_lazy(d, W.x, W.y, q);
+          Y = mul_shoup_lazy<QS>(d, W.x, W.y, q);
         }
       }
     }
@@ -309,36 +319,36 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
 }
 
 // all phases of one sub-NTT, phases of 3 stages (the last one shorter)
-template <int LM, bool FWD>
+template <int LM, bool FWD, bool QS>
 __device__ __forceinline__ void ntt2_sub(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
   constexpr int NPH = (LM + 2) / 3;
   if (FWD) {
-    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), true>(sub, tws, tl, q, q2);
+    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), true, QS>(sub, tws, tl, q, q2);
     __syncthreads();
     if constexpr (NPH > 1) {
-      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), true>(sub, tws, tl, q, q2);
+      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), true, QS>(sub, tws, tl, q, q2);
       __syncthreads();
     }
     if constexpr (NPH > 2) {
-      ntt2_phase<LM, 6, LM - 6, true>(sub, tws, tl, q, q2);
+      ntt2_phase<LM, 6, LM - 6, true, QS>(sub, tws, tl, q, q2);
       __syncthreads();
     }
   } else {
     if constexpr (NPH > 2) {
-      ntt2_phase<LM, 6, LM - 6, false>(sub, tws, tl, q, q2);
+      ntt2_phase<LM, 6, LM - 6, false, QS>(sub, tws, tl, q, q2);
       __syncthreads();
     }
     if constexpr (NPH > 1) {
-      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), false>(sub, tws, tl, q, q2);
+      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), false, QS>(sub, tws, tl, q, q2);
       __syncthreads();
     }
-    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), false>(sub, tws, tl, q, q2);
+    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), false, QS>(sub, tws, tl, q, q2);
     __syncthreads();
   }
 }
 
 // PASS 0: 2^LB strided columns of 2^LA points; PASS 1: 2^LA contiguous rows of 2^LB points
-template <int LA, int LB, bool FWD, int PASS>
+template <int LA, int LB, bool FWD, int PASS, bool QS>
 __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   extern __shared__ u64 sm2[];
   constexpr int LOGN = LA + LB;
@@ -355,7 +365,8 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   const int tid = threadIdx.x;
   u64 *data = sm2;
   ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm2 + ((G * PADM + 1) & ~1));
-  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(FWD ? Md.tw : Md.itw);
+  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(
+      PASS == 0 ? (FWD ? Md.tw : Md.itw) : (FWD ? Md.tw1 : Md.itw1));
   const int first = tile * G;
   // element e = tid + i*T of the tile -> (sub-NTT g, index k) and global word
   auto gidx = [&](int e, int &g, int &k) -> u64 {
@@ -391,14 +402,11 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   // stage twiddles while the tile loads are in flight
   if (PASS == 0) {
     for (int i = tid; i < M; i += NTT2_T) tws[i] = __ldg(gtw + i);
-  } else {
+  } else {  // row tiles: the table is pre-permuted, the CTA's pairs are contiguous
 #pragma unroll
     for (int j = 0; j < NTT2_TILE / NTT2_T; j++) {
-      const int e = tid + j * NTT2_T, g = e >> LM, i = e & (M - 1);
-      if (i) {
-        const int sp = 31 - __clz(i), gi = i - (1 << sp);
-        tws[e] = __ldg(gtw + (1 << (LA + sp)) + ((first + g) << sp) + gi);
-      }
+      const int e = tid + j * NTT2_T;
+      tws[e] = __ldg(gtw + ((u64)first << LM) + e);
     }
   }
 #pragma unroll
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   __syncthreads();
   {
     const int g = tid / TPS, tl = tid & (TPS - 1);
-    ntt2_sub<LM, FWD>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, q, q2);
+    ntt2_sub<LM, FWD, QS>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, q, q2);
   }
   const bool last = FWD ? (PASS == 1) : (PASS == 0);
   const u64 ni = Md.ninv, nis = Md.ninv_sh;
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
         x = x >= q2 ? x - q2 : x;
         x = x >= q ? x - q : x;
       } else {
-        x = mul_shoup(x, ni, nis, q);
+        x = mul_shoup<QS>(x, ni, nis, q);
       }
     }
     p[w] = x;
