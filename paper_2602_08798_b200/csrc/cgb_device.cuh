@@ -158,6 +158,10 @@ __device__ __forceinline__ const u64 *job_src(const NttJob &job, int item, int s
   return nullptr;
 }
 
+// two-pass NTT tiles: one pad word per 8 (conflict-free 64-bit accesses for the
+// row strides 16, 2 and 1 of the 3+3+1-stage phases and for column writes)
+__device__ __forceinline__ int spad8(int i) { return i + (i >> 3); }
+
 // lazy Shoup: a * w mod q in [0, 2q) for any a < 2^64
 template <bool QS = true>
 __device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
@@ -280,13 +284,13 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
   constexpr int S = (1 << LM) >> S0, ST = S >> RP;
   // word k of a row sits at spad(base) + off(k) with a compile-time off(k) when
   // the stride is a multiple of 16 or the row lies inside one 16-word block
-  constexpr bool CONST_OFF = (ST % 16 == 0) || (S <= 16);
+  constexpr bool CONST_OFF = (ST % 8 == 0) || (S <= 8);
 #pragma unroll
   for (int u = 0; u < R; u++) {
     const int row = tl * R + u;
     const int blk = row / ST, base = blk * S + (row & (ST - 1));
-    const int pb = spad(base);
-    auto addr = [&](int k) { return CONST_OFF ? pb + k * ST + ((ST % 16 == 0) ? (k * ST) >> 4 : 0) : spad(base + k * ST); };
+    const int pb = spad8(base);
+    auto addr = [&](int k) { return CONST_OFF ? pb + k * ST + ((ST % 8 == 0) ? (k * ST) >> 3 : 0) : spad8(base + k * ST); };
     u64 x[K];
 #pragma unroll
     for (int k = 0; k < K; k++) x[k] = sub[addr(k)];
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   constexpr int LM = PASS == 0 ? LA : LB, M = 1 << LM;
   constexpr int G = NTT2_TILE / M, LG = 11 - LM;
   constexpr int NSUBS = 1 << (PASS == 0 ? LB : LA), TILES = NSUBS / G;
-  constexpr int PADM = M + (M >> 4) + 1, TPS = M / 8;  // odd row pitch: conflict-free column writes
+  constexpr int PADM = M + (M >> 3) + 1, TPS = M / 8;  // odd row pitch: conflict-free column writes
   static_assert(G * M == NTT2_TILE && (1 << LG) == G, "tile shape");
   const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
   const int item = unit / job.nsub, sub = unit - item * job.nsub;
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   for (int i = 0; i < 8; i++) {
     int g, k;
     gidx(tid + i * NTT2_T, g, k);
-    data[g * PADM + spad(k)] = lift ? centred_to(v[i], qs, q) : v[i];
+    data[g * PADM + spad8(k)] = lift ? centred_to(v[i], qs, q) : v[i];
   }
   __syncthreads();
   {
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   for (int i = 0; i < 8; i++) {
     int g, k;
     const u64 w = gidx(tid + i * NTT2_T, g, k);
-    u64 x = data[g * PADM + spad(k)];
+    u64 x = data[g * PADM + spad8(k)];
     if (last) {
       if (FWD) {
         x = x >= q2 ? x - q2 : x;
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
 
 template <int LA, int LB>
 __host__ size_t ntt2_smem_bytes(int pass) {
-  const int M = 1 << (pass == 0 ? LA : LB), G = NTT2_TILE / M, PADM = M + (M >> 4) + 1;
+  const int M = 1 << (pass == 0 ? LA : LB), G = NTT2_TILE / M, PADM = M + (M >> 3) + 1;
   return sizeof(u64) * (size_t)((G * PADM + 1) & ~1) + 16 * (size_t)(pass == 0 ? M : NTT2_TILE);
 }
 
