@@ -60,6 +60,11 @@ typedef struct cgb_ring cgb_ring;
 int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
                     int one_row, const uint32_t key_seed[8], int64_t arena_cts,
                     int64_t arena_pts, cgb_ring **out);
+/* as cgb_ring_create with Q primes < 2^q_bits (P and B primes < 2^(q_bits+1));
+ * cgb_ring_create uses q_bits = 60 */
+int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bits, int n_slots,
+                       int one_row, const uint32_t key_seed[8], int64_t arena_cts,
+                       int64_t arena_pts, cgb_ring **out);
 void cgb_ring_destroy(cgb_ring *ring);
 /* moduli in order Q[0..L) | P | B[0..L]; returns how many were written */
 int cgb_ring_moduli(const cgb_ring *ring, uint64_t *out, int cap);
@@ -78,6 +83,9 @@ int cgb_timing_report(cgb_ring *ring, char *buf, size_t cap);
 /* measured integer-pipe peak of the NTT's 64-bit Shoup modular multiply
  * (register-resident independent chains over the whole GPU), per second */
 int cgb_modmul_peak(cgb_ring *ring, double *modmuls_per_s);
+/* microbenchmark: average ms of one batched forward (fwd=1) / inverse NTT over
+ * count ciphertexts (2 L limb-polys each), timed over iters launches */
+int cgb_bench_ntt(cgb_ring *ring, int count, int fwd, int iters, double *ms_out);
 
 /* ---- ciphertext / plaintext storage -------------------------------------
  * Ciphertext handles replace SlotCiphertext (backend.py:216-230); the

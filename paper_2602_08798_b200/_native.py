@@ -61,6 +61,8 @@ _vp = ctypes.c_void_p
 SIGNATURES = {
     "cgb_ring_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        _u32p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "cgb_ring_create_ex": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, _u32p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(_vp)]),
     "cgb_ring_destroy": (None, [_vp]),
     "cgb_ring_moduli": (ctypes.c_int, [_vp, _u64p, ctypes.c_int]),
     "cgb_ct_words": (ctypes.c_size_t, [_vp]),
@@ -71,6 +73,7 @@ SIGNATURES = {
     "cgb_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "cgb_timing_report": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_size_t]),
     "cgb_modmul_peak": (ctypes.c_int, [_vp, _dblp]),
+    "cgb_bench_ntt": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dblp]),
     "cgb_ct_alloc": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_ct_free": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_ct_copy": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p]),

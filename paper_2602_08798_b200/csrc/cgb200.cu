@@ -162,6 +162,7 @@ static inline u64 nonce_of(u64 dom, u64 sub) { return (dom << 56) | sub; }
 // ============================================================================
 struct cgb_ring {
   int logN, N, L, nB, nmod, n_slots, one_row;
+  int q_bits = 60;  // Q primes < 2^q_bits, P / B primes < 2^(q_bits+1)
   int iP, iB0, iT;  // modulus indices of P, B[0], t
   u64 t;
   std::vector<u64> mods;  // Q | P | B | t
@@ -1163,9 +1164,9 @@ static void chacha_host(const ChaKey &key, u64 ctr, u64 nonce, u32 out[16]) {
 static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
   const int N = r->N, L = r->L, nB = r->nB, logN = r->logN;
   memcpy(r->keyseed.k, key_seed, sizeof r->keyseed.k);
-  take_primes(r, 60, L);
-  take_primes(r, 61, 1);
-  take_primes(r, 61, nB);
+  take_primes(r, r->q_bits, L);
+  take_primes(r, r->q_bits + 1, 1);
+  take_primes(r, r->q_bits + 1, nB);
   r->iP = L;
   r->iB0 = L + 1;
   r->iT = L + 1 + nB;
@@ -1325,7 +1326,13 @@ const char *cgb_last_error(void) { return g_err.c_str(); }
 
 int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots, int one_row,
                     const uint32_t key_seed[8], int64_t arena_cts, int64_t arena_pts, cgb_ring **out) {
+  return cgb_ring_create_ex(log_n, plain_modulus, n_limbs, 60, n_slots, one_row, key_seed, arena_cts, arena_pts, out);
+}
+
+int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bits, int n_slots, int one_row,
+                       const uint32_t key_seed[8], int64_t arena_cts, int64_t arena_pts, cgb_ring **out) {
   API_BEGIN
+  if (q_bits < 40 || q_bits > 60) FAIL(CGB_ERR_PARAM, "q_bits %d outside [40, 60]", q_bits);
   if (log_n < 2 || log_n > 16) FAIL(CGB_ERR_PARAM, "log_n %d outside [2, 16]", log_n);
   if (n_limbs < 1 || n_limbs > MAXL) FAIL(CGB_ERR_PARAM, "n_limbs %d outside [1, %d]", n_limbs, MAXL);
   u64 N = 1ull << log_n;
@@ -1336,6 +1343,7 @@ int cgb_ring_create(int log_n, uint64_t plain_modulus, int n_limbs, int n_slots,
     FAIL(CGB_ERR_PARAM, "n_slots %d does not match ring degree %llu (one_row=%d)", n_slots, (unsigned long long)N,
          one_row);
   cgb_ring *r = new cgb_ring();
+  r->q_bits = q_bits;
   r->logN = log_n;
   r->N = (int)N;
   r->L = n_limbs;
@@ -1432,6 +1440,33 @@ int cgb_modmul_peak(cgb_ring *r, double *modmuls_per_s) {
   cudaEventDestroy(b);
   CK(cudaFreeAsync(sink, r->stream));
   *modmuls_per_s = (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+  API_END
+}
+
+// ---- kernel microbenchmarks -------------------------
+// `iters` back-to-back batched transforms of count ciphertexts (2 L limb-polys
+// each) on scratch data; returns the average milliseconds per batch.
+int cgb_bench_ntt(cgb_ring *r, int count, int fwd, int iters, double *ms_out) {
+  API_BEGIN
+  const int L = r->L, N = r->N;
+  Scratch S(r);
+  u64 *buf = S.alloc<u64>((size_t)count * 2 * L * N);
+  CK(cudaMemsetAsync(buf, 0, sizeof(u64) * (size_t)count * 2 * L * N, r->stream));
+  std::vector<int> qm;
+  q_mod_idx(r, qm);
+  ntt_items(r, fwd != 0, buf, nullptr, 2ull * L * N, count, 2, L, qm.data());  // warm-up
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, r->stream));
+  for (int i = 0; i < iters; i++) ntt_items(r, fwd != 0, buf, nullptr, 2ull * L * N, count, 2, L, qm.data());
+  CK(cudaEventRecord(b, r->stream));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms_out = ms / iters;
   API_END
 }
 

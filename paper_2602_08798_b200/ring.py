@@ -25,7 +25,7 @@ def _ids(a) -> np.ndarray:
 
 class Ring:
     def __init__(self, log_n: int, t: int, n_limbs: int, n_slots: int, one_row: bool, key_seed,
-                 arena_cts: int | None = None, arena_pts: int | None = None):
+                 arena_cts: int | None = None, arena_pts: int | None = None, q_bits: int = 60):
         self.log_n, self.N, self.t, self.L = log_n, 1 << log_n, int(t), int(n_limbs)
         self.n_slots, self.one_row = int(n_slots), bool(one_row)
         self.ct_words = 2 * self.L * self.N
@@ -39,8 +39,8 @@ class Ring:
         ks = np.ascontiguousarray(np.asarray(key_seed, dtype=np.uint32).reshape(8))
         h = ctypes.c_void_p()
         L = nat.lib()
-        nat.check(L.cgb_ring_create(log_n, self.t, self.L, self.n_slots, int(one_row), nat.u32ptr(ks),
-                                    self.arena_cts, self.arena_pts, ctypes.byref(h)), "cgb_ring_create")
+        nat.check(L.cgb_ring_create_ex(log_n, self.t, self.L, int(q_bits), self.n_slots, int(one_row), nat.u32ptr(ks),
+                                       self.arena_cts, self.arena_pts, ctypes.byref(h)), "cgb_ring_create")
         self._h = h
         mods = np.zeros(64, dtype=np.uint64)
         k = L.cgb_ring_moduli(self._h, nat.u64ptr(mods), 64)
@@ -81,6 +81,11 @@ class Ring:
     def modmul_peak(self) -> float:
         out = np.zeros(1, dtype=np.float64)
         nat.check(nat.lib().cgb_modmul_peak(self._h, nat.dblptr(out)), "cgb_modmul_peak")
+        return float(out[0])
+
+    def bench_ntt(self, count: int, fwd: bool, iters: int = 10) -> float:
+        out = np.zeros(1, dtype=np.float64)
+        nat.check(nat.lib().cgb_bench_ntt(self._h, int(count), int(fwd), int(iters), nat.dblptr(out)), "cgb_bench_ntt")
         return float(out[0])
 
     def sync(self):
