@@ -1366,7 +1366,9 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   CK(cudaFuncSetAttribute(k_ntt<EE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
   CK(cudaFuncSetAttribute(k_ntt<EE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
   CK(cudaFuncSetAttribute(k_ntt<EE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
+    if (log_n < 12) {  // single-kernel NTT (whole vector in shared memory)
+      SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
+    }
 #undef SETSMEM
     switch (log_n) {
       case 12: ntt2_attrs<6, 6>(); break;
