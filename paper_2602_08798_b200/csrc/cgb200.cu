@@ -411,41 +411,52 @@ static void ntt_items(cgb_ring *r, bool fwd, u64 *base, u64 *const *items, u64 i
 
 // elementwise kernels --------------------------------------------------------
 // out[p][l][j] = a + b  (mod q_l), per-item pointers
+// Pointwise kernels: each thread moves two consecutive words with 16-byte
+// loads/stores; grid = (word pairs / TPB, items).
+__device__ __forceinline__ ulonglong2 ld2(const u64 *p) { return __ldg(reinterpret_cast<const ulonglong2 *>(p)); }
+__device__ __forceinline__ void st2(u64 *p, u64 x, u64 y) { *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(x, y); }
+
 __global__ void k_add(u64 *const *out, const u64 *const *a, const u64 *const *b, const ModTab *mods, int L, int logN,
                       u64 words) {
-  int item = blockIdx.y;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = blockIdx.y;
+  const u64 i = 2 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= words) return;
-  int l = (int)((i >> logN) % L);
-  out[item][i] = add_mod(a[item][i], b[item][i], mods[l].q);
+  const u64 q = mods[(int)((i >> logN) % L)].q;
+  const ulonglong2 x = ld2(a[item] + i), y = ld2(b[item] + i);
+  st2(out[item] + i, add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
 }
-// out = a + b + c (three-way; used by rotate_add combine)
+// c0 * pt, c1 * pt: the plaintext limb is read once for both polys; words = L N
 __global__ void k_mult_plain(u64 *const *out, const u64 *const *a, const u64 *const *pt, const ModTab *mods, int L,
                              int logN, u64 words) {
-  int item = blockIdx.y;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = blockIdx.y;
+  const u64 i = 2 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= words) return;
-  u64 li = (i >> logN);
-  int l = (int)(li % L);
-  u64 j = i & ((1ull << logN) - 1);
-  out[item][i] = mul_mod(a[item][i], pt[item][((u64)l << logN) + j], mods[l]);
+  const ModTab &M = mods[(int)(i >> logN)];
+  const u64 *A = a[item];
+  u64 *O = out[item];
+  const ulonglong2 p = ld2(pt[item] + i), x0 = ld2(A + i), x1 = ld2(A + words + i);
+  st2(O + i, mul_mod(x0.x, p.x, M), mul_mod(x0.y, p.y, M));
+  st2(O + words + i, mul_mod(x1.x, p.x, M), mul_mod(x1.y, p.y, M));
 }
+// c0 + pt, c1 copied; words = L N
 __global__ void k_add_plain(u64 *const *out, const u64 *const *a, const u64 *const *pt, const ModTab *mods, int L,
                             int logN, u64 words) {
-  int item = blockIdx.y;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = blockIdx.y;
+  const u64 i = 2 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= words) return;
-  u64 half = (u64)L << logN;
-  int l = (int)((i >> logN) % L);
-  u64 v = a[item][i];
-  if (i < half) v = add_mod(v, pt[item][i], mods[l].q);
-  out[item][i] = v;
+  const u64 q = mods[(int)(i >> logN)].q;
+  const u64 *A = a[item];
+  u64 *O = out[item];
+  const ulonglong2 p = ld2(pt[item] + i), x0 = ld2(A + i), x1 = ld2(A + words + i);
+  st2(O + i, add_mod(x0.x, p.x, q), add_mod(x0.y, p.y, q));
+  st2(O + words + i, x1.x, x1.y);
 }
 __global__ void k_copy(u64 *const *out, const u64 *const *a, u64 words) {
-  int item = blockIdx.y;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const int item = blockIdx.y;
+  const u64 i = 2 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= words) return;
-  out[item][i] = a[item][i];
+  const ulonglong2 x = ld2(a[item] + i);
+  st2(out[item] + i, x.x, x.y);
 }
 // gather items into a strided workspace: dst[item * dstride + w] = src[item][off + w]
 __global__ void k_gather(u64 *dst, u64 dstride, const u64 *const *src, u64 off, u64 words) {
@@ -456,12 +467,16 @@ __global__ void k_gather(u64 *dst, u64 dstride, const u64 *const *src, u64 off, 
 }
 // sum of count items (tree in one kernel: each thread sums one word over all items)
 __global__ void k_sum(u64 *out, const u64 *const *a, int count, const ModTab *mods, int L, int logN, u64 words) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 i = 2 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= words) return;
-  int l = (int)((i >> logN) % L);
-  u64 q = mods[l].q, s = 0;
-  for (int k = 0; k < count; k++) s = add_mod(s, a[k][i], q);
-  out[i] = s;
+  const u64 q = mods[(int)((i >> logN) % L)].q;
+  u64 s0 = 0, s1 = 0;
+  for (int k = 0; k < count; k++) {
+    const ulonglong2 x = ld2(a[k] + i);
+    s0 = add_mod(s0, x.x, q);
+    s1 = add_mod(s1, x.y, q);
+  }
+  st2(out + i, s0, s1);
 }
 
 // Galois automorphism in the evaluation domain: out[k] = in[perm_g(k)]
@@ -1030,10 +1045,10 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
       u64 **d_src = S.up(src.data(), 1), **d_dst = S.up(dst.data(), 1);
       launch_begin(r);
       if (add_input) {
-        k_add<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
+        k_add<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
                                                                  (const u64 *const *)d_src, r->d_mods, L, r->logN, ctw);
       } else {
-        k_copy<<<dim3(GRID1(ctw, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
+        k_copy<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
       }
       launch_end(r, add_input ? "add" : "copy", (add_input ? 24.0 : 16.0) * ctw);
     } else {
@@ -1581,7 +1596,7 @@ int cgb_ct_copy(cgb_ring *r, int count, const uint32_t *src, const uint32_t *dst
   Scratch S(r);
   auto ps = ct_ptrs(r, count, src), pd = ct_ptrs(r, count, dst);
   u64 **ds = S.up(ps.data(), count), **dd = S.up(pd.data(), count);
-  LAUNCH("copy", BYTES_copy, k_copy<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dd, (const u64 *const *)ds, r->ct_words));
+  LAUNCH("copy", BYTES_copy, k_copy<<<dim3(GRID1(r->ct_words / 2, TPB).x, count), TPB, 0, r->stream>>>(dd, (const u64 *const *)ds, r->ct_words));
   API_END
 }
 int cgb_ct_store(cgb_ring *r, int count, const uint32_t *ids, uint64_t *host) {
@@ -1754,7 +1769,7 @@ int cgb_add(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const 
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pb = ct_ptrs(r, count, b), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **db = S.up(pb.data(), count), **dout = S.up(po.data(), count);
-  LAUNCH("add", BYTES_add, k_add<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(dout, (const u64 *const *)da,
+  LAUNCH("add", BYTES_add, k_add<<<dim3(GRID1(r->ct_words / 2, TPB).x, count), TPB, 0, r->stream>>>(dout, (const u64 *const *)da,
                                                                        (const u64 *const *)db, r->d_mods, r->L,
                                                                        r->logN, r->ct_words));
   API_END
@@ -1765,8 +1780,8 @@ int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt,
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
-  LAUNCH("add_plain", BYTES_add_plain, k_add_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
-      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words));
+  LAUNCH("add_plain", BYTES_add_plain, k_add_plain<<<dim3(GRID1((u64)r->L * r->N / 2, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, (u64)r->L * r->N));
   API_END
 }
 int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
@@ -1775,8 +1790,8 @@ int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
   u64 **da = S.up(pa.data(), count), **dp = S.up(pp.data(), count), **dout = S.up(po.data(), count);
-  LAUNCH("mult_plain", BYTES_mult_plain, k_mult_plain<<<dim3(GRID1(r->ct_words, TPB).x, count), TPB, 0, r->stream>>>(
-      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, r->ct_words));
+  LAUNCH("mult_plain", BYTES_mult_plain, k_mult_plain<<<dim3(GRID1((u64)r->L * r->N / 2, TPB).x, count), TPB, 0, r->stream>>>(
+      dout, (const u64 *const *)da, (const u64 *const *)dp, r->d_mods, r->L, r->logN, (u64)r->L * r->N));
   API_END
 }
 int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
@@ -1785,7 +1800,7 @@ int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), po = ct_ptrs(r, 1, &out);
   u64 **da = S.up(pa.data(), count);
-  LAUNCH("sum", BYTES_sum, k_sum<<<GRID1(r->ct_words, TPB), TPB, 0, r->stream>>>(po[0], (const u64 *const *)da, count, r->d_mods, r->L,
+  LAUNCH("sum", BYTES_sum, k_sum<<<GRID1(r->ct_words / 2, TPB), TPB, 0, r->stream>>>(po[0], (const u64 *const *)da, count, r->d_mods, r->L,
                                                         r->logN, r->ct_words));
   API_END
 }
