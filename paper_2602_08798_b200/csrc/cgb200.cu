@@ -313,8 +313,9 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 #define GRID1(n, b) dim3((unsigned)(((n) + (b)-1) / (b)))
 
 // NTT launcher -------------------------------------------------------------
-template <int LA, int LB, bool QS>
-static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
+static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
+template <int LA, int LB, bool QS, int E>
+static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
   second.src_base = nullptr;  // fused loads (lift / permutation) happen in the first pass only
   second.src_items = nullptr;
@@ -325,20 +326,28 @@ static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
     return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
   };
   const size_t s0 = ntt2_smem_bytes<LA, LB>(0), s1 = ntt2_smem_bytes<LA, LB>(1);
+  const int T = NTT2_TILE / E;
   if (fwd) {
-    k_ntt2<LA, LB, true, 0, QS><<<grid(LA), NTT2_T, s0, r->stream>>>(job);
-    k_ntt2<LA, LB, true, 1, QS><<<grid(LB), NTT2_T, s1, r->stream>>>(second);
+    k_ntt2<LA, LB, true, 0, QS, E><<<grid(LA), T, s0, r->stream>>>(job);
+    k_ntt2<LA, LB, true, 1, QS, E><<<grid(LB), T, s1, r->stream>>>(second);
   } else {
-    k_ntt2<LA, LB, false, 1, QS><<<grid(LB), NTT2_T, s1, r->stream>>>(job);
-    k_ntt2<LA, LB, false, 0, QS><<<grid(LA), NTT2_T, s0, r->stream>>>(second);
+    k_ntt2<LA, LB, false, 1, QS, E><<<grid(LB), T, s1, r->stream>>>(job);
+    k_ntt2<LA, LB, false, 0, QS, E><<<grid(LA), T, s0, r->stream>>>(second);
   }
+}
+template <int LA, int LB, bool QS>
+static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
+  if (g_ntt2_e == 16) launch_ntt2_e<LA, LB, QS, 16>(r, fwd, job, count);
+  else launch_ntt2_e<LA, LB, QS, 8>(r, fwd, job, count);
 }
 template <int LA, int LB>
 static void ntt2_attrs() {
   const int s = (int)std::max(ntt2_smem_bytes<LA, LB>(0), ntt2_smem_bytes<LA, LB>(1));
-#define NTT2A(F, P, Q) CK(cudaFuncSetAttribute(k_ntt2<LA, LB, F, P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
-  NTT2A(true, 0, true) NTT2A(true, 1, true) NTT2A(false, 0, true) NTT2A(false, 1, true)
-  NTT2A(true, 0, false) NTT2A(true, 1, false) NTT2A(false, 0, false) NTT2A(false, 1, false)
+#define NTT2A(F, P, Q, E) CK(cudaFuncSetAttribute(k_ntt2<LA, LB, F, P, Q, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  NTT2A(true, 0, true, 8) NTT2A(true, 1, true, 8) NTT2A(false, 0, true, 8) NTT2A(false, 1, true, 8)
+  NTT2A(true, 0, false, 8) NTT2A(true, 1, false, 8) NTT2A(false, 0, false, 8) NTT2A(false, 1, false, 8)
+  NTT2A(true, 0, true, 16) NTT2A(true, 1, true, 16) NTT2A(false, 0, true, 16) NTT2A(false, 1, true, 16)
+  NTT2A(true, 0, false, 16) NTT2A(true, 1, false, 16) NTT2A(false, 0, false, 16) NTT2A(false, 1, false, 16)
 #undef NTT2A
 }
 static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
@@ -1394,6 +1403,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
       default: break;
     }
   }
+  if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
   r->pin_cap = 8u << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
   build_ring(r, key_seed);

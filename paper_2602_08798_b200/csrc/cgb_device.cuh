@@ -278,9 +278,9 @@ constexpr int NTT2_T = 256;      // threads per CTA (8 words each)
 
 // one register phase of RP radix-2 stages starting at local stage S0 of an
 // M = 2^LM point sub-NTT; each thread owns 8 words = 8/2^RP rows of 2^RP
-template <int LM, int S0, int RP, bool FWD, bool QS>
+template <int LM, int S0, int RP, bool FWD, bool QS, int E = 8>
 __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
-  constexpr int K = 1 << RP, R = 8 / K;
+  constexpr int K = 1 << RP, R = E / K;
   constexpr int S = (1 << LM) >> S0, ST = S >> RP;
   // word k of a row sits at spad(base) + off(k) with a compile-time off(k) when
   // the stride is a multiple of 16 or the row lies inside one 16-word block
@@ -322,44 +322,31 @@ __device__ __forceinline__ void ntt2_phase(u64 *sub, const ulonglong2 *tws, int 
   }
 }
 
-// all phases of one sub-NTT, phases of 3 stages (the last one shorter)
-template <int LM, bool FWD, bool QS>
+// all phases of one sub-NTT: phases of RMAX = log2(E) stages (the last one
+// shorter), forward in increasing stage order, inverse in decreasing order
+template <int LM, int E, bool FWD, bool QS, int PH = 0>
 __device__ __forceinline__ void ntt2_sub(u64 *sub, const ulonglong2 *tws, int tl, u64 q, u64 q2) {
-  constexpr int NPH = (LM + 2) / 3;
-  if (FWD) {
-    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), true, QS>(sub, tws, tl, q, q2);
+  constexpr int RMAX = E == 16 ? 4 : 3;
+  constexpr int NPH = (LM + RMAX - 1) / RMAX;
+  if constexpr (PH < NPH) {
+    constexpr int PI = FWD ? PH : NPH - 1 - PH;
+    constexpr int S0 = PI * RMAX, RP = (LM - S0 < RMAX) ? LM - S0 : RMAX;
+    ntt2_phase<LM, S0, RP, FWD, QS, E>(sub, tws, tl, q, q2);
     __syncthreads();
-    if constexpr (NPH > 1) {
-      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), true, QS>(sub, tws, tl, q, q2);
-      __syncthreads();
-    }
-    if constexpr (NPH > 2) {
-      ntt2_phase<LM, 6, LM - 6, true, QS>(sub, tws, tl, q, q2);
-      __syncthreads();
-    }
-  } else {
-    if constexpr (NPH > 2) {
-      ntt2_phase<LM, 6, LM - 6, false, QS>(sub, tws, tl, q, q2);
-      __syncthreads();
-    }
-    if constexpr (NPH > 1) {
-      ntt2_phase<LM, 3, (LM - 3 < 3 ? LM - 3 : 3), false, QS>(sub, tws, tl, q, q2);
-      __syncthreads();
-    }
-    ntt2_phase<LM, 0, (LM < 3 ? LM : 3), false, QS>(sub, tws, tl, q, q2);
-    __syncthreads();
+    ntt2_sub<LM, E, FWD, QS, PH + 1>(sub, tws, tl, q, q2);
   }
 }
 
 // PASS 0: 2^LB strided columns of 2^LA points; PASS 1: 2^LA contiguous rows of 2^LB points
-template <int LA, int LB, bool FWD, int PASS, bool QS>
-__global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
+template <int LA, int LB, bool FWD, int PASS, bool QS, int E = 8>
+__global__ void __launch_bounds__(NTT2_TILE / E) k_ntt2(NttJob job) {
+  constexpr int T = NTT2_TILE / E;
   extern __shared__ u64 sm2[];
   constexpr int LOGN = LA + LB;
   constexpr int LM = PASS == 0 ? LA : LB, M = 1 << LM;
   constexpr int G = NTT2_TILE / M, LG = 11 - LM;
   constexpr int NSUBS = 1 << (PASS == 0 ? LB : LA), TILES = NSUBS / G;
-  constexpr int PADM = M + (M >> 3) + 1, TPS = M / 8;  // odd row pitch: conflict-free column writes
+  constexpr int PADM = M + (M >> 3) + 1, TPS = M / E;  // odd row pitch: conflict-free column writes
   static_assert(G * M == NTT2_TILE && (1 << LG) == G, "tile shape");
   const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
   const int item = unit / job.nsub, sub = unit - item * job.nsub;
@@ -389,47 +376,47 @@ __global__ void __launch_bounds__(NTT2_T) k_ntt2(NttJob job) {
   const bool lift = job.lift != 0;
   const u64 qs = lift ? job.mods[job.src_mod[sub]].q : 0;
   const u64 gal = job.galois ? job.galois[item] : 1;
-  u64 v[8];
+  u64 v[E];
   if (gal == 1) {
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < E; i++) {
       int g, k;
-      v[i] = __ldcs(src + gidx(tid + i * NTT2_T, g, k));
+      v[i] = __ldcs(src + gidx(tid + i * T, g, k));
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
+    for (int i = 0; i < E; i++) {
       int g, k;
-      v[i] = __ldg(src + perm_g((u32)gidx(tid + i * NTT2_T, g, k), gal, LOGN));
+      v[i] = __ldg(src + perm_g((u32)gidx(tid + i * T, g, k), gal, LOGN));
     }
   }
   // stage twiddles while the tile loads are in flight
   if (PASS == 0) {
-    for (int i = tid; i < M; i += NTT2_T) tws[i] = __ldg(gtw + i);
+    for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
   } else {  // row tiles: the table is pre-permuted, the CTA's pairs are contiguous
 #pragma unroll
-    for (int j = 0; j < NTT2_TILE / NTT2_T; j++) {
-      const int e = tid + j * NTT2_T;
+    for (int j = 0; j < E; j++) {
+      const int e = tid + j * T;
       tws[e] = __ldg(gtw + ((u64)first << LM) + e);
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
+  for (int i = 0; i < E; i++) {
     int g, k;
-    gidx(tid + i * NTT2_T, g, k);
+    gidx(tid + i * T, g, k);
     data[g * PADM + spad8(k)] = lift ? centred_to(v[i], qs, q) : v[i];
   }
   __syncthreads();
   {
     const int g = tid / TPS, tl = tid & (TPS - 1);
-    ntt2_sub<LM, FWD, QS>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, q, q2);
+    ntt2_sub<LM, E, FWD, QS>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, q, q2);
   }
   const bool last = FWD ? (PASS == 1) : (PASS == 0);
   const u64 ni = Md.ninv, nis = Md.ninv_sh;
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
+  for (int i = 0; i < E; i++) {
     int g, k;
-    const u64 w = gidx(tid + i * NTT2_T, g, k);
+    const u64 w = gidx(tid + i * T, g, k);
     u64 x = data[g * PADM + spad8(k)];
     if (last) {
       if (FWD) {
