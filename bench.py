@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
     ap.add_argument("--L", type=int, default=128, help="cached prefill length per head")
     ap.add_argument("--heads", type=int, default=HEADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -146,6 +147,59 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(x: float, world: int) -> float:
+    """Max of a per-rank timing over all ranks (device tensors under NCCL,
+    CPU tensors under gloo); the value every rank reports."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_prefill(args):
+    """Config 2: encrypted prefill Q.K^T and P.V for `heads` heads at prompt length L."""
+    import torch
+
+    import paper_2602_08798_b200 as api
+    from paper_2602_08798_b200 import _native
+    from paper_2602_08798_b200.backend import GpuContext
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    _native.build()
+    params = api.BackendParams()
+    root = GpuContext(params, 0)
+    fp = api.FixedPointParams(F, P)
+    rng = np.random.default_rng(0)
+    ctxs = [root.fork() for _ in range(args.heads)]
+    mats = [[api.encode(fp_tokens(rng, args.L, D2), api.EncodingKind.OUTER, c) for _ in range(3)] for c in ctxs]
+    chans = [api.MpcChannel(P, seed=2000 + h) for h in range(args.heads)]
+    ring = root.ring
+    stream = torch.cuda.current_stream()
+    ring.set_stream(stream.cuda_stream)
+    run = lambda: api.prefill_attention_heads([m[0] for m in mats], [m[1] for m in mats], [m[2] for m in mats], fp,
+                                              ctxs, chans)
+    run()  # warm-up (key generation)
+    torch.cuda.synchronize()
+    l0 = ring.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        run()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    print(json.dumps({"metric": f"HE prefill attention ms (Q.K^T and P.V, {args.heads} heads, L={args.L})",
+                      "value": ms, "unit": "ms", "higher_is_better": False, "steps": args.steps,
+                      "config": {"workload": f"prefill_attention_{args.heads}h_L{args.L}", "heads": args.heads,
+                                 "d_head": D2, "n_slots": N_SLOTS},
+                      "gpu_launches": int((ring.launches() - l0) / args.steps)}), flush=True)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -232,14 +286,7 @@ def run_ours(args):
     ring.timing(False)
     peak_mm = ring.modmul_peak()
 
-    def maxall(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    ms, ms_e2e = maxall(ms), maxall(ms_e2e)
+    ms, ms_e2e = max_over_ranks(ms, world), max_over_ranks(ms_e2e, world)
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -356,5 +403,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "prefill":
+        run_prefill(a)
     else:
         run_ours(a)

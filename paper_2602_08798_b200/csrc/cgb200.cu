@@ -152,6 +152,10 @@ struct Consts {
   u64 QBhatInv[MAXL], BQhatInv[MAXL + 1], sc_omega[MAXL][MAXL + 1], sc_th_hi[MAXL], sc_th_lo[MAXL];
   u64 tBhat[MAXL + 1];
   u64 BhatInv[MAXL + 1], BhatModQ[MAXL + 1][MAXL], BmodQ[MAXL];
+  // Shoup companions of the base-conversion constants (w' = floor(w 2^64 / modulus))
+  u64 QhatInv_sh[MAXL], QhatModB_sh[MAXL][MAXL + 1], QmodB_sh[MAXL + 1];
+  u64 QBhatInv_sh[MAXL], BQhatInv_sh[MAXL + 1], sc_omega_sh[MAXL][MAXL + 1], tBhat_sh[MAXL + 1];
+  u64 BhatInv_sh[MAXL + 1], BhatModQ_sh[MAXL + 1][MAXL], BmodQ_sh[MAXL];
 };
 
 static const u64 DOM_SK = 1, DOM_KSK_A = 2, DOM_KSK_E = 3, DOM_ENC_A = 4, DOM_ENC_E = 5;
@@ -334,6 +338,13 @@ static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
     k_ntt2<LA, LB, false, 1, QS, E><<<grid(LB), T, s1, r->stream>>>(job);
     k_ntt2<LA, LB, false, 0, QS, E><<<grid(LA), T, s0, r->stream>>>(second);
   }
+}
+// one pass of the two-pass forward NTT (pass 0: columns, with the job's fused load)
+template <int LA, int LB>
+static void launch_ntt2_colpass(cgb_ring *r, const NttJob &job, int count) {
+  const int G = NTT2_TILE / (1 << LA), nsubs = 1 << LB;
+  k_ntt2<LA, LB, true, 0, true, 8><<<dim3((unsigned)((size_t)count * job.nsub * (nsubs / G))), NTT2_TILE / 8,
+                                    ntt2_smem_bytes<LA, LB>(0), r->stream>>>(job);
 }
 template <int LA, int LB, bool QS>
 static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
@@ -630,6 +641,153 @@ __global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W,
   out[item][i] = v;
 }
 
+// Fused key-switch passes ----------------------------------------------------
+// Shared tile plumbing of the two-pass NTT's second (row) pass: the CTA owns
+// G consecutive row blocks of M = 2^LB words of one limb-poly.
+template <int LA, int LB, int E>
+struct RowTile {
+  static constexpr int M = 1 << LB, G = NTT2_TILE / M, T = NTT2_TILE / E, TILES = (1 << LA) / G;
+  static constexpr int PADM = M + (M >> 3) + 1, TPS = M / E;
+  static __host__ size_t smem() { return sizeof(u64) * (size_t)((G * PADM + 1) & ~1) + 16 * (size_t)NTT2_TILE; }
+};
+
+// load row tile `first` of a pass-0 output limb-poly into smem, run the forward row
+// pass, leave canonical values in regs v[] (element e = tid + i T <-> word first M + e)
+template <int LA, int LB, int E>
+__device__ __forceinline__ void row_pass_fwd(const u64 *src, u64 *data, const ulonglong2 *tws, int first, u64 q,
+                                             u64 v[E]) {
+  using RT = RowTile<LA, LB, E>;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < E; i++) v[i] = __ldcs(src + ((u64)first << LB) + tid + i * RT::T);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const int e = tid + i * RT::T;
+    data[(e >> LB) * RT::PADM + spad8(e & (RT::M - 1))] = v[i];
+  }
+  __syncthreads();
+  const int g = tid / RT::TPS, tl = tid & (RT::TPS - 1);
+  ntt2_sub<LB, E, true, true>(data + g * RT::PADM, tws + g * RT::M, tl, q, 2 * q);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const int e = tid + i * RT::T;
+    u64 x = data[(e >> LB) * RT::PADM + spad8(e & (RT::M - 1))];
+    x = x >= 2 * q ? x - 2 * q : x;
+    v[i] = x >= q ? x - q : x;
+  }
+  __syncthreads();  // smem is reused by the caller's next tile
+}
+
+template <int LA, int LB, int E>
+__device__ __forceinline__ void stage_row_twiddles(ulonglong2 *tws, const ModTab &Md, int first) {
+  using RT = RowTile<LA, LB, E>;
+  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(Md.tw1);
+#pragma unroll
+  for (int j = 0; j < E; j++) {
+    const int e = threadIdx.x + j * RT::T;
+    tws[e] = __ldg(gtw + ((u64)first << LB) + e);
+  }
+}
+
+// ModUp row pass fused with the key inner product:
+//   acc[item][p][l] = sum_j NTT_l(lift_l(digit j)) * key[j][p][l]   (j == l: the input limb itself)
+// D holds the column-pass outputs [item][j][l][N] (units j(L+1)+l, l != j).
+template <int LA, int LB, int L, int E>
+__global__ void __launch_bounds__(NTT2_TILE / E) k_modup_ks(const u64 *D, KsSrc x, const u64 *const *keys, u64 kw,
+                                                           u64 *acc, const ModTab *mods) {
+  using RT = RowTile<LA, LB, E>;
+  constexpr int LP = L + 1, LOGN = LA + LB;
+  constexpr u64 N = 1ull << LOGN;
+  extern __shared__ u64 smf[];
+  const int unit = blockIdx.x / RT::TILES, tile = blockIdx.x - unit * RT::TILES;
+  const int item = unit / LP, l = unit - item * LP;
+  const ModTab &Md = mods[l];  // Q limbs then P (index L)
+  const u64 q = Md.q;
+  u64 *data = smf;
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(smf + ((RT::G * RT::PADM + 1) & ~1));
+  const int first = tile * RT::G, tid = threadIdx.x;
+  stage_row_twiddles<LA, LB, E>(tws, Md, first);
+  const u64 *K = keys[item];
+  u64 a0[E], a1[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) a0[i] = a1[i] = 0;
+#pragma unroll 1
+  for (int j = 0; j < L; j++) {
+    u64 v[E];
+    if (j == l) {
+#pragma unroll
+      for (int i = 0; i < E; i++) v[i] = ks_src_word(x, item, j, (u32)(((u64)first << LB) + tid + i * RT::T), LOGN);
+    } else {
+      row_pass_fwd<LA, LB, E>(D + (((u64)item * L + j) * LP + l) * N, data, tws, first, q, v);
+    }
+    const u64 *kb = K + ((u64)j * 2 + 0) * LP * N + (u64)l * N + ((u64)first << LB);
+    const u64 *ka = K + ((u64)j * 2 + 1) * LP * N + (u64)l * N + ((u64)first << LB);
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      const int e = tid + i * RT::T;
+      a0[i] += mul_shoup_lazy(v[i], __ldg(kb + e), __ldg(kb + kw + e), q);
+      a1[i] += mul_shoup_lazy(v[i], __ldg(ka + e), __ldg(ka + kw + e), q);
+      if ((j & 3) == 3) {
+        a0[i] = a0[i] >= 4 * q ? a0[i] - 4 * q : a0[i];
+        a0[i] = a0[i] >= 2 * q ? a0[i] - 2 * q : a0[i];
+        a1[i] = a1[i] >= 4 * q ? a1[i] - 4 * q : a1[i];
+        a1[i] = a1[i] >= 2 * q ? a1[i] - 2 * q : a1[i];
+      }
+    }
+  }
+  u64 *o0 = acc + (((u64)item * 2 + 0) * LP + l) * N + ((u64)first << LB);
+  u64 *o1 = acc + (((u64)item * 2 + 1) * LP + l) * N + ((u64)first << LB);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    u64 s0 = a0[i], s1 = a1[i];
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const u64 m = (4ull >> r) * q;
+      s0 = s0 >= m ? s0 - m : s0;
+      s1 = s1 >= m ? s1 - m : s1;
+    }
+    o0[tid + i * RT::T] = s0;
+    o1[tid + i * RT::T] = s1;
+  }
+}
+
+// ModDown row pass fused with the combine:
+//   out[p][l] = (acc[p][l] - NTT_l(lift_l(acc[p][P]))) * P^-1 + (p == 0 ? add0 : 0) + add1[p][l]
+// W holds the column-pass outputs [item][p][l][N] (units pL + l).
+template <int LA, int LB, int E>
+__global__ void __launch_bounds__(NTT2_TILE / E) k_moddown_fused(const u64 *W, const u64 *acc, u64 *const *out,
+                                                                KsSrc add0, const u64 *const *add1,
+                                                                const ModTab *mods, const Consts *C, int L) {
+  using RT = RowTile<LA, LB, E>;
+  constexpr int LOGN = LA + LB;
+  constexpr u64 N = 1ull << LOGN;
+  extern __shared__ u64 smf[];
+  const int unit = blockIdx.x / RT::TILES, tile = blockIdx.x - unit * RT::TILES;
+  const int item = unit / (2 * L), pl = unit - item * 2 * L, p = pl / L, l = pl - p * L;
+  const ModTab &Md = mods[l];
+  const u64 q = Md.q;
+  u64 *data = smf;
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(smf + ((RT::G * RT::PADM + 1) & ~1));
+  const int first = tile * RT::G, tid = threadIdx.x;
+  stage_row_twiddles<LA, LB, E>(tws, Md, first);
+  u64 v[E];
+  row_pass_fwd<LA, LB, E>(W + ((u64)item * 2 * L + pl) * N, data, tws, first, q, v);
+  const u64 LP = L + 1;
+  const u64 *A = acc + (((u64)item * 2 + p) * LP + l) * N;
+  const u64 pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
+  u64 *O = out[item] + (u64)pl * N;
+  const u64 *A1 = add1 ? add1[item] + (u64)pl * N : nullptr;
+  const bool has0 = p == 0 && (add0.items || add0.base);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const u64 k = ((u64)first << LB) + tid + i * RT::T;
+    u64 r = mul_shoup(sub_mod(A[k], v[i], q), pi, pis, q);
+    if (has0) r = add_mod(r, ks_src_word(add0, item, l, (u32)k, LOGN), q);
+    if (A1) r = add_mod(r, A1[k], q);
+    O[k] = r;
+  }
+}
+
 // BFV multiplication --------------------------------------------------------
 // lift coefficient-form Q residues of one poly into B: dst[item][p][L + k][N]
 __global__ void k_lift_QB(u64 *dst /*[item][4][L+nB][N]*/, const u64 *coef /*[item][4][L][N]*/, const ModTab *mods,
@@ -658,6 +816,99 @@ __global__ void k_lift_QB(u64 *dst /*[item][4][L+nB][N]*/, const u64 *coef /*[it
     d[(u64)(L + k) * N + jn] = acc;
   }
 }
+// L-templated, Shoup-constant versions of the two base-conversion kernels
+// (every multiplier is a per-ring constant; lazy sums reduced every 4 terms)
+__device__ __forceinline__ u64 lazy_fold(u64 a, u64 q) {
+  a = a >= 4 * q ? a - 4 * q : a;
+  return a >= 2 * q ? a - 2 * q : a;
+}
+__device__ __forceinline__ u64 lazy_final(u64 a, u64 q) {
+  a = lazy_fold(a, q);
+  return a >= q ? a - q : a;
+}
+template <int L>
+__global__ void k_lift_QB_t(u64 *dst, const u64 *coef, const ModTab *mods, const Consts *C, int iB0, int logN) {
+  constexpr int nB = L + 1;
+  const int item = blockIdx.y;
+  const u64 N = 1ull << logN;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 4 * N) return;
+  const u64 jn = i & (N - 1);
+  const int p = (int)(i >> logN);
+  const u64 *src = coef + ((u64)item * 4 + p) * L * N;
+  u64 y[L];
+  double s = 0.0;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    y[l] = mul_shoup(src[(u64)l * N + jn], C->QhatInv[l], C->QhatInv_sh[l], mods[l].q);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(y[l]), C->invq[l]));
+  }
+  const u64 v = (u64)__dadd_rn(s, 0.5);
+  u64 *d = dst + ((u64)item * 4 + p) * (L + nB) * N;
+#pragma unroll
+  for (int k = 0; k < nB; k++) {
+    const u64 q = mods[iB0 + k].q;
+    u64 acc = 0;
+#pragma unroll
+    for (int l = 0; l < L; l++) {
+      acc += mul_shoup_lazy(y[l], C->QhatModB[l][k], C->QhatModB_sh[l][k], q);
+      if ((l & 3) == 3) acc = lazy_fold(acc, q);
+    }
+    acc = lazy_final(acc, q);
+    d[(u64)(L + k) * N + jn] = sub_mod(acc, mul_shoup(v, C->QmodB[k], C->QmodB_sh[k], q), q);
+  }
+}
+template <int L>
+__global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int iB0, int logN) {
+  constexpr int nB = L + 1, nt = L + nB;
+  const int item = blockIdx.y;
+  const u64 N = 1ull << logN;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * N) return;
+  const u64 jn = i & (N - 1);
+  const int p = (int)(i >> logN);
+  const u64 *cp = ten + ((u64)item * 3 + p) * nt * N;
+  u64 y[L];
+  u128 S = 0;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    y[l] = mul_shoup(cp[(u64)l * N + jn], C->QBhatInv[l], C->QBhatInv_sh[l], mods[l].q);
+    S += (u128)y[l] * C->sc_th_hi[l] + (u128)__umul64hi(y[l], C->sc_th_lo[l]);
+  }
+  const u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
+  u64 yk[nB];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < nB; k++) {
+    const u64 q = mods[iB0 + k].q;
+    u64 acc = reduce4(R, q);
+#pragma unroll
+    for (int l = 0; l < L; l++) {
+      acc += mul_shoup_lazy(y[l], C->sc_omega[l][k], C->sc_omega_sh[l][k], q);
+      if ((l & 3) == 2) acc = lazy_fold(acc, q);
+    }
+    acc = lazy_fold(acc, q);
+    const u64 z = mul_shoup(cp[(u64)(L + k) * N + jn], C->BQhatInv[k], C->BQhatInv_sh[k], q);
+    acc = lazy_final(acc + mul_shoup_lazy(z, C->tBhat[k], C->tBhat_sh[k], q), q);
+    yk[k] = mul_shoup(acc, C->BhatInv[k], C->BhatInv_sh[k], q);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(yk[k]), C->invb[k]));
+  }
+  const u64 v = (u64)__dadd_rn(s, 0.5);
+  u64 *o = d + ((u64)item * 3 + p) * L * N;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    const u64 q = mods[l].q;
+    u64 acc = 0;
+#pragma unroll
+    for (int k = 0; k < nB; k++) {
+      acc += mul_shoup_lazy(yk[k], C->BhatModQ[k][l], C->BhatModQ_sh[k][l], q);
+      if ((k & 3) == 3) acc = lazy_fold(acc, q);
+    }
+    acc = lazy_final(acc, q);
+    o[(u64)l * N + jn] = sub_mod(acc, mul_shoup(v, C->BmodQ[l], C->BmodQ_sh[l], q), q);
+  }
+}
+
 // tensor over Q u B: ten[item][3][L+nB][N]
 __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const ModTab *mods, int L, int nt, int iB0,
                          int logN) {
@@ -935,11 +1186,144 @@ static void encode_slots(cgb_ring *r, Scratch &S, const u64 *slots_host, int cou
 
 static u64 *get_key(cgb_ring *r, u64 g);
 
+// ---- fused key switch (two-pass rings): column passes as NTT launches, the row
+// passes fused with the key inner product (ModUp) and the combine (ModDown)
+template <int LA, int LB, int L>
+static void keyswitch_fused_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys,
+                              u64 *const *d_out, const KsSrc &add0, const u64 *const *d_add1) {
+  constexpr int LP = L + 1, E = 8;
+  const int N = r->N, logN = r->logN;
+  using RT = RowTile<LA, LB, E>;
+  // digits in coefficient form (automorphism fused into the inverse NTT's load)
+  u64 *xc = S.alloc<u64>((size_t)count * L * N);
+  {
+    NttJob job{};
+    job.base = xc;
+    job.item_stride = (u64)L * N;
+    job.src_items = x.items;
+    job.src_base = x.items ? nullptr : x.base;
+    job.src_stride = x.stride;
+    job.galois = x.g;
+    const int off = (int)(x.items ? x.off / (u64)N : 0);
+    for (int l = 0; l < L; l++) {
+      job.sub_off[l] = (unsigned short)l;
+      job.sub_mod[l] = (unsigned char)l;
+      job.src_off[l] = (unsigned short)(off + l);
+    }
+    job.nsub = L;
+    launch_ntt(r, false, job, count);
+  }
+  // ModUp column pass (centred lift fused into the load) -> D
+  u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
+  {
+    NttJob job{};
+    job.base = D;
+    job.item_stride = (u64)L * LP * N;
+    job.src_base = xc;
+    job.src_stride = (u64)L * N;
+    job.lift = 1;
+    job.mods = r->d_mods;
+    job.logN = logN;
+    int n = 0;
+    for (int j = 0; j < L; j++)
+      for (int l = 0; l < LP; l++) {
+        if (l == j) continue;
+        job.sub_off[n] = (unsigned short)(j * LP + l);
+        job.sub_mod[n] = (unsigned char)(l == L ? r->iP : l);
+        job.src_off[n] = (unsigned short)j;
+        job.src_mod[n] = (unsigned char)j;
+        n++;
+      }
+    job.nsub = n;
+    launch_begin(r);
+    launch_ntt2_colpass<LA, LB>(r, job, count);
+    launch_end(r, "ntt_fwd", 16.0 * (double)count * n * N);
+  }
+  // ModUp row pass + key inner product -> acc
+  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
+  {
+    const u64 kw = (u64)L * 2 * LP * N;
+    launch_begin(r);
+    k_modup_ks<LA, LB, L, E><<<dim3((unsigned)((size_t)count * LP * RT::TILES)), RT::T, RT::smem(), r->stream>>>(
+        D, x, d_keys, kw, acc, r->d_mods);
+    launch_end(r, "modup_ks", 8.0 * (double)count * LP * N * (L * 2.0 + 2.0));
+  }
+  // ModDown: INTT the P limbs (both passes), column pass of their lift into Q -> W
+  {
+    NttJob job{};
+    job.base = acc;
+    job.item_stride = 2ull * LP * N;
+    job.sub_off[0] = (unsigned short)L;
+    job.sub_mod[0] = (unsigned char)r->iP;
+    job.sub_off[1] = (unsigned short)(LP + L);
+    job.sub_mod[1] = (unsigned char)r->iP;
+    job.nsub = 2;
+    launch_ntt(r, false, job, count);
+  }
+  u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
+  {
+    NttJob job{};
+    job.base = W;
+    job.item_stride = 2ull * L * N;
+    job.src_base = acc;
+    job.src_stride = 2ull * LP * N;
+    job.lift = 1;
+    job.mods = r->d_mods;
+    job.logN = logN;
+    int n = 0;
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        job.sub_off[n] = (unsigned short)(pp * L + l);
+        job.sub_mod[n] = (unsigned char)l;
+        job.src_off[n] = (unsigned short)(pp * LP + L);
+        job.src_mod[n] = (unsigned char)r->iP;
+        n++;
+      }
+    job.nsub = n;
+    launch_begin(r);
+    launch_ntt2_colpass<LA, LB>(r, job, count);
+    launch_end(r, "ntt_fwd", 16.0 * (double)count * n * N);
+  }
+  launch_begin(r);
+  k_moddown_fused<LA, LB, E><<<dim3((unsigned)((size_t)count * 2 * L * RT::TILES)), RT::T, RT::smem(), r->stream>>>(
+      W, acc, d_out, add0, d_add1, r->d_mods, r->d_c, L);
+  launch_end(r, "moddown_fused", 8.0 * (double)count * 2 * L * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)));
+}
+template <int LA, int LB, int L>
+static void fused_attrs() {
+  const int s = (int)RowTile<LA, LB, 8>::smem();
+  CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+}
+static bool g_ks_fused = true;  // CGB_KS_FUSED=0 selects the unfused reference pipeline
+static bool keyswitch_fused(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
+                            const KsSrc &add0, const u64 *const *d_add1) {
+  if (!g_ks_fused) return false;
+#define KSF(A, B, LL)                                                                \
+  if (r->logN == A + B && r->L == LL) {                                              \
+    keyswitch_fused_t<A, B, LL>(r, S, x, count, d_keys, d_out, add0, d_add1);        \
+    return true;                                                                     \
+  }
+#define KSF_L(A, B) KSF(A, B, 2) KSF(A, B, 3) KSF(A, B, 4) KSF(A, B, 5) KSF(A, B, 6) KSF(A, B, 8)
+  KSF_L(6, 7) KSF_L(7, 7) KSF_L(7, 8) KSF_L(8, 8)
+#undef KSF_L
+#undef KSF
+  return false;
+}
+static void fused_attrs_for(int logN, int L) {
+#define FA(A, B, LL) if (logN == A + B && L == LL) fused_attrs<A, B, LL>();
+#define FA_L(A, B) FA(A, B, 2) FA(A, B, 3) FA(A, B, 4) FA(A, B, 5) FA(A, B, 6) FA(A, B, 8)
+  FA_L(6, 7) FA_L(7, 7) FA_L(7, 8) FA_L(8, 8)
+#undef FA_L
+#undef FA
+}
+
 // key switch of `count` NTT-form polys (descriptor x: contiguous, or arena items read
 // through an automorphism) with per-item keys; result combined into out pointers:
 // out = (ks0 + add0 + add1, ks1 + add1)
 static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                       const KsSrc &add0, const u64 *const *d_add1) {
+  if (keyswitch_fused(r, S, x, count, d_keys, d_out, add0, d_add1)) return;
   const int L = r->L, N = r->N, LP = L + 1, logN = r->logN;
   // digits in coefficient form (automorphism fused into the inverse NTT's load)
   u64 *xc = S.alloc<u64>((size_t)count * L * N);
@@ -1319,6 +1703,22 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     for (int k = 0; k < nB; k++) C.sc_omega[l][k] = T.mod(b[k]);
     h_frac128(rem, q[l], &C.sc_th_hi[l], &C.sc_th_lo[l]);
   }
+  for (int l = 0; l < L; l++) {
+    C.QhatInv_sh[l] = h_shoup(C.QhatInv[l], q[l]);
+    C.QBhatInv_sh[l] = h_shoup(C.QBhatInv[l], q[l]);
+    C.BmodQ_sh[l] = h_shoup(C.BmodQ[l], q[l]);
+    for (int k = 0; k < nB; k++) {
+      C.QhatModB_sh[l][k] = h_shoup(C.QhatModB[l][k], b[k]);
+      C.sc_omega_sh[l][k] = h_shoup(C.sc_omega[l][k], b[k]);
+      C.BhatModQ_sh[k][l] = h_shoup(C.BhatModQ[k][l], q[l]);
+    }
+  }
+  for (int k = 0; k < nB; k++) {
+    C.QmodB_sh[k] = h_shoup(C.QmodB[k], b[k]);
+    C.BQhatInv_sh[k] = h_shoup(C.BQhatInv[k], b[k]);
+    C.tBhat_sh[k] = h_shoup(C.tBhat[k], b[k]);
+    C.BhatInv_sh[k] = h_shoup(C.BhatInv[k], b[k]);
+  }
   CK(cudaMalloc((void **)&r->d_c, sizeof(Consts)));
   CK(cudaMemcpy(r->d_c, &C, sizeof(Consts), cudaMemcpyHostToDevice));
   // secret key: ternary from ChaCha20(key_seed, DOM_SK), word j -> (w mod 3) - 1
@@ -1404,6 +1804,8 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
     }
   }
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
+  if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e) != 0;
+  fused_attrs_for(log_n, n_limbs);
   r->pin_cap = 8u << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
   build_ring(r, key_seed);
@@ -1883,8 +2285,17 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
                                                                          off, (u64)L * N));
     }
     ntt_items(r, false, coef, nullptr, 4ull * L * N, n, 4, L, qm.data());
-    LAUNCH("lift_QB", BYTES_lift_QB, k_lift_QB<<<dim3(GRID1(4ull * N, TPB).x, n), TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0,
-                                                                      logN));
+    {
+      const dim3 grid(GRID1(4ull * N, TPB).x, n);
+      launch_begin(r);
+      switch (L) {
+#define LQB(LL) case LL: k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); break;
+        LQB(1) LQB(2) LQB(3) LQB(4) LQB(5) LQB(6) LQB(7) LQB(8)
+#undef LQB
+        default: k_lift_QB<<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0, logN);
+      }
+      launch_end(r, "lift_QB", BYTES_lift_QB);
+    }
     {
       NttJob job{};
       job.base = in;
@@ -1903,8 +2314,17 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, r->d_mods, L, nt, r->iB0, logN));
     ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
-    LAUNCH("scale_round", BYTES_scale_round, k_scale_round<<<dim3(GRID1(3ull * N, TPB).x, n), TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0,
-                                                                         logN));
+    {
+      const dim3 grid(GRID1(3ull * N, TPB).x, n);
+      launch_begin(r);
+      switch (L) {
+#define LSR(LL) case LL: k_scale_round_t<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN); break;
+        LSR(1) LSR(2) LSR(3) LSR(4) LSR(5) LSR(6) LSR(7) LSR(8)
+#undef LSR
+        default: k_scale_round<<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0, logN);
+      }
+      launch_end(r, "scale_round", BYTES_scale_round);
+    }
     ntt_items(r, true, d, nullptr, 3ull * L * N, n, 3, L, qm.data());
     // relinearise d2, add (d0, d1)
     u64 *x = S.alloc<u64>((size_t)n * L * N);
