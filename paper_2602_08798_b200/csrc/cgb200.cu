@@ -45,9 +45,13 @@ struct CgbError {
   } while (0)
 
 #define API_BEGIN try {
-#define API_END                          \
-  return CGB_OK;                         \
-  }                                      \
+#define API_END                                                                       \
+  {                                                                                   \
+    cudaError_t _le = cudaGetLastError();                                             \
+    if (_le != cudaSuccess) FAIL(CGB_ERR_CUDA, "%s left error: %s", __func__, cudaGetErrorString(_le)); \
+  }                                                                                   \
+  return CGB_OK;                                                                      \
+  }                                                                                   \
   catch (const CgbError &e) {            \
     g_err = e.msg;                       \
     return e.code;                       \
@@ -272,7 +276,10 @@ static void launch_begin(cgb_ring *r) {
 }
 static void launch_end(cgb_ring *r, const char *name, double bytes) {
   r->launches++;
-  CK(cudaGetLastError());
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) FAIL(CGB_ERR_CUDA, "launch of %s (N=%d, L=%d): %s", name, r->N, r->L, cudaGetErrorString(e));
+  }
   if (!r->timing) return;
   cudaEvent_t b = take_event(r);
   CK(cudaEventRecord(b, r->stream));
@@ -1784,15 +1791,18 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
     CK(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    size_t smem = sizeof(u64) * (size_t)(N + (N >> 4) + 1);
+    // kernel attributes are process-global: size the single-kernel NTT for the
+    // largest ring it serves (log N <= 11), once
+    static std::once_flag attrs_once;
+    std::call_once(attrs_once, [] {
+      const size_t smem = sizeof(u64) * (size_t)((1 << 11) + (1 << 7) + 1);
 #define SETSMEM(EE)                                                                                           \
   CK(cudaFuncSetAttribute(k_ntt<EE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
   CK(cudaFuncSetAttribute(k_ntt<EE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
   CK(cudaFuncSetAttribute(k_ntt<EE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
   CK(cudaFuncSetAttribute(k_ntt<EE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (log_n < 12) {  // single-kernel NTT (whole vector in shared memory)
       SETSMEM(32) SETSMEM(16) SETSMEM(8) SETSMEM(4) SETSMEM(2)
-    }
+    });
 #undef SETSMEM
     switch (log_n) {
       case 12: ntt2_attrs<6, 6>(); break;

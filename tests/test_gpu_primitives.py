@@ -90,3 +90,18 @@ def test_mult_cipher_bitexact(pair, rng):
     ref = o.mult_cipher(ra, rb)
     assert np.array_equal(g.store(out)[0], ref)
     assert np.array_equal(g.decrypt(out)[0], (v * w) % o.t)
+
+
+def test_rings_of_different_sizes_coexist():
+    """Kernel attributes are process-global: a smaller ring created later must not
+    break a larger one created earlier (regression)."""
+    from paper_2602_08798_b200.ring import Ring
+
+    big = Ring(5, 193, 3, 16, True, KEY, arena_cts=8, arena_pts=4)
+    small = Ring(3, 17, 2, 4, True, KEY, arena_cts=8, arena_pts=4)
+    for r in (big, small, big):
+        ids = r.alloc(1)
+        v = np.arange(r.n_slots) % r.t
+        r.encrypt(v, ENC, 0, ids)
+        assert np.array_equal(r.decrypt(ids)[0], v)
+        r.free(ids)
