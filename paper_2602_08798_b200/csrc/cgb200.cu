@@ -880,7 +880,7 @@ __global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, cons
 #pragma unroll
   for (int l = 0; l < L; l++) {
     y[l] = mul_shoup(cp[(u64)l * N + jn], C->QBhatInv[l], C->QBhatInv_sh[l], mods[l].q);
-    S += (u128)y[l] * C->sc_th_hi[l] + (u128)umulhi64(y[l], C->sc_th_lo[l]);
+    S += (u128)y[l] * C->sc_th_hi[l] + (u128)__umul64hi(y[l], C->sc_th_lo[l]);
   }
   const u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
   u64 yk[nB];
@@ -947,7 +947,7 @@ __global__ void k_scale_round(u64 *d, const u64 *ten, const ModTab *mods, const 
   u128 S = 0;
   for (int l = 0; l < L; l++) {
     y[l] = mul_mod(cp[(u64)l * N + jn], C->QBhatInv[l], mods[l]);
-    S += (u128)y[l] * C->sc_th_hi[l] + (u128)umulhi64(y[l], C->sc_th_lo[l]);
+    S += (u128)y[l] * C->sc_th_hi[l] + (u128)__umul64hi(y[l], C->sc_th_lo[l]);
   }
   u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
   u64 yk[MAXL + 1];
@@ -1096,7 +1096,7 @@ __global__ void k_dec_scale(u64 *m, const u64 *X, const Consts *C, int L, int lo
   u64 I = 0;
   for (int l = 0; l < L; l++) {
     u64 x = X[((u64)item * L + l) * N + jn];
-    S += (u128)x * C->dec_th_hi[l] + (u128)umulhi64(x, C->dec_th_lo[l]);
+    S += (u128)x * C->dec_th_hi[l] + (u128)__umul64hi(x, C->dec_th_lo[l]);
     I = (I + (u64)(((u128)(x % t) * C->dec_omega[l]) % t)) % t;
   }
   u64 R = (u64)((S + ((u128)1 << 63)) >> 64);

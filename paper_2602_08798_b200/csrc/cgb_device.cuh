@@ -32,16 +32,8 @@ struct ModTab {
 // ---------------------------------------------------------------------------
 // scalar modular arithmetic
 // ---------------------------------------------------------------------------
-// High 64 bits of a 64x64 product from four full-rate IMAD.WIDE.U32 steps.
-// (__umul64hi lowers to IMAD.HI, which issues at half the IMAD rate on sm_100a:
-// measured 28 vs 58-61 ops/clk/SM, scripts/micro/imad_rates.cu.)
-__device__ __forceinline__ u64 umulhi64(u64 a, u64 b) {
-  const u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
-  const u64 p00 = (u64)a0 * b0;
-  const u64 t = (u64)a0 * b1 + (p00 >> 32);  // < 2^64: (2^32-1)^2 + 2^32 - 1
-  const u64 u = (u64)a1 * b0 + (u32)t;
-  return (u64)a1 * b1 + (t >> 32) + (u >> 32);
-}
+// (A four-IMAD.WIDE high product was tried instead of __umul64hi and measured
+// slower in both the NTT and the modmul-peak kernel; scripts/micro/imad_rates.cu.)
 __device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) {
   u64 s = a + b;
   return s >= q ? s - q : s;
@@ -58,17 +50,17 @@ __device__ __forceinline__ u64 mul_q(u64 x, u64 q) {
 // a * w mod q with w' = floor(w 2^64 / q); any a < 2^64, result in [0, q)
 template <bool QS = true>
 __device__ __forceinline__ u64 mul_shoup(u64 a, u64 w, u64 wsh, u64 q) {
-  u64 hi = umulhi64(a, wsh);
+  u64 hi = __umul64hi(a, wsh);
   u64 r = a * w - mul_q<QS>(hi, q);
   return r >= q ? r - q : r;
 }
 
 // a * b mod q, a, b < q < 2^62 (Barrett with mu = floor(2^(2k)/q), k = bits(q))
 __device__ __forceinline__ u64 mul_mod(u64 a, u64 b, u64 q, u64 mu, int bits) {
-  u64 lo = a * b, hi = umulhi64(a, b);
+  u64 lo = a * b, hi = __umul64hi(a, b);
   const int s = bits - 1, s2 = bits + 1;
   u64 xs = (hi << (64 - s)) | (lo >> s);
-  u64 ph = umulhi64(xs, mu), pl = xs * mu;
+  u64 ph = __umul64hi(xs, mu), pl = xs * mu;
   u64 qh = (ph << (64 - s2)) | (pl >> s2);
   u64 r = lo - mul_q(qh, q);
   if (r >= q) r -= q;
@@ -175,7 +167,7 @@ __device__ __forceinline__ int spad8(int i) { return i + (i >> 3); }
 // lazy Shoup: a * w mod q in [0, 2q) for any a < 2^64
 template <bool QS = true>
 __device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
-  return a * w - mul_q<QS>(umulhi64(a, wsh), q);
+  return a * w - mul_q<QS>(__umul64hi(a, wsh), q);
 }
 
 template <int E, int RP, bool FWD, bool QS>
