@@ -1268,29 +1268,34 @@ static void keyswitch_fused_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count
     launch_ntt(r, false, job, count);
   }
   u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
-  {
-    NttJob job{};
-    job.base = W;
-    job.item_stride = 2ull * L * N;
-    job.src_base = acc;
-    job.src_stride = 2ull * LP * N;
-    job.lift = 1;
-    job.mods = r->d_mods;
-    job.logN = logN;
-    int n = 0;
-    for (int pp = 0; pp < 2; pp++)
-      for (int l = 0; l < L; l++) {
-        job.sub_off[n] = (unsigned short)(pp * L + l);
-        job.sub_mod[n] = (unsigned char)l;
-        job.src_off[n] = (unsigned short)(pp * LP + L);
-        job.src_mod[n] = (unsigned char)r->iP;
-        n++;
-      }
-    job.nsub = n;
-    launch_begin(r);
-    launch_ntt2_colpass<LA, LB>(r, job, count);
-    launch_end(r, "ntt_fwd", 16.0 * (double)count * n * N);
+  NttJob job{};
+  job.base = W;
+  job.item_stride = 2ull * L * N;
+  job.src_base = acc;
+  job.src_stride = 2ull * LP * N;
+  job.lift = 1;
+  job.mods = r->d_mods;
+  job.logN = logN;
+  int n = 0;
+  for (int pp = 0; pp < 2; pp++)
+    for (int l = 0; l < L; l++) {
+      job.sub_off[n] = (unsigned short)(pp * L + l);
+      job.sub_mod[n] = (unsigned char)l;
+      job.src_off[n] = (unsigned short)(pp * LP + L);
+      job.src_mod[n] = (unsigned char)r->iP;
+      n++;
+    }
+  job.nsub = n;
+  if (!(g_ks_fused & 2)) {  // ModDown: full NTT of the lift, then the separate combine
+    launch_ntt(r, true, job, count);
+    LAUNCH("moddown_combine", BYTES_moddown_combine,
+           k_moddown_combine<<<dim3(GRID1(2ull * L * N, TPB).x, count), TPB, 0, r->stream>>>(
+               d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
+    return;
   }
+  launch_begin(r);
+  launch_ntt2_colpass<LA, LB>(r, job, count);
+  launch_end(r, "ntt_fwd", 16.0 * (double)count * n * N);
   launch_begin(r);
   k_moddown_fused<LA, LB, E><<<dim3((unsigned)((size_t)count * 2 * L * RT::TILES)), RT::T, RT::smem(), r->stream>>>(
       W, acc, d_out, add0, d_add1, r->d_mods, r->d_c, L);
@@ -1302,10 +1307,12 @@ static void fused_attrs() {
   CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
   CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
 }
-static bool g_ks_fused = true;  // CGB_KS_FUSED=0 selects the unfused reference pipeline
+// key-switch fusion: bit 0 = ModUp row pass + inner product, bit 1 = ModDown row pass
+// + combine (CGB_KS_FUSED; 0 = the unfused pipeline)
+static int g_ks_fused = 3;
 static bool keyswitch_fused(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                             const KsSrc &add0, const u64 *const *d_add1) {
-  if (!g_ks_fused) return false;
+  if (!(g_ks_fused & 1)) return false;
 #define KSF(A, B, LL)                                                                \
   if (r->logN == A + B && r->L == LL) {                                              \
     keyswitch_fused_t<A, B, LL>(r, S, x, count, d_keys, d_out, add0, d_add1);        \
@@ -1814,7 +1821,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
     }
   }
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
-  if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = 8u << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
