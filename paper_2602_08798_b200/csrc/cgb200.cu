@@ -1193,6 +1193,10 @@ static void encode_slots(cgb_ring *r, Scratch &S, const u64 *slots_host, int cou
 
 static u64 *get_key(cgb_ring *r, u64 g);
 
+// key-switch fusion: bit 0 = ModUp row pass + inner product, bit 1 = ModDown row pass
+// + combine (CGB_KS_FUSED; 0 = the unfused pipeline)
+static int g_ks_fused = 3;
+
 // ---- fused key switch (two-pass rings): column passes as NTT launches, the row
 // passes fused with the key inner product (ModUp) and the combine (ModDown)
 template <int LA, int LB, int L>
@@ -1307,9 +1311,6 @@ static void fused_attrs() {
   CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
   CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
 }
-// key-switch fusion: bit 0 = ModUp row pass + inner product, bit 1 = ModDown row pass
-// + combine (CGB_KS_FUSED; 0 = the unfused pipeline)
-static int g_ks_fused = 3;
 static bool keyswitch_fused(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                             const KsSrc &add0, const u64 *const *d_add1) {
   if (!(g_ks_fused & 1)) return false;
