@@ -272,15 +272,17 @@ static void auto_coeff_mod(int N, const u64 *in, u64 g, u64 q, u64 *out) {
     }
 }
 
-void *ora_create(int logN, u64 t, int L, int n_slots, int one_row, const u32 keyseed[8]) {
+void *ora_create(int logN, u64 t, int L, int n_slots, int one_row, const u32 keyseed[8], int q_bits) {
     ora_ctx *c = calloc(1, sizeof(ora_ctx));
     c->logN = logN; c->N = 1 << logN; c->L = L; c->nB = L + 1; c->t = t;
     c->n_slots = n_slots; c->one_row = one_row;
     memcpy(c->keyseed, keyseed, sizeof c->keyseed);
     int N = c->N;
-    int at = take_primes(c, 60, L, 0);
-    at = take_primes(c, 61, 1, at);
-    at = take_primes(c, 61, c->nB, at);
+    /* Q primes < 2^q_bits; P and B one bit wider, or also < 2^q_bits when q_bits <= 49 */
+    int pb = q_bits <= 49 ? q_bits : q_bits + 1;
+    int at = take_primes(c, q_bits, L, 0);
+    at = take_primes(c, pb, 1, at);
+    at = take_primes(c, pb, c->nB, at);
     c->nmods = at;
     for (int i = 0; i < c->nmods; i++) make_tables(N, logN, c->mods[i], &c->tw[i], &c->itw[i], &c->ninv[i]);
     make_tables(N, logN, t, &c->tw_t, &c->itw_t, &c->ninv_t);

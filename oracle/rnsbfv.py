@@ -43,7 +43,8 @@ def lib():
             build()
         L = ctypes.CDLL(str(_SO))
         L.ora_create.restype = ctypes.c_void_p
-        L.ora_create.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u32p]
+        L.ora_create.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u32p,
+                                 ctypes.c_int]
         L.ora_destroy.argtypes = [ctypes.c_void_p]
         L.ora_moduli.argtypes = [ctypes.c_void_p, _u64p]
         L.ora_moduli.restype = ctypes.c_int
@@ -70,12 +71,12 @@ def lib():
 class OracleRing:
     """One parameter set of the restatement (ring, primes, keys)."""
 
-    def __init__(self, log_n: int, t: int, n_limbs: int, n_slots: int, one_row: bool, keyseed):
+    def __init__(self, log_n: int, t: int, n_limbs: int, n_slots: int, one_row: bool, keyseed, q_bits: int = 60):
         self.log_n, self.N, self.t, self.L = log_n, 1 << log_n, int(t), n_limbs
         self.n_slots, self.one_row = n_slots, bool(one_row)
         ks = np.ascontiguousarray(np.asarray(keyseed, dtype=np.uint32))
         assert ks.shape == (8,)
-        self._h = lib().ora_create(log_n, self.t, n_limbs, n_slots, int(one_row), ks)
+        self._h = lib().ora_create(log_n, self.t, n_limbs, n_slots, int(one_row), ks, int(q_bits))
         mods = np.zeros(64, dtype=np.uint64)
         k = lib().ora_moduli(self._h, mods)
         self.moduli = [int(x) for x in mods[:k]]

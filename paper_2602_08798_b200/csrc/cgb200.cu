@@ -170,7 +170,8 @@ static inline u64 nonce_of(u64 dom, u64 sub) { return (dom << 56) | sub; }
 // ============================================================================
 struct cgb_ring {
   int logN, N, L, nB, nmod, n_slots, one_row;
-  int q_bits = 60;  // Q primes < 2^q_bits, P / B primes < 2^(q_bits+1)
+  int q_bits = 60;  // Q primes < 2^q_bits; P / B primes < 2^(q_bits+1), or < 2^q_bits when <= 49
+  bool fp_ntt = false;  // two-pass NTT on the FP64 pipe (log N >= 12, all primes < 2^49)
   int iP, iB0, iT;  // modulus indices of P, B[0], t
   u64 t;
   std::vector<u64> mods;  // Q | P | B | t
@@ -353,9 +354,31 @@ static void launch_ntt2_colpass(cgb_ring *r, const NttJob &job, int count) {
   k_ntt2<LA, LB, true, 0, true, 8><<<dim3((unsigned)((size_t)count * job.nsub * (nsubs / G))), NTT2_TILE / 8,
                                     ntt2_smem_bytes<LA, LB>(0), r->stream>>>(job);
 }
+template <int LA, int LB>
+static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) {
+  NttJob second = job;
+  second.src_base = nullptr;
+  second.src_items = nullptr;
+  second.galois = nullptr;
+  second.lift = 0;
+  auto grid = [&](int lm) {
+    int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
+    return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
+  };
+  const size_t s0 = ntt2_smem_bytes<LA, LB>(0), s1 = ntt2_smem_bytes<LA, LB>(1);
+  const int T = NTT2_TILE / 8;
+  if (fwd) {
+    k_ntt2_fp<LA, LB, true, 0><<<grid(LA), T, s0, r->stream>>>(job);
+    k_ntt2_fp<LA, LB, true, 1><<<grid(LB), T, s1, r->stream>>>(second);
+  } else {
+    k_ntt2_fp<LA, LB, false, 1><<<grid(LB), T, s1, r->stream>>>(job);
+    k_ntt2_fp<LA, LB, false, 0><<<grid(LA), T, s0, r->stream>>>(second);
+  }
+}
 template <int LA, int LB, bool QS>
 static void launch_ntt2(cgb_ring *r, bool fwd, const NttJob &job, int count) {
-  if (g_ntt2_e == 16) launch_ntt2_e<LA, LB, QS, 16>(r, fwd, job, count);
+  if (r->fp_ntt) launch_ntt2_fp<LA, LB>(r, fwd, job, count);
+  else if (g_ntt2_e == 16) launch_ntt2_e<LA, LB, QS, 16>(r, fwd, job, count);
   else launch_ntt2_e<LA, LB, QS, 8>(r, fwd, job, count);
 }
 template <int LA, int LB>
@@ -367,6 +390,10 @@ static void ntt2_attrs() {
   NTT2A(true, 0, true, 16) NTT2A(true, 1, true, 16) NTT2A(false, 0, true, 16) NTT2A(false, 1, true, 16)
   NTT2A(true, 0, false, 16) NTT2A(true, 1, false, 16) NTT2A(false, 0, false, 16) NTT2A(false, 1, false, 16)
 #undef NTT2A
+  CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
 }
 static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
   if (count <= 0 || job.nsub <= 0) return;
@@ -1195,7 +1222,7 @@ static u64 *get_key(cgb_ring *r, u64 g);
 
 // key-switch fusion: bit 0 = ModUp row pass + inner product, bit 1 = ModDown row pass
 // + combine (CGB_KS_FUSED; 0 = the unfused pipeline)
-static int g_ks_fused = 3;
+static int g_ks_fused = 0;  // measured: the unfused pipeline is faster (profiles/r01)
 
 // ---- fused key switch (two-pass rings): column passes as NTT launches, the row
 // passes fused with the key inner product (ModUp) and the combine (ModDown)
@@ -1587,18 +1614,21 @@ static void chacha_host(const ChaKey &key, u64 ctr, u64 nonce, u32 out[16]) {
 static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
   const int N = r->N, L = r->L, nB = r->nB, logN = r->logN;
   memcpy(r->keyseed.k, key_seed, sizeof r->keyseed.k);
+  // q_bits <= 49: every prime < 2^q_bits (FP64-pipe NTT); otherwise P / B one bit wider
+  const int pb = r->q_bits <= 49 ? r->q_bits : r->q_bits + 1;
   take_primes(r, r->q_bits, L);
-  take_primes(r, r->q_bits + 1, 1);
-  take_primes(r, r->q_bits + 1, nB);
+  take_primes(r, pb, 1);
+  take_primes(r, pb, nB);
   r->iP = L;
   r->iB0 = L + 1;
   r->iT = L + 1 + nB;
   for (u64 m : r->mods)
     if ((m & 0xffffffffull) != 1) FAIL(CGB_ERR_STATE, "modulus %llu is not 1 mod 2^32", (unsigned long long)m);
+  r->fp_ntt = logN >= 12 && r->q_bits <= 49 && !getenv("CGB_INT_NTT");
   r->mods.push_back(r->t);
   r->nmod = (int)r->mods.size();
   // twiddle tables
-  size_t per = 8ull * N;  // tw | itw | row-tile ordered tw1 | itw1 : N (w, w') pairs = 2N words each
+  size_t per = 16ull * N;  // tw | itw | tw1 | itw1 (u64 (w, w') pairs) | the same four as (w, w/q) doubles
   CK(cudaMalloc((void **)&r->d_tables, sizeof(u64) * per * r->nmod));
   std::vector<u64> tab(per);
   r->h_mods.resize(r->nmod);
@@ -1629,6 +1659,14 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
           tab[6 * N + 2 * dst + 1] = tab[2 * N + 2 * src + 1];
         }
     }
+    // FP64 copies: (double(w), double(w)/double(q)) in the same four orders
+    for (int o = 0; o < 4; o++)
+      for (int k = 0; k < N; k++) {
+        const u64 w = tab[(size_t)o * 2 * N + 2 * k];
+        double wd = (double)w, wq = wd / (double)q;
+        memcpy(&tab[8ull * N + (size_t)o * 2 * N + 2 * k], &wd, 8);
+        memcpy(&tab[8ull * N + (size_t)o * 2 * N + 2 * k + 1], &wq, 8);
+      }
     u64 *dt = r->d_tables + per * i;
     CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
     ModTab &M = r->h_mods[i];
@@ -1645,6 +1683,14 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.itw_sh = nullptr;
     M.tw1 = dt + 4 * N;
     M.itw1 = dt + 6 * N;
+    M.ftw = dt + 8 * N;
+    M.fitw = dt + 10 * N;
+    M.ftw1 = dt + 12 * N;
+    M.fitw1 = dt + 14 * N;
+    M.qd = (double)q;
+    M.qinv = 1.0 / (double)q;
+    M.ninv_fp = (double)M.ninv;
+    M.ninv_fpq = (double)M.ninv / (double)q;
   }
   CK(cudaMalloc((void **)&r->d_mods, sizeof(ModTab) * r->nmod));
   CK(cudaMemcpy(r->d_mods, r->h_mods.data(), sizeof(ModTab) * r->nmod, cudaMemcpyHostToDevice));

@@ -25,6 +25,9 @@ struct ModTab {
   u64 ninv, ninv_sh;
   const u64 *tw, *tw_sh, *itw, *itw_sh;  // bit-reversed psi powers + Shoup companions
   const u64 *tw1, *itw1;                 // the same pairs in two-pass row-tile order (see k_ntt2)
+  const u64 *ftw, *fitw, *ftw1, *fitw1;  // FP64 twiddles (w, w/q) as double pairs, same orders
+  double qd, qinv;                       // q and 1/q as doubles (FP64 NTT)
+  double ninv_fp, ninv_fpq;              // N^-1 and N^-1 / q as doubles
   int bits;
   int pad_;
 };
@@ -436,6 +439,170 @@ template <int LA, int LB>
 __host__ size_t ntt2_smem_bytes(int pass) {
   const int M = 1 << (pass == 0 ? LA : LB), G = NTT2_TILE / M, PADM = M + (M >> 3) + 1;
   return sizeof(u64) * (size_t)((G * PADM + 1) & ~1) + 16 * (size_t)(pass == 0 ? M : NTT2_TILE);
+}
+
+// ---------------------------------------------------------------------------
+// FP64-pipe NTT (rings whose primes are < 2^49).  The B200 issues DFMA at the
+// IMAD rate, and an exact modular product costs ~6 FP64 ops via error-free
+// transformations (hi = a w, lo = fma(a, w, -hi), r = fma(-rint(a w/q), q, hi) + lo)
+// against ~14 integer ops for the 64-bit Shoup product.  Values are signed
+// doubles: |x| <= q/2 after a reduction, growing by < 2q per stage, reduced at
+// every phase start, so every intermediate is an integer < 2^52 and exact.
+// Loads and stores move canonical u64 residues, so the transform is the same
+// function as the integer NTT (bit-exact against the oracle).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double u2d(u64 v) {  // exact for v < 2^52
+  return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+__device__ __forceinline__ double fp_reduce(double x, double q, double qinv) {  // -> [-q/2, q/2]
+  return fma(-rint(x * qinv), q, x);
+}
+__device__ __forceinline__ u64 fp_canon(double x, double q, double qinv) {  // -> [0, q) as u64
+  double r = fp_reduce(x, q, qinv);
+  r = r < 0.0 ? r + q : r;
+  return (u64)__double_as_longlong(r + 4503599627370496.0) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double fp_mulmod(double a, double w, double wq, double q) {  // in (-2q, 2q)
+  const double hi = a * w;
+  const double lo = fma(a, w, -hi);
+  return fma(-rint(a * wq), q, hi) + lo;
+}
+
+template <int LM, int S0, int RP, bool FWD, int E>
+__device__ __forceinline__ void ntt2_phase_fp(double *sub, const double2 *tws, int tl, double q, double qinv) {
+  constexpr int K = 1 << RP, R = E / K;
+  constexpr int S = (1 << LM) >> S0, ST = S >> RP;
+  constexpr bool CONST_OFF = (ST % 8 == 0) || (S <= 8);
+#pragma unroll
+  for (int u = 0; u < R; u++) {
+    const int row = tl * R + u;
+    const int blk = row / ST, base = blk * S + (row & (ST - 1));
+    const int pb = spad8(base);
+    auto addr = [&](int k) { return CONST_OFF ? pb + k * ST + ((ST % 8 == 0) ? (k * ST) >> 3 : 0) : spad8(base + k * ST); };
+    double x[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) x[k] = fp_reduce(sub[addr(k)], q, qinv);
+#pragma unroll
+    for (int ll = 0; ll < RP; ll++) {
+      const int l = FWD ? ll : RP - 1 - ll;
+      const int half = K >> (l + 1);
+      double2 W;
+#pragma unroll
+      for (int k = 0; k < K; k++) {
+        if (k & half) continue;
+        if ((k & ((1 << (RP - l)) - 1)) == 0) W = tws[(1 << (S0 + l)) + (blk << l) + (k >> (RP - l))];
+        double &X = x[k], &Y = x[k + half];
+        if (FWD) {
+          const double t = fp_mulmod(Y, W.x, W.y, q);
+          Y = X - t;
+          X = X + t;
+        } else {  // GS: the sum is reduced so it cannot double every stage
+          const double d = X - Y;
+          X = fp_reduce(X + Y, q, qinv);
+          Y = fp_mulmod(d, W.x, W.y, q);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) sub[addr(k)] = x[k];
+  }
+}
+
+template <int LM, int E, bool FWD, int PH = 0>
+__device__ __forceinline__ void ntt2_sub_fp(double *sub, const double2 *tws, int tl, double q, double qinv) {
+  constexpr int RMAX = E == 16 ? 4 : 3;
+  constexpr int NPH = (LM + RMAX - 1) / RMAX;
+  if constexpr (PH < NPH) {
+    constexpr int PI = FWD ? PH : NPH - 1 - PH;
+    constexpr int S0 = PI * RMAX, RP = (LM - S0 < RMAX) ? LM - S0 : RMAX;
+    ntt2_phase_fp<LM, S0, RP, FWD, E>(sub, tws, tl, q, qinv);
+    __syncthreads();
+    ntt2_sub_fp<LM, E, FWD, PH + 1>(sub, tws, tl, q, qinv);
+  }
+}
+
+// same tiling / fused loads as k_ntt2; every pass stores canonical u64
+template <int LA, int LB, bool FWD, int PASS, int E = 8>
+__global__ void __launch_bounds__(NTT2_TILE / E) k_ntt2_fp(NttJob job) {
+  extern __shared__ u64 sm2[];
+  constexpr int T = NTT2_TILE / E;
+  constexpr int LOGN = LA + LB;
+  constexpr int LM = PASS == 0 ? LA : LB, M = 1 << LM;
+  constexpr int G = NTT2_TILE / M, LG = 11 - LM;
+  constexpr int NSUBS = 1 << (PASS == 0 ? LB : LA), TILES = NSUBS / G;
+  constexpr int PADM = M + (M >> 3) + 1, TPS = M / E;
+  const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
+  const int item = unit / job.nsub, sub = unit - item * job.nsub;
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << LOGN);
+  const ModTab &Md = job.mods[job.sub_mod[sub]];
+  const u64 q = Md.q;
+  const double qd = Md.qd, qinv = Md.qinv;
+  const int tid = threadIdx.x;
+  double *data = reinterpret_cast<double *>(sm2);
+  double2 *tws = reinterpret_cast<double2 *>(sm2 + ((G * PADM + 1) & ~1));
+  const double2 *gtw = reinterpret_cast<const double2 *>(
+      PASS == 0 ? (FWD ? Md.ftw : Md.fitw) : (FWD ? Md.ftw1 : Md.fitw1));
+  const int first = tile * G;
+  auto gidx = [&](int e, int &g, int &k) -> u64 {
+    if (PASS == 0) {
+      g = e & (G - 1);
+      k = e >> LG;
+      return ((u64)k << LB) + first + g;
+    } else {
+      g = e >> LM;
+      k = e & (M - 1);
+      return ((u64)first << LM) + e;
+    }
+  };
+  const u64 *src = job_src(job, item, sub, LOGN);
+  if (!src) src = p;
+  const bool lift = job.lift != 0;
+  const u64 qs = lift ? job.mods[job.src_mod[sub]].q : 0;
+  const u64 gal = job.galois ? job.galois[item] : 1;
+  u64 v[E];
+  if (gal == 1) {
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      int g, k;
+      v[i] = __ldcs(src + gidx(tid + i * T, g, k));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      int g, k;
+      v[i] = __ldg(src + perm_g((u32)gidx(tid + i * T, g, k), gal, LOGN));
+    }
+  }
+  if (PASS == 0) {
+    for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; j++) {
+      const int e = tid + j * T;
+      tws[e] = __ldg(gtw + ((u64)first << LM) + e);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    int g, k;
+    gidx(tid + i * T, g, k);
+    data[g * PADM + spad8(k)] = u2d(lift ? centred_to(v[i], qs, q) : v[i]);
+  }
+  __syncthreads();
+  {
+    const int g = tid / TPS, tl = tid & (TPS - 1);
+    ntt2_sub_fp<LM, E, FWD>(data + g * PADM, PASS == 0 ? tws : tws + g * M, tl, qd, qinv);
+  }
+  const bool last = FWD ? (PASS == 1) : (PASS == 0);
+  const double ni = Md.ninv_fp;
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    int g, k;
+    const u64 w = gidx(tid + i * T, g, k);
+    double x = data[g * PADM + spad8(k)];
+    if (last && !FWD) x = fp_mulmod(fp_reduce(x, qd, qinv), ni, Md.ninv_fpq, qd);
+    p[w] = fp_canon(x, qd, qinv);
+  }
 }
 
 }  // namespace cgb

@@ -28,6 +28,7 @@ class Ring:
                  arena_cts: int | None = None, arena_pts: int | None = None, q_bits: int = 60):
         self.log_n, self.N, self.t, self.L = log_n, 1 << log_n, int(t), int(n_limbs)
         self.n_slots, self.one_row = int(n_slots), bool(one_row)
+        self.q_bits = int(q_bits)
         self.ct_words = 2 * self.L * self.N
         if arena_cts is None:
             arena_cts = max(64, min(65536, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))

@@ -8,23 +8,26 @@ KEY = np.arange(8, dtype=np.uint32) * 7 + 1
 ENC = np.arange(8, dtype=np.uint32) + 1000
 
 CASES = [
-    # (log_n, t, L, n_slots, one_row)
-    (4, 97, 3, 8, True),
-    (3, 17, 2, 8, False),
-    (7, 67109633, 4, 64, True),
-    (14, 536903681, 4, 8192, True),
+    # (log_n, t, L, n_slots, one_row, q_bits)
+    (4, 97, 3, 8, True, 60),
+    (3, 17, 2, 8, False, 60),
+    (7, 67109633, 4, 64, True, 60),
+    (14, 536903681, 4, 8192, True, 60),   # integer-pipe NTT
+    (14, 536903681, 4, 8192, True, 49),   # FP64-pipe NTT
+    (13, 536903681, 3, 4096, True, 49),
 ]
 
 
-@pytest.fixture(scope="module", params=CASES, ids=lambda c: f"logN{c[0]}_t{c[1]}_L{c[2]}_{'row' if c[4] else 'two'}")
+@pytest.fixture(scope="module", params=CASES,
+                ids=lambda c: f"logN{c[0]}_t{c[1]}_L{c[2]}_{'row' if c[4] else 'two'}_q{c[5]}")
 def pair(request, oracle_mod):
     from paper_2602_08798_b200._native import build
     from paper_2602_08798_b200.ring import Ring
 
     build()
-    log_n, t, L, n, one_row = request.param
-    g = Ring(log_n, t, L, n, one_row, KEY, arena_cts=64, arena_pts=16)
-    o = oracle_mod.OracleRing(log_n, t, L, n, one_row, KEY)
+    log_n, t, L, n, one_row, qb = request.param
+    g = Ring(log_n, t, L, n, one_row, KEY, arena_cts=64, arena_pts=16, q_bits=qb)
+    o = oracle_mod.OracleRing(log_n, t, L, n, one_row, KEY, q_bits=qb)
     return g, o
 
 
