@@ -63,11 +63,18 @@ def metric_name(L):
     return f"HE attention decode ms/token at L={L} (12 heads, d_head=64, n=8192)"
 
 
+def _ring_desc():
+    from paper_2602_08798_b200.backend import default_limbs, default_qbits
+
+    L, qb = default_limbs(16384), default_qbits(16384)
+    return (f"RNS-BFV N=16384, Q={L}x{qb}b primes, P {qb if qb <= 49 else qb + 1}b, dnum={L}, "
+            f"{'FP64' if qb <= 49 else 'integer'}-pipe NTT")
+
+
 def workload(args):
     return {"workload": f"decode_attention_{args.heads}h_L{args.L}", "heads": args.heads, "d_head": D2,
             "n_slots": N_SLOTS, "plain_modulus": P, "cached_len": args.L, "steps_appended": 1,
-            "ring": "RNS-BFV N=16384, Q=%dx60b, P=61b, dnum=L" % __import__("paper_2602_08798_b200.backend",
-                                                                         fromlist=["x"]).default_limbs(16384), "l2": "working set >1.5 GB per step (> 126 MB L2)"}
+            "ring": _ring_desc(), "l2": "working set >1.5 GB per step (> 126 MB L2)"}
 
 
 # ----------------------------------------------------------------------------

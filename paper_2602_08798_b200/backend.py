@@ -237,18 +237,26 @@ def ring_layout(n_slots: int, p: int) -> tuple[int, bool]:
     return n_slots.bit_length() - 1, False
 
 
+def default_qbits(ring_degree: int) -> int:
+    """Bit size of the Q primes (CGB_QBITS overrides): 60 -> integer-pipe NTT,
+    <= 49 -> FP64-pipe NTT on rings of degree >= 4096."""
+    env = os.environ.get("CGB_QBITS")
+    return int(env) if env else 60
+
+
 def ring_for(params, n_limbs: int | None = None, key_seed: int | None = None):
     from .ring import Ring
 
     log_n, one_row = ring_layout(params.n_slots, params.plain_modulus)
     L = n_limbs or default_limbs(1 << log_n)
+    qb = default_qbits(1 << log_n)
     ks = _KEY_SEED if key_seed is None else key_seed
-    key = (params.n_slots, params.plain_modulus, L, ks)
+    key = (params.n_slots, params.plain_modulus, L, qb, ks)
     with _rings_lock:
         r = _rings.get(key)
         if r is None:
             seed = np.random.SeedSequence([0xB200_4B45, ks]).generate_state(8, dtype=np.uint32)
-            r = Ring(log_n, params.plain_modulus, L, params.n_slots, one_row, seed)
+            r = Ring(log_n, params.plain_modulus, L, params.n_slots, one_row, seed, q_bits=qb)
             _rings[key] = r
         return r
 
