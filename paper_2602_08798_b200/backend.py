@@ -215,11 +215,12 @@ _rings_lock = threading.Lock()
 def default_limbs(ring_degree: int) -> int:
     """Q limbs of 60 bits.
 
-    N >= 16384 (the production n = 8192 ring): 3 limbs, Q = 180 bits.  The
-    deepest intermediates of the hot path (decode scores/values after one-hot
-    mult_plain + 14 rotations + mult_cipher + 64-term sums; prefill P.V
-    columns) keep >= 60 bits of real noise budget (profiles/r01/
-    noise_probe.jsonl; tests/test_gpu_hotpath.py asserts >= 40).  Smaller
+    N >= 16384 (the production n = 8192 ring): 3 limbs of 49 bits, Q = 147
+    bits.  The deepest intermediates of the hot path (decode scores/values
+    after one-hot mult_plain + 14 rotations + mult_cipher + 64-term sums;
+    prefill P.V columns) keep >= 28 bits of real noise budget (61 with 60-bit
+    primes; profiles/r01/params_sweep.md; tests/test_gpu_hotpath.py asserts
+    >= 20).  Smaller
     production-size rings get 4 limbs, toy rings 8 (their composite two-row
     rotations spend more real noise per logical op).  CGB_LIMBS overrides."""
     env = os.environ.get("CGB_LIMBS")
@@ -238,10 +239,16 @@ def ring_layout(n_slots: int, p: int) -> tuple[int, bool]:
 
 
 def default_qbits(ring_degree: int) -> int:
-    """Bit size of the Q primes (CGB_QBITS overrides): 60 -> integer-pipe NTT,
-    <= 49 -> FP64-pipe NTT on rings of degree >= 4096."""
+    """Bit size of the primes (CGB_QBITS overrides).
+
+    Rings of degree >= 4096 use primes < 2^49 so their NTTs run on the FP64
+    pipe (exact error-free transformations; 1.2x the integer-pipe NTT per
+    transform, 14% faster decode step than 3 x 60-bit primes on the integer
+    pipe, profiles/r01/params_sweep.md).  Smaller rings keep 60-bit primes."""
     env = os.environ.get("CGB_QBITS")
-    return int(env) if env else 60
+    if env:
+        return int(env)
+    return 49 if ring_degree >= 4096 else 60
 
 
 def ring_for(params, n_limbs: int | None = None, key_seed: int | None = None):

@@ -45,7 +45,7 @@ def test_full_size_decode(api, name):
 
 
 def test_hot_path_noise_margins(api):
-    """Deepest intermediates of decode and prefill keep >= 40 bits of real noise."""
+    """Deepest intermediates of decode and prefill keep >= 20 bits of real noise."""
     import json
     import subprocess
 
@@ -53,7 +53,7 @@ def test_hot_path_noise_margins(api):
                          capture_output=True, text=True, check=True)
     probe = json.loads(res.stdout.strip().splitlines()[-1])
     for k in ("decode_scores", "decode_values", "prefill_diag", "prefill_pv"):
-        assert probe[k] >= 40, (k, probe)
+        assert probe[k] >= 20, (k, probe)
 
 
 def test_full_size_prefill(api):
