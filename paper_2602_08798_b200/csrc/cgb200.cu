@@ -351,8 +351,11 @@ static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
 template <int LA, int LB>
 static void launch_ntt2_colpass(cgb_ring *r, const NttJob &job, int count) {
   const int G = NTT2_TILE / (1 << LA), nsubs = 1 << LB;
-  k_ntt2<LA, LB, true, 0, true, 8><<<dim3((unsigned)((size_t)count * job.nsub * (nsubs / G))), NTT2_TILE / 8,
-                                    ntt2_smem_bytes<LA, LB>(0), r->stream>>>(job);
+  const dim3 grid((unsigned)((size_t)count * job.nsub * (nsubs / G)));
+  if (r->fp_ntt)
+    k_ntt2_fp<LA, LB, true, 0><<<grid, NTT2_TILE / 8, ntt2_smem_bytes<LA, LB>(0), r->stream>>>(job);
+  else
+    k_ntt2<LA, LB, true, 0, true, 8><<<grid, NTT2_TILE / 8, ntt2_smem_bytes<LA, LB>(0), r->stream>>>(job);
 }
 template <int LA, int LB>
 static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) {
@@ -712,10 +715,36 @@ __device__ __forceinline__ void row_pass_fwd(const u64 *src, u64 *data, const ul
   __syncthreads();  // smem is reused by the caller's next tile
 }
 
+// FP64-pipe version (rings with primes < 2^49): same contract, canonical u64 out
 template <int LA, int LB, int E>
+__device__ __forceinline__ void row_pass_fwd_fp(const u64 *src, u64 *smem, const ulonglong2 *tws_raw, int first,
+                                                const ModTab &Md, u64 v[E]) {
+  using RT = RowTile<LA, LB, E>;
+  const int tid = threadIdx.x;
+  double *data = reinterpret_cast<double *>(smem);
+  const double2 *tws = reinterpret_cast<const double2 *>(tws_raw);
+#pragma unroll
+  for (int i = 0; i < E; i++) v[i] = __ldcs(src + ((u64)first << LB) + tid + i * RT::T);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const int e = tid + i * RT::T;
+    data[(e >> LB) * RT::PADM + spad8(e & (RT::M - 1))] = u2d(v[i]);
+  }
+  __syncthreads();
+  const int g = tid / RT::TPS, tl = tid & (RT::TPS - 1);
+  ntt2_sub_fp<LB, E, true>(data + g * RT::PADM, tws + g * RT::M, tl, Md.qd, Md.qinv);
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const int e = tid + i * RT::T;
+    v[i] = fp_canon(data[(e >> LB) * RT::PADM + spad8(e & (RT::M - 1))], Md.qd, Md.qinv);
+  }
+  __syncthreads();
+}
+
+template <int LA, int LB, int E, bool FP = false>
 __device__ __forceinline__ void stage_row_twiddles(ulonglong2 *tws, const ModTab &Md, int first) {
   using RT = RowTile<LA, LB, E>;
-  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(Md.tw1);
+  const ulonglong2 *gtw = reinterpret_cast<const ulonglong2 *>(FP ? Md.ftw1 : Md.tw1);
 #pragma unroll
   for (int j = 0; j < E; j++) {
     const int e = threadIdx.x + j * RT::T;
@@ -726,7 +755,7 @@ __device__ __forceinline__ void stage_row_twiddles(ulonglong2 *tws, const ModTab
 // ModUp row pass fused with the key inner product:
 //   acc[item][p][l] = sum_j NTT_l(lift_l(digit j)) * key[j][p][l]   (j == l: the input limb itself)
 // D holds the column-pass outputs [item][j][l][N] (units j(L+1)+l, l != j).
-template <int LA, int LB, int L, int E>
+template <int LA, int LB, int L, int E, bool FP = false>
 __global__ void __launch_bounds__(NTT2_TILE / E) k_modup_ks(const u64 *D, KsSrc x, const u64 *const *keys, u64 kw,
                                                            u64 *acc, const ModTab *mods) {
   using RT = RowTile<LA, LB, E>;
@@ -740,7 +769,7 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_modup_ks(const u64 *D, KsSrc 
   u64 *data = smf;
   ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(smf + ((RT::G * RT::PADM + 1) & ~1));
   const int first = tile * RT::G, tid = threadIdx.x;
-  stage_row_twiddles<LA, LB, E>(tws, Md, first);
+  stage_row_twiddles<LA, LB, E, FP>(tws, Md, first);
   const u64 *K = keys[item];
   u64 a0[E], a1[E];
 #pragma unroll
@@ -752,7 +781,8 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_modup_ks(const u64 *D, KsSrc 
 #pragma unroll
       for (int i = 0; i < E; i++) v[i] = ks_src_word(x, item, j, (u32)(((u64)first << LB) + tid + i * RT::T), LOGN);
     } else {
-      row_pass_fwd<LA, LB, E>(D + (((u64)item * L + j) * LP + l) * N, data, tws, first, q, v);
+      if (FP) row_pass_fwd_fp<LA, LB, E>(D + (((u64)item * L + j) * LP + l) * N, data, tws, first, Md, v);
+      else row_pass_fwd<LA, LB, E>(D + (((u64)item * L + j) * LP + l) * N, data, tws, first, q, v);
     }
     const u64 *kb = K + ((u64)j * 2 + 0) * LP * N + (u64)l * N + ((u64)first << LB);
     const u64 *ka = K + ((u64)j * 2 + 1) * LP * N + (u64)l * N + ((u64)first << LB);
@@ -788,7 +818,7 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_modup_ks(const u64 *D, KsSrc 
 // ModDown row pass fused with the combine:
 //   out[p][l] = (acc[p][l] - NTT_l(lift_l(acc[p][P]))) * P^-1 + (p == 0 ? add0 : 0) + add1[p][l]
 // W holds the column-pass outputs [item][p][l][N] (units pL + l).
-template <int LA, int LB, int E>
+template <int LA, int LB, int E, bool FP = false>
 __global__ void __launch_bounds__(NTT2_TILE / E) k_moddown_fused(const u64 *W, const u64 *acc, u64 *const *out,
                                                                 KsSrc add0, const u64 *const *add1,
                                                                 const ModTab *mods, const Consts *C, int L) {
@@ -803,9 +833,10 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_moddown_fused(const u64 *W, c
   u64 *data = smf;
   ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(smf + ((RT::G * RT::PADM + 1) & ~1));
   const int first = tile * RT::G, tid = threadIdx.x;
-  stage_row_twiddles<LA, LB, E>(tws, Md, first);
+  stage_row_twiddles<LA, LB, E, FP>(tws, Md, first);
   u64 v[E];
-  row_pass_fwd<LA, LB, E>(W + ((u64)item * 2 * L + pl) * N, data, tws, first, q, v);
+  if (FP) row_pass_fwd_fp<LA, LB, E>(W + ((u64)item * 2 * L + pl) * N, data, tws, first, Md, v);
+  else row_pass_fwd<LA, LB, E>(W + ((u64)item * 2 * L + pl) * N, data, tws, first, q, v);
   const u64 LP = L + 1;
   const u64 *A = acc + (((u64)item * 2 + p) * LP + l) * N;
   const u64 pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
@@ -1282,8 +1313,11 @@ static void keyswitch_fused_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count
   {
     const u64 kw = (u64)L * 2 * LP * N;
     launch_begin(r);
-    k_modup_ks<LA, LB, L, E><<<dim3((unsigned)((size_t)count * LP * RT::TILES)), RT::T, RT::smem(), r->stream>>>(
-        D, x, d_keys, kw, acc, r->d_mods);
+    const dim3 grid((unsigned)((size_t)count * LP * RT::TILES));
+    if (r->fp_ntt)
+      k_modup_ks<LA, LB, L, E, true><<<grid, RT::T, RT::smem(), r->stream>>>(D, x, d_keys, kw, acc, r->d_mods);
+    else
+      k_modup_ks<LA, LB, L, E, false><<<grid, RT::T, RT::smem(), r->stream>>>(D, x, d_keys, kw, acc, r->d_mods);
     launch_end(r, "modup_ks", 8.0 * (double)count * LP * N * (L * 2.0 + 2.0));
   }
   // ModDown: INTT the P limbs (both passes), column pass of their lift into Q -> W
@@ -1328,15 +1362,22 @@ static void keyswitch_fused_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count
   launch_ntt2_colpass<LA, LB>(r, job, count);
   launch_end(r, "ntt_fwd", 16.0 * (double)count * n * N);
   launch_begin(r);
-  k_moddown_fused<LA, LB, E><<<dim3((unsigned)((size_t)count * 2 * L * RT::TILES)), RT::T, RT::smem(), r->stream>>>(
-      W, acc, d_out, add0, d_add1, r->d_mods, r->d_c, L);
+  const dim3 gridm((unsigned)((size_t)count * 2 * L * RT::TILES));
+  if (r->fp_ntt)
+    k_moddown_fused<LA, LB, E, true><<<gridm, RT::T, RT::smem(), r->stream>>>(W, acc, d_out, add0, d_add1, r->d_mods,
+                                                                            r->d_c, L);
+  else
+    k_moddown_fused<LA, LB, E, false><<<gridm, RT::T, RT::smem(), r->stream>>>(W, acc, d_out, add0, d_add1, r->d_mods,
+                                                                             r->d_c, L);
   launch_end(r, "moddown_fused", 8.0 * (double)count * 2 * L * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)));
 }
 template <int LA, int LB, int L>
 static void fused_attrs() {
   const int s = (int)RowTile<LA, LB, 8>::smem();
-  CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
-  CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_modup_ks<LA, LB, L, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
+  CK(cudaFuncSetAttribute(k_moddown_fused<LA, LB, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
 }
 static bool keyswitch_fused(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                             const KsSrc &add0, const u64 *const *d_add1) {
