@@ -291,6 +291,7 @@ def run_ours(args):
     one_step(dev_tokens[args.warmup])
     rep = ring.timing_report()
     ring.timing(False)
+    idle_ms = rep.pop("(idle)", (0, 0.0, 0.0))[1]
     peak_mm = ring.modmul_peak()
 
     ms, ms_e2e = max_over_ranks(ms, world), max_over_ranks(ms_e2e, world)
@@ -328,6 +329,7 @@ def run_ours(args):
         "kernels": {k: {"launches": v[0], "ms": round(v[1], 4), "GBps": round(v[2] / (v[1] * 1e-3) / 1e9, 1)
                         if v[1] else None} for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])},
         "clocks": clk.summary(),
+        "gpu_idle_ms_per_step": round(idle_ms, 2),
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, samples=1)

@@ -2036,6 +2036,19 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
     it->second.ms += ms;
     it->second.bytes += rc.bytes;
   }
+  // GPU idle time between consecutive recorded launches (host gaps, syncs)
+  double idle = 0, idle_max = 0;
+  for (size_t i = 1; i < r->recs.size(); i++) {
+    float g = 0;
+    CK(cudaEventElapsedTime(&g, r->recs[i - 1].b, r->recs[i].a));
+    if (g > 0) {
+      idle += g;
+      idle_max = std::max(idle_max, (double)g);
+    }
+  }
+  agg.push_back({"(idle)", Agg{}});
+  agg.back().second.n = (long)r->recs.size();
+  agg.back().second.ms = idle;
   std::string out;
   for (auto &kv : agg) {
     char line[256];
