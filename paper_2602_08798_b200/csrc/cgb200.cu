@@ -194,9 +194,12 @@ struct cgb_ring {
   std::vector<char> pt_used;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  // pinned staging for pointer tables / host payloads
+  // pinned staging for pointer tables / host payloads: two halves used in turn;
+  // entering a half waits only for the event recorded when it was last left
   char *pin = nullptr;
   size_t pin_cap = 0, pin_off = 0;
+  int pin_half = 0;
+  cudaEvent_t pin_left[2] = {nullptr, nullptr};
   u64 launches = 0;
   std::mutex mu;
   // per-launch timing (cgb_timing_enable): events around every kernel
@@ -226,15 +229,19 @@ static T *stage_to_device(cgb_ring *r, const T *host, size_t n, std::vector<void
   T *dev;
   CK(cudaMallocAsync((void **)&dev, bytes, r->stream));
   frees.push_back(dev);
-  if (bytes > r->pin_cap) {  // large payload: staged by the driver
+  const size_t half = r->pin_cap / 2;
+  if (bytes > half) {  // large payload: staged by the driver
     CK(cudaMemcpyAsync(dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
     return dev;
   }
-  if (r->pin_off + bytes > r->pin_cap) {
-    CK(cudaStreamSynchronize(r->stream));  // ring wrap: previous copies have consumed the buffer
+  if (r->pin_off + bytes > half) {  // switch halves
+    if (!r->pin_left[r->pin_half]) CK(cudaEventCreateWithFlags(&r->pin_left[r->pin_half], cudaEventDisableTiming));
+    CK(cudaEventRecord(r->pin_left[r->pin_half], r->stream));
+    r->pin_half ^= 1;
+    if (r->pin_left[r->pin_half]) CK(cudaEventSynchronize(r->pin_left[r->pin_half]));
     r->pin_off = 0;
   }
-  char *dst = r->pin + r->pin_off;
+  char *dst = r->pin + (size_t)r->pin_half * half + r->pin_off;
   memcpy(dst, host, sizeof(T) * n);
   CK(cudaMemcpyAsync(dev, dst, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
   r->pin_off += bytes;
@@ -1911,7 +1918,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
-  r->pin_cap = 8u << 20;
+  r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
   build_ring(r, key_seed);
   r->ct_words = 2ull * r->L * r->N;
@@ -1939,6 +1946,8 @@ void cgb_ring_destroy(cgb_ring *r) {
   cudaFree(r->d_s);
   cudaFree(r->d_c);
   cudaFreeHost(r->pin);
+  for (auto e : r->pin_left)
+    if (e) cudaEventDestroy(e);
   if (r->own_stream) cudaStreamDestroy(r->stream);
   delete r;
 }
