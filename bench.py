@@ -292,6 +292,9 @@ def run_ours(args):
     rep = ring.timing_report()
     ring.timing(False)
     idle_ms = rep.pop("(idle)", (0, 0.0, 0.0))[1]
+    gaps = {k: round(v[1], 3) for k, v in rep.items() if k.startswith("(gap")}
+    for k in gaps:
+        rep.pop(k)
     peak_mm = ring.modmul_peak()
 
     ms, ms_e2e = max_over_ranks(ms, world), max_over_ranks(ms_e2e, world)
@@ -330,6 +333,7 @@ def run_ours(args):
                         if v[1] else None} for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])},
         "clocks": clk.summary(),
         "gpu_idle_ms_per_step": round(idle_ms, 2),
+        "gpu_idle_top_gaps_ms": gaps,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, samples=1)

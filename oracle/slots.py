@@ -247,7 +247,7 @@ class SlotContext:
                         SlotContext._charge(wa, "add"))
 
     @staticmethod
-    def w_add_plain(wave, vecs):
+    def w_add_plain(wave, vecs, one_shot=False):
         if hasattr(vecs, "build"):
             vecs = vecs.build(vecs.keys)
         c = wave.ctxs[0]
@@ -257,7 +257,7 @@ class SlotContext:
                         SlotContext._charge(wave, "add_plain"))
 
     @staticmethod
-    def w_mult_plain(wave, vecs):
+    def w_mult_plain(wave, vecs, one_shot=False):
         if hasattr(vecs, "build"):  # PlainBatch (symbolic rows)
             vecs = vecs.build(vecs.keys)
         c = wave.ctxs[0]

@@ -472,7 +472,7 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
             acc = C.w_sum(pieces, [np.arange(k * m, (k + 1) * m) for k in range(cs.size)])
             # he_to_shares with the planned masks, then truncate / re-encrypt
             r = np.stack([plan[c][0] for c in cs])
-            masked = C.w_add_plain(acc, (p - r) % p)
+            masked = C.w_add_plain(acc, (p - r) % p, one_shot=True)
             client = C.w_decrypt(masked)
             trs = []
             for k, c in enumerate(cs):

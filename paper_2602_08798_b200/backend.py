@@ -661,7 +661,7 @@ class GpuContext:
         return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "add"))
 
     @staticmethod
-    def _plain_op(wave: Wave, vecs, kind, field_name):
+    def _plain_op(wave: Wave, vecs, kind, field_name, one_shot: bool = False):
         c0 = wave.ctxs[0]
         cost = getattr(c0.params.noise_costs, field_name)
         b = GpuContext._spend_all(wave.budgets, cost)
@@ -669,19 +669,29 @@ class GpuContext:
             vecs = np.mod(np.asarray(vecs, dtype=np.int64), c0.params.plain_modulus)
             if vecs.ndim == 1:
                 vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
-        _, pts = c0._plaintexts(vecs, kind)
+        ring = c0._ring
+        fn = ring.add_plain if kind == nat.CGB_PT_ADD else ring.mult_plain
         blk, ids = c0._new(len(wave))
-        fn = c0._ring.add_plain if kind == nat.CGB_PT_ADD else c0._ring.mult_plain
-        fn(wave.aids, pts, ids)
+        if one_shot and not isinstance(vecs, PlainBatch):
+            # random masks never recur: encode into scratch plaintexts, no hashing, no cache
+            pts = ring.alloc_pt(len(wave))
+            try:
+                ring.encode_pt(vecs, kind, pts)
+                fn(wave.aids, pts, ids)
+            finally:
+                ring.free_pt(pts)  # stream-ordered: later encodes run after this op
+        else:
+            _, pts = c0._plaintexts(vecs, kind)
+            fn(wave.aids, pts, ids)
         return Wave(wave.ctxs, wave.owner, ids, b, [blk], GpuContext._charge(wave, field_name))
 
     @staticmethod
-    def w_add_plain(wave: Wave, vecs) -> Wave:
-        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain")
+    def w_add_plain(wave: Wave, vecs, one_shot: bool = False) -> Wave:
+        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain", one_shot)
 
     @staticmethod
-    def w_mult_plain(wave: Wave, vecs) -> Wave:
-        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_MUL, "mult_plain")
+    def w_mult_plain(wave: Wave, vecs, one_shot: bool = False) -> Wave:
+        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_MUL, "mult_plain", one_shot)
 
     @staticmethod
     def w_mult_cipher(wa: Wave, wb: Wave) -> Wave:

@@ -2046,18 +2046,27 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
     it->second.bytes += rc.bytes;
   }
   // GPU idle time between consecutive recorded launches (host gaps, syncs)
-  double idle = 0, idle_max = 0;
+  double idle = 0;
+  std::vector<std::pair<float, size_t>> gaps;
   for (size_t i = 1; i < r->recs.size(); i++) {
     float g = 0;
     CK(cudaEventElapsedTime(&g, r->recs[i - 1].b, r->recs[i].a));
     if (g > 0) {
       idle += g;
-      idle_max = std::max(idle_max, (double)g);
+      gaps.push_back({g, i});
     }
   }
   agg.push_back({"(idle)", Agg{}});
   agg.back().second.n = (long)r->recs.size();
   agg.back().second.ms = idle;
+  std::sort(gaps.begin(), gaps.end(), [](auto &x, auto &y) { return x.first > y.first; });
+  for (size_t k = 0; k < std::min<size_t>(5, gaps.size()); k++) {
+    char nm[96];
+    snprintf(nm, sizeof nm, "(gap%zu:%s->%s)", k, r->recs[gaps[k].second - 1].name, r->recs[gaps[k].second].name);
+    agg.push_back({nm, Agg{}});
+    agg.back().second.n = (long)gaps[k].second;
+    agg.back().second.ms = gaps[k].first;
+  }
   std::string out;
   for (auto &kv : agg) {
     char line[256];

@@ -212,12 +212,12 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     owners = [ctxs[s[0]] for s in sel]
     start = {id(c): c._next_id for c in owners}
     wave = C.wave_of([s[3] for s in sel], owners)
-    masked = C.w_add_plain(wave, (p - r) % p)
+    masked = C.w_add_plain(wave, (p - r) % p, one_shot=True)
     view = C.w_decrypt(masked)
     fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view)
     for h, _, _, _ in sel:
         chans[h].transfer("refresh", n, trips=2)
-    restored = _retag(C.w_add_plain(fresh, r).handles(), _chain_ids(owners, [3] * len(sel), start))
+    restored = _retag(C.w_add_plain(fresh, r, one_shot=True).handles(), _chain_ids(owners, [3] * len(sel), start))
     out = []
     for h, cache in enumerate(caches):
         mine = [(k, s) for k, s in enumerate(sel) if s[0] == h]

@@ -97,7 +97,7 @@ def he_to_shares_wave(wave, chans, lengths) -> list:
         if not 0 < L <= n:
             raise ParameterError(f"share length {L} out of range")
     r = np.stack([ch.sample_mask(n) for ch in chans]) if len(chans) else np.zeros((0, n), np.int64)
-    masked = C.w_add_plain(wave, (p - r) % p)
+    masked = C.w_add_plain(wave, (p - r) % p, one_shot=True)
     client = C.w_decrypt(masked)
     out = []
     for i, ch in enumerate(chans):
@@ -116,7 +116,7 @@ def shares_to_he_wave(shares, ctxs, chans, record: bool = True):
     client = np.stack([c.plain_from_dense(s.client) for c, s in zip(ctxs, shares)])
     server = np.stack([c.plain_from_dense(s.server) for c, s in zip(ctxs, shares)])
     enc = C.w_encrypt(ctxs, client)
-    out = C.w_add_plain(enc, server)
+    out = C.w_add_plain(enc, server, one_shot=True)
     if record:
         for ch in chans:
             ch.transfer("shares_to_he", n)
