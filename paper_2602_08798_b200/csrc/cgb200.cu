@@ -333,6 +333,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 
 // NTT launcher -------------------------------------------------------------
 static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
+static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
 template <int LA, int LB, bool QS, int E>
 static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
@@ -376,6 +377,37 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
     return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
   };
   const size_t s0 = ntt2_smem_bytes<LA, LB>(0), s1 = ntt2_smem_bytes<LA, LB>(1);
+  if (g_fp_regio && LA >= 5 && LB >= 5 && LA <= 8 && LB <= 8) {
+    const size_t f0 = fpr_smem_bytes<LA, LB>(0), f1 = fpr_smem_bytes<LA, LB>(1);
+    // register-I/O passes (16 words/thread) where CGB_FP_REGIO's bit for the pass is set
+    const bool r0 = g_fp_regio & 1, r1 = g_fp_regio & 2;
+    auto pass0 = [&](const NttJob &j, bool f) {
+      if (r0) {
+        if (f) k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j);
+        else k_ntt2_fpr<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j);
+      } else {
+        if (f) k_ntt2_fp<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
+        else k_ntt2_fp<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
+      }
+    };
+    auto pass1 = [&](const NttJob &j, bool f) {
+      if (r1) {
+        if (f) k_ntt2_fpr<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j);
+        else k_ntt2_fpr<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j);
+      } else {
+        if (f) k_ntt2_fp<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
+        else k_ntt2_fp<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
+      }
+    };
+    if (fwd) {
+      pass0(job, true);
+      pass1(second, true);
+    } else {
+      pass1(job, false);
+      pass0(second, false);
+    }
+    return;
+  }
   const int T = NTT2_TILE / 8;
   if (fwd) {
     k_ntt2_fp<LA, LB, true, 0><<<grid(LA), T, s0, r->stream>>>(job);
@@ -400,6 +432,11 @@ static void ntt2_attrs() {
   NTT2A(true, 0, true, 16) NTT2A(true, 1, true, 16) NTT2A(false, 0, true, 16) NTT2A(false, 1, true, 16)
   NTT2A(true, 0, false, 16) NTT2A(true, 1, false, 16) NTT2A(false, 0, false, 16) NTT2A(false, 1, false, 16)
 #undef NTT2A
+  const int f0 = (int)fpr_smem_bytes<LA, LB>(0), f1 = (int)fpr_smem_bytes<LA, LB>(1);
+  CK(cudaFuncSetAttribute(k_ntt2_fpr<LA, LB, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, f0));
+  CK(cudaFuncSetAttribute(k_ntt2_fpr<LA, LB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, f1));
+  CK(cudaFuncSetAttribute(k_ntt2_fpr<LA, LB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, f0));
+  CK(cudaFuncSetAttribute(k_ntt2_fpr<LA, LB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, f1));
   CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
   CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
   CK(cudaFuncSetAttribute(k_ntt2_fp<LA, LB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, s));
@@ -1676,7 +1713,9 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
   r->mods.push_back(r->t);
   r->nmod = (int)r->mods.size();
   // twiddle tables
-  size_t per = 16ull * N;  // tw | itw | tw1 | itw1 (u64 (w, w') pairs) | the same four as (w, w/q) doubles
+  // tw | itw | tw1 | itw1 (u64 (w, w') pairs) | the same four as (w, w/q) doubles | ftw1 / fitw1 with
+  // each row's levels >= 4 transposed ([j][blk]) for the register-I/O FP64 kernel (k_ntt2_fpr)
+  size_t per = 20ull * N;
   CK(cudaMalloc((void **)&r->d_tables, sizeof(u64) * per * r->nmod));
   std::vector<u64> tab(per);
   r->h_mods.resize(r->nmod);
@@ -1715,6 +1754,22 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
         memcpy(&tab[8ull * N + (size_t)o * 2 * N + 2 * k], &wd, 8);
         memcpy(&tab[8ull * N + (size_t)o * 2 * N + 2 * k + 1], &wq, 8);
       }
+    if (logN >= 12) {
+      const int M = 1 << (logN - logN / 2);
+      for (int o = 0; o < 2; o++)
+        for (int row = 0; row < N / M; row++)
+          for (int ii = 0; ii < M; ii++) {
+            int pos = ii;
+            if (ii >= 16) {
+              const int sl = 31 - __builtin_clz((unsigned)ii), l = sl - 4, off = ii - (1 << sl);
+              pos = (1 << sl) + ((off & ((1 << l) - 1)) << 4) + (off >> l);
+            }
+            const size_t from = 12ull * N + (size_t)o * 2 * N + 2ull * ((size_t)row * M + ii);
+            const size_t to = 16ull * N + (size_t)o * 2 * N + 2ull * ((size_t)row * M + pos);
+            tab[to] = tab[from];
+            tab[to + 1] = tab[from + 1];
+          }
+    }
     u64 *dt = r->d_tables + per * i;
     CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
     ModTab &M = r->h_mods[i];
@@ -1735,6 +1790,8 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.fitw = dt + 10 * N;
     M.ftw1 = dt + 12 * N;
     M.fitw1 = dt + 14 * N;
+    M.ftw1t = dt + 16 * N;
+    M.fitw1t = dt + 18 * N;
     M.qd = (double)q;
     M.qinv = 1.0 / (double)q;
     M.ninv_fp = (double)M.ninv;
@@ -1916,6 +1973,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
     }
   }
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
+  if (const char *e = getenv("CGB_FP_REGIO")) g_fp_regio = atoi(e) & 3;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;

@@ -26,6 +26,7 @@ struct ModTab {
   const u64 *tw, *tw_sh, *itw, *itw_sh;  // bit-reversed psi powers + Shoup companions
   const u64 *tw1, *itw1;                 // the same pairs in two-pass row-tile order (see k_ntt2)
   const u64 *ftw, *fitw, *ftw1, *fitw1;  // FP64 twiddles (w, w/q) as double pairs, same orders
+  const u64 *ftw1t, *fitw1t;             // ftw1 / fitw1, levels >= 4 of each row transposed
   double qd, qinv;                       // q and 1/q as doubles (FP64 NTT)
   double ninv_fp, ninv_fpq;              // N^-1 and N^-1 / q as doubles
   int bits;
@@ -602,6 +603,190 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_ntt2_fp(NttJob job) {
     double x = data[g * PADM + spad8(k)];
     if (last && !FWD) x = fp_mulmod(fp_reduce(x, qd, qinv), ni, Md.ninv_fpq, qd);
     p[w] = fp_canon(x, qd, qinv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 two-pass NTT, register I/O: the first phase reads global memory straight
+// into registers and the last phase writes registers straight back, so a pass
+// with 16 words per thread needs a single shared-memory exchange.  Pass 0
+// (columns) maps consecutive threads to consecutive columns and pass 1 (rows)
+// to consecutive words of a row, which keeps both ends coalesced.
+// ---------------------------------------------------------------------------
+// 256-bit global accesses (one full 32-byte sector per thread; sm_100 LDG/STG.256)
+__device__ __forceinline__ void ld256(const u64 *p, u64 *v) {
+  asm volatile("ld.global.cs.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st256(u64 *p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
+// Row padding of k_ntt2_fpr's shared tile: word i of a row sits at i + (i >> fpr_psh)
+// in a row of fpr_padm words.  Chosen with scripts/sim/smem_banks.py (per
+// half-warp bank model, matches ncu) so the shared accesses of both phases take
+// the 2-wavefront minimum of a warp of doubles (3 for the 32-point row pass).
+__host__ __device__ constexpr int fpr_psh(int LM, int pass) { return LM == 8 ? 4 : (pass == 1 && LM <= 6) ? 2 : 3; }
+__host__ __device__ constexpr int fpr_padm(int LM, int pass) {
+  return (1 << LM) + ((1 << LM) >> fpr_psh(LM, pass)) +
+         (LM == 8 ? 2 : pass == 0 ? 1 : LM == 7 ? 8 : LM == 6 ? 4 : 2);
+}
+template <int LA, int LB>
+__host__ size_t fpr_smem_bytes(int pass) {  // data tile (+ the shared column-pass twiddles)
+  const int LM = pass == 0 ? LA : LB, G = NTT2_TILE >> LM;
+  return sizeof(u64) * (size_t)((G * fpr_padm(LM, pass) + 1) & ~1) + (pass == 0 ? 16 * (size_t)(1 << LM) : 0);
+}
+
+template <int LM, int S0, int RP, int E>
+struct PhaseShape {
+  static constexpr int K = 1 << RP, R = E / K, S = (1 << LM) >> S0, ST = S >> RP;
+  static constexpr int TPS = (1 << LM) / E;  // threads per sub-NTT
+  // local index (inside the sub-NTT) of register u*K + k of thread tl; a thread's
+  // rows are interleaved (tl, tl + TPS, ...) so consecutive threads take consecutive
+  // blocks and read consecutive twiddles
+  static __device__ __forceinline__ int row(int tl, int u) { return tl + u * TPS; }
+  static __device__ __forceinline__ int idx(int tl, int u, int k) {
+    const int r = row(tl, u), blk = r / ST;
+    return blk * S + (r & (ST - 1)) + k * ST;
+  }
+};
+// TRANS: stage levels >= S0 of the twiddle table are stored transposed
+// ([j][blk] instead of [blk][j], see k_ntt2_fpr) so threads on consecutive
+// blocks read consecutive entries.
+// GTW: tws is a global table (read through the read-only path) instead of shared memory
+template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false>
+__device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, int tl, double q, double qinv) {
+  using PS = PhaseShape<LM, S0, RP, E>;
+  constexpr int K = PS::K, R = PS::R;
+#pragma unroll
+  for (int u = 0; u < R; u++) {
+    const int blk = PS::row(tl, u) / PS::ST;
+#pragma unroll
+    for (int ll = 0; ll < RP; ll++) {
+      const int l = FWD ? ll : RP - 1 - ll;
+      const int half = K >> (l + 1);
+      double2 W;
+#pragma unroll
+      for (int k = 0; k < K; k++) {
+        if (k & half) continue;
+        if ((k & ((1 << (RP - l)) - 1)) == 0) {
+          const int ti = TRANS ? (1 << (S0 + l)) + ((k >> (RP - l)) << S0) + blk
+                               : (1 << (S0 + l)) + (blk << l) + (k >> (RP - l));
+          W = GTW ? __ldg(tws + ti) : tws[ti];
+        }
+        double &X = x[u * K + k], &Y = x[u * K + k + half];
+        if (FWD) {
+          const double t = fp_mulmod(Y, W.x, W.y, q);
+          Y = X - t;
+          X = X + t;
+        } else {
+          const double d = X - Y;
+          X = fp_reduce(X + Y, q, qinv);
+          Y = fp_mulmod(d, W.x, W.y, q);
+        }
+      }
+    }
+  }
+}
+
+// LM-point sub-NTT in two register phases (RA stages then LM - RA), E = 16
+template <int LA, int LB, bool FWD, int PASS>
+__global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job) {
+  extern __shared__ u64 sm2[];
+  constexpr int E = 16, T = NTT2_TILE / E;
+  constexpr int LOGN = LA + LB;
+  constexpr int LM = PASS == 0 ? LA : LB, M = 1 << LM;
+  constexpr int G = NTT2_TILE / M, TPS = M / E;
+  constexpr int NSUBS = 1 << (PASS == 0 ? LB : LA), TILES = NSUBS / G;
+  constexpr int PSH = fpr_psh(LM, PASS), PADM = fpr_padm(LM, PASS);
+  auto spad = [](int i) { return i + (i >> PSH); };
+  constexpr int RA = 4, RB = LM - 4;  // forward: stages [0,4) then [4,LM); inverse: the reverse
+  static_assert(RB >= 1 && RB <= 4, "sub-NTT of 32..256 points");
+  const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
+  const int item = unit / job.nsub, sub = unit - item * job.nsub;
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << LOGN);
+  const ModTab &Md = job.mods[job.sub_mod[sub]];
+  const u64 q = Md.q;
+  const double qd = Md.qd, qinv = Md.qinv;
+  const int tid = threadIdx.x;
+  double *data = reinterpret_cast<double *>(sm2);
+  double2 *tws = reinterpret_cast<double2 *>(sm2 + ((G * PADM + 1) & ~1));
+  const double2 *gtw = reinterpret_cast<const double2 *>(
+      PASS == 0 ? (FWD ? Md.ftw : Md.fitw) : (FWD ? Md.ftw1t : Md.fitw1t));
+  const int first = tile * G;
+  // thread -> (sub-NTT g, thread-in-sub tl): columns fast in pass 0, words fast in pass 1
+  const int g = PASS == 0 ? (tid % G) : (tid / TPS);
+  const int tl = PASS == 0 ? (tid / G) : (tid % TPS);
+  auto gaddr = [&](int i) -> u64 {
+    return PASS == 0 ? (((u64)i << LB) + first + g) : (((u64)(first + g) << LM) + i);
+  };
+  // pass 0 shares one M-entry table (staged); pass 1 reads its row's table from global
+  if (PASS == 0)
+    for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
+  // first phase straight from global memory (fused lift / automorphism)
+  const u64 *src = job_src(job, item, sub, LOGN);
+  if (!src) src = p;
+  const bool lift = job.lift != 0;
+  const u64 qs = lift ? job.mods[job.src_mod[sub]].q : 0;
+  const u64 gal = job.galois ? job.galois[item] : 1;
+  constexpr int S0A = FWD ? 0 : RA, RPA = FWD ? RA : RB;   // first phase (stages)
+  constexpr int S0B = FWD ? RA : 0, RPB = FWD ? RB : RA;   // second phase
+  using PA = PhaseShape<LM, S0A, RPA, E>;
+  using PB = PhaseShape<LM, S0B, RPB, E>;
+  double x[E];
+  {
+    u64 v[E];
+    if (PASS == 1 && PA::ST == 1 && PA::K % 4 == 0 && gal == 1) {  // K consecutive words: full-sector loads
+#pragma unroll
+      for (int u = 0; u < PA::R; u++)
+#pragma unroll
+        for (int k = 0; k < PA::K; k += 4) ld256(src + gaddr(PA::idx(tl, u, k)), &v[u * PA::K + k]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < PA::R; u++)
+#pragma unroll
+        for (int k = 0; k < PA::K; k++) {
+          const u64 a = gaddr(PA::idx(tl, u, k));
+          v[u * PA::K + k] = gal == 1 ? __ldcs(src + a) : __ldg(src + perm_g((u32)a, gal, LOGN));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < E; i++) x[i] = u2d(lift ? centred_to(v[i], qs, q) : v[i]);
+  }
+  __syncthreads();  // twiddles staged
+  const double2 *tw_g = PASS == 0 ? tws : gtw + ((u64)(first + g) << LM);
+  phase_regs_fp<LM, S0A, RPA, FWD, E, PASS == 1 && S0A == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
+  double *sd = data + g * PADM;
+#pragma unroll
+  for (int u = 0; u < PA::R; u++)
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, u, k))] = x[u * PA::K + k];
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < PB::R; u++)
+#pragma unroll
+    for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = fp_reduce(sd[spad(PB::idx(tl, u, k))], qd, qinv);
+  phase_regs_fp<LM, S0B, RPB, FWD, E, PASS == 1 && S0B == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
+  const bool last = FWD ? (PASS == 1) : (PASS == 0);
+  const double ni = Md.ninv_fp, niq = Md.ninv_fpq;
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    if (last && !FWD) x[i] = fp_mulmod(fp_reduce(x[i], qd, qinv), ni, niq, qd);
+  }
+  if (PASS == 1 && PB::ST == 1 && PB::K % 4 == 0) {  // K consecutive words: full-sector stores
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k += 4) {
+        const double *y = &x[u * PB::K + k];
+        st256(p + gaddr(PB::idx(tl, u, k)), fp_canon(y[0], qd, qinv), fp_canon(y[1], qd, qinv),
+              fp_canon(y[2], qd, qinv), fp_canon(y[3], qd, qinv));
+      }
+  } else {
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k++) p[gaddr(PB::idx(tl, u, k))] = fp_canon(x[u * PB::K + k], qd, qinv);
   }
 }
 
