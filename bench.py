@@ -325,8 +325,10 @@ def run_ours(args):
                      "frac": achieved / hbm_peak, "traffic": None, "launches_per_step": nl,
                      "share_of_step": kms / step_kernel_ms if step_kernel_ms else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
-        "int_pipe": {"kernel": "ntt_fwd+ntt_inv", "modmuls_per_s": ntt_mm / (ntt_ms * 1e-3) if ntt_ms else None,
+        "ntt_pipe": {"kernel": "ntt_fwd+ntt_inv", "pipe": "fp64" if ring.fp_ntt else "int64",
+                     "modmuls_per_s": ntt_mm / (ntt_ms * 1e-3) if ntt_ms else None,
                      "peak_modmuls_per_s": peak_mm,
+                     "peak_source": "cgb_modmul_peak: measured chains of the same modular product",
                      "frac": (ntt_mm / (ntt_ms * 1e-3)) / peak_mm if ntt_ms else None,
                      "share_of_step": ntt_ms / step_kernel_ms if step_kernel_ms else None},
         "kernels": {k: {"launches": v[0], "ms": round(v[1], 4), "GBps": round(v[2] / (v[1] * 1e-3) / 1e9, 1)

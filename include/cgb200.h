@@ -80,8 +80,10 @@ int cgb_timing_enable(cgb_ring *ring, int on);
 /* aggregate of the recorded launches, one line per kernel:
  * "<name> <launches> <total ms> <algorithmic bytes>\n" */
 int cgb_timing_report(cgb_ring *ring, char *buf, size_t cap);
-/* measured integer-pipe peak of the NTT's 64-bit Shoup modular multiply
- * (register-resident independent chains over the whole GPU), per second */
+/* measured peak of the modular multiply on the pipe this ring's NTT uses
+ * (register-resident independent chains over the whole GPU), per second:
+ * the FP64 error-free product for rings of primes < 2^49 (FP64-pipe NTT),
+ * else the 64-bit integer Shoup product */
 int cgb_modmul_peak(cgb_ring *ring, double *modmuls_per_s);
 /* microbenchmark: average ms of one batched forward (fwd=1) / inverse NTT over
  * count ciphertexts (2 L limb-polys each), timed over iters launches */

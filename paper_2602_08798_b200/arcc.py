@@ -287,6 +287,20 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
     parts = []
     for kind, idx in waves:
         parts.append((pref_acc if kind == "p" else auto_sc).take([idx]))
+    # Every channel draw of this step is known now: score masks, weight re-share,
+    # output masks, truncation re-share.  Drawing them while the GPU works on the
+    # scores takes the RNG off the two client round trips (same calls, same order).
+    plan = [(ch, n) for ch in chans]
+    for h in range(H):
+        cache = caches[h]
+        if cache.m > 0:
+            plan.append((mpcs[h], cache.m))
+        if cache.t_auto > 0:
+            plan.extend((mpcs[h], n) for _ in range(len(cache.auto_V.parts)))
+    plan.extend((mpcs[h], n) for h in range(H))
+    plan.extend((mpcs[h], caches[h].d2) for h in range(H))
+    for ch, length in plan:
+        ch.predraw([length])
     shares = he_to_shares_wave(W.concat(parts), chans, lens) if parts else []
     # ---- client: reassemble scores, softmax -------------------------------------
     weights, si = [], 0

@@ -399,11 +399,21 @@ def onehot_batch(n: int, slots) -> PlainBatch:
 _context_uid = itertools.count()
 
 
+def residues(values, t: int) -> np.ndarray:
+    """int64 residues mod t.  Inputs already in [0, t) (shares, masks, decoded
+    slots) are returned as they are: the integer modulo is the costliest host
+    pass on the client round trips."""
+    arr = np.asarray(values, dtype=np.int64)
+    if arr.size == 0 or (arr.min() >= 0 and arr.max() < t):
+        return arr
+    return np.mod(arr, t)
+
+
 def _as_slots(values, params) -> np.ndarray:
     arr = np.asarray(values, dtype=np.int64)
     if arr.ndim != 1 or arr.shape[0] != params.n_slots:
         raise ParameterError(f"expected a vector of length {params.n_slots}, got shape {arr.shape}")
-    return np.mod(arr, params.plain_modulus)
+    return residues(arr, params.plain_modulus)
 
 
 class GpuContext:
@@ -439,7 +449,7 @@ class GpuContext:
             raise ParameterError("vector longer than slot count")
         out = np.zeros(self.params.n_slots, dtype=np.int64)
         out[: arr.shape[0]] = arr
-        return np.mod(out, self.params.plain_modulus)
+        return residues(out, self.params.plain_modulus)
 
     def zeros(self) -> PlainVector:
         return np.zeros(self.params.n_slots, dtype=np.int64)
@@ -629,7 +639,7 @@ class GpuContext:
     def w_encrypt(ctxs, vecs) -> Wave:
         """Encrypt rows of ``vecs`` (item i by ctxs[i]); one nonce per item in order."""
         uniq, owner = _owners(ctxs)
-        vecs = np.ascontiguousarray(np.mod(np.asarray(vecs, dtype=np.int64), uniq[0].params.plain_modulus))
+        vecs = np.ascontiguousarray(residues(vecs, uniq[0].params.plain_modulus))
         ring = uniq[0]._ring
         ids = ring.alloc(len(owner))
         blk = _Block(ring, ids)
@@ -666,7 +676,7 @@ class GpuContext:
         cost = getattr(c0.params.noise_costs, field_name)
         b = GpuContext._spend_all(wave.budgets, cost)
         if not isinstance(vecs, PlainBatch):
-            vecs = np.mod(np.asarray(vecs, dtype=np.int64), c0.params.plain_modulus)
+            vecs = residues(vecs, c0.params.plain_modulus)
             if vecs.ndim == 1:
                 vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
         ring = c0._ring

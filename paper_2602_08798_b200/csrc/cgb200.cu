@@ -1255,6 +1255,21 @@ __global__ void k_modmul_peak(u64 *sink, u64 q, u64 w, u64 wsh, int iters) {
   if (acc == 0x1234567) sink[0] = acc;
 }
 
+// the same chains on the FP64 pipe (the exact error-free product of the FP64 NTT)
+__global__ void k_modmul_peak_fp(u64 *sink, double q, double w, double wq, int iters) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = (double)(threadIdx.x * 8 + k + 1);
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = fp_mulmod(x[k], w, wq, q);
+  }
+  double acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) acc += x[k];
+  if (acc == 0.5) sink[0] = 1;
+}
+
 // ============================================================================
 // host orchestration
 // ============================================================================
@@ -2027,12 +2042,18 @@ int cgb_modmul_peak(cgb_ring *r, double *modmuls_per_s) {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int threads = 512, blocks = sms * 4, iters = 4096;
-  k_modmul_peak<<<blocks, threads, 0, r->stream>>>(sink, q, w, wsh, 64);  // warm-up
+  const double qd = (double)q, wd = (double)w, wq = wd / qd;
+  // the pipe this ring's NTT runs on: FP64 exact products or 64-bit Shoup products
+  auto run = [&](int n) {
+    if (r->fp_ntt) k_modmul_peak_fp<<<blocks, threads, 0, r->stream>>>(sink, qd, wd, wq, n);
+    else k_modmul_peak<<<blocks, threads, 0, r->stream>>>(sink, q, w, wsh, n);
+  };
+  run(64);  // warm-up
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   CK(cudaEventRecord(a, r->stream));
-  k_modmul_peak<<<blocks, threads, 0, r->stream>>>(sink, q, w, wsh, iters);
+  run(iters);
   CK(cudaEventRecord(b, r->stream));
   CK(cudaEventSynchronize(b));
   float ms = 0;

@@ -52,7 +52,10 @@ def to_signed(v, p: int):
 
 
 def from_signed(v, p: int):
-    return np.mod(np.asarray(v, dtype=np.int64), p)
+    v = np.asarray(v, dtype=np.int64)
+    if v.size and v.min() > -p and v.max() < p:  # the usual case: one conditional add, no modulo
+        return np.where(v < 0, v + p, v)
+    return np.mod(v, p)
 
 
 def fp_encode(x, fp: FixedPointParams) -> np.ndarray:

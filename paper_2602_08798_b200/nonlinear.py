@@ -14,6 +14,7 @@ draw item by item, which is the order the per-op code would draw in.
 
 from __future__ import annotations
 
+import collections
 import json
 from dataclasses import dataclass
 
@@ -49,6 +50,7 @@ class MpcChannel:
         ss = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
         self.rng = np.random.default_rng(ss)
         self.transcript: list = []
+        self._pre = collections.deque()  # masks drawn ahead of use, in draw order
 
     def vector_bytes(self, elements: int) -> int:
         return elements * self.word_bits // 8
@@ -60,7 +62,20 @@ class MpcChannel:
         self.transcript.append({"op": op, "elements": elements, "trips": trips, "bytes": nbytes})
 
     def sample_mask(self, length: int) -> np.ndarray:
+        if self._pre:
+            r = self._pre.popleft()
+            if r.shape[0] != length:
+                raise RuntimeError(f"pre-drawn mask of {r.shape[0]} words, {length} requested: "
+                                   "the draw sequence diverged from the predraw plan")
+            return r
         return self.rng.integers(0, self.p, size=length, dtype=np.int64)
+
+    def predraw(self, lengths) -> None:
+        """Draw the next masks now (same generator calls, same order) so a
+        later ``sample_mask`` is off the critical path; the masks, and so
+        every share and ciphertext, are unchanged."""
+        for n in lengths:
+            self._pre.append(self.rng.integers(0, self.p, size=int(n), dtype=np.int64))
 
     def transcript_json(self) -> str:
         return json.dumps({"bytes_sent": self.bytes_sent, "rounds": self.rounds, "log": self.transcript}, indent=2)
@@ -73,7 +88,9 @@ def reconstruct(s: SharePair) -> np.ndarray:
 def share_vector(values, ch: MpcChannel) -> SharePair:
     secret = from_signed(values, ch.p)
     r = ch.sample_mask(secret.shape[0])
-    return SharePair((secret - r) % ch.p, r, ch.p, secret.shape[0])
+    d = secret - r  # both in [0, p): (secret - r) mod p is one conditional add
+    d[d < 0] += ch.p
+    return SharePair(d, r, ch.p, secret.shape[0])
 
 
 def truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel) -> SharePair:
@@ -97,7 +114,9 @@ def he_to_shares_wave(wave, chans, lengths) -> list:
         if not 0 < L <= n:
             raise ParameterError(f"share length {L} out of range")
     r = np.stack([ch.sample_mask(n) for ch in chans]) if len(chans) else np.zeros((0, n), np.int64)
-    masked = C.w_add_plain(wave, (p - r) % p, one_shot=True)
+    neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
+    neg[neg == p] = 0
+    masked = C.w_add_plain(wave, neg, one_shot=True)
     client = C.w_decrypt(masked)
     out = []
     for i, ch in enumerate(chans):

@@ -29,6 +29,8 @@ class Ring:
         self.log_n, self.N, self.t, self.L = log_n, 1 << log_n, int(t), int(n_limbs)
         self.n_slots, self.one_row = int(n_slots), bool(one_row)
         self.q_bits = int(q_bits)
+        # the library's NTT pipe (build_ring): FP64 for rings of primes < 2^49 from 2^12 up
+        self.fp_ntt = log_n >= 12 and self.q_bits <= 49 and not os.environ.get("CGB_INT_NTT")
         self.ct_words = 2 * self.L * self.N
         if arena_cts is None:
             arena_cts = max(64, min(65536, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))
@@ -138,6 +140,8 @@ class Ring:
         a = np.asarray(slots, dtype=np.int64)
         if a.ndim == 1:
             a = a.reshape(1, -1)
+        if a.size and a.min() >= 0 and a.max() < self.t:  # already residues: zero-copy view
+            return np.ascontiguousarray(a).view(np.uint64)
         return np.ascontiguousarray(np.mod(a, self.t).astype(np.uint64))
 
     def encode_pt(self, slots, kind: int, ids):
