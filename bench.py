@@ -309,7 +309,7 @@ def run_ours(args):
     name, (nl, kms, kbytes) = top
     achieved = kbytes / (kms * 1e-3) / 1e9
     # NTT integer-pipe utilisation: N/2 log N Shoup modmuls per limb-poly transform
-    ntt = [v for k, v in rep.items() if k.startswith("ntt")]
+    ntt = [v for k, v in rep.items() if k in ("ntt_fwd", "ntt_inv")]  # pure transforms (not fused epilogues)
     ntt_ms = sum(v[1] for v in ntt)
     ntt_polys = sum(v[2] for v in ntt) / (16.0 * 2 * N_SLOTS)
     ntt_mm = ntt_polys * (N_SLOTS) * 14  # (N/2) log2 N with N = 2 n_slots

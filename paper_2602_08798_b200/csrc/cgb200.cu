@@ -334,6 +334,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 // NTT launcher -------------------------------------------------------------
 static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
 static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
+static bool g_md_epi = true;  // ModDown combine fused into its NTT's row pass (CGB_MD_EPI=0 -> separate kernel)
 template <int LA, int LB, bool QS, int E>
 static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
@@ -383,8 +384,8 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
     const bool r0 = g_fp_regio & 1, r1 = g_fp_regio & 2;
     auto pass0 = [&](const NttJob &j, bool f) {
       if (r0) {
-        if (f) k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j);
-        else k_ntt2_fpr<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j);
+        if (f) k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j, NoEpi{});
+        else k_ntt2_fpr<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j, NoEpi{});
       } else {
         if (f) k_ntt2_fp<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
         else k_ntt2_fp<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
@@ -392,8 +393,8 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
     };
     auto pass1 = [&](const NttJob &j, bool f) {
       if (r1) {
-        if (f) k_ntt2_fpr<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j);
-        else k_ntt2_fpr<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j);
+        if (f) k_ntt2_fpr<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j, NoEpi{});
+        else k_ntt2_fpr<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j, NoEpi{});
       } else {
         if (f) k_ntt2_fp<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
         else k_ntt2_fp<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
@@ -653,7 +654,18 @@ __global__ void k_ks_inner(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *
   const int it0 = blockIdx.y * per_block, it1 = min(count, it0 + per_block);
   const u64 *kprev = nullptr;
   u64 kv[2][L], ks[2][L];
+  // digits of the next item are loaded before the current one is reduced, so
+  // the loads of consecutive items overlap (the kernel is load-latency bound)
+  auto load_digits = [&](int item, u64 *d) {
+    const u64 *Di = D + (u64)item * L * LP * N;
+#pragma unroll
+    for (int j = 0; j < L; j++)
+      d[j] = (l == j) ? ks_src_word(xin, item, j, (u32)jn, logN) : __ldcs(Di + (u64)j * LP * N + i);
+  };
+  u64 dc[L], dn[L];
+  if (it0 < it1) load_digits(it0, dc);
   for (int item = it0; item < it1; item++) {
+    if (item + 1 < it1) load_digits(item + 1, dn);
     const u64 *K = keys[item];
     if (K != kprev) {
 #pragma unroll
@@ -666,11 +678,10 @@ __global__ void k_ks_inner(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *
         }
       kprev = K;
     }
-    const u64 *Di = D + (u64)item * L * LP * N;
     u64 s0 = 0, s1 = 0;
 #pragma unroll
     for (int j = 0; j < L; j++) {
-      const u64 d = (l == j) ? ks_src_word(xin, item, j, (u32)jn, logN) : Di[(u64)j * LP * N + i];
+      const u64 d = dc[j];
       s0 += mul_shoup_lazy(d, kv[0][j], ks[0][j], q);
       s1 += mul_shoup_lazy(d, kv[1][j], ks[1][j], q);
       if ((j & 3) == 3 || j == L - 1) {  // keep lazy sums below 8q < 2^64
@@ -681,6 +692,8 @@ __global__ void k_ks_inner(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *
         s1 = s1 >= q2 ? s1 - q2 : s1;
       }
     }
+#pragma unroll
+    for (int j = 0; j < L; j++) dc[j] = dn[j];
     acc[((u64)item * 2 + 0) * LP * N + i] = s0 >= q ? s0 - q : s0;
     acc[((u64)item * 2 + 1) * LP * N + i] = s1 >= q ? s1 - q : s1;
   }
@@ -720,6 +733,82 @@ __global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W,
   if (p == 0 && (add0.items || add0.base)) v = add_mod(v, ks_src_word(add0, item, l, (u32)jn, logN), q);
   if (add1) v = add_mod(v, add1[item][i], q);
   out[item][i] = v;
+}
+
+// ModDown combine as the store epilogue of the forward row pass that produces
+// W = NTT_l(lift_P(INTT_P(acc_P))): out = (acc_l - W) P^-1 (+ add0 on poly 0)
+// (+ add1), the same words as k_moddown_combine without W's round trip.
+struct MdEpi {
+  static constexpr bool active = true;
+  u64 *const *out;
+  const u64 *acc;
+  KsSrc add0;
+  const u64 *const *add1;
+  const ModTab *mods;
+  const Consts *C;
+  int L, logN;
+  __device__ void store(int item, int unit, u64 pos, const u64 *w, int n) const {
+    const int pp = unit / L, l = unit - pp * L;
+    const u64 N = 1ull << logN, q = mods[l].q, pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
+    const u64 *a = acc + (((u64)item * 2 + pp) * (L + 1) + l) * N + pos;
+    u64 *o = out[item] + (u64)unit * N + pos;
+    const u64 *b = add1 ? add1[item] + (u64)unit * N + pos : nullptr;
+    const bool a0 = pp == 0 && (add0.items || add0.base);
+    if (n == 4) {
+      u64 av[4], bv[4] = {0, 0, 0, 0};
+      ld256(a, av);
+      if (b) ld256(b, bv);
+      u64 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        v[k] = mul_shoup(sub_mod(av[k], w[k], q), pi, pis, q);
+        if (a0) v[k] = add_mod(v[k], ks_src_word(add0, item, l, (u32)(pos + k), logN), q);
+        if (b) v[k] = add_mod(v[k], bv[k], q);
+      }
+      st256(o, v[0], v[1], v[2], v[3]);
+    } else {
+      for (int k = 0; k < n; k++) {
+        u64 v = mul_shoup(sub_mod(a[k], w[k], q), pi, pis, q);
+        if (a0) v = add_mod(v, ks_src_word(add0, item, l, (u32)(pos + k), logN), q);
+        if (b) v = add_mod(v, b[k], q);
+        o[k] = v;
+      }
+    }
+  }
+};
+
+// ModDown's forward NTT with the combine fused into its row pass (FP64 register-I/O
+// kernels only); false when this ring's NTT takes another path
+template <int LA, int LB>
+static void moddown_ntt_fused_t(cgb_ring *r, const NttJob &job, int count, const MdEpi &epi) {
+  NttJob second = job;
+  second.src_base = nullptr;
+  second.src_items = nullptr;
+  second.galois = nullptr;
+  second.lift = 0;
+  auto grid = [&](int lm) {
+    int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
+    return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
+  };
+  k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
+  k_ntt2_fpr<LA, LB, true, 1, MdEpi><<<grid(LB), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(second, epi);
+}
+static bool moddown_fusable(const cgb_ring *r) {
+  return r->fp_ntt && (g_fp_regio & 3) == 3 && g_md_epi && r->logN >= 12 && r->logN <= 16;
+}
+static bool moddown_ntt_fused(cgb_ring *r, NttJob &job, int count, const MdEpi &epi) {
+  if (!moddown_fusable(r) || count <= 0) return false;
+  job.mods = r->d_mods;
+  job.logN = r->logN;
+  switch (r->logN) {
+    case 12: moddown_ntt_fused_t<6, 6>(r, job, count, epi); break;
+    case 13: moddown_ntt_fused_t<6, 7>(r, job, count, epi); break;
+    case 14: moddown_ntt_fused_t<7, 7>(r, job, count, epi); break;
+    case 15: moddown_ntt_fused_t<7, 8>(r, job, count, epi); break;
+    case 16: moddown_ntt_fused_t<8, 8>(r, job, count, epi); break;
+    default: return false;
+  }
+  return true;
 }
 
 // Fused key-switch passes ----------------------------------------------------
@@ -1553,6 +1642,16 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
         n++;
       }
     job.nsub = n;
+    if (moddown_fusable(r)) {
+      const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, logN};
+      launch_begin(r);
+      moddown_ntt_fused(r, job, count, epi);
+      r->launches++;  // two kernels
+      // column pass (read + write) + row pass reading W, then the combine's traffic without W
+      launch_end(r, "ntt_fwd_moddown",
+                 24.0 * (double)count * n * N + BYTES_moddown_combine - 8.0 * (double)count * 2 * L * N);
+      return;
+    }
     launch_ntt(r, true, job, count);
   }
   LAUNCH("moddown_combine", BYTES_moddown_combine,
@@ -1989,6 +2088,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   }
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
   if (const char *e = getenv("CGB_FP_REGIO")) g_fp_regio = atoi(e) & 3;
+  if (const char *e = getenv("CGB_MD_EPI")) g_md_epi = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;

@@ -689,9 +689,17 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
   }
 }
 
+// store epilogue of k_ntt2_fpr's last pass: NoEpi writes the transform; a fused
+// consumer (e.g. the ModDown combine, cgb200.cu) receives the canonical words
+// (n = 4 consecutive words, or 1) of unit `unit` of item `item` at word `pos`
+struct NoEpi {
+  static constexpr bool active = false;
+  __device__ void store(int, int, u64, const u64 *, int) const {}
+};
+
 // LM-point sub-NTT in two register phases (RA stages then LM - RA), E = 16
-template <int LA, int LB, bool FWD, int PASS>
-__global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job) {
+template <int LA, int LB, bool FWD, int PASS, class EPI = NoEpi>
+__global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job, EPI epi) {
   extern __shared__ u64 sm2[];
   constexpr int E = 16, T = NTT2_TILE / E;
   constexpr int LOGN = LA + LB;
@@ -779,14 +787,20 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job) {
 #pragma unroll
       for (int k = 0; k < PB::K; k += 4) {
         const double *y = &x[u * PB::K + k];
-        st256(p + gaddr(PB::idx(tl, u, k)), fp_canon(y[0], qd, qinv), fp_canon(y[1], qd, qinv),
-              fp_canon(y[2], qd, qinv), fp_canon(y[3], qd, qinv));
+        const u64 w[4] = {fp_canon(y[0], qd, qinv), fp_canon(y[1], qd, qinv), fp_canon(y[2], qd, qinv),
+                          fp_canon(y[3], qd, qinv)};
+        if constexpr (EPI::active) epi.store(item, job.sub_off[sub], gaddr(PB::idx(tl, u, k)), w, 4);
+        else st256(p + gaddr(PB::idx(tl, u, k)), w[0], w[1], w[2], w[3]);
       }
   } else {
 #pragma unroll
     for (int u = 0; u < PB::R; u++)
 #pragma unroll
-      for (int k = 0; k < PB::K; k++) p[gaddr(PB::idx(tl, u, k))] = fp_canon(x[u * PB::K + k], qd, qinv);
+      for (int k = 0; k < PB::K; k++) {
+        const u64 w = fp_canon(x[u * PB::K + k], qd, qinv);
+        if constexpr (EPI::active) epi.store(item, job.sub_off[sub], gaddr(PB::idx(tl, u, k)), &w, 1);
+        else p[gaddr(PB::idx(tl, u, k))] = w;
+      }
   }
 }
 

@@ -1,8 +1,12 @@
 #!/bin/bash
-# A/B of an env toggle on the decode bench: ENVS="CGB_FP_REGIO=0;CGB_FP_REGIO=1"
+# GPU tests under each PARITY_ENVS variant, then decode bench A/B: ENVS="A=0;A=1"
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_primitives.py -m gpu -x -q 2>&1 | tail -3 > gpurun_out/ab_tests.log
+IFS=';' read -ra PV <<< "${PARITY_ENVS:-X=0}"
+for v in "${PV[@]}"; do
+  echo "== $v" >> gpurun_out/ab_tests.log
+  env $v timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 >> gpurun_out/ab_tests.log
+done
 IFS=';' read -ra VARIANTS <<< "${ENVS}"
 for v in "${VARIANTS[@]}"; do
   for rep in 1 2; do
