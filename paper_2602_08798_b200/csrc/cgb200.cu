@@ -335,6 +335,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
 static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
 static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
 static bool g_md_epi = true;  // ModDown combine fused into its NTT's row pass (CGB_MD_EPI=0 -> separate kernel)
+static bool g_ks_row = true;  // ModUp row pass fused with the key inner product (CGB_KS_ROW=0 -> ks_inner)
 template <int LA, int LB, bool QS, int E>
 static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
@@ -776,6 +777,133 @@ struct MdEpi {
     }
   }
 };
+
+// ModUp's forward row pass fused with the key inner product.  One CTA owns row
+// tile `tile` of limb l (of Q u P) of one item: for every digit j != l it runs the
+// forward row pass of D unit (j, l) (the column pass's output) in registers and
+// multiplies by the key words at the same positions; digit l is the key-switched
+// polynomial itself (NTT form, read through the automorphism).  Products and the
+// sum stay FP64: |row pass output| < 7q, each product lies in (-3q, 3q) with the
+// key's w/q formed by one DMUL, so the 3-digit sum is an exact integer < 2^53 and
+// its canonical residue equals the integer path's.  acc[item][p][l] is written
+// once; D's row-pass output never reaches memory.
+template <int LA, int LB, int L>
+__global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
+                                                           const u64 *const *keys, const ModTab *mods, int iP,
+                                                           int count) {
+  extern __shared__ u64 sm3[];
+  constexpr int E = 16, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
+  constexpr int G = NTT2_TILE / M, TPS = M / E, TILES = (1 << LA) / G;
+  constexpr int PSH = fpr_psh(LM, 1), PADM = fpr_padm(LM, 1);
+  constexpr int RA = 4, RB = LM - 4;
+  using PA = PhaseShape<LM, 0, RA, E>;
+  using PB = PhaseShape<LM, RA, RB, E>;
+  static_assert(PB::ST == 1 && PB::K % 4 == 0, "row-pass output: runs of >= 4 consecutive words");
+  const u64 N = 1ull << LOGN;
+  const int tile = blockIdx.x % TILES, rest = blockIdx.x / TILES;
+  const int l = rest % LP, item = rest / LP;
+  const ModTab &Md = mods[l == L ? iP : l];
+  const double qd = Md.qd, qinv = Md.qinv;
+  const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
+  const u64 row0 = (u64)(first + g) << LM;  // word offset of this thread's row
+  const double2 *tw = reinterpret_cast<const double2 *>(Md.ftw1t) + row0;
+  double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
+  auto spad = [](int i) { return i + (i >> PSH); };
+  const u64 *K = keys[item];
+  double a0[E], a1[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) a0[i] = a1[i] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < L; j++) {
+    double x[E];
+    if (j == l) {  // the digit's own limb: the input itself, already in NTT form
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++)
+          x[u * PB::K + k] = u2d(ks_src_word(xin, item, j, (u32)(row0 + PB::idx(tl, u, k)), LOGN));
+    } else {
+      const u64 *src = D + ((u64)item * L * LP + (u64)j * LP + l) * N + row0;
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) x[k] = u2d(__ldcs(src + PA::idx(tl, 0, k)));
+      phase_regs_fp<LM, 0, RA, true, E, false, true>(x, tw, tl, qd, qinv);
+      __syncthreads();  // the previous digit's phase-B reads are done
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = fp_reduce(sd[spad(PB::idx(tl, u, k))], qd, qinv);
+      phase_regs_fp<LM, RA, RB, true, E, true, true>(x, tw, tl, qd, qinv);
+    }
+    const u64 *k0 = K + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = K + ((u64)(j * 2 + 1) * LP + l) * N + row0;
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k += 4) {
+        const int o = PB::idx(tl, u, k);
+        u64 w0[4], w1[4];
+        ld256(k0 + o, w0);
+        ld256(k1 + o, w1);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const double xv = x[u * PB::K + k + e];
+          const double d0 = u2d(w0[e]), d1 = u2d(w1[e]);
+          a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+          a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+        }
+      }
+  }
+  u64 *o0 = acc + ((u64)item * 2 * LP + l) * N + row0, *o1 = acc + ((u64)item * 2 * LP + LP + l) * N + row0;
+#pragma unroll
+  for (int u = 0; u < PB::R; u++)
+#pragma unroll
+    for (int k = 0; k < PB::K; k += 4) {
+      const int o = PB::idx(tl, u, k);
+      const double *y0 = &a0[u * PB::K + k], *y1 = &a1[u * PB::K + k];
+      st256(o0 + o, fp_canon(y0[0], qd, qinv), fp_canon(y0[1], qd, qinv), fp_canon(y0[2], qd, qinv),
+            fp_canon(y0[3], qd, qinv));
+      st256(o1 + o, fp_canon(y1[0], qd, qinv), fp_canon(y1[1], qd, qinv), fp_canon(y1[2], qd, qinv),
+            fp_canon(y1[3], qd, qinv));
+    }
+}
+
+// ModUp column pass (fused lift) + k_ks_row: D holds only the column-pass output
+template <int LA, int LB, int L>
+static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, const u64 *D, const KsSrc &x,
+                           u64 *const *d_keys) {
+  const int G0 = NTT2_TILE >> LA, G1 = NTT2_TILE >> LB;
+  const dim3 g0((unsigned)((size_t)count * job.nsub * ((1 << LB) / G0)));
+  k_ntt2_fpr<LA, LB, true, 0><<<g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
+  const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
+  k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+                                                                                   r->iP, count);
+}
+static bool ks_row_fusable(const cgb_ring *r) {
+  return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
+         r->L <= 6;
+}
+static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u64 *D, const KsSrc &x,
+                         u64 *const *d_keys) {
+  job.mods = r->d_mods;
+  job.logN = r->logN;
+#define MKR(A, B)                                                              \
+  switch (r->L) {                                                              \
+    case 2: modup_ks_row_t<A, B, 2>(r, job, count, acc, D, x, d_keys); break; \
+    case 3: modup_ks_row_t<A, B, 3>(r, job, count, acc, D, x, d_keys); break; \
+    case 4: modup_ks_row_t<A, B, 4>(r, job, count, acc, D, x, d_keys); break; \
+    case 5: modup_ks_row_t<A, B, 5>(r, job, count, acc, D, x, d_keys); break; \
+    default: modup_ks_row_t<A, B, 6>(r, job, count, acc, D, x, d_keys); break; \
+  }
+  switch (r->logN) {
+    case 13: MKR(6, 7) break;
+    case 14: MKR(7, 7) break;
+    case 15: MKR(7, 8) break;
+    default: MKR(8, 8) break;
+  }
+#undef MKR
+}
 
 // ModDown's forward NTT with the combine fused into its row pass (FP64 register-I/O
 // kernels only); false when this ring's NTT takes another path
@@ -1577,6 +1705,7 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
   }
   // ModUp: digit j centre-lifted into every other limb of Q u P, fused into the NTT load
   u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
+  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
   {
     NttJob job{};
     job.base = D;
@@ -1595,11 +1724,18 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
         n++;
       }
     job.nsub = n;
-    launch_ntt(r, true, job, count);
+    if (ks_row_fusable(r)) {
+      launch_begin(r);
+      modup_ks_row(r, job, count, acc, D, x, d_keys);
+      r->launches++;  // two kernels
+      // column pass (read digit + write D) + row pass (read D) + keys + digit's own limb + acc
+      launch_end(r, "modup_ks_row", 24.0 * (double)count * n * N + BYTES_ks_inner - 8.0 * count * (double)n * N);
+    } else {
+      launch_ntt(r, true, job, count);
+    }
   }
   // inner product with the evaluation key
-  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
-  {
+  if (!ks_row_fusable(r)) {
     const int per_block = 16;
     const dim3 grid(GRID1((u64)LP * N, TPB).x, (count + per_block - 1) / per_block);
     const u64 kw = (u64)L * 2 * LP * N;
@@ -2089,6 +2225,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_NTT_E")) g_ntt2_e = atoi(e) == 16 ? 16 : 8;
   if (const char *e = getenv("CGB_FP_REGIO")) g_fp_regio = atoi(e) & 3;
   if (const char *e = getenv("CGB_MD_EPI")) g_md_epi = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KS_ROW")) g_ks_row = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
