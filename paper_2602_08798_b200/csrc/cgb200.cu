@@ -336,6 +336,7 @@ static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_
 static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
 static bool g_md_epi = true;  // ModDown combine fused into its NTT's row pass (CGB_MD_EPI=0 -> separate kernel)
 static bool g_ks_row = true;  // ModUp row pass fused with the key inner product (CGB_KS_ROW=0 -> ks_inner)
+static bool g_col_fused = true;  // INTT column pass + lift + forward column passes in one kernel (CGB_COL_FUSED)
 template <int LA, int LB, bool QS, int E>
 static void launch_ntt2_e(cgb_ring *r, bool fwd, const NttJob &job, int count) {
   NttJob second = job;
@@ -783,9 +784,10 @@ struct MdEpi {
 // forward row pass of D unit (j, l) (the column pass's output) in registers and
 // multiplies by the key words at the same positions; digit l is the key-switched
 // polynomial itself (NTT form, read through the automorphism).  Products and the
-// sum stay FP64: |row pass output| < 7q, each product lies in (-3q, 3q) with the
-// key's w/q formed by one DMUL, so the 3-digit sum is an exact integer < 2^53 and
-// its canonical residue equals the integer path's.  acc[item][p][l] is written
+// sum stay FP64: |row pass output| < 12q (unreduced forward pass), each product lies
+// in (-2.7q, 2.7q) with the key's w/q formed by one DMUL (scripts/sim/fp_bounds.py),
+// so a sum of <= 4 digits is an exact integer < 11q < 2^53 and its canonical residue
+// equals the integer path's.  acc[item][p][l] is written
 // once; D's row-pass output never reaches memory.
 template <int LA, int LB, int L>
 __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
@@ -834,7 +836,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
-        for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = fp_reduce(sd[spad(PB::idx(tl, u, k))], qd, qinv);
+        for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
       phase_regs_fp<LM, RA, RB, true, E, true, true>(x, tw, tl, qd, qinv);
     }
     const u64 *k0 = K + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = K + ((u64)(j * 2 + 1) * LP + l) * N + row0;
@@ -856,6 +858,29 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
       }
   }
   u64 *o0 = acc + ((u64)item * 2 * LP + l) * N + row0, *o1 = acc + ((u64)item * 2 * LP + LP + l) * N + row0;
+  if (l == L) {  // P limb: ModDown's inverse row pass runs here, on the accumulators
+    const double2 *itw = reinterpret_cast<const double2 *>(Md.fitw1t) + row0;
+#pragma unroll 1
+    for (int pp = 0; pp < 2; pp++) {
+      double y[E];
+#pragma unroll
+      for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
+      phase_regs_fp<LM, RA, RB, false, E, true, true>(y, itw, tl, qd, qinv);
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++) sd[spad(PB::idx(tl, u, k))] = y[u * PB::K + k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
+      phase_regs_fp<LM, 0, RA, false, E, false, true>(y, itw, tl, qd, qinv);
+      u64 *o = pp ? o1 : o0;
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = fp_canon(y[k], qd, qinv);
+    }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < PB::R; u++)
 #pragma unroll
@@ -867,6 +892,130 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
       st256(o1 + o, fp_canon(y1[0], qd, qinv), fp_canon(y1[1], qd, qinv), fp_canon(y1[2], qd, qinv),
             fp_canon(y1[3], qd, qinv));
     }
+}
+
+// Column-pass fusion: inverse column pass of a source limb-poly (its row pass already
+// done) followed, in the same CTA, by the centred lift into NT target moduli and each
+// target's forward column pass.  The inverse's last phase and the forward's first
+// phase share one register shape, so the coefficients never leave registers; the
+// coefficient-domain polynomial is neither written nor re-read.
+struct ColJob {
+  const u64 *src;     // source items (row-pass output of the inverse NTT)
+  u64 src_stride;
+  u64 *dst;           // destination items (column-pass output of the forward NTTs)
+  u64 dst_stride;
+  const ModTab *mods;
+  int nsrc;
+  unsigned short src_off[8];
+  unsigned char src_mod[8];
+  unsigned short dst_off[8][8];
+  unsigned char dst_mod[8][8];
+};
+template <int LA, int LB, int NT>
+__global__ void __launch_bounds__(NTT2_TILE / 16) k_col_fused(ColJob job) {
+  extern __shared__ u64 sm4[];
+  constexpr int E = 16, LM = LA, M = 1 << LM, LOGN = LA + LB;
+  constexpr int G = NTT2_TILE / M, T = NTT2_TILE / E, TILES = (1 << LB) / G;
+  constexpr int PSH = fpr_psh(LM, 0), PADM = fpr_padm(LM, 0);
+  constexpr int RA = 4, RB = LM - 4;
+  using PF = PhaseShape<LM, 0, RA, E>;   // forward first / inverse last phase
+  using PS = PhaseShape<LM, RA, RB, E>;  // forward second / inverse first phase
+  const int tile = blockIdx.x % TILES, rest = blockIdx.x / TILES;
+  const int s = rest % job.nsrc, item = rest / job.nsrc;
+  const int tid = threadIdx.x, g = tid % G, tl = tid / G, first = tile * G;
+  double *data = reinterpret_cast<double *>(sm4);
+  double2 *tws = reinterpret_cast<double2 *>(sm4 + ((G * PADM + 1) & ~1));  // (NT + 1) tables of M
+  auto spad = [](int i) { return i + (i >> PSH); };
+  auto gaddr = [&](int i) -> u64 { return ((u64)i << LB) + first + g; };
+  const ModTab &Ms = job.mods[job.src_mod[s]];
+  for (int i = tid; i < M; i += T) tws[i] = __ldg(reinterpret_cast<const double2 *>(Ms.fitw) + i);
+#pragma unroll
+  for (int t = 0; t < NT; t++) {
+    const double2 *ft = reinterpret_cast<const double2 *>(job.mods[job.dst_mod[s][t]].ftw);
+    for (int i = tid; i < M; i += T) tws[(t + 1) * M + i] = __ldg(ft + i);
+  }
+  const u64 *src = job.src + (u64)item * job.src_stride + ((u64)job.src_off[s] << LOGN);
+  double x[E];
+#pragma unroll
+  for (int u = 0; u < PS::R; u++)
+#pragma unroll
+    for (int k = 0; k < PS::K; k++) {
+      x[u * PS::K + k] = u2d(__ldcs(src + gaddr(PS::idx(tl, u, k))));
+      if (RB == 4) x[u * PS::K + k] = fp_reduce(x[u * PS::K + k], Ms.qd, Ms.qinv);  // 4-stage inverse phase
+    }
+  double *sd = data + g * PADM;
+  const double qs = Ms.qd, qsi = Ms.qinv;
+  __syncthreads();  // twiddles staged
+  // inverse column pass (the NTT's last: scale by N^-1)
+  phase_regs_fp<LM, RA, RB, false, E>(x, tws, tl, qs, qsi);
+#pragma unroll
+  for (int u = 0; u < PS::R; u++)
+#pragma unroll
+    for (int k = 0; k < PS::K; k++) sd[spad(PS::idx(tl, u, k))] = x[u * PS::K + k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PF::K; k++) x[k] = fp_reduce(sd[spad(PF::idx(tl, 0, k))], qs, qsi);
+  phase_regs_fp<LM, 0, RA, false, E>(x, tws, tl, qs, qsi);
+  u64 c[E];  // canonical coefficients mod q_src at the PF positions
+#pragma unroll
+  for (int k = 0; k < E; k++) c[k] = fp_canon(fp_mulmod(fp_reduce(x[k], qs, qsi), Ms.ninv_fp, Ms.ninv_fpq, qs), qs, qsi);
+  const u64 qsrc = Ms.q;
+#pragma unroll 1
+  for (int t = 0; t < NT; t++) {
+    const ModTab &Mt = job.mods[job.dst_mod[s][t]];
+    const double qt = Mt.qd, qti = Mt.qinv;
+    const double2 *tw_t = tws + (t + 1) * M;
+#pragma unroll
+    for (int k = 0; k < E; k++) x[k] = u2d(centred_to(c[k], qsrc, Mt.q));
+    phase_regs_fp<LM, 0, RA, true, E>(x, tw_t, tl, qt, qti);
+    __syncthreads();  // previous target's (or the inverse's) smem reads are done
+#pragma unroll
+    for (int k = 0; k < PF::K; k++) sd[spad(PF::idx(tl, 0, k))] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PS::R; u++)
+#pragma unroll
+      for (int k = 0; k < PS::K; k++) x[u * PS::K + k] = sd[spad(PS::idx(tl, u, k))];  // forward: unreduced
+    phase_regs_fp<LM, RA, RB, true, E>(x, tw_t, tl, qt, qti);
+    u64 *dst = job.dst + (u64)item * job.dst_stride + ((u64)job.dst_off[s][t] << LOGN);
+#pragma unroll
+    for (int u = 0; u < PS::R; u++)
+#pragma unroll
+      for (int k = 0; k < PS::K; k++) dst[gaddr(PS::idx(tl, u, k))] = fp_canon(x[u * PS::K + k], qt, qti);
+  }
+}
+template <int LA, int LB>
+__host__ size_t col_fused_smem(int nt) {
+  const int G = NTT2_TILE >> LA;
+  return sizeof(u64) * (size_t)((G * fpr_padm(LA, 0) + 1) & ~1) + 16 * (size_t)(nt + 1) * (1 << LA);
+}
+template <int LA, int LB>
+static void col_fused_t(cgb_ring *r, const ColJob &job, int count, int nt) {
+  const int G = NTT2_TILE >> LA;
+  const dim3 grid((unsigned)((size_t)count * job.nsrc * ((1 << LB) / G)));
+  const size_t sm = col_fused_smem<LA, LB>(nt);
+  switch (nt) {
+    case 2: k_col_fused<LA, LB, 2><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
+    case 3: k_col_fused<LA, LB, 3><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
+    case 4: k_col_fused<LA, LB, 4><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
+    default: k_col_fused<LA, LB, 1><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
+  }
+}
+static bool col_fusable(const cgb_ring *r) {
+  return r->fp_ntt && (g_fp_regio & 3) == 3 && g_col_fused && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
+         r->L <= 4;
+}
+// inverse column pass of job.nsrc source units + lift + forward column passes into nt targets
+static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *name) {
+  job.mods = r->d_mods;
+  launch_begin(r);
+  switch (r->logN) {
+    case 13: col_fused_t<6, 7>(r, job, count, nt); break;
+    case 14: col_fused_t<7, 7>(r, job, count, nt); break;
+    case 15: col_fused_t<7, 8>(r, job, count, nt); break;
+    default: col_fused_t<8, 8>(r, job, count, nt); break;
+  }
+  launch_end(r, name, 8.0 * (double)count * job.nsrc * r->N * (1 + nt));
 }
 
 // ModUp column pass (fused lift) + k_ks_row: D holds only the column-pass output
@@ -882,7 +1031,7 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
 }
 static bool ks_row_fusable(const cgb_ring *r) {
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
-         r->L <= 6;
+         r->L <= 4;  // <= 4 digits: the FP64 inner-product sum stays below 2^53
 }
 static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u64 *D, const KsSrc &x,
                          u64 *const *d_keys) {
@@ -892,9 +1041,7 @@ static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u6
   switch (r->L) {                                                              \
     case 2: modup_ks_row_t<A, B, 2>(r, job, count, acc, D, x, d_keys); break; \
     case 3: modup_ks_row_t<A, B, 3>(r, job, count, acc, D, x, d_keys); break; \
-    case 4: modup_ks_row_t<A, B, 4>(r, job, count, acc, D, x, d_keys); break; \
-    case 5: modup_ks_row_t<A, B, 5>(r, job, count, acc, D, x, d_keys); break; \
-    default: modup_ks_row_t<A, B, 6>(r, job, count, acc, D, x, d_keys); break; \
+    default: modup_ks_row_t<A, B, 4>(r, job, count, acc, D, x, d_keys); break; \
   }
   switch (r->logN) {
     case 13: MKR(6, 7) break;
@@ -903,6 +1050,26 @@ static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u6
     default: MKR(8, 8) break;
   }
 #undef MKR
+}
+
+// the inverse NTT's column pass alone (its row pass ran inside k_ks_row)
+template <int LA, int LB>
+static void ntt_inv_col_t(cgb_ring *r, const NttJob &job, int count) {
+  const int G0 = NTT2_TILE >> LA;
+  const dim3 g0((unsigned)((size_t)count * job.nsub * ((1 << LB) / G0)));
+  k_ntt2_fpr<LA, LB, false, 0><<<g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
+}
+static void ntt_inv_col(cgb_ring *r, NttJob &job, int count) {
+  job.mods = r->d_mods;
+  job.logN = r->logN;
+  launch_begin(r);
+  switch (r->logN) {
+    case 13: ntt_inv_col_t<6, 7>(r, job, count); break;
+    case 14: ntt_inv_col_t<7, 7>(r, job, count); break;
+    case 15: ntt_inv_col_t<7, 8>(r, job, count); break;
+    default: ntt_inv_col_t<8, 8>(r, job, count); break;
+  }
+  launch_end(r, "ntt_inv_col", 16.0 * (double)count * job.nsub * r->N);
 }
 
 // ModDown's forward NTT with the combine fused into its row pass (FP64 register-I/O
@@ -1680,9 +1847,130 @@ static void fused_attrs_for(int logN, int L) {
 // key switch of `count` NTT-form polys (descriptor x: contiguous, or arena items read
 // through an automorphism) with per-item keys; result combined into out pointers:
 // out = (ks0 + add0 + add1, ks1 + add1)
+// The FP64-ring key switch in five launches:
+//   1 inverse row pass of the digits (automorphism fused into its load)      -> xr
+//   2 k_col_fused: inverse column pass + lift + forward column passes (ModUp) -> D
+//   3 k_ks_row: forward row passes + key inner product; P limb: inverse row   -> acc
+//   4 k_col_fused: P limb inverse column pass + lift into Q + column passes   -> W
+//   5 forward row pass of W with the ModDown combine as its store epilogue    -> out
+template <int LA, int LB, int L>
+static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys,
+                           u64 *const *d_out, const KsSrc &add0, const u64 *const *d_add1) {
+  constexpr int LP = L + 1, N = 1 << (LA + LB), G0 = NTT2_TILE >> LA, G1 = NTT2_TILE >> LB;
+  u64 *xr = S.alloc<u64>((size_t)count * L * N);
+  u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
+  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
+  u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
+  const dim3 rows_grid1((unsigned)((size_t)count * L * ((1 << LA) / G1)));
+  {  // 1
+    NttJob job{};
+    job.base = xr;
+    job.item_stride = (u64)L * N;
+    job.src_items = x.items;
+    job.src_base = x.items ? nullptr : x.base;
+    job.src_stride = x.stride;
+    job.galois = x.g;
+    const int off = (int)(x.items ? x.off / (u64)N : 0);
+    for (int l = 0; l < L; l++) {
+      job.sub_off[l] = (unsigned short)l;
+      job.sub_mod[l] = (unsigned char)l;
+      job.src_off[l] = (unsigned short)(off + l);
+    }
+    job.nsub = L;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    launch_begin(r);
+    k_ntt2_fpr<LA, LB, false, 1><<<rows_grid1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, NoEpi{});
+    launch_end(r, "ks_digit_rows", 16.0 * (double)count * L * N);
+  }
+  {  // 2
+    ColJob cj{};
+    cj.src = xr;
+    cj.src_stride = (u64)L * N;
+    cj.dst = D;
+    cj.dst_stride = (u64)L * LP * N;
+    cj.nsrc = L;
+    for (int j = 0; j < L; j++) {
+      cj.src_off[j] = (unsigned short)j;
+      cj.src_mod[j] = (unsigned char)j;
+      int t = 0;
+      for (int l = 0; l < LP; l++) {
+        if (l == j) continue;
+        cj.dst_off[j][t] = (unsigned short)(j * LP + l);
+        cj.dst_mod[j][t] = (unsigned char)(l == L ? r->iP : l);
+        t++;
+      }
+    }
+    col_fused(r, cj, count, L, "ks_modup_cols");
+  }
+  {  // 3
+    const dim3 g1((unsigned)((size_t)count * LP * ((1 << LA) / G1)));
+    launch_begin(r);
+    k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+                                                                                     r->iP, count);
+    launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N);
+  }
+  {  // 4
+    ColJob cj{};
+    cj.src = acc;
+    cj.src_stride = 2ull * LP * N;
+    cj.dst = W;
+    cj.dst_stride = 2ull * L * N;
+    cj.nsrc = 2;
+    for (int pp = 0; pp < 2; pp++) {
+      cj.src_off[pp] = (unsigned short)(pp * LP + L);
+      cj.src_mod[pp] = (unsigned char)r->iP;
+      for (int l = 0; l < L; l++) {
+        cj.dst_off[pp][l] = (unsigned short)(pp * L + l);
+        cj.dst_mod[pp][l] = (unsigned char)l;
+      }
+    }
+    col_fused(r, cj, count, L, "ks_moddown_cols");
+  }
+  {  // 5
+    NttJob job{};
+    job.base = W;
+    job.item_stride = 2ull * L * N;
+    int n = 0;
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        job.sub_off[n] = (unsigned short)(pp * L + l);
+        job.sub_mod[n] = (unsigned char)l;
+        n++;
+      }
+    job.nsub = n;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
+    const dim3 g((unsigned)((size_t)count * n * ((1 << LA) / G1)));
+    launch_begin(r);
+    k_ntt2_fpr<LA, LB, true, 1, MdEpi><<<g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, epi);
+    launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)));
+  }
+}
+static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
+                         const KsSrc &add0, const u64 *const *d_add1) {
+  if (!(col_fusable(r) && ks_row_fusable(r) && moddown_fusable(r)) || count <= 0) return false;
+#define KFP(A, B)                                                                      \
+  switch (r->L) {                                                                      \
+    case 2: keyswitch_fp_t<A, B, 2>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    case 3: keyswitch_fp_t<A, B, 3>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    default: keyswitch_fp_t<A, B, 4>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+  }
+  switch (r->logN) {
+    case 13: KFP(6, 7) break;
+    case 14: KFP(7, 7) break;
+    case 15: KFP(7, 8) break;
+    default: KFP(8, 8) break;
+  }
+#undef KFP
+  return true;
+}
+
 static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                       const KsSrc &add0, const u64 *const *d_add1) {
   if (keyswitch_fused(r, S, x, count, d_keys, d_out, add0, d_add1)) return;
+  if (keyswitch_fp(r, S, x, count, d_keys, d_out, add0, d_add1)) return;
   const int L = r->L, N = r->N, LP = L + 1, logN = r->logN;
   // digits in coefficient form (automorphism fused into the inverse NTT's load)
   u64 *xc = S.alloc<u64>((size_t)count * L * N);
@@ -1758,7 +2046,8 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
     job.sub_off[1] = (unsigned short)(LP + L);
     job.sub_mod[1] = (unsigned char)r->iP;
     job.nsub = 2;
-    launch_ntt(r, false, job, count);
+    if (ks_row_fusable(r)) ntt_inv_col(r, job, count);  // row pass done by k_ks_row
+    else launch_ntt(r, false, job, count);
   }
   u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
   {
@@ -2226,6 +2515,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_FP_REGIO")) g_fp_regio = atoi(e) & 3;
   if (const char *e = getenv("CGB_MD_EPI")) g_md_epi = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_ROW")) g_ks_row = atoi(e) != 0;
+  if (const char *e = getenv("CGB_COL_FUSED")) g_col_fused = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;

@@ -679,9 +679,9 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
           const double t = fp_mulmod(Y, W.x, W.y, q);
           Y = X - t;
           X = X + t;
-        } else {
+        } else {  // X + Y left unreduced: scripts/sim/fp_bounds.py bounds a phase by 8q < 2^53
           const double d = X - Y;
-          X = fp_reduce(X + Y, q, qinv);
+          X = X + Y;
           Y = fp_mulmod(d, W.x, W.y, q);
         }
       }
@@ -759,7 +759,10 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job, EPI epi
         }
     }
 #pragma unroll
-    for (int i = 0; i < E; i++) x[i] = u2d(lift ? centred_to(v[i], qs, q) : v[i]);
+    for (int i = 0; i < E; i++) {
+      x[i] = u2d(lift ? centred_to(v[i], qs, q) : v[i]);
+      if (!FWD && RPA == 4) x[i] = fp_reduce(x[i], qd, qinv);  // a 4-stage inverse phase starts reduced
+    }
   }
   __syncthreads();  // twiddles staged
   const double2 *tw_g = PASS == 0 ? tws : gtw + ((u64)(first + g) << LM);
@@ -773,7 +776,11 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job, EPI epi
 #pragma unroll
   for (int u = 0; u < PB::R; u++)
 #pragma unroll
-    for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = fp_reduce(sd[spad(PB::idx(tl, u, k))], qd, qinv);
+    for (int k = 0; k < PB::K; k++) {
+      // forward: no reduction inside a pass (|x| < 12q < 2^53, scripts/sim/fp_bounds.py)
+      const double v = sd[spad(PB::idx(tl, u, k))];
+      x[u * PB::K + k] = FWD ? v : fp_reduce(v, qd, qinv);
+    }
   phase_regs_fp<LM, S0B, RPB, FWD, E, PASS == 1 && S0B == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
   const bool last = FWD ? (PASS == 1) : (PASS == 0);
   const double ni = Md.ninv_fp, niq = Md.ninv_fpq;
