@@ -78,7 +78,7 @@ uint64_t cgb_launch_count(const cgb_ring *ring);
 /* per-launch CUDA-event timing: enable (clears earlier records) / disable */
 int cgb_timing_enable(cgb_ring *ring, int on);
 /* aggregate of the recorded launches, one line per kernel:
- * "<name> <launches> <total ms> <algorithmic bytes>\n" */
+ * "<name> <launches> <total ms> <algorithmic bytes> <algorithmic modular products>\n" */
 int cgb_timing_report(cgb_ring *ring, char *buf, size_t cap);
 /* measured peak of the modular multiply on the pipe this ring's NTT uses
  * (register-resident independent chains over the whole GPU), per second:

@@ -105,7 +105,8 @@ def load_library(path: Path | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else SO_PATH
+    # CGB_LIB: an alternative in-tree build of the same library (build-variant experiments)
+    p = Path(path) if path else Path(os.environ.get("CGB_LIB", SO_PATH))
     if not p.exists():
         raise BackendUnavailable(
             f"{p} is missing: run __graft_entry__.build() (nvcc, sm_100a) first"

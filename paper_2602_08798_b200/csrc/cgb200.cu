@@ -207,6 +207,7 @@ struct cgb_ring {
   struct Rec {
     const char *name;
     double bytes;
+    double mm;
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs;
@@ -282,7 +283,9 @@ static void launch_begin(cgb_ring *r) {
   r->pending = take_event(r);
   CK(cudaEventRecord(r->pending, r->stream));
 }
-static void launch_end(cgb_ring *r, const char *name, double bytes) {
+// bytes: algorithmic HBM bytes; mm: algorithmic modular products (NTT butterflies,
+// key and constant products) for the arithmetic-pipe roofline
+static void launch_end(cgb_ring *r, const char *name, double bytes, double mm = 0.0) {
   r->launches++;
   {
     cudaError_t e = cudaGetLastError();
@@ -291,7 +294,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes) {
   if (!r->timing) return;
   cudaEvent_t b = take_event(r);
   CK(cudaEventRecord(b, r->stream));
-  r->recs.push_back({name, bytes, r->pending, b});
+  r->recs.push_back({name, bytes, mm, r->pending, b});
 }
 // algorithmic bytes per launch (read + write once; shared key / table reads once)
 #define BYTES_add (24.0 * count * r->ct_words)
@@ -464,7 +467,7 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
     }
 #undef LN2
     r->launches++;  // two kernels per transform (launch_end counts the other)
-    launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes);
+    launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes, (double)count * job.nsub * (r->N / 2) * r->logN);
     return;
   }
   int E = r->ntt_E(), T = r->ntt_threads();
@@ -491,7 +494,7 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
     default: LNTT(2); break;
   }
 #undef LNTT
-  launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", bytes);
+  launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", bytes, (double)count * job.nsub * (r->N / 2) * r->logN);
 }
 // NTT over `nlimb` limbs of `npoly` polys per item, limb l of poly p at unit p*nlimb+l
 static void ntt_items(cgb_ring *r, bool fwd, u64 *base, u64 *const *items, u64 item_stride, int count, int npoly,
@@ -912,7 +915,10 @@ struct ColJob {
   unsigned char dst_mod[8][8];
 };
 template <int LA, int LB, int NT>
-__global__ void __launch_bounds__(NTT2_TILE / 16) k_col_fused(ColJob job) {
+#ifndef CGB_COLF_MINB
+#define CGB_COLF_MINB 5
+#endif
+__global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(ColJob job) {
   extern __shared__ u64 sm4[];
   constexpr int E = 16, LM = LA, M = 1 << LM, LOGN = LA + LB;
   constexpr int G = NTT2_TILE / M, T = NTT2_TILE / E, TILES = (1 << LB) / G;
@@ -1069,7 +1075,8 @@ static void ntt_inv_col(cgb_ring *r, NttJob &job, int count) {
     case 15: ntt_inv_col_t<7, 8>(r, job, count); break;
     default: ntt_inv_col_t<8, 8>(r, job, count); break;
   }
-  launch_end(r, "ntt_inv_col", 16.0 * (double)count * job.nsub * r->N);
+  launch_end(r, "ntt_inv_col", 16.0 * (double)count * job.nsub * r->N,
+             (double)count * job.nsub * ((r->N / 2) * (r->logN - r->logN / 2) + r->N));
 }
 
 // ModDown's forward NTT with the combine fused into its row pass (FP64 register-I/O
@@ -1881,7 +1888,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     job.logN = LA + LB;
     launch_begin(r);
     k_ntt2_fpr<LA, LB, false, 1><<<rows_grid1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, NoEpi{});
-    launch_end(r, "ks_digit_rows", 16.0 * (double)count * L * N);
+    launch_end(r, "ks_digit_rows", 16.0 * (double)count * L * N, (double)count * L * (N / 2) * LB);
   }
   {  // 2
     ColJob cj{};
@@ -1908,7 +1915,8 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     launch_begin(r);
     k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(acc, D, x, d_keys, r->d_mods,
                                                                                      r->iP, count);
-    launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N);
+    launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
+               (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
   {  // 4
     ColJob cj{};
@@ -1945,7 +1953,8 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     const dim3 g((unsigned)((size_t)count * n * ((1 << LA) / G1)));
     launch_begin(r);
     k_ntt2_fpr<LA, LB, true, 1, MdEpi><<<g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, epi);
-    launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)));
+    launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)),
+               (double)count * n * ((N / 2) * LB + N));
   }
 }
 static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
@@ -2636,7 +2645,7 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
   CK(cudaStreamSynchronize(r->stream));
   struct Agg {
     long n = 0;
-    double ms = 0, bytes = 0;
+    double ms = 0, bytes = 0, mm = 0;
   };
   std::vector<std::pair<std::string, Agg>> agg;
   for (auto &rc : r->recs) {
@@ -2650,6 +2659,7 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
     it->second.n++;
     it->second.ms += ms;
     it->second.bytes += rc.bytes;
+    it->second.mm += rc.mm;
   }
   // GPU idle time between consecutive recorded launches (host gaps, syncs)
   double idle = 0;
@@ -2676,7 +2686,8 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
   std::string out;
   for (auto &kv : agg) {
     char line[256];
-    snprintf(line, sizeof line, "%s %ld %.6f %.0f\n", kv.first.c_str(), kv.second.n, kv.second.ms, kv.second.bytes);
+    snprintf(line, sizeof line, "%s %ld %.6f %.0f %.0f\n", kv.first.c_str(), kv.second.n, kv.second.ms,
+             kv.second.bytes, kv.second.mm);
     out += line;
   }
   if (out.size() + 1 > cap) FAIL(CGB_ERR_PARAM, "timing report needs %zu bytes", out.size() + 1);

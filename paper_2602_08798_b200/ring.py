@@ -72,13 +72,13 @@ class Ring:
         nat.check(nat.lib().cgb_timing_enable(self._h, int(on)), "cgb_timing_enable")
 
     def timing_report(self) -> dict:
-        """{kernel: (launches, total_ms, algorithmic_bytes)} of the recorded launches."""
+        """{kernel: (launches, total_ms, algorithmic_bytes, algorithmic_modmuls)} of the recorded launches."""
         buf = ctypes.create_string_buffer(1 << 16)
         nat.check(nat.lib().cgb_timing_report(self._h, buf, len(buf)), "cgb_timing_report")
         out = {}
         for line in buf.value.decode().splitlines():
-            name, k, ms, b = line.split()
-            out[name] = (int(k), float(ms), float(b))
+            name, k, ms, b, mm = line.split()
+            out[name] = (int(k), float(ms), float(b), float(mm))
         return out
 
     def modmul_peak(self) -> float:

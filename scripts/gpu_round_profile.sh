@@ -10,9 +10,4 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --nvtx --nvtx-include "timed_step/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "list rc=$?"
-ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed_step/" \
-    -k regex:k_ntt2_fp -s 60 -c 2 -o gpurun_out/prof_ntt2fp $CMD > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?"
-ncu --set full --clock-control none --nvtx --nvtx-include "timed_step/" \
-    -k regex:"k_ks_inner|k_moddown_combine" -s 10 -c 2 -o gpurun_out/prof_ks $CMD > gpurun_out/ncu_full2.log 2>&1
-echo "full2 rc=$?"
+bash scripts/gpu_ncu.sh ${NCU_SPECS:-"k_ks_row:20:1:ks_row" "k_col_fused:20:2:col_fused" "k_ntt2_fpr:40:2:ntt2_fpr"}

@@ -53,6 +53,7 @@ if __name__ == "__main__":
     src = ROOT / "gpurun_out"
     if (src / "launches.csv").exists():
         (dst / "launch_share.md").write_text(launch_share(src / "launches.csv"))
-    for rep in sorted(src.glob("prof_*.ncu-rep")):
-        (dst / f"ncu_{rep.stem[5:]}.md").write_text(full_report(rep))
+    for rep in sorted(src.glob("prof_*.ncu-rep")) + sorted(src.glob("prof_*_raw.csv")):
+        tag = rep.name[5:].replace("_raw.csv", "").replace(".ncu-rep", "")
+        (dst / f"ncu_{tag}.md").write_text(full_report(rep))
     print("wrote", sorted(p.name for p in dst.iterdir()))
