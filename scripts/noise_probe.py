@@ -25,7 +25,7 @@ tok = lambda r, c: np.mod(np.round(rng.uniform(-1, 1, (r, c)) * 256).astype(np.i
 K = cg.encode(tok(128, d2), cg.EncodingKind.OUTER, ctx)
 V = cg.encode(tok(128, d2), cg.EncodingKind.OUTER, ctx)
 q = ctx.encrypt(ctx.plain_from_dense(tok(1, d2)[0]))
-out = {"L": L, "fresh": ctx.noise_budget_bits(q)}
+out = {"L": L, "q_bits": ctx._ring.q_bits, "fresh": ctx.noise_budget_bits(q)}
 # decode scores: 64 broadcasts (one-hot, 14 rotations) x mult_cipher, summed
 qw = C.wave_of([q] * d2, [ctx] * d2)
 b = broadcast_wave(qw, np.arange(d2), n)
