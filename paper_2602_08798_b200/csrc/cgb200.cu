@@ -811,7 +811,18 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
   const double qd = Md.qd, qinv = Md.qinv;
   const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
   const u64 row0 = (u64)(first + g) << LM;  // word offset of this thread's row
-  const double2 *tw = reinterpret_cast<const double2 *>(Md.ftw1t) + row0;
+  // the tile's row twiddles (same for every digit) staged once: rows of M + 1 pairs
+  double2 *tws = reinterpret_cast<double2 *>(sm3 + ((G * PADM + 1) & ~1));
+  auto stage_tw = [&](const u64 *table) {
+    const double2 *gt = reinterpret_cast<const double2 *>(table) + ((u64)first << LM);
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      const int e = tid + i * (NTT2_TILE / E);
+      tws[e + (e >> LM)] = __ldg(gt + e);
+    }
+  };
+  stage_tw(Md.ftw1t);
+  const double2 *tw = tws + g * (M + 1);
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
   const u64 *K = keys[item];
@@ -831,8 +842,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
       const u64 *src = D + ((u64)item * L * LP + (u64)j * LP + l) * N + row0;
 #pragma unroll
       for (int k = 0; k < PA::K; k++) x[k] = u2d(__ldcs(src + PA::idx(tl, 0, k)));
-      phase_regs_fp<LM, 0, RA, true, E, false, true>(x, tw, tl, qd, qinv);
-      __syncthreads();  // the previous digit's phase-B reads are done
+      __syncthreads();  // twiddles staged; the previous digit's phase-B reads are done
+      phase_regs_fp<LM, 0, RA, true, E, false, false>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
       __syncthreads();
@@ -840,7 +851,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
-      phase_regs_fp<LM, RA, RB, true, E, true, true>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, true, E, true, false>(x, tw, tl, qd, qinv);
     }
     const u64 *k0 = K + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = K + ((u64)(j * 2 + 1) * LP + l) * N + row0;
 #pragma unroll
@@ -862,13 +873,16 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
   }
   u64 *o0 = acc + ((u64)item * 2 * LP + l) * N + row0, *o1 = acc + ((u64)item * 2 * LP + LP + l) * N + row0;
   if (l == L) {  // P limb: ModDown's inverse row pass runs here, on the accumulators
-    const double2 *itw = reinterpret_cast<const double2 *>(Md.fitw1t) + row0;
+    __syncthreads();  // every thread is done with the forward twiddles
+    stage_tw(Md.fitw1t);
+    const double2 *itw = tw;
 #pragma unroll 1
     for (int pp = 0; pp < 2; pp++) {
       double y[E];
 #pragma unroll
       for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
-      phase_regs_fp<LM, RA, RB, false, E, true, true>(y, itw, tl, qd, qinv);
+      __syncthreads();  // inverse twiddles staged / previous poly's reads done
+      phase_regs_fp<LM, RA, RB, false, E, true, false>(y, itw, tl, qd, qinv);
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
@@ -877,7 +891,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
-      phase_regs_fp<LM, 0, RA, false, E, false, true>(y, itw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, false, E, false, false>(y, itw, tl, qd, qinv);
       u64 *o = pp ? o1 : o0;
 #pragma unroll
       for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = fp_canon(y[k], qd, qinv);
@@ -1024,6 +1038,19 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
   launch_end(r, name, 8.0 * (double)count * job.nsrc * r->N * (1 + nt));
 }
 
+template <int LA, int LB>
+static size_t ks_row_smem() {  // row-pass data tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
+  return sizeof(u64) * (size_t)((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1) +
+         16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB));
+}
+template <int LA, int LB, int L>
+static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ks_row_smem<LA, LB>());
+  });
+}
+
 // ModUp column pass (fused lift) + k_ks_row: D holds only the column-pass output
 template <int LA, int LB, int L>
 static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, const u64 *D, const KsSrc &x,
@@ -1032,8 +1059,9 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
   const dim3 g0((unsigned)((size_t)count * job.nsub * ((1 << LB) / G0)));
   k_ntt2_fpr<LA, LB, true, 0><<<g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
   const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
-  k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(acc, D, x, d_keys, r->d_mods,
-                                                                                   r->iP, count);
+  ks_row_attrs<LA, LB, L>();
+  k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+                                                                               r->iP, count);
 }
 static bool ks_row_fusable(const cgb_ring *r) {
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
@@ -1913,8 +1941,9 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   {  // 3
     const dim3 g1((unsigned)((size_t)count * LP * ((1 << LA) / G1)));
     launch_begin(r);
-    k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(acc, D, x, d_keys, r->d_mods,
-                                                                                     r->iP, count);
+    ks_row_attrs<LA, LB, L>();
+    k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+                                                                                 r->iP, count);
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
