@@ -111,6 +111,12 @@ int cgb_pt_encode(cgb_ring *ring, int count, const uint64_t *slots, int kind,
  * randomness of ciphertext i is ChaCha20(enc_key, first_index + i). */
 int cgb_encrypt(cgb_ring *ring, int count, const uint64_t *slots,
                 const uint32_t enc_key[8], uint64_t first_index, const uint32_t *out);
+/* cgb_encrypt over items of several contexts in one launch sequence: item i uses
+ * the 8-word key enc_keys[8 i .. 8 i + 8) and encryption index indices[i] (the
+ * per-context counters of Context.encrypt, backend.py:307-310, for a wave of
+ * encryptions owned by different contexts) */
+int cgb_encrypt_batch(cgb_ring *ring, int count, const uint64_t *slots, const uint32_t *enc_keys,
+                      const uint64_t *indices, const uint32_t *out_ids);
 /* Context.decrypt (backend.py:312-319) */
 int cgb_decrypt(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *slots_out);
 /* client-side diagnostic: invariant noise budget in bits of each ciphertext */

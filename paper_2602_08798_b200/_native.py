@@ -84,6 +84,7 @@ SIGNATURES = {
     "cgb_pt_free": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_pt_encode": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, ctypes.c_int, _u32p]),
     "cgb_encrypt": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, _u32p, ctypes.c_uint64, _u32p]),
+    "cgb_encrypt_batch": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, _u32p, _u64p, _u32p]),
     "cgb_decrypt": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p]),
     "cgb_noise_budget": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _dblp]),
     "cgb_add": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),

@@ -29,6 +29,8 @@ and channel transcripts are charged exactly as that sequence charges them.
 
 from __future__ import annotations
 
+import os
+import time
 from dataclasses import dataclass
 from enum import Enum
 
@@ -36,7 +38,8 @@ import numpy as np
 
 from .backend import ParameterError, onehot_batch
 from .encodings import EncodingKind, PackedMatrix, next_pow2, tile_wave
-from .fixedpoint import FixedPointParams, attention_weights, causal_attention_weights, fp_truncate
+from .fixedpoint import (FixedPointParams, attention_weights, attention_weights_rows, causal_attention_weights,
+                         fp_truncate)
 from .linear_kernels import fold_wave
 from .nonlinear import MpcChannel, SharePair, he_to_shares_wave, reconstruct, share_vector, shares_to_he_wave
 
@@ -65,6 +68,15 @@ class ScoreVector:
 def _onehots(n: int, slots):
     """One-hot plaintext masks as a symbolic batch (cached on the device by key)."""
     return onehot_batch(n, slots)
+
+
+# list of (label, perf_counter) when CGB_HOST_TRACE is set (host timeline of a step)
+_TRACE = [] if os.environ.get("CGB_HOST_TRACE") else None
+
+
+def _mark(label):
+    if _TRACE is not None:
+        _TRACE.append((label, time.perf_counter()))
 
 
 def _C(ctx):
@@ -230,6 +242,7 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
     ``attention_step`` calls would; ctxs may repeat only if the heads would
     have run back to back on that context (then encryptions are assigned in
     head order, which is the sequential order)."""
+    _mark("step.start")
     H = len(qs)
     c0 = ctxs[0]
     C = _C(c0)
@@ -299,11 +312,14 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
             plan.extend((mpcs[h], n) for _ in range(len(cache.auto_V.parts)))
     plan.extend((mpcs[h], n) for h in range(H))
     plan.extend((mpcs[h], caches[h].d2) for h in range(H))
+    _mark("scores.enqueued")
     for ch, length in plan:
         ch.predraw([length])
+    _mark("masks.predrawn")
     shares = he_to_shares_wave(W.concat(parts), chans, lens) if parts else []
+    _mark("scores.decrypted")
     # ---- client: reassemble scores, softmax -------------------------------------
-    weights, si = [], 0
+    rows, si = [], 0
     for h in range(H):
         cache = caches[h]
         pieces = []
@@ -311,13 +327,18 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
             pieces.append(reconstruct(shares[si]))
             si += 1
         for qi in range(len(cache.auto_K.parts) if cache.t_auto > 0 else 0):
-            vals = reconstruct(shares[si])
+            sp = shares[si]
             si += 1
             rows_here = min(cache.B, cache.t_auto - qi * cache.B)
-            pieces.append(vals[np.arange(rows_here) * cache.d2])
-        a = attention_weights(np.concatenate(pieces), cache.d2, fp)
-        mpcs[h].transfer("decode_softmax", cache.m + cache.t_auto, trips=3 + fp.reciprocal_iters)
-        weights.append(a)
+            at = np.arange(rows_here) * cache.d2  # only the block starts carry scores
+            pieces.append(reconstruct(SharePair(sp.client[at], sp.server[at], sp.p, rows_here)))
+        rows.append(np.concatenate(pieces))
+    if len({r.shape[0] for r in rows}) == 1 and len({c.d2 for c in caches}) == 1:
+        weights = list(attention_weights_rows(np.stack(rows), caches[0].d2, fp))  # all heads at once
+    else:
+        weights = [attention_weights(rows[h], caches[h].d2, fp) for h in range(H)]
+    for h in range(H):
+        mpcs[h].transfer("decode_softmax", caches[h].m + caches[h].t_auto, trips=3 + fp.reciprocal_iters)
     # ---- weights back under encryption: a_pref, then one coefficient ct per auto part
     sp_list, s_ctx, s_ch, s_tag = [], [], [], []
     for h in range(H):
@@ -333,7 +354,9 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
                 coeff[: rows_here * cache.d2] = np.repeat(seg, cache.d2)
                 sp_list.append(share_vector(coeff, mpcs[h]))
                 s_ctx.append(ctxs[h]); s_ch.append(mpcs[h]); s_tag.append(("a", h, qi))
+    _mark("softmax.done")
     enc = shares_to_he_wave(sp_list, s_ctx, s_ch) if sp_list else None
+    _mark("weights.encrypted")
     # ---- values: prefill segment, sum_c dot_into_slot(a_pref, V_c, c) ------------
     o_parts, o_groups = [], []
     pv = None
@@ -385,11 +408,15 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
         else:
             o_list.append(av.take([j]))
     ow = W.concat(o_list)
+    _mark("values.enqueued")
     # ---- output: masked decrypt (d2 slots), truncate, re-encrypt -----------------
     d2s = [c.d2 for c in caches]
     sh = he_to_shares_wave(ow, mpcs, d2s)
+    _mark("values.decrypted")
     tr = [_truncate(s, fp, ch) for s, ch in zip(sh, mpcs)]
-    return shares_to_he_wave(tr, ctxs, mpcs).handles()
+    out = shares_to_he_wave(tr, ctxs, mpcs).handles()
+    _mark("step.end")
+    return out
 
 
 def _truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel, mask=None) -> SharePair:

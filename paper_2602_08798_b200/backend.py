@@ -643,12 +643,15 @@ class GpuContext:
         ring = uniq[0]._ring
         ids = ring.alloc(len(owner))
         blk = _Block(ring, ids)
+        # item i takes its context's next encryption index, in item order (the per-context
+        # sequence of Context.encrypt calls); all contexts go through one launch sequence
+        idx = np.zeros(len(owner), np.uint64)
         for k, c in enumerate(uniq):
             sel = np.nonzero(owner == k)[0]
-            if sel.size == 0:
-                continue
-            ring.encrypt(vecs[sel], c._enc_key, c._enc_index, ids[sel])
+            idx[sel] = c._enc_index + np.arange(sel.size, dtype=np.uint64)
             c._enc_index += sel.size
+        keys = np.stack([np.asarray(c._enc_key, dtype=np.uint32).reshape(8) for c in uniq])[owner]
+        ring.encrypt_batch(vecs, keys, idx, ids)
         w = Wave(uniq, owner, ids, np.full(len(owner), uniq[0].params.initial_noise_budget, np.int64), [blk])
         w.cids = GpuContext._charge(w, "encrypt")
         return w

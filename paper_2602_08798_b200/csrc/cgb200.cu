@@ -1530,13 +1530,14 @@ __device__ __forceinline__ u64 u128_mod(u64 hi, u64 lo, const ModTab &M) {
   return add_mod(mul_mod(hi % M.q, M.r64, M), lo % M.q, M.q);
 }
 // uniform residues in NTT form from ChaCha20: element e = l*N + j uses words 4e..4e+3
-__global__ void k_sample_uniform(u64 *const *dst, ChaKey key, const u64 *nonces, int nl, const int *mod_idx,
+__global__ void k_sample_uniform(u64 *const *dst, const ChaKey *keys, const u64 *nonces, int nl, const int *mod_idx,
                                  const ModTab *mods, int logN) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, nblk = ((u64)nl * N + 3) / 4;
   u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nblk) return;
   u32 w[16];
+  const ChaKey key = keys[item];
   chacha_block(key, c, nonces[item], w);
 #pragma unroll
   for (int r = 0; r < 4; r++) {
@@ -1549,12 +1550,13 @@ __global__ void k_sample_uniform(u64 *const *dst, ChaKey key, const u64 *nonces,
   }
 }
 // centred binomial (eta = 21) errors: element j uses words 2j, 2j+1
-__global__ void k_sample_cbd(i64 *e, ChaKey key, const u64 *nonces, int logN) {
+__global__ void k_sample_cbd(i64 *e, const ChaKey *keys, const u64 *nonces, int logN) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, nblk = (N + 7) / 8;
   u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nblk) return;
   u32 w[16];
+  const ChaKey key = keys[item];
   chacha_block(key, c, nonces[item], w);
 #pragma unroll
   for (int r = 0; r < 8; r++) {
@@ -2179,18 +2181,21 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
 // ============================================================================
 // key generation
 // ============================================================================
-static void sample_cbd(cgb_ring *r, Scratch &S, i64 *e, const ChaKey &key, const std::vector<u64> &nonces) {
+// keys: one ChaCha20 key per item (device copy made here)
+static void sample_cbd(cgb_ring *r, Scratch &S, i64 *e, const ChaKey *keys, const std::vector<u64> &nonces) {
   int n = (int)nonces.size();
   u64 *d_n = S.up(nonces.data(), n);
+  ChaKey *d_k = S.up(keys, n);
   u64 nblk = ((u64)r->N + 7) / 8;
-  LAUNCH("sample_cbd", BYTES_sample_cbd, k_sample_cbd<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(e, key, d_n, r->logN));
+  LAUNCH("sample_cbd", BYTES_sample_cbd, k_sample_cbd<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(e, d_k, d_n, r->logN));
 }
-static void sample_uniform(cgb_ring *r, Scratch &S, u64 *const *d_dst, int n, const ChaKey &key,
+static void sample_uniform(cgb_ring *r, Scratch &S, u64 *const *d_dst, int n, const ChaKey *keys,
                            const std::vector<u64> &nonces, int nl, const int *mod_idx_host) {
   u64 *d_n = S.up(nonces.data(), n);
+  ChaKey *d_k = S.up(keys, n);
   int *d_mi = S.up(mod_idx_host, nl);
   u64 nblk = ((u64)nl * r->N + 3) / 4;
-  LAUNCH("sample_uniform", BYTES_sample_uniform, k_sample_uniform<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(d_dst, key, d_n, nl, d_mi, r->d_mods, r->logN));
+  LAUNCH("sample_uniform", BYTES_sample_uniform, k_sample_uniform<<<dim3(GRID1(nblk, 128).x, n), 128, 0, r->stream>>>(d_dst, d_k, d_n, nl, d_mi, r->d_mods, r->logN));
 }
 
 static u64 *get_key(cgb_ring *r, u64 g) {
@@ -2219,8 +2224,8 @@ static u64 *get_key(cgb_ring *r, u64 g) {
     u64 sub = (g << 8) | (u64)j;
     std::vector<u64 *> adst = {key + ((u64)j * 2 + 1) * LPN};
     u64 **d_a = S.up(adst.data(), 1);
-    sample_uniform(r, S, d_a, 1, r->keyseed, {nonce_of(DOM_KSK_A, sub)}, LP, mi.data());
-    sample_cbd(r, S, e, r->keyseed, {nonce_of(DOM_KSK_E, sub)});
+    sample_uniform(r, S, d_a, 1, &r->keyseed, {nonce_of(DOM_KSK_A, sub)}, LP, mi.data());
+    sample_cbd(r, S, e, &r->keyseed, {nonce_of(DOM_KSK_E, sub)});
     LAUNCH("ksk_b", BYTES_ksk_b, k_ksk_b<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, e, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
     ntt_items(r, true, key + ((u64)j * 2 + 0) * LPN, nullptr, 0, 1, 1, LP, mi.data());
     LAUNCH("ksk_fin", BYTES_ksk_fin, k_ksk_fin<<<GRID1(LPN, TPB), TPB, 0, r->stream>>>(key, j, r->d_s, sp, r->d_mods, r->d_c, L, r->iP, r->logN));
@@ -2830,13 +2835,11 @@ int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const
   API_END
 }
 
-int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t enc_key[8], uint64_t first_index,
-                const uint32_t *out) {
-  API_BEGIN
-  if (count <= 0) return CGB_OK;
+// encryption of `count` slot vectors, item i with ChaCha20 key keys[i] and encryption
+// index idx[i] (nonces DOM_ENC_A / DOM_ENC_E); one launch sequence for the batch
+static void encrypt_items(cgb_ring *r, int count, const uint64_t *slots, const ChaKey *keys, const u64 *idx,
+                          const uint32_t *out) {
   Scratch S(r);
-  ChaKey key;
-  memcpy(key.k, enc_key, sizeof key.k);
   u64 *m = S.alloc<u64>((size_t)count * r->N);
   encode_slots(r, S, slots, count, m);
   auto pc = ct_ptrs(r, count, out);
@@ -2845,19 +2848,41 @@ int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t en
   std::vector<u64> na(count), ne(count);
   for (int i = 0; i < count; i++) {
     c1[i] = pc[i] + (size_t)r->L * r->N;
-    na[i] = nonce_of(DOM_ENC_A, first_index + i);
-    ne[i] = nonce_of(DOM_ENC_E, first_index + i);
+    na[i] = nonce_of(DOM_ENC_A, idx[i]);
+    ne[i] = nonce_of(DOM_ENC_E, idx[i]);
   }
   u64 **dc1 = S.up(c1.data(), count);
   std::vector<int> qm;
   q_mod_idx(r, qm);
-  sample_uniform(r, S, dc1, count, key, na, r->L, qm.data());
+  sample_uniform(r, S, dc1, count, keys, na, r->L, qm.data());
   i64 *e = S.alloc<i64>((size_t)count * r->N);
-  sample_cbd(r, S, e, key, ne);
+  sample_cbd(r, S, e, keys, ne);
   u64 words = (u64)r->L * r->N;
   LAUNCH("enc_c0", BYTES_enc_c0, k_enc_c0<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, m, e, r->d_mods, r->d_c, r->L, r->logN));
   ntt_items(r, true, nullptr, dc, 0, count, 1, r->L, qm.data());
   LAUNCH("enc_sub_as", BYTES_enc_sub_as, k_enc_sub_as<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dc, r->d_s, r->d_mods, r->L, r->logN));
+}
+
+int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t enc_key[8], uint64_t first_index,
+                const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  ChaKey key;
+  memcpy(key.k, enc_key, sizeof key.k);
+  std::vector<ChaKey> keys(count, key);
+  std::vector<u64> idx(count);
+  for (int i = 0; i < count; i++) idx[i] = first_index + i;
+  encrypt_items(r, count, slots, keys.data(), idx.data(), out);
+  API_END
+}
+
+int cgb_encrypt_batch(cgb_ring *r, int count, const uint64_t *slots, const uint32_t *enc_keys,
+                      const uint64_t *indices, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  std::vector<ChaKey> keys(count);
+  for (int i = 0; i < count; i++) memcpy(keys[i].k, enc_keys + 8 * (size_t)i, sizeof keys[i].k);
+  encrypt_items(r, count, slots, keys.data(), indices, out);
   API_END
 }
 
@@ -3108,20 +3133,13 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       launch_end(r, "scale_round", BYTES_scale_round);
     }
     ntt_items(r, true, d, nullptr, 3ull * L * N, n, 3, L, qm.data());
-    // relinearise d2, add (d0, d1)
-    u64 *x = S.alloc<u64>((size_t)n * L * N);
-    CK(cudaMemcpy2DAsync(x, sizeof(u64) * L * N, d + 2ull * L * N, sizeof(u64) * 3 * L * N, sizeof(u64) * L * N, n,
-                         cudaMemcpyDeviceToDevice, r->stream));
-    u64 *d01 = S.alloc<u64>((size_t)n * 2 * L * N);
-    CK(cudaMemcpy2DAsync(d01, sizeof(u64) * 2 * L * N, d, sizeof(u64) * 3 * L * N, sizeof(u64) * 2 * L * N, n,
-                         cudaMemcpyDeviceToDevice, r->stream));
+    // relinearise d2 and add (d0, d1), both read in place from d = [item][d0 d1 d2][L][N]
     std::vector<u64 *> keys(n, rk);
     u64 **dk = S.up(keys.data(), n), **dout = S.up(po.data(), n);
-    // out = ks + d01 : reuse add0 for poly 0 and an add1 table for poly 1 via a second pass
     std::vector<u64 *> d01p(n);
-    for (int i = 0; i < n; i++) d01p[i] = d01 + (size_t)i * 2 * L * N;
+    for (int i = 0; i < n; i++) d01p[i] = d + (size_t)i * 3 * L * N;
     u64 **dd01 = S.up(d01p.data(), n);
-    KsSrc xin{x, (u64)L * N, nullptr, 0, nullptr};
+    KsSrc xin{d + 2ull * L * N, 3ull * L * N, nullptr, 0, nullptr};
     KsSrc none{nullptr, 0, nullptr, 0, nullptr};
     keyswitch(r, S, xin, n, dk, dout, none, (const u64 *const *)dd01);
   }

@@ -100,6 +100,39 @@ def fp_softmax(s, fp: FixedPointParams) -> np.ndarray:
     return (e * rec + (1 << (q - 1))) >> q
 
 
+def fp_softmax_rows(S, fp: FixedPointParams) -> np.ndarray:
+    """fp_softmax of every row of S (rows of one length), vectorised over rows.
+
+    Same integer operations as fp_softmax row by row; the Newton reciprocal runs
+    on int64 vectors, exact while every intermediate stays below 2^62 (checked:
+    rows whose exponent sum could overflow fall back to the per-row path)."""
+    f = fp.f
+    S = np.asarray(S, dtype=np.int64)
+    if S.ndim != 2 or S.shape[1] <= 1:
+        return np.stack([fp_softmax(row, fp) for row in S]) if len(S) else S
+    c2, c1, c0 = (fp.quantize(c) for c in EXP_COEFFS)
+    x = S - S.max(axis=1, keepdims=True)
+    z = ((-x) * fp.quantize(1.0 / math.log(2.0))) >> (2 * f)
+    r = x + z * fp.quantize(math.log(2.0))
+    poly = np.maximum(((c2 * ((r * r) >> f)) >> f) + ((c1 * r) >> f) + c0, 0)
+    e = poly >> np.minimum(z, SHIFT_CAP)
+    tot = e.sum(axis=1)
+    q = 2 * f
+    if tot.min() <= 0 or int(tot.max()).bit_length() + f + q > 61 or 3 * q + 2 * f > 61:
+        return np.stack([fp_softmax(row, fp) for row in S])
+    bits = np.frexp(tot.astype(np.float64))[1].astype(np.int64)  # bit length (tot < 2^53: exact)
+    y = np.left_shift(np.int64(1), np.maximum(0, f + q - bits))
+    two = np.int64(1) << (q + 1)
+    for _ in range(fp.reciprocal_iters):
+        y = (y * (two - ((tot * y) >> f))) >> q
+    return (e * y[:, None] + (np.int64(1) << (q - 1))) >> q
+
+
+def attention_weights_rows(S_2f, d2: int, fp: FixedPointParams) -> np.ndarray:
+    """attention_weights of every row of S_2f (one head per row)."""
+    return fp_softmax_rows(_scaled_scores(S_2f, d2, fp), fp)
+
+
 def _scaled_scores(scores_2f, d2: int, fp: FixedPointParams) -> np.ndarray:
     s1 = fp_truncate(np.asarray(scores_2f, dtype=np.int64), fp.f)
     return (s1 * fp.quantize(1.0 / math.sqrt(d2))) >> fp.f

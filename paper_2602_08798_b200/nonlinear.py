@@ -82,7 +82,12 @@ class MpcChannel:
 
 
 def reconstruct(s: SharePair) -> np.ndarray:
-    return to_signed((s.client + s.server) % s.p, s.p)
+    v = s.client + s.server
+    if v.size and v.min() >= 0 and v.max() < 2 * s.p:  # both shares in [0, p): one conditional subtract
+        v = np.where(v >= s.p, v - s.p, v)
+    else:
+        v = v % s.p
+    return to_signed(v, s.p)
 
 
 def share_vector(values, ch: MpcChannel) -> SharePair:
@@ -132,8 +137,14 @@ def shares_to_he_wave(shares, ctxs, chans, record: bool = True):
     c0 = ctxs[0]
     C = type(c0)
     n = c0.params.n_slots
-    client = np.stack([c.plain_from_dense(s.client) for c, s in zip(ctxs, shares)])
-    server = np.stack([c.plain_from_dense(s.server) for c, s in zip(ctxs, shares)])
+    # shares are residues in [0, p) (share_vector / reconstruct); zero-padded to n slots
+    client = np.zeros((len(shares), n), np.int64)
+    server = np.zeros((len(shares), n), np.int64)
+    for i, sh in enumerate(shares):
+        if sh.client.shape[0] > n:
+            raise ParameterError("vector longer than slot count")
+        client[i, : sh.client.shape[0]] = sh.client
+        server[i, : sh.server.shape[0]] = sh.server
     enc = C.w_encrypt(ctxs, client)
     out = C.w_add_plain(enc, server, one_shot=True)
     if record:

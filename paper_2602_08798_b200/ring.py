@@ -157,6 +157,15 @@ class Ring:
                                         nat.u32ptr(ids)), "cgb_encrypt")
         self.h2d_bytes += s.nbytes
 
+    def encrypt_batch(self, slots, enc_keys, indices, ids):
+        """Item i encrypted with key enc_keys[i] (8 words) at encryption index indices[i]."""
+        s, ids = self._slots2d(slots), _ids(ids)
+        k = np.ascontiguousarray(np.asarray(enc_keys, dtype=np.uint32).reshape(ids.size, 8))
+        ix = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(ids.size))
+        nat.check(nat.lib().cgb_encrypt_batch(self._h, ids.size, nat.u64ptr(s), nat.u32ptr(k), nat.u64ptr(ix),
+                                              nat.u32ptr(ids)), "cgb_encrypt_batch")
+        self.h2d_bytes += s.nbytes
+
     def decrypt(self, ids) -> np.ndarray:
         ids = _ids(ids)
         out = np.zeros((ids.size, self.n_slots), dtype=np.uint64)

@@ -57,3 +57,18 @@ def test_reference_path_restatement_matches_goldens(api):
         fn, kw = harness.SMALL[name]
         rec, _ = fn(ns, slot_ctx, **kw)
         compare(rec, np.load(GOLD / f"{name}.npz"))
+
+
+def test_softmax_rows_equals_per_row():
+    """The head-batched integer softmax (fixedpoint.attention_weights_rows) equals
+    the per-row restatement of fixedpoint.py:204-209 on random score ranges."""
+    from paper_2602_08798_b200.fixedpoint import FixedPointParams, attention_weights, attention_weights_rows
+    p = 536903681
+    rng = np.random.default_rng(7)
+    for f in (6, 8, 11):
+        fp = FixedPointParams(f, p)
+        for n in (2, 17, 129, 513):
+            for scale in (1, 2 ** f, 2 ** (2 * f + 6)):
+                S = rng.integers(-4 * scale, 4 * scale, (12, n))
+                ref = np.stack([attention_weights(S[h], 64, fp) for h in range(12)])
+                assert (attention_weights_rows(S, 64, fp) == ref).all()
