@@ -646,6 +646,19 @@ __device__ __forceinline__ u64 ks_src_word(const KsSrc &x, int item, int limb, u
   }
   return x.base[(u64)item * x.stride + ((u64)limb << logN) + k];
 }
+// words k0 .. k0 + 3 (k0 a multiple of 4) of ks_src_word: one sector per 4 words
+__device__ __forceinline__ void ks_src_block4(const KsSrc &x, int item, int limb, u32 k0, int logN, u64 out[4]) {
+  if (x.items) {
+    const u64 *p = x.items[item] + x.off + ((u64)limb << logN);
+    if (x.g) {
+      gather4(p, k0, x.g[item], logN, out);
+    } else {
+      ld256(p + k0, out);
+    }
+    return;
+  }
+  ld256(x.base + (u64)item * x.stride + ((u64)limb << logN) + k0, out);
+}
 template <int L>
 __global__ void k_ks_inner(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *keys, u64 kw,
                            const ModTab *mods, int logN, int count, int per_block) {
@@ -760,14 +773,15 @@ struct MdEpi {
     const u64 *b = add1 ? add1[item] + (u64)unit * N + pos : nullptr;
     const bool a0 = pp == 0 && (add0.items || add0.base);
     if (n == 4) {
-      u64 av[4], bv[4] = {0, 0, 0, 0};
+      u64 av[4], bv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
       ld256(a, av);
       if (b) ld256(b, bv);
+      if (a0) ks_src_block4(add0, item, l, (u32)pos, logN, cv);
       u64 v[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         v[k] = mul_shoup(sub_mod(av[k], w[k], q), pi, pis, q);
-        if (a0) v[k] = add_mod(v[k], ks_src_word(add0, item, l, (u32)(pos + k), logN), q);
+        if (a0) v[k] = add_mod(v[k], cv[k], q);
         if (b) v[k] = add_mod(v[k], bv[k], q);
       }
       st256(o, v[0], v[1], v[2], v[3]);
@@ -792,8 +806,16 @@ struct MdEpi {
 // so a sum of <= 4 digits is an exact integer < 11q < 2^53 and its canonical residue
 // equals the integer path's.  acc[item][p][l] is written
 // once; D's row-pass output never reaches memory.
+#ifndef CGB_KSROW_G4
+#define CGB_KSROW_G4 0  // measured: the per-word own-digit loads are faster here (profiles/r02)
+#endif
+#ifdef CGB_KSROW_MINB
+#define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_KSROW_MINB)
+#else  // no minimum: ptxas picks 168 registers (a minimum of 1 lets it take 228)
+#define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16)
+#endif
 template <int LA, int LB, int L>
-__global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
+__global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
                                                            const u64 *const *keys, const ModTab *mods, int iP,
                                                            int count) {
   extern __shared__ u64 sm3[];
@@ -833,11 +855,23 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ks_row(u64 *acc, const u64 *
   for (int j = 0; j < L; j++) {
     double x[E];
     if (j == l) {  // the digit's own limb: the input itself, already in NTT form
+#if CGB_KSROW_G4
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k += 4) {
+          u64 w[4];
+          ks_src_block4(xin, item, j, (u32)(row0 + PB::idx(tl, u, k)), LOGN, w);
+#pragma unroll
+          for (int e = 0; e < 4; e++) x[u * PB::K + k + e] = u2d(w[e]);
+        }
+#else
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++)
           x[u * PB::K + k] = u2d(ks_src_word(xin, item, j, (u32)(row0 + PB::idx(tl, u, k)), LOGN));
+#endif
     } else {
       const u64 *src = D + ((u64)item * L * LP + (u64)j * LP + l) * N + row0;
 #pragma unroll

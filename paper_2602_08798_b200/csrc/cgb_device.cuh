@@ -157,6 +157,25 @@ __device__ __forceinline__ u32 perm_g(u32 k, u64 g, int logN) {
   const u32 se = (u32)((e * g) & ((2ull << logN) - 1));
   return __brev((se - 1) >> 1) >> (32 - logN);
 }
+// Aligned blocks of 2^b consecutive output words read an aligned block of 2^b
+// input words (the automorphism acts on the top bits of brev(k) by an affine map
+// and leaves the low bits' block fixed), so a gather of 4 consecutive outputs is
+// ONE 32-byte sector load plus an in-register selection.
+__device__ __forceinline__ u64 sel4(const u64 w[4], u32 s) {
+  const u64 lo = (s & 1) ? w[1] : w[0], hi = (s & 1) ? w[3] : w[2];
+  return (s & 2) ? hi : lo;
+}
+// out[i] = src[perm_g(k0 + i)], i < 4, k0 a multiple of 4
+__device__ __forceinline__ void gather4(const u64 *src, u32 k0, u64 g, int logN, u64 out[4]) {
+  const u32 p0 = perm_g(k0, g, logN);
+  u64 w[4];
+  asm("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(src + (p0 & ~3u)));
+  out[0] = sel4(w, p0 & 3);
+#pragma unroll
+  for (int i = 1; i < 4; i++) out[i] = sel4(w, perm_g(k0 + i, g, logN) & 3);
+}
+
 // source pointer of unit `sub` of `item` for a fused load (null: in place)
 __device__ __forceinline__ const u64 *job_src(const NttJob &job, int item, int sub, int logN) {
   if (job.src_items) return job.src_items[item] + ((u64)job.src_off[sub] << logN);
@@ -698,8 +717,13 @@ struct NoEpi {
 };
 
 // LM-point sub-NTT in two register phases (RA stages then LM - RA), E = 16
+#ifdef CGB_FPR_MINB
+#define FPR_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_FPR_MINB)
+#else
+#define FPR_BOUNDS __launch_bounds__(NTT2_TILE / 16)
+#endif
 template <int LA, int LB, bool FWD, int PASS, class EPI = NoEpi>
-__global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job, EPI epi) {
+__global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   extern __shared__ u64 sm2[];
   constexpr int E = 16, T = NTT2_TILE / E;
   constexpr int LOGN = LA + LB;
@@ -749,6 +773,11 @@ __global__ void __launch_bounds__(NTT2_TILE / 16) k_ntt2_fpr(NttJob job, EPI epi
       for (int u = 0; u < PA::R; u++)
 #pragma unroll
         for (int k = 0; k < PA::K; k += 4) ld256(src + gaddr(PA::idx(tl, u, k)), &v[u * PA::K + k]);
+    } else if (PASS == 1 && PA::ST == 1 && PA::K % 4 == 0) {  // automorphism: one sector per 4 words
+#pragma unroll
+      for (int u = 0; u < PA::R; u++)
+#pragma unroll
+        for (int k = 0; k < PA::K; k += 4) gather4(src, (u32)gaddr(PA::idx(tl, u, k)), gal, LOGN, &v[u * PA::K + k]);
     } else {
 #pragma unroll
       for (int u = 0; u < PA::R; u++)
