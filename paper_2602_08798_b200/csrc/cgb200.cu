@@ -278,6 +278,23 @@ static cudaEvent_t take_event(cgb_ring *r) {
   CK(cudaEventCreate(&e));
   return e;
 }
+// Launch with programmatic stream serialization (kernels that call pdl_wait()
+// before touching their predecessor's output); CGB_PDL=0 turns it off.
+static bool g_pdl = true;
+template <typename... KP, typename... A>
+static void launch_pdl(cgb_ring *r, void (*k)(KP...), dim3 grid, dim3 block, size_t smem, A... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = r->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (g_pdl && !r->timing) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, ((KP)args)...);
+}
 static void launch_begin(cgb_ring *r) {
   if (!r->timing) return;
   r->pending = take_event(r);
@@ -389,8 +406,8 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
     const bool r0 = g_fp_regio & 1, r1 = g_fp_regio & 2;
     auto pass0 = [&](const NttJob &j, bool f) {
       if (r0) {
-        if (f) k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j, NoEpi{});
-        else k_ntt2_fpr<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 16, f0, r->stream>>>(j, NoEpi{});
+        if (f) launch_pdl(r, k_ntt2_fpr<LA, LB, true, 0>, grid(LA), NTT2_TILE / 16, f0, j, NoEpi{});
+        else launch_pdl(r, k_ntt2_fpr<LA, LB, false, 0>, grid(LA), NTT2_TILE / 16, f0, j, NoEpi{});
       } else {
         if (f) k_ntt2_fp<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
         else k_ntt2_fp<LA, LB, false, 0><<<grid(LA), NTT2_TILE / 8, s0, r->stream>>>(j);
@@ -398,8 +415,8 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
     };
     auto pass1 = [&](const NttJob &j, bool f) {
       if (r1) {
-        if (f) k_ntt2_fpr<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j, NoEpi{});
-        else k_ntt2_fpr<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 16, f1, r->stream>>>(j, NoEpi{});
+        if (f) launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1>, grid(LB), NTT2_TILE / 16, f1, j, NoEpi{});
+        else launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1>, grid(LB), NTT2_TILE / 16, f1, j, NoEpi{});
       } else {
         if (f) k_ntt2_fp<LA, LB, true, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
         else k_ntt2_fp<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
@@ -844,6 +861,8 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     }
   };
   stage_tw(Md.ftw1t);
+  pdl_start_dependents();
+  pdl_wait();
   const double2 *tw = tws + g * (M + 1);
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
@@ -988,6 +1007,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
     const double2 *ft = reinterpret_cast<const double2 *>(job.mods[job.dst_mod[s][t]].ftw);
     for (int i = tid; i < M; i += T) tws[(t + 1) * M + i] = __ldg(ft + i);
   }
+  pdl_start_dependents();
+  pdl_wait();
   const u64 *src = job.src + (u64)item * job.src_stride + ((u64)job.src_off[s] << LOGN);
   double x[E];
 #pragma unroll
@@ -1049,10 +1070,10 @@ static void col_fused_t(cgb_ring *r, const ColJob &job, int count, int nt) {
   const dim3 grid((unsigned)((size_t)count * job.nsrc * ((1 << LB) / G)));
   const size_t sm = col_fused_smem<LA, LB>(nt);
   switch (nt) {
-    case 2: k_col_fused<LA, LB, 2><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
-    case 3: k_col_fused<LA, LB, 3><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
-    case 4: k_col_fused<LA, LB, 4><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
-    default: k_col_fused<LA, LB, 1><<<grid, NTT2_TILE / 16, sm, r->stream>>>(job); break;
+    case 2: launch_pdl(r, k_col_fused<LA, LB, 2>, grid, NTT2_TILE / 16, sm, job); break;
+    case 3: launch_pdl(r, k_col_fused<LA, LB, 3>, grid, NTT2_TILE / 16, sm, job); break;
+    case 4: launch_pdl(r, k_col_fused<LA, LB, 4>, grid, NTT2_TILE / 16, sm, job); break;
+    default: launch_pdl(r, k_col_fused<LA, LB, 1>, grid, NTT2_TILE / 16, sm, job); break;
   }
 }
 static bool col_fusable(const cgb_ring *r) {
@@ -1091,10 +1112,10 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
                            u64 *const *d_keys) {
   const int G0 = NTT2_TILE >> LA, G1 = NTT2_TILE >> LB;
   const dim3 g0((unsigned)((size_t)count * job.nsub * ((1 << LB) / G0)));
-  k_ntt2_fpr<LA, LB, true, 0><<<g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
+  launch_pdl(r, k_ntt2_fpr<LA, LB, true, 0>, g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), job, NoEpi{});
   const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
   ks_row_attrs<LA, LB, L>();
-  k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+  launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
                                                                                r->iP, count);
 }
 static bool ks_row_fusable(const cgb_ring *r) {
@@ -1125,7 +1146,7 @@ template <int LA, int LB>
 static void ntt_inv_col_t(cgb_ring *r, const NttJob &job, int count) {
   const int G0 = NTT2_TILE >> LA;
   const dim3 g0((unsigned)((size_t)count * job.nsub * ((1 << LB) / G0)));
-  k_ntt2_fpr<LA, LB, false, 0><<<g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
+  launch_pdl(r, k_ntt2_fpr<LA, LB, false, 0>, g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), job, NoEpi{});
 }
 static void ntt_inv_col(cgb_ring *r, NttJob &job, int count) {
   job.mods = r->d_mods;
@@ -1154,8 +1175,8 @@ static void moddown_ntt_fused_t(cgb_ring *r, const NttJob &job, int count, const
     int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
     return dim3((unsigned)((size_t)count * job.nsub * (nsubs / G)));
   };
-  k_ntt2_fpr<LA, LB, true, 0><<<grid(LA), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), r->stream>>>(job, NoEpi{});
-  k_ntt2_fpr<LA, LB, true, 1, MdEpi><<<grid(LB), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(second, epi);
+  launch_pdl(r, k_ntt2_fpr<LA, LB, true, 0>, grid(LA), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), job, NoEpi{});
+  launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, grid(LB), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), second, epi);
 }
 static bool moddown_fusable(const cgb_ring *r) {
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_md_epi && r->logN >= 12 && r->logN <= 16;
@@ -1951,7 +1972,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     job.mods = r->d_mods;
     job.logN = LA + LB;
     launch_begin(r);
-    k_ntt2_fpr<LA, LB, false, 1><<<rows_grid1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, NoEpi{});
+    launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1>, rows_grid1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), job, NoEpi{});
     launch_end(r, "ks_digit_rows", 16.0 * (double)count * L * N, (double)count * L * (N / 2) * LB);
   }
   {  // 2
@@ -1978,7 +1999,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     const dim3 g1((unsigned)((size_t)count * LP * ((1 << LA) / G1)));
     launch_begin(r);
     ks_row_attrs<LA, LB, L>();
-    k_ks_row<LA, LB, L><<<g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), r->stream>>>(acc, D, x, d_keys, r->d_mods,
+    launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
                                                                                  r->iP, count);
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
@@ -2017,7 +2038,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
     const dim3 g((unsigned)((size_t)count * n * ((1 << LA) / G1)));
     launch_begin(r);
-    k_ntt2_fpr<LA, LB, true, 1, MdEpi><<<g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), r->stream>>>(job, epi);
+    launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), job, epi);
     launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)),
                (double)count * n * ((N / 2) * LB + N));
   }
@@ -2594,6 +2615,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_ROW")) g_ks_row = atoi(e) != 0;
   if (const char *e = getenv("CGB_COL_FUSED")) g_col_fused = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
+  if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));

@@ -157,6 +157,12 @@ __device__ __forceinline__ u32 perm_g(u32 k, u64 g, int logN) {
   const u32 se = (u32)((e * g) & ((2ull << logN) - 1));
   return __brev((se - 1) >> 1) >> (32 - logN);
 }
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor drains; it stages constant tables (twiddles), then
+// waits for the predecessor's writes.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_start_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Aligned blocks of 2^b consecutive output words read an aligned block of 2^b
 // input words (the automorphism acts on the top bits of brev(k) by an affine map
 // and leaves the low bits' block fixed), so a gather of 4 consecutive outputs is
@@ -736,7 +742,6 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   static_assert(RB >= 1 && RB <= 4, "sub-NTT of 32..256 points");
   const int unit = blockIdx.x / TILES, tile = blockIdx.x - unit * TILES;
   const int item = unit / job.nsub, sub = unit - item * job.nsub;
-  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << LOGN);
   const ModTab &Md = job.mods[job.sub_mod[sub]];
   const u64 q = Md.q;
   const double qd = Md.qd, qinv = Md.qinv;
@@ -755,6 +760,9 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   // pass 0 shares one M-entry table (staged); pass 1 reads its row's table from global
   if (PASS == 0)
     for (int i = tid; i < M; i += T) tws[i] = __ldg(gtw + i);
+  pdl_start_dependents();
+  pdl_wait();  // the predecessor's output is complete from here on
+  u64 *p = (job.items ? job.items[item] : job.base + (u64)item * job.item_stride) + ((u64)job.sub_off[sub] << LOGN);
   // first phase straight from global memory (fused lift / automorphism)
   const u64 *src = job_src(job, item, sub, LOGN);
   if (!src) src = p;
