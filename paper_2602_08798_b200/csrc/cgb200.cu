@@ -355,6 +355,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes, double mm = 
 static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
 static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
 static bool g_md_epi = true;  // ModDown combine fused into its NTT's row pass (CGB_MD_EPI=0 -> separate kernel)
+static bool g_ks_md = true;   // ModDown row pass + combine fused into the Q limbs' k_ks_row (CGB_KS_MD)
 static bool g_ks_row = true;  // ModUp row pass fused with the key inner product (CGB_KS_ROW=0 -> ks_inner)
 static bool g_col_fused = true;  // INTT column pass + lift + forward column passes in one kernel (CGB_COL_FUSED)
 template <int LA, int LB, bool QS, int E>
@@ -790,8 +791,27 @@ struct MdEpi {
     const u64 *b = add1 ? add1[item] + (u64)unit * N + pos : nullptr;
     const bool a0 = pp == 0 && (add0.items || add0.base);
     if (n == 4) {
-      u64 av[4], bv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
+      u64 av[4];
       ld256(a, av);
+      combine4(item, unit, pos, w, av);
+    } else {
+      for (int k = 0; k < n; k++) {
+        u64 v = mul_shoup(sub_mod(a[k], w[k], q), pi, pis, q);
+        if (a0) v = add_mod(v, ks_src_word(add0, item, l, (u32)(pos + k), logN), q);
+        if (b) v = add_mod(v, b[k], q);
+        o[k] = v;
+      }
+    }
+  }
+  // words pos .. pos + 3 of unit `unit`: W's words w, the accumulator's words av
+  __device__ void combine4(int item, int unit, u64 pos, const u64 *w, const u64 *av) const {
+    const int pp = unit / L, l = unit - pp * L;
+    const u64 N = 1ull << logN, q = mods[l].q, pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
+    u64 *o = out[item] + (u64)unit * N + pos;
+    const u64 *b = add1 ? add1[item] + (u64)unit * N + pos : nullptr;
+    const bool a0 = pp == 0 && (add0.items || add0.base);
+    {
+      u64 bv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
       if (b) ld256(b, bv);
       if (a0) ks_src_block4(add0, item, l, (u32)pos, logN, cv);
       u64 v[4];
@@ -802,13 +822,6 @@ struct MdEpi {
         if (b) v[k] = add_mod(v[k], bv[k], q);
       }
       st256(o, v[0], v[1], v[2], v[3]);
-    } else {
-      for (int k = 0; k < n; k++) {
-        u64 v = mul_shoup(sub_mod(a[k], w[k], q), pi, pis, q);
-        if (a0) v = add_mod(v, ks_src_word(add0, item, l, (u32)(pos + k), logN), q);
-        if (b) v = add_mod(v, b[k], q);
-        o[k] = v;
-      }
     }
   }
 };
@@ -823,18 +836,26 @@ struct MdEpi {
 // so a sum of <= 4 digits is an exact integer < 11q < 2^53 and its canonical residue
 // equals the integer path's.  acc[item][p][l] is written
 // once; D's row-pass output never reaches memory.
+// k_ks_row's bulk-copy landing tile: rows of 2^LB words at a pitch of 2^LB + 8
+// (consecutive rows alternate between the two bank halves)
+__host__ __device__ constexpr int ksr_pitch(int LB) { return (1 << LB) + 8; }
+#ifndef CGB_KSROW_TMA
+#define CGB_KSROW_TMA 0  // D / W row tiles prefetched by bulk async copies (one tile ahead): measured slower
+#endif
 #ifndef CGB_KSROW_G4
 #define CGB_KSROW_G4 0  // measured: the per-word own-digit loads are faster here (profiles/r02)
 #endif
-#ifdef CGB_KSROW_MINB
-#define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_KSROW_MINB)
-#else  // no minimum: ptxas picks 168 registers (a minimum of 1 lets it take 228)
-#define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16)
+#ifndef CGB_KSROW_MINB
+#define CGB_KSROW_MINB 3  // <= 168 registers: 3 CTAs per SM (MODE 2 would otherwise take 208)
 #endif
-template <int LA, int LB, int L>
+#define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_KSROW_MINB)
+// MODE 0: every limb of Q u P; 1: the P limb only; 2: the Q limbs, followed by
+// ModDown's forward row pass of W (the column-pass output of lift(INTT(acc_P)))
+// with the combine as its epilogue -- the Q limbs' accumulators never reach memory.
+template <int LA, int LB, int L, int MODE = 0>
 __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
                                                            const u64 *const *keys, const ModTab *mods, int iP,
-                                                           int count) {
+                                                           int count, const u64 *W, MdEpi epi) {
   extern __shared__ u64 sm3[];
   constexpr int E = 16, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
   constexpr int G = NTT2_TILE / M, TPS = M / E, TILES = (1 << LA) / G;
@@ -845,7 +866,8 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   static_assert(PB::ST == 1 && PB::K % 4 == 0, "row-pass output: runs of >= 4 consecutive words");
   const u64 N = 1ull << LOGN;
   const int tile = blockIdx.x % TILES, rest = blockIdx.x / TILES;
-  const int l = rest % LP, item = rest / LP;
+  constexpr int NL = MODE == 0 ? LP : MODE == 1 ? 1 : L;  // limbs per item in the grid
+  const int l = MODE == 1 ? L : rest % NL, item = rest / NL;
   const ModTab &Md = mods[l == L ? iP : l];
   const double qd = Md.qd, qinv = Md.qinv;
   const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
@@ -861,8 +883,57 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     }
   };
   stage_tw(Md.ftw1t);
+  // row tiles this CTA reads, in order: D(j, l) for the digits j != l, then (MODE 2) W(0, l), W(1, l)
+  constexpr int NT_MAX = L + 2;
+  const int ntile = (l == L ? L : L - 1) + (MODE == 2 ? 2 : 0);
+  auto tile_src = [&](int t) -> const u64 * {
+    const int nd = l == L ? L : L - 1;
+    if (t < nd) {
+      const int j = (l == L || t < l) ? t : t + 1;
+      return D + ((u64)item * L * LP + (u64)j * LP + l) * N + ((u64)first << LM);
+    }
+    return W + ((u64)item * 2 * L + (u64)(t - nd) * L + l) * N + ((u64)first << LM);
+  };
+  (void)NT_MAX;
+#if CGB_KSROW_TMA
+  constexpr int PITCH = ksr_pitch(LM);
+  u64 *land = sm3 + ((G * PADM + 1) & ~1) + 2 * (NTT2_TILE + G);  // after the twiddle rows
+  u64 *bar = land + G * PITCH;
+  auto issue = [&](int t) {  // one thread: the G rows of tile t
+    mbar_expect_tx(bar, (u32)(G * M * sizeof(u64)));
+    const u64 *src = tile_src(t);
+    for (int rr = 0; rr < G; rr++) bulk_g2s(land + rr * PITCH, src + ((u64)rr << LM), M * sizeof(u64), bar);
+  };
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
   pdl_start_dependents();
   pdl_wait();
+  if (tid == 0 && ntile > 0) issue(0);
+  int tcur = 0;
+  // PA-phase words of the next tile: from the landing tile, then release it to the next copy
+  auto load_tile = [&](double *x) {
+    mbar_wait(bar, (u32)(tcur & 1));
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) x[k] = u2d(land[g * PITCH + PA::idx(tl, 0, k)]);
+    __syncthreads();  // every thread has its words (and the previous tile's phase-B reads are done)
+    if (tid == 0 && tcur + 1 < ntile) {
+      fence_proxy_async();
+      issue(tcur + 1);
+    }
+    tcur++;
+  };
+#else
+  pdl_start_dependents();
+  pdl_wait();
+  int tcur = 0;
+  auto load_tile = [&](double *x) {
+    const u64 *src = tile_src(tcur) + ((u64)g << LM);
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) x[k] = u2d(__ldcs(src + PA::idx(tl, 0, k)));
+    __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
+    tcur++;
+  };
+#endif
   const double2 *tw = tws + g * (M + 1);
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
@@ -892,10 +963,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
           x[u * PB::K + k] = u2d(ks_src_word(xin, item, j, (u32)(row0 + PB::idx(tl, u, k)), LOGN));
 #endif
     } else {
-      const u64 *src = D + ((u64)item * L * LP + (u64)j * LP + l) * N + row0;
-#pragma unroll
-      for (int k = 0; k < PA::K; k++) x[k] = u2d(__ldcs(src + PA::idx(tl, 0, k)));
-      __syncthreads();  // twiddles staged; the previous digit's phase-B reads are done
+      load_tile(x);
       phase_regs_fp<LM, 0, RA, true, E, false, false>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
@@ -923,6 +991,35 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
           a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
         }
       }
+  }
+  if constexpr (MODE == 2) {  // ModDown: row pass of W[pp][l] (same forward twiddles), combine, store
+#pragma unroll 1
+    for (int pp = 0; pp < 2; pp++) {
+      double x[E];
+      load_tile(x);
+      phase_regs_fp<LM, 0, RA, true, E, false, false>(x, tw, tl, qd, qinv);
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];
+      phase_regs_fp<LM, RA, RB, true, E, true, false>(x, tw, tl, qd, qinv);
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k += 4) {
+          u64 w[4], av[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            w[e] = fp_canon(x[u * PB::K + k + e], qd, qinv);
+            av[e] = fp_canon(pp ? a1[u * PB::K + k + e] : a0[u * PB::K + k + e], qd, qinv);
+          }
+          epi.combine4(item, pp * L + l, row0 + PB::idx(tl, u, k), w, av);
+        }
+    }
+    return;
   }
   u64 *o0 = acc + ((u64)item * 2 * LP + l) * N + row0, *o1 = acc + ((u64)item * 2 * LP + LP + l) * N + row0;
   if (l == L) {  // P limb: ModDown's inverse row pass runs here, on the accumulators
@@ -1096,13 +1193,22 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
 template <int LA, int LB>
 static size_t ks_row_smem() {  // row-pass data tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
   return sizeof(u64) * (size_t)((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1) +
-         16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB));
+         16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)) +
+         (CGB_KSROW_TMA ? sizeof(u64) * ((size_t)(NTT2_TILE >> LB) * ksr_pitch(LB) + 2) : 0);
 }
 template <int LA, int LB, int L>
 static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(k_ks_row<LA, LB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ks_row_smem<LA, LB>());
+    const int sm = (int)ks_row_smem<LA, LB>();
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+#ifdef CGB_KSROW_CARVE
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
+#endif
   });
 }
 
@@ -1116,7 +1222,7 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
   const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
   ks_row_attrs<LA, LB, L>();
   launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
-                                                                               r->iP, count);
+             r->iP, count, (const u64 *)nullptr, MdEpi{});
 }
 static bool ks_row_fusable(const cgb_ring *r) {
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
@@ -1995,12 +2101,20 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     }
     col_fused(r, cj, count, L, "ks_modup_cols");
   }
-  {  // 3
-    const dim3 g1((unsigned)((size_t)count * LP * ((1 << LA) / G1)));
+  const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
+  const int TILES = (1 << LA) / G1;
+  ks_row_attrs<LA, LB, L>();
+  if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
-    ks_row_attrs<LA, LB, L>();
-    launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
-                                                                                 r->iP, count);
+    launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
+               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi);
+    launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
+               (double)count * ((N / 2) * LB * (L + 2.0) + 2.0 * L * N));
+  } else {  // 3
+    const dim3 g1((unsigned)((size_t)count * LP * TILES));
+    launch_begin(r);
+    launch_pdl(r, k_ks_row<LA, LB, L, 0>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
+               r->iP, count, (const u64 *)nullptr, epi);
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
@@ -2021,6 +2135,17 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     }
     col_fused(r, cj, count, L, "ks_moddown_cols");
   }
+  if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
+    launch_begin(r);
+    launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
+               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi);
+    // D (L-1 digits) + own digit + W (2) + out (2) per limb, c0 / add1 when present; keys once
+    launch_end(r, "ks_row_md",
+               8.0 * (double)count * N * L * (L + 4.0 + (add0.items || add0.base ? 1 : 0) + (d_add1 ? 2 : 0)) +
+                   16.0 * L * (double)L * N,
+               (double)count * ((N / 2) * LB * (L * (L - 1.0) + 2.0 * L) + 2.0 * L * L * N + 2.0 * L * N));
+    return;
+  }
   {  // 5
     NttJob job{};
     job.base = W;
@@ -2035,7 +2160,6 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     job.nsub = n;
     job.mods = r->d_mods;
     job.logN = LA + LB;
-    const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
     const dim3 g((unsigned)((size_t)count * n * ((1 << LA) / G1)));
     launch_begin(r);
     launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), job, epi);
@@ -2616,6 +2740,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_COL_FUSED")) g_col_fused = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KS_MD")) g_ks_md = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
