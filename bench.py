@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
+    ap.add_argument("--workload", default="decode", choices=["decode", "prefill", "layer"])
     ap.add_argument("--L", type=int, default=128, help="cached prefill length per head")
     ap.add_argument("--heads", type=int, default=HEADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -205,6 +205,94 @@ def run_prefill(args):
                       "config": {"workload": f"prefill_attention_{args.heads}h_L{args.L}", "heads": args.heads,
                                  "d_head": D2, "n_slots": N_SLOTS},
                       "gpu_launches": int((ring.launches() - l0) / args.steps)}), flush=True)
+
+
+GPT2_VOCAB = 50257
+
+
+def layer_model(args):
+    from paper_2602_08798_b200 import model as M
+
+    cfg = M.ModelConfig(layers=1, d1=HEADS * D2, heads=HEADS, ffn_dim=4 * HEADS * D2, vocab=GPT2_VOCAB,
+                        max_seq=args.L + args.steps + 1, f=F, unembed_vocab=N_SLOTS)
+    return M, M.gpt2_layer_model(cfg, seed=0)
+
+
+def run_layer(args):
+    """Config 3: one GPT-2-small decoder layer (d_model 768, 12 heads, d_ff 3072,
+    N(0, 0.02) weights), a prompt of L token ids uniform over 50257, then
+    `steps` greedy tokens, every cache part force-refreshed before each step.
+    The unembedding covers the first 8192 vocabulary entries (n_slots)."""
+    import torch
+
+    from paper_2602_08798_b200 import _native
+    from paper_2602_08798_b200.backend import BackendParams, GpuContext
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    _native.build()
+    M, mdl = layer_model(args)
+    ctx = GpuContext(BackendParams(), 0)
+    ring = ctx.ring
+    stream = torch.cuda.current_stream()
+    ring.set_stream(stream.cuda_stream)
+    prompt = np.random.default_rng(0).integers(0, GPT2_VOCAB, args.L).tolist()
+    chans = M.channels(0, 1, HEADS, P)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 2)]
+    torch.cuda.synchronize()
+    l0 = ring.launches()
+    t0 = time.perf_counter()
+    ev[0].record(stream)
+    state = M.prefill(mdl, prompt, ctx, chans)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter() - t0
+    l1 = ring.launches()
+    toks = []
+    for i in range(args.steps):
+        tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
+        toks.append(tok)
+        ev[i + 2].record(stream)
+    torch.cuda.synchronize()
+    t_all = time.perf_counter() - t0
+    pre_ms = ev[0].elapsed_time(ev[1])
+    step_ms = [ev[i + 1].elapsed_time(ev[i + 2]) for i in range(args.steps)]
+    line = {"metric": f"HE decoder-layer decode ms/token (GPT-2 small layer, prompt {args.L}, "
+                      f"{args.steps} tokens, refresh each step)",
+            "value": float(np.mean(step_ms)), "unit": "ms/token", "higher_is_better": False, "n_gpus": 1,
+            "steps": args.steps, "dtype": "u64", "data": "synthetic (token ids uniform over 50257, N(0,0.02) weights)",
+            "config": {"workload": f"gpt2_layer_prompt{args.L}_gen{args.steps}", "d_model": HEADS * D2,
+                       "heads": HEADS, "d_ff": 4 * HEADS * D2, "vocab": GPT2_VOCAB, "unembed_vocab": N_SLOTS,
+                       "n_slots": N_SLOTS, "plain_modulus": P, "ring": _ring_desc()},
+            "prefill_ms": pre_ms, "decode_ms_per_token": step_ms,
+            "wall_s": {"prefill": t_pre, "total": t_all},
+            "gpu_launches": {"prefill": int(l1 - l0), "decode_per_token": int((ring.launches() - l1) / args.steps)},
+            "tokens": toks, "counters": ctx.counter.as_dict()}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = layer_cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+
+
+def layer_cpu_baseline(args):
+    """One decode step of the same layer on the reference's CPU path (this
+    package's host code over the slot emulation, oracle/slots.py), with the
+    caches built directly by encode (config 4's shortcut) instead of a prefill."""
+    from oracle.slots import SlotContext
+    import paper_2602_08798_b200 as api
+    from paper_2602_08798_b200.backend import BackendParams
+
+    M, mdl = layer_model(args)
+    ctx = SlotContext(BackendParams(), 0)
+    rng = np.random.default_rng(0)
+    caches = [[api.init_cache(*(api.encode(fp_tokens(rng, args.L, D2), api.EncodingKind.OUTER, ctx)
+                                for _ in range(2)), ctx) for _ in range(HEADS)]]
+    state = M.GenerationState(position=args.L, caches=caches, next_logits=np.zeros(8, np.int64))
+    chans = M.channels(0, 1, HEADS, P)
+    t0 = time.perf_counter()
+    M.decode_step(mdl, state, ctx, chans, force_refresh=True)
+    dt = time.perf_counter() - t0
+    return {"value": dt * 1e3, "unit": "ms/token", "cores": 1, "kind": "port",
+            "sample": f"one decode step of the layer at cached length {args.L} (caches by encode), slot emulation",
+            "host": _cpu_model()}
 
 
 def run_ours(args):
@@ -425,5 +513,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.workload == "prefill":
         run_prefill(a)
+    elif a.workload == "layer":
+        run_layer(a)
     else:
         run_ours(a)

@@ -687,6 +687,7 @@ class GpuContext:
         blk, ids = c0._new(len(wave))
         if one_shot and not isinstance(vecs, PlainBatch):
             # random masks never recur: encode into scratch plaintexts, no hashing, no cache
+            _pt_cache(ring).make_room(len(wave))
             pts = ring.alloc_pt(len(wave))
             try:
                 ring.encode_pt(vecs, kind, pts)
@@ -885,6 +886,11 @@ class _PtCache:
                     self.map[k] = [int(pid), self.tick]
                     out[idxs] = pid
         return None, out
+
+    def make_room(self, need: int):
+        """Leave `need` arena slots free for scratch (one-shot) plaintexts."""
+        with self.lock:
+            self._evict(need)
 
     def _evict(self, need: int):
         free = self.ring.arena_pts - len(self.map)

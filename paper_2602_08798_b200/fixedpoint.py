@@ -148,3 +148,69 @@ def causal_attention_weights(row_2f, row_index: int, d2: int, fp: FixedPointPara
     s2 = _scaled_scores(row_2f, d2, fp)
     s2[row_index + 1:] -= 1 << (fp.f + CAUSAL_MASK_EXPONENT)
     return fp_softmax(s2, fp)
+
+
+# ----------------------------------------------------------------------------
+# client-side activations of the decoder layer (BASELINE config 3 harness)
+# ----------------------------------------------------------------------------
+# GELU on [0, 3.2] as c4 (x^2 + beta x)^2 + c2' x^2 + c1 x (the reference's
+# frozen quartic, fixedpoint.py:43-49); beta = c3 / (2 c4), c2' = c2 - c4 beta^2
+GELU_CLIP = 3.2
+_GELU_C = (0.0203101927, -0.1792823041, 0.5309976652, 0.4701539873)  # c4, c3, c2, c1
+
+
+def fp_gelu(x, fp: FixedPointParams) -> np.ndarray:
+    """GELU on signed scale-f integers, elementwise (fixedpoint.py:109-128):
+    the quartic on |x| <= clip, GELU(x) = x + GELU(-x) for x < 0, identity /
+    zero beyond the clip."""
+    c4f, c3f, c2f, c1f = _GELU_C
+    beta_f = c3f / (2.0 * c4f)
+    f = fp.f
+    x = np.asarray(x, dtype=np.int64)
+    clip = fp.quantize(GELU_CLIP)
+    c4, beta, c2p, c1 = (fp.quantize(v) for v in (c4f, beta_f, c2f - c4f * beta_f * beta_f, c1f))
+    ax = np.minimum(np.abs(x), clip)
+    sq = (ax * ax) >> f
+    u = sq + ((beta * ax) >> f)
+    g = ((c4 * ((u * u) >> f)) >> f) + ((c2p * sq) >> f) + ((c1 * ax) >> f)
+    near = np.where(x >= 0, g, x + g)
+    far = np.where(x > 0, x, 0)
+    return np.where(np.abs(x) > clip, far, near)
+
+
+def _div_round(a: np.ndarray, d: int) -> np.ndarray:
+    """Round-half-away-from-zero a / d for int64 arrays (fixedpoint.py:194-198)."""
+    a = np.asarray(a, dtype=np.int64)
+    pos = (2 * a + d) // (2 * d)
+    neg = -((2 * (-a) + d) // (2 * d))
+    return np.where(a >= 0, pos, neg)
+
+
+def fp_layernorm_rows(X, gain, bias, fp: FixedPointParams) -> np.ndarray:
+    """LayerNorm of every row of X (signed scale-f), Newton inverse square
+    root seeded from the integer square root, 3 iterations
+    (fixedpoint.py:178-191, :224-243); a zero-variance row yields the bias."""
+    f = fp.f
+    X = np.atleast_2d(np.asarray(X, dtype=np.int64))
+    gain = np.asarray(gain, dtype=np.int64)
+    bias = np.asarray(bias, dtype=np.int64)
+    d = X.shape[1]
+    if d < 2:
+        raise ParameterError("layernorm needs at least two values")
+    mu = _div_round(X.sum(axis=1), d)
+    c = X - mu[:, None]
+    var = _div_round((c * c).sum(axis=1), d)  # scale 2f
+    seed = np.array([math.isqrt(int(v)) for v in var], dtype=np.int64)
+    y = (np.int64(1) << (2 * f)) // np.maximum(seed, 1)
+    three = np.int64(3) << f
+    for _ in range(3):
+        t = (((var * y) >> (2 * f)) * y) >> f
+        y = (y * (three - t)) >> (f + 1)
+    out = ((gain[None, :] * ((c * y[:, None]) >> f)) >> f) + bias[None, :]
+    out[var == 0] = bias
+    return out
+
+
+def fp_layernorm(x, gain, bias, fp: FixedPointParams) -> np.ndarray:
+    """One vector (fixedpoint.py:224-243)."""
+    return fp_layernorm_rows(np.asarray(x)[None, :], gain, bias, fp)[0]

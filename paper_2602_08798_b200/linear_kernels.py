@@ -110,14 +110,25 @@ def cpmm_outer_diagonal(X: PackedMatrix, W: PackedMatrix, ctx) -> PackedMatrix:
         groups.append(np.concatenate([[gi], np.arange(pos + ri, pos + ri + k)]).astype(np.int64))
         ri += k
     work = C.w_sum(allw, groups)
-    # one plaintext product per (output column c, working ct g), column-major
-    pts = np.zeros((d2 * len(starts), n), dtype=np.int64)
-    for c in range(d2):
-        for gi, g in enumerate(starts):
-            row = pts[c * len(starts) + gi]
-            for u in range(min(group, d1 - g)):
-                row[u * w: u * w + m] = Wv[g + u, c]
-    prods = C.w_mult_plain(work.take(np.tile(np.arange(len(starts)), d2)), pts)
-    prods = fold_wave(prods, group, first_step=w) if group > 1 else prods
-    cols = C.w_sum(prods, [np.arange(c * len(starts), (c + 1) * len(starts)) for c in range(d2)])
-    return PackedMatrix(Encoding(EncodingKind.OUTER, m, d2), cols.handles(), encrypted=True, slot_period=w)
+    # one plaintext product per (output column c, working ct g), column-major; wide
+    # outputs (e.g. the 768 x 3072 FFN projection: 36864 products) go in column
+    # chunks of at most CPMM_CHUNK products so the products' ciphertexts stay a few
+    # GB -- every column's chain is independent, so its words are unchanged
+    ng = len(starts)
+    chunk = max(1, CPMM_CHUNK // ng) if d2 * ng > CPMM_CHUNK else d2
+    out = []
+    for c0 in range(0, d2, chunk):
+        cs = range(c0, min(d2, c0 + chunk))
+        pts = np.zeros((len(cs) * ng, n), dtype=np.int64)
+        for ci, c in enumerate(cs):
+            for gi, g in enumerate(starts):
+                row = pts[ci * ng + gi]
+                for u in range(min(group, d1 - g)):
+                    row[u * w: u * w + m] = Wv[g + u, c]
+        prods = C.w_mult_plain(work.take(np.tile(np.arange(ng), len(cs))), pts, one_shot=chunk < d2)
+        prods = fold_wave(prods, group, first_step=w) if group > 1 else prods
+        out += C.w_sum(prods, [np.arange(ci * ng, (ci + 1) * ng) for ci in range(len(cs))]).handles()
+    return PackedMatrix(Encoding(EncodingKind.OUTER, m, d2), out, encrypted=True, slot_period=w)
+
+
+CPMM_CHUNK = 4096  # plaintext products per wave of cpmm_outer_diagonal

@@ -1,0 +1,76 @@
+"""Decoder-layer pipeline (paper_2602_08798_b200.model, BASELINE config 3) vs the
+reference's own encrypted pipeline: golden tests/golden/layer_toy.npz recorded
+by tests/golden/make_layer_golden.py (reference toy model, 2 layers, 4 heads,
+prompt 6, 3 greedy steps, every cache part force-refreshed before each step).
+Tokens, every step's logits, op counters and MPC byte totals must be equal."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+GOLD = Path(__file__).resolve().parent / "golden" / "layer_toy.npz"
+
+
+def _run(make_ctx):
+    from paper_2602_08798_b200 import model as M
+    from paper_2602_08798_b200.backend import BackendParams
+
+    g = np.load(GOLD)
+    cfg = M.ModelConfig(**json.loads(str(g["config"])))
+    mdl = M.Model(cfg, {k[2:]: g[k] for k in g.files if k.startswith("w_")})
+    p = int(g["p"])
+    ctx = make_ctx(BackendParams(n_slots=int(g["n"]), plain_modulus=p), 0)
+    chans = M.channels(0, cfg.layers, cfg.heads, p)
+    state = M.prefill(mdl, [int(t) for t in g["prompt"]], ctx, chans)
+    logits, toks = [state.next_logits], []
+    for _ in range(len(g["tokens"])):
+        tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
+        toks.append(tok)
+        logits.append(state.next_logits)
+    assert toks == [int(t) for t in g["tokens"]]
+    assert np.array_equal(np.stack(logits), g["logits"])
+    assert ctx.counter.as_dict() == json.loads(str(g["counters"]))
+    assert sum(ch.bytes_sent for ch in chans.values()) == int(g["mpc_bytes"])
+    return ctx, state
+
+
+def test_layer_pipeline_on_slot_oracle():
+    from oracle.slots import SlotContext
+
+    _run(SlotContext)
+
+
+@pytest.mark.gpu
+def test_layer_pipeline_on_gpu():
+    assert gpu_available()
+    from paper_2602_08798_b200._native import build
+    from paper_2602_08798_b200.backend import GpuContext
+
+    build()
+    ctx, state = _run(GpuContext)
+    assert all(c.noise_budget > 0 for cache in state.caches[0] for c in cache.prefill_K.parts)
+
+
+def test_cpmm_chunked_equals_unchunked():
+    """Wide CPMM outputs are computed in column chunks: same decrypted columns."""
+    from oracle.slots import SlotContext
+    from paper_2602_08798_b200 import linear_kernels as LK
+    from paper_2602_08798_b200.backend import BackendParams
+    from paper_2602_08798_b200.encodings import EncodingKind, decode, encode
+
+    p = 67109633
+    ctx = SlotContext(BackendParams(n_slots=64, plain_modulus=p), 0)
+    rng = np.random.default_rng(3)
+    X = encode(rng.integers(0, 50, (8, 24)), EncodingKind.OUTER, ctx)
+    W = encode(rng.integers(-30, 30, (24, 40)), EncodingKind.DIAGONAL, ctx, encrypted=False)
+    full = decode(LK.cpmm_outer_diagonal(X, W, ctx), ctx)
+    old = LK.CPMM_CHUNK
+    try:
+        LK.CPMM_CHUNK = 7
+        chunked = decode(LK.cpmm_outer_diagonal(X, W, ctx), ctx)
+    finally:
+        LK.CPMM_CHUNK = old
+    assert np.array_equal(full, chunked)
