@@ -223,6 +223,7 @@ def run_layer(args):
     N(0, 0.02) weights), a prompt of L token ids uniform over 50257, then
     `steps` greedy tokens, every cache part force-refreshed before each step.
     The unembedding covers the first 8192 vocabulary entries (n_slots)."""
+    os.environ.setdefault("CGB_ARENA_GIB", "64")  # the FFN prefill keeps ~20k ciphertexts live
     import torch
 
     from paper_2602_08798_b200 import _native

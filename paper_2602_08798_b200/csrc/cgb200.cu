@@ -423,12 +423,17 @@ static void launch_ntt2_fp(cgb_ring *r, bool fwd, const NttJob &job, int count) 
         else k_ntt2_fp<LA, LB, false, 1><<<grid(LB), NTT2_TILE / 8, s1, r->stream>>>(j);
       }
     };
+    NttJob first = job, next = second;
+    if (r0 && r1) {  // the words between the passes stay reduced doubles
+      first.out_raw = 1;
+      next.in_raw = 1;
+    }
     if (fwd) {
-      pass0(job, true);
-      pass1(second, true);
+      pass0(first, true);
+      pass1(next, true);
     } else {
-      pass1(job, false);
-      pass0(second, false);
+      pass1(first, false);
+      pass0(next, false);
     }
     return;
   }
@@ -855,7 +860,7 @@ __host__ __device__ constexpr int ksr_pitch(int LB) { return (1 << LB) + 8; }
 template <int LA, int LB, int L, int MODE = 0>
 __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
                                                            const u64 *const *keys, const ModTab *mods, int iP,
-                                                           int count, const u64 *W, MdEpi epi) {
+                                                           int count, const u64 *W, MdEpi epi, int raw) {
   extern __shared__ u64 sm3[];
   constexpr int E = 16, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
   constexpr int G = NTT2_TILE / M, TPS = M / E, TILES = (1 << LA) / G;
@@ -914,7 +919,10 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   auto load_tile = [&](double *x) {
     mbar_wait(bar, (u32)(tcur & 1));
 #pragma unroll
-    for (int k = 0; k < PA::K; k++) x[k] = u2d(land[g * PITCH + PA::idx(tl, 0, k)]);
+    for (int k = 0; k < PA::K; k++) {
+      const u64 v = land[g * PITCH + PA::idx(tl, 0, k)];
+      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+    }
     __syncthreads();  // every thread has its words (and the previous tile's phase-B reads are done)
     if (tid == 0 && tcur + 1 < ntile) {
       fence_proxy_async();
@@ -929,7 +937,10 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   auto load_tile = [&](double *x) {
     const u64 *src = tile_src(tcur) + ((u64)g << LM);
 #pragma unroll
-    for (int k = 0; k < PA::K; k++) x[k] = u2d(__ldcs(src + PA::idx(tl, 0, k)));
+    for (int k = 0; k < PA::K; k++) {
+      const u64 v = __ldcs(src + PA::idx(tl, 0, k));
+      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+    }
     __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
   };
@@ -1044,7 +1055,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       phase_regs_fp<LM, 0, RA, false, E, false, false>(y, itw, tl, qd, qinv);
       u64 *o = pp ? o1 : o0;
 #pragma unroll
-      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = fp_canon(y[k], qd, qinv);
+      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (raw & 2) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
     }
     return;
   }
@@ -1073,6 +1084,7 @@ struct ColJob {
   u64 dst_stride;
   const ModTab *mods;
   int nsrc;
+  unsigned char in_raw, out_raw;  // pass-boundary words as reduced doubles (see NttJob)
   unsigned short src_off[8];
   unsigned char src_mod[8];
   unsigned short dst_off[8][8];
@@ -1112,7 +1124,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
   for (int u = 0; u < PS::R; u++)
 #pragma unroll
     for (int k = 0; k < PS::K; k++) {
-      x[u * PS::K + k] = u2d(__ldcs(src + gaddr(PS::idx(tl, u, k))));
+      const u64 v = __ldcs(src + gaddr(PS::idx(tl, u, k)));
+      x[u * PS::K + k] = job.in_raw ? r2d(v) : u2d(v);
       if (RB == 4) x[u * PS::K + k] = fp_reduce(x[u * PS::K + k], Ms.qd, Ms.qinv);  // 4-stage inverse phase
     }
   double *sd = data + g * PADM;
@@ -1153,7 +1166,9 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
 #pragma unroll
     for (int u = 0; u < PS::R; u++)
 #pragma unroll
-      for (int k = 0; k < PS::K; k++) dst[gaddr(PS::idx(tl, u, k))] = fp_canon(x[u * PS::K + k], qt, qti);
+      for (int k = 0; k < PS::K; k++)
+        dst[gaddr(PS::idx(tl, u, k))] =
+            job.out_raw ? fp_raw(x[u * PS::K + k], qt, qti) : fp_canon(x[u * PS::K + k], qt, qti);
   }
 }
 template <int LA, int LB>
@@ -1222,7 +1237,7 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
   const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
   ks_row_attrs<LA, LB, L>();
   launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
-             r->iP, count, (const u64 *)nullptr, MdEpi{});
+             r->iP, count, (const u64 *)nullptr, MdEpi{}, 0);
 }
 static bool ks_row_fusable(const cgb_ring *r) {
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
@@ -2077,6 +2092,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     job.nsub = L;
     job.mods = r->d_mods;
     job.logN = LA + LB;
+    job.out_raw = 1;  // pass boundary: the column pass (k_col_fused) reads reduced doubles
     launch_begin(r);
     launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1>, rows_grid1, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), job, NoEpi{});
     launch_end(r, "ks_digit_rows", 16.0 * (double)count * L * N, (double)count * L * (N / 2) * LB);
@@ -2088,6 +2104,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     cj.dst = D;
     cj.dst_stride = (u64)L * LP * N;
     cj.nsrc = L;
+    cj.in_raw = cj.out_raw = 1;
     for (int j = 0; j < L; j++) {
       cj.src_off[j] = (unsigned short)j;
       cj.src_mod[j] = (unsigned char)j;
@@ -2107,14 +2124,14 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
     launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi);
+               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, 3);
     launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
                (double)count * ((N / 2) * LB * (L + 2.0) + 2.0 * L * N));
   } else {  // 3
     const dim3 g1((unsigned)((size_t)count * LP * TILES));
     launch_begin(r);
     launch_pdl(r, k_ks_row<LA, LB, L, 0>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
-               r->iP, count, (const u64 *)nullptr, epi);
+               r->iP, count, (const u64 *)nullptr, epi, 3);
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
@@ -2125,6 +2142,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     cj.dst = W;
     cj.dst_stride = 2ull * L * N;
     cj.nsrc = 2;
+    cj.in_raw = cj.out_raw = 1;
     for (int pp = 0; pp < 2; pp++) {
       cj.src_off[pp] = (unsigned short)(pp * LP + L);
       cj.src_mod[pp] = (unsigned char)r->iP;
@@ -2138,7 +2156,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
     launch_begin(r);
     launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi);
+               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
     // D (L-1 digits) + own digit + W (2) + out (2) per limb, c0 / add1 when present; keys once
     launch_end(r, "ks_row_md",
                8.0 * (double)count * N * L * (L + 4.0 + (add0.items || add0.base ? 1 : 0) + (d_add1 ? 2 : 0)) +
@@ -2160,6 +2178,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     job.nsub = n;
     job.mods = r->d_mods;
     job.logN = LA + LB;
+    job.in_raw = 1;  // W: reduced doubles from k_col_fused
     const dim3 g((unsigned)((size_t)count * n * ((1 << LA) / G1)));
     launch_begin(r);
     launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, g, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), job, epi);

@@ -140,6 +140,8 @@ struct NttJob {
   u64 *const *src_items;     // or per-item source pointers
   const u64 *galois;         // per-item Galois element: load src[perm_g(k)] (evaluation-domain automorphism)
   int lift;                  // centre-lift from src_mod on load
+  unsigned char in_raw;      // FP64 register-I/O kernels: source words are reduced doubles (a pass boundary)
+  unsigned char out_raw;     //   ... store reduced doubles in [-q/2, q/2] instead of canonical u64
   const ModTab *mods;
   int logN;
   int nsub;                                // (poly, limb) units per item
@@ -509,6 +511,11 @@ __device__ __forceinline__ double u2d(u64 v) {  // exact for v < 2^52
 __device__ __forceinline__ double fp_reduce(double x, double q, double qinv) {  // -> [-q/2, q/2]
   return fma(-rint(x * qinv), q, x);
 }
+// a pass-boundary word: the reduced double's bits (the next pass loads it with r2d)
+__device__ __forceinline__ u64 fp_raw(double x, double q, double qinv) {
+  return (u64)__double_as_longlong(fp_reduce(x, q, qinv));
+}
+__device__ __forceinline__ double r2d(u64 v) { return __longlong_as_double((long long)v); }
 __device__ __forceinline__ u64 fp_canon(double x, double q, double qinv) {  // -> [0, q) as u64
   double r = fp_reduce(x, q, qinv);
   r = r < 0.0 ? r + q : r;
@@ -823,7 +830,7 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
     }
 #pragma unroll
     for (int i = 0; i < E; i++) {
-      x[i] = u2d(lift ? centred_to(v[i], qs, q) : v[i]);
+      x[i] = job.in_raw ? r2d(v[i]) : u2d(lift ? centred_to(v[i], qs, q) : v[i]);
       if (!FWD && RPA == 4) x[i] = fp_reduce(x[i], qd, qinv);  // a 4-stage inverse phase starts reduced
     }
   }
@@ -857,8 +864,9 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
 #pragma unroll
       for (int k = 0; k < PB::K; k += 4) {
         const double *y = &x[u * PB::K + k];
-        const u64 w[4] = {fp_canon(y[0], qd, qinv), fp_canon(y[1], qd, qinv), fp_canon(y[2], qd, qinv),
-                          fp_canon(y[3], qd, qinv)};
+        u64 w[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) w[e] = job.out_raw ? fp_raw(y[e], qd, qinv) : fp_canon(y[e], qd, qinv);
         if constexpr (EPI::active) epi.store(item, job.sub_off[sub], gaddr(PB::idx(tl, u, k)), w, 4);
         else st256(p + gaddr(PB::idx(tl, u, k)), w[0], w[1], w[2], w[3]);
       }
@@ -867,7 +875,7 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
     for (int u = 0; u < PB::R; u++)
 #pragma unroll
       for (int k = 0; k < PB::K; k++) {
-        const u64 w = fp_canon(x[u * PB::K + k], qd, qinv);
+        const u64 w = job.out_raw ? fp_raw(x[u * PB::K + k], qd, qinv) : fp_canon(x[u * PB::K + k], qd, qinv);
         if constexpr (EPI::active) epi.store(item, job.sub_off[sub], gaddr(PB::idx(tl, u, k)), &w, 1);
         else p[gaddr(PB::idx(tl, u, k))] = w;
       }

@@ -214,6 +214,7 @@ def prefill(model: Model, prompt: list, ctx, chans=None) -> GenerationState:
                 ich += [hch[h]] * len(P.parts)
                 lens += [P.encoding.rows] * len(P.parts)
         tr = _trunc_wave(C.wave_of(items, ictx), lens, fp, ictx, ich).handles()
+        del items  # the raw projections' ciphertexts are released here (arena headroom)
         mats, k = {}, 0
         for h in range(c.heads):
             for name in ("wq", "wk", "wv"):
@@ -221,30 +222,41 @@ def prefill(model: Model, prompt: list, ctx, chans=None) -> GenerationState:
                 mats[(h, name)] = PackedMatrix(P.encoding, tr[k:k + len(P.parts)], encrypted=True, slot_period=None)
                 k += len(P.parts)
         Qs, Ks, Vs = ([mats[(h, nm)] for h in range(c.heads)] for nm in ("wq", "wk", "wv"))
+        del proj, mats, tr
         Os = prefill_attention_heads(Qs, Ks, Vs, fp, hctxs, hch, causal=True)
+        del Qs
         o_parts = []
         for h in range(c.heads):
             ctx.join(hctxs[h])
             caches[l][h] = init_cache(Ks[h], Vs[h], hctxs[h])
             o_parts.extend(Os[h].parts)
         O_cat = PackedMatrix(replace(X_enc.encoding, cols=c.d1), o_parts, encrypted=True, slot_period=None)
+        del Os, o_parts
 
         ch = chans["common"]
         attn = cpmm_outer_diagonal(O_cat, model.diag(f"{l}.wo", model.layer(l, "wo"), ctx), ctx)
+        del O_cat
         attn = _trunc_wave(C.wave_of(attn.parts, [ctx] * c.d1), [m] * c.d1, fp, [ctx] * c.d1, [ch] * c.d1).handles()
         resid = C.w_add(C.wave_of(X_enc.parts, [ctx] * c.d1), C.wave_of(attn, [ctx] * c.d1)).handles()
         g1, b1 = model.layer(l, "ln1_g"), model.layer(l, "ln1_b")
+        del attn
         ln1 = _matrix_roundtrip(resid, m, ctx, ch, lambda M: fp_layernorm_rows(M, g1, b1, fp))
+        del resid
         X_enc = PackedMatrix(replace(X_enc.encoding, cols=c.d1), ln1, encrypted=True)
 
         h1 = cpmm_outer_diagonal(X_enc, model.diag(f"{l}.w1", model.layer(l, "w1"), ctx), ctx)
         h1p = _bias_parts(h1.parts, model.layer(l, "b1") << fp.f, m, ctx)
+        del h1
         hact = _matrix_roundtrip(h1p, m, ctx, ch, lambda M: fp_gelu(fp_truncate(M, fp.f), fp))
+        del h1p
         Hm = PackedMatrix(replace(X_enc.encoding, cols=c.ffn_dim), hact, encrypted=True)
 
         h2 = cpmm_outer_diagonal(Hm, model.diag(f"{l}.w2", model.layer(l, "w2"), ctx), ctx)
+        del Hm, hact
         h2p = _bias_parts(h2.parts, model.layer(l, "b2") << fp.f, m, ctx)
+        del h2
         h2t = _matrix_roundtrip(h2p, m, ctx, ch, lambda M: fp_truncate(M, fp.f))
+        del h2p
         resid2 = C.w_add(C.wave_of(ln1, [ctx] * c.d1), C.wave_of(h2t, [ctx] * c.d1)).handles()
         g2, b2 = model.layer(l, "ln2_g"), model.layer(l, "ln2_b")
         ln2 = _matrix_roundtrip(resid2, m, ctx, ch, lambda M: fp_layernorm_rows(M, g2, b2, fp))
