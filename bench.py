@@ -224,6 +224,7 @@ def run_layer(args):
     `steps` greedy tokens, every cache part force-refreshed before each step.
     The unembedding covers the first 8192 vocabulary entries (n_slots)."""
     os.environ.setdefault("CGB_ARENA_GIB", "64")  # the FFN prefill keeps ~20k ciphertexts live
+    os.environ.setdefault("CGB_PT_ARENA_GIB", "12")  # every decode-step weight diagonal stays resident
     import torch
 
     from paper_2602_08798_b200 import _native

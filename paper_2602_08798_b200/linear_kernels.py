@@ -11,12 +11,14 @@ ciphertext words equal the reference op sequence's.
 
 from __future__ import annotations
 
+import itertools
+
 import numpy as np
 
-from .backend import ParameterError
+from .backend import ParameterError, PlainBatch
 from .encodings import Encoding, EncodingKind, PackedMatrix, decode, next_pow2
 
-__all__ = ["cpmm_outer_diagonal", "cpvm_inner_diagonal", "fold_sum", "fold_wave"]
+__all__ = ["cpmm_outer_diagonal", "cpvm_inner_diagonal", "cpvm_inner_diagonal_heads", "fold_sum", "fold_wave"]
 
 
 def _fold_checks(block: int, n: int):
@@ -49,33 +51,74 @@ def _diagonal_weights(W: PackedMatrix, ctx) -> np.ndarray:
 
 def cpvm_inner_diagonal(x, W: PackedMatrix, ctx):
     """x (inner, length d1) times diagonal plaintext W (d1 x d2) -> slots [0, d2)."""
-    C = type(ctx)
-    Wv = _diagonal_weights(W, ctx)
-    d1, d2 = W.encoding.rows, W.encoding.cols
-    n = ctx.params.n_slots
+    return cpvm_inner_diagonal_heads([x], [W], [ctx])[0]
+
+
+def cpvm_inner_diagonal_heads(xs, Ws, ctxs) -> list:
+    """``cpvm_inner_diagonal`` for B independent (x, W, ctx) triples of one
+    shape (e.g. the 3 x 12 per-head decode projections, model.py:521-526):
+    each rotation amount is one batched key switch over all B items; item i's
+    ops are charged to ctxs[i] exactly as its own call would charge them."""
+    B = len(xs)
+    C = type(ctxs[0])
+    Wv = [_diagonal_weights(W, c) for W, c in zip(Ws, ctxs)]
+    d1, d2 = Ws[0].encoding.rows, Ws[0].encoding.cols
+    if any((W.encoding.rows, W.encoding.cols) != (d1, d2) for W in Ws):
+        raise ParameterError("batched cpvm needs one weight shape")
+    n, p = ctxs[0].params.n_slots, ctxs[0].params.plain_modulus
     wd1, wd2 = next_pow2(d1), next_pow2(d2)
     wp = max(wd1, wd2)
     if wp > n:
         raise ParameterError(f"operand width {wp} exceeds {n} slots")
-    xw = C.wave_of([x], [ctx])
+    xw = C.wave_of(xs, ctxs)
     if wp != n:
         xw = C.w_rotate(xw, -wp, add_input=True)
-    # generalized diagonals k = 0 .. wd2-1 as one plaintext batch
-    j = np.arange(wp)
-    col = j % wd2
-    pts = np.zeros((wd2, n), dtype=np.int64)
-    for k in range(wd2):
-        row = (j + k) % wp
-        ok = (row < d1) & (col < d2)
-        pts[k, :wp][ok] = Wv[row[ok], col[ok]]
+    # generalized diagonals k = 0 .. wd2-1 of each weight: built once per weight and
+    # named symbolically, so the device plaintext cache keeps them across steps
+    rows = {}
+    for W, wv in zip(Ws, Wv):
+        uid, r = _diagonal_rows(W, wv, n, p, wd2, wp)
+        rows[uid] = r
+    uids = [_diagonal_rows(W, None, n, p, wd2, wp)[0] for W in Ws]
+
+    def build(keys):
+        return np.stack([rows[k[1]][k[4]] for k in keys])
+
+    key = lambda b, k: ("cpvm", uids[b], n, p, k)
     if wd2 > 1:
-        rot = C.w_rotate(xw.take(np.zeros(wd2 - 1, np.int64)), np.arange(1, wd2))
-        xs = type(xw).concat([xw, rot])
+        rot = C.w_rotate(xw.take(np.repeat(np.arange(B), wd2 - 1)), np.tile(np.arange(1, wd2), B))
+        xs_w = type(xw).concat([xw, rot])
+        # item b: [b, B + b (wd2 - 1) .. B + (b + 1)(wd2 - 1) - 1] <-> diagonals 0 .. wd2-1
+        keys = [key(b, 0) for b in range(B)] + [key(b, k) for b in range(B) for k in range(1, wd2)]
+        groups = [np.concatenate([[b], B + b * (wd2 - 1) + np.arange(wd2 - 1)]) for b in range(B)]
     else:
-        xs = xw
-    prods = C.w_mult_plain(xs, pts)
-    acc = C.w_sum(prods, [np.arange(wd2)])
-    return fold_wave(acc, wp // wd2, first_step=wd2).handles()[0] if wp > wd2 else acc.handles()[0]
+        xs_w, keys, groups = xw, [key(b, 0) for b in range(B)], [np.array([b]) for b in range(B)]
+    prods = C.w_mult_plain(xs_w, PlainBatch(keys, build))
+    acc = C.w_sum(prods, groups)
+    return (fold_wave(acc, wp // wd2, first_step=wd2) if wp > wd2 else acc).handles()
+
+
+_uids = itertools.count()
+
+
+def _diagonal_rows(W: PackedMatrix, Wv, n: int, p: int, wd2: int, wp: int):
+    """(uid, residues[wd2, n]) of W's generalized diagonals: row k holds
+    W[(j + k) mod wp, j mod wd2] at slot j (linear_kernels.py:105-142)."""
+    cache = W.__dict__.setdefault("_cpvm_rows", {})
+    uid = W.__dict__.setdefault("_cpvm_uid", next(_uids))
+    got = cache.get((n, p))
+    if got is None and Wv is not None:
+        d1, d2 = Wv.shape
+        j = np.arange(wp)
+        col = j % wd2
+        got = np.zeros((wd2, n), dtype=np.int64)
+        for k in range(wd2):
+            row = (j + k) % wp
+            ok = (row < d1) & (col < d2)
+            got[k, :wp][ok] = Wv[row[ok], col[ok]]
+        got = np.mod(got, p)
+        cache[(n, p)] = got
+    return uid, got
 
 
 def cpmm_outer_diagonal(X: PackedMatrix, W: PackedMatrix, ctx) -> PackedMatrix:
@@ -118,14 +161,16 @@ def cpmm_outer_diagonal(X: PackedMatrix, W: PackedMatrix, ctx) -> PackedMatrix:
     chunk = max(1, CPMM_CHUNK // ng) if d2 * ng > CPMM_CHUNK else d2
     out = []
     for c0 in range(0, d2, chunk):
-        cs = range(c0, min(d2, c0 + chunk))
-        pts = np.zeros((len(cs) * ng, n), dtype=np.int64)
-        for ci, c in enumerate(cs):
-            for gi, g in enumerate(starts):
-                row = pts[ci * ng + gi]
-                for u in range(min(group, d1 - g)):
-                    row[u * w: u * w + m] = Wv[g + u, c]
-        prods = C.w_mult_plain(work.take(np.tile(np.arange(ng), len(cs))), pts, one_shot=chunk < d2)
+        cs = np.arange(c0, min(d2, c0 + chunk))
+        # row (ci, gi): W[g_gi + u, c] on the m live slots of block u (zero past d1)
+        Wpad = np.zeros((ng * group, d2), dtype=np.int64)
+        Wpad[:d1] = Wv
+        blocks = Wpad[:, cs].reshape(ng, group, len(cs)).transpose(2, 0, 1)  # [ci][gi][u]
+        pts = np.zeros((len(cs), ng, group, w), dtype=np.int64)
+        pts[..., :m] = blocks[..., None]
+        # projection weights are used once per call: encoded as scratch plaintexts
+        prods = C.w_mult_plain(work.take(np.tile(np.arange(ng), len(cs))), pts.reshape(len(cs) * ng, n),
+                               one_shot=True)
         prods = fold_wave(prods, group, first_step=w) if group > 1 else prods
         out += C.w_sum(prods, [np.arange(ci * ng, (ci + 1) * ng) for ci in range(len(cs))]).handles()
     return PackedMatrix(Encoding(EncodingKind.OUTER, m, d2), out, encrypted=True, slot_period=w)

@@ -32,7 +32,7 @@ from .backend import ParameterError
 from .encodings import EncodingKind, PackedMatrix, encode
 from .fixedpoint import FixedPointParams, fp_gelu, fp_layernorm_rows, fp_truncate, to_signed
 from .kv_cache import append_token_heads, init_cache, maybe_refresh_heads
-from .linear_kernels import cpmm_outer_diagonal, cpvm_inner_diagonal
+from .linear_kernels import cpmm_outer_diagonal, cpvm_inner_diagonal, cpvm_inner_diagonal_heads
 from .nonlinear import MpcChannel, he_to_shares_wave, reconstruct, share_vector, shares_to_he_wave, truncate
 
 __all__ = ["GenerationState", "Model", "ModelConfig", "decode_step", "generate", "gpt2_layer_model", "prefill"]
@@ -302,13 +302,13 @@ def decode_step(model: Model, state: GenerationState, ctx, chans=None, force_ref
     for l in range(c.layers):
         hctxs = [ctx.fork() for _ in range(c.heads)]
         hch = [chans[(l, h)] for h in range(c.heads)]
-        raw, ictx, ich = [], [], []
+        Ws, ictx, ich = [], [], []
         for h in range(c.heads):
             for name in ("wq", "wk", "wv"):
-                W = model.diag(f"{l}.{name}.{h}", model.head_slice(l, name, h), hctxs[h])
-                raw.append(cpvm_inner_diagonal(x, W, hctxs[h]))
+                Ws.append(model.diag(f"{l}.{name}.{h}", model.head_slice(l, name, h), hctxs[h]))
                 ictx.append(hctxs[h])
                 ich.append(hch[h])
+        raw = cpvm_inner_diagonal_heads([x] * len(Ws), Ws, ictx)
         qkv = _trunc_wave(C.wave_of(raw, ictx), [c.d2] * len(raw), fp, ictx, ich).handles()
         qs, ks, vs = qkv[0::3], qkv[1::3], qkv[2::3]
         cs = append_token_heads(caches[l], ks, vs, hctxs)

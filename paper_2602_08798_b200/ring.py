@@ -35,7 +35,7 @@ class Ring:
         if arena_cts is None:
             arena_cts = max(64, min(65536, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))
         if arena_pts is None:
-            arena_pts = max(64, min(16384, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
+            arena_pts = max(64, min(65536, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
         self.arena_cts, self.arena_pts = int(arena_cts), int(arena_pts)
         self.h2d_bytes = 0  # host payload bytes moved to / from the device (slot vectors, raw words)
         self.d2h_bytes = 0
