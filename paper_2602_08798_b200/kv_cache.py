@@ -208,11 +208,16 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     if not sel:
         return list(caches)
     # masks drawn per part in order from each head's channel
-    r = np.stack([chans[h].sample_mask(n) for h, _, _, _ in sel])
+    r = np.empty((len(sel), n), np.int64)
+    for k, (h, _, _, _) in enumerate(sel):
+        r[k] = chans[h].sample_mask(n)
     owners = [ctxs[s[0]] for s in sel]
     start = {id(c): c._next_id for c in owners}
     wave = C.wave_of([s[3] for s in sel], owners)
-    masked = C.w_add_plain(wave, (p - r) % p, one_shot=True)
+    neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
+    neg[neg == p] = 0
+    masked = C.w_add_plain(wave, neg, one_shot=True)
+    del neg
     view = C.w_decrypt(masked)
     fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view)
     for h, _, _, _ in sel:

@@ -61,7 +61,9 @@ def cpvm_inner_diagonal_heads(xs, Ws, ctxs) -> list:
     ops are charged to ctxs[i] exactly as its own call would charge them."""
     B = len(xs)
     C = type(ctxs[0])
-    Wv = [_diagonal_weights(W, c) for W, c in zip(Ws, ctxs)]
+    for W in Ws:
+        if W.encrypted or W.encoding.kind is not EncodingKind.DIAGONAL:
+            raise ParameterError("weights must be a plaintext diagonal PackedMatrix")
     d1, d2 = Ws[0].encoding.rows, Ws[0].encoding.cols
     if any((W.encoding.rows, W.encoding.cols) != (d1, d2) for W in Ws):
         raise ParameterError("batched cpvm needs one weight shape")
@@ -70,6 +72,9 @@ def cpvm_inner_diagonal_heads(xs, Ws, ctxs) -> list:
     wp = max(wd1, wd2)
     if wp > n:
         raise ParameterError(f"operand width {wp} exceeds {n} slots")
+    # the dense weight is decoded only the first time a weight is seen
+    Wv = [None if _diagonal_rows(W, None, n, p, wd2, wp)[1] is not None else _diagonal_weights(W, c)
+          for W, c in zip(Ws, ctxs)]
     xw = C.wave_of(xs, ctxs)
     if wp != n:
         xw = C.w_rotate(xw, -wp, add_input=True)
