@@ -297,6 +297,20 @@ def layer_cpu_baseline(args):
             "host": _cpu_model()}
 
 
+def _traffic(kernel: str, alg_bytes_per_launch: float):
+    """DRAM bytes per launch of the dominant kernel: the algorithmic bytes scaled by
+    the dram/algorithmic ratio of its committed ncu --set full capture
+    (profiles/r01/ncu_traffic.json), or None when no capture is committed."""
+    f = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    cap = json.loads(f.read_text()).get(kernel)
+    if not cap:
+        return None
+    return {"bytes_per_launch": alg_bytes_per_launch * cap["ratio"], "dram_over_algorithmic": cap["ratio"],
+            "source": "profiles/r01/ncu_traffic.json (" + cap["kernel"] + ")"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -411,7 +425,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "launches_per_step": nl,
+                     "frac": achieved / hbm_peak, "traffic": _traffic(name, kbytes / nl), "launches_per_step": nl,
                      "share_of_step": kms / step_kernel_ms if step_kernel_ms else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                      "pipe": {"name": "fp64" if ring.fp_ntt else "int64", "unit": "modmul/s",

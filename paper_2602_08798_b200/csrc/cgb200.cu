@@ -1202,7 +1202,10 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
     case 15: col_fused_t<7, 8>(r, job, count, nt); break;
     default: col_fused_t<8, 8>(r, job, count, nt); break;
   }
-  launch_end(r, name, 8.0 * (double)count * job.nsrc * r->N * (1 + nt));
+  // butterflies of the inverse column pass and nt forward column passes, plus the N^-1 scaling
+  const int LA = r->logN / 2;  // column pass length (col_fused_t<LA, LB>)
+  launch_end(r, name, 8.0 * (double)count * job.nsrc * r->N * (1 + nt),
+             (double)count * job.nsrc * ((r->N / 2.0) * LA * (1 + nt) + r->N));
 }
 
 template <int LA, int LB>
@@ -1614,16 +1617,23 @@ __global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, cons
 }
 
 // tensor over Q u B: ten[item][3][L+nB][N]
-__global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const ModTab *mods, int L, int nt, int iB0,
-                         int logN) {
+// Q limbs straight from the operand ciphertexts (pa / pb: per-item [2][L][N]),
+// B limbs from the lifted buffer
+__global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64 *const *pa, const u64 *const *pb,
+                         const ModTab *mods, int L, int nt, int iB0, int logN) {
   int item = blockIdx.y;
-  u64 N = 1ull << logN, P = (u64)nt * N;
+  u64 N = 1ull << logN, P = (u64)nt * N, LN = (u64)L * N;
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   int l = (int)(i >> logN);
   const ModTab &M = mods[l < L ? l : iB0 + (l - L)];
   const u64 *x = in + (u64)item * 4 * P;
-  u64 a0 = x[i], a1 = x[P + i], b0 = x[2 * P + i], b1 = x[3 * P + i];
+  u64 a0, a1, b0, b1;
+  if (l < L) {
+    a0 = pa[item][i], a1 = pa[item][LN + i], b0 = pb[item][i], b1 = pb[item][LN + i];
+  } else {
+    a0 = x[i], a1 = x[P + i], b0 = x[2 * P + i], b1 = x[3 * P + i];
+  }
   u64 *o = ten + (u64)item * 3 * P;
   o[i] = mul_mod(a0, b0, M);
   o[P + i] = add_mod(mul_mod(a0, b1, M), mul_mod(a1, b0, M), M.q);
@@ -3283,15 +3293,27 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     u64 *in = S.alloc<u64>((size_t)n * 4 * nt * N);
     u64 *coef = S.alloc<u64>((size_t)n * 4 * L * N);
     u64 **dpa = S.up(pa.data(), n), **dpb = S.up(pb.data(), n);
-    for (int p = 0; p < 4; p++) {
-      const u64 *const *src = (const u64 *const *)(p < 2 ? dpa : dpb);
-      u64 off = (p & 1) ? (u64)L * N : 0;
-      LAUNCH("gather", BYTES_gather, k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(in + (u64)p * nt * N, 4ull * nt * N, src,
-                                                                         off, (u64)L * N));
-      LAUNCH("gather", BYTES_gather, k_gather<<<dim3(GRID1((u64)L * N, TPB).x, n), TPB, 0, r->stream>>>(coef + (u64)p * L * N, 4ull * L * N, src,
-                                                                         off, (u64)L * N));
+    {  // INTT of both operands straight from the arena into coef: 2n items of 2L units
+      std::vector<u64 *> dst(2 * (size_t)n), src(2 * (size_t)n);
+      for (int i = 0; i < n; i++) {
+        dst[i] = coef + (size_t)i * 4 * L * N;
+        dst[n + i] = coef + (size_t)i * 4 * L * N + 2ull * L * N;
+        src[i] = pa[i];
+        src[n + i] = pb[i];
+      }
+      NttJob job{};
+      job.items = S.up(dst.data(), 2 * n);
+      job.src_items = S.up(src.data(), 2 * n);
+      int u = 0;
+      for (int p = 0; p < 2; p++)
+        for (int l = 0; l < L; l++) {
+          job.sub_off[u] = job.src_off[u] = (unsigned short)(p * L + l);
+          job.sub_mod[u] = (unsigned char)qm[l];
+          u++;
+        }
+      job.nsub = u;
+      launch_ntt(r, false, job, 2 * n);
     }
-    ntt_items(r, false, coef, nullptr, 4ull * L * N, n, 4, L, qm.data());
     {
       const dim3 grid(GRID1(4ull * N, TPB).x, n);
       launch_begin(r);
@@ -3318,7 +3340,7 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       launch_ntt(r, true, job, n);
     }
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
-    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, r->d_mods, L, nt, r->iB0, logN));
+    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, r->d_mods, L, nt, r->iB0, logN));
     ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
     {
