@@ -1141,17 +1141,20 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
 #pragma unroll
   for (int k = 0; k < PF::K; k++) x[k] = fp_reduce(sd[spad(PF::idx(tl, 0, k))], qs, qsi);
   phase_regs_fp<LM, 0, RA, false, E>(x, tws, tl, qs, qsi);
-  u64 c[E];  // canonical coefficients mod q_src at the PF positions
+  // the centred lift of each coefficient: fp_reduce's residue in [-q_src/2, q_src/2]
+  // IS the centred representative (q_src odd), and since every modulus of Q u P has
+  // the same bit length (|r| <= q_src / 2 < q_t, col_fusable) it is a valid input of
+  // each target's forward pass as it stands -- no canonical form, no integer lift
+  double c[E];
 #pragma unroll
-  for (int k = 0; k < E; k++) c[k] = fp_canon(fp_mulmod(fp_reduce(x[k], qs, qsi), Ms.ninv_fp, Ms.ninv_fpq, qs), qs, qsi);
-  const u64 qsrc = Ms.q;
+  for (int k = 0; k < E; k++) c[k] = fp_reduce(fp_mulmod(fp_reduce(x[k], qs, qsi), Ms.ninv_fp, Ms.ninv_fpq, qs), qs, qsi);
 #pragma unroll 1
   for (int t = 0; t < NT; t++) {
     const ModTab &Mt = job.mods[job.dst_mod[s][t]];
     const double qt = Mt.qd, qti = Mt.qinv;
     const double2 *tw_t = tws + (t + 1) * M;
 #pragma unroll
-    for (int k = 0; k < E; k++) x[k] = u2d(centred_to(c[k], qsrc, Mt.q));
+    for (int k = 0; k < E; k++) x[k] = c[k];
     phase_regs_fp<LM, 0, RA, true, E>(x, tw_t, tl, qt, qti);
     __syncthreads();  // previous target's (or the inverse's) smem reads are done
 #pragma unroll
@@ -1189,8 +1192,14 @@ static void col_fused_t(cgb_ring *r, const ColJob &job, int count, int nt) {
   }
 }
 static bool col_fusable(const cgb_ring *r) {
+  u64 lo = ~0ull, hi = 0;  // k_col_fused feeds centred residues (|r| <= q_src / 2) to every target's pass
+  for (int i = 0; i <= r->L; i++) {
+    const u64 q = r->mods[i == r->L ? r->iP : i];
+    lo = q < lo ? q : lo;
+    hi = q > hi ? q : hi;
+  }
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_col_fused && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
-         r->L <= 4;
+         r->L <= 4 && hi < 2 * lo;
 }
 // inverse column pass of job.nsrc source units + lift + forward column passes into nt targets
 static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *name) {
