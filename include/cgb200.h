@@ -119,6 +119,13 @@ int cgb_encrypt_batch(cgb_ring *ring, int count, const uint64_t *slots, const ui
                       const uint64_t *indices, const uint32_t *out_ids);
 /* Context.decrypt (backend.py:312-319) */
 int cgb_decrypt(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *slots_out);
+/* The same decryption split at the client round trip: _start enqueues it (and the
+   device->host copy into library-owned pinned memory) and returns a ticket; _finish
+   waits for that ticket only and copies the count x n_slots residues out.  Lets a
+   caller compute on the client side of one batch while the device works on the next
+   (Context.decrypt semantics per ciphertext are unchanged). */
+int cgb_decrypt_start(cgb_ring *ring, int count, const uint32_t *cts, void **ticket_out);
+int cgb_decrypt_finish(cgb_ring *ring, void *ticket, uint64_t *slots_out);
 /* client-side diagnostic: invariant noise budget in bits of each ciphertext */
 int cgb_noise_budget(cgb_ring *ring, int count, const uint32_t *cts, double *bits_out);
 

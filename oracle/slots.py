@@ -240,6 +240,14 @@ class SlotContext:
         return wave.vals.copy()
 
     @staticmethod
+    def w_decrypt_start(wave):
+        return SlotContext.w_decrypt(wave)
+
+    @staticmethod
+    def w_decrypt_finish(pending):
+        return pending
+
+    @staticmethod
     def w_add(wa, wb):
         c = wa.ctxs[0]
         b = SlotContext._spend(np.minimum(wa.budgets, wb.budgets), c.params.noise_costs.add)

@@ -41,7 +41,8 @@ from .encodings import EncodingKind, PackedMatrix, next_pow2, tile_wave
 from .fixedpoint import (FixedPointParams, attention_weights, attention_weights_rows, causal_attention_weights,
                          fp_truncate)
 from .linear_kernels import fold_wave
-from .nonlinear import MpcChannel, SharePair, he_to_shares_wave, reconstruct, share_vector, shares_to_he_wave
+from .nonlinear import (MpcChannel, SharePair, he_to_shares_finish, he_to_shares_start, he_to_shares_wave, reconstruct,
+                        share_vector, shares_to_he_wave)
 
 __all__ = ["ScoreLayout", "ScoreVector", "arcc_inner_inner", "arcc_inner_outer", "attention_step",
            "attention_step_heads", "broadcast_slot", "broadcast_wave", "compact_scores", "prefill_attention",
@@ -234,14 +235,47 @@ def attention_step(q, cache, fp: FixedPointParams, ctx, mpc: MpcChannel):
     return attention_step_heads([q], [cache], fp, [ctx], [mpc])[0]
 
 
-def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
+HEAD_GROUPS = int(os.environ.get("CGB_HEAD_GROUPS", "2"))
+
+
+def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs, groups: int | None = None) -> list:
     """``attention_step`` for H independent heads in one wave schedule.
 
     Head h uses context ctxs[h] (its counters, ids and encryption stream)
     and channel mpcs[h] (its masks and transcript), exactly as H sequential
     ``attention_step`` calls would; ctxs may repeat only if the heads would
     have run back to back on that context (then encryptions are assigned in
-    head order, which is the sequential order)."""
+    head order, which is the sequential order).
+
+    With distinct contexts the heads run as ``groups`` interleaved groups: the
+    client side of one group's round trips (decrypt, softmax / truncation,
+    re-encrypt) overlaps the device work of the next group, each group's
+    decryption waited for on its own.  Every head's op sequence is unchanged."""
+    H = len(qs)
+    groups = HEAD_GROUPS if groups is None else groups
+    if groups <= 1 or H < 2 * groups or len({id(c) for c in ctxs}) < H:
+        return _drive([_attention_step_gen(qs, caches, fp, ctxs, mpcs)])[0]
+    cuts = np.linspace(0, H, groups + 1).astype(int)
+    gens = [_attention_step_gen(qs[a:b], caches[a:b], fp, ctxs[a:b], mpcs[a:b]) for a, b in zip(cuts, cuts[1:])]
+    return [o for outs in _drive(gens) for o in outs]
+
+
+def _drive(gens) -> list:
+    """Advance the generators round-robin to completion; their return values."""
+    out = [None] * len(gens)
+    live = list(range(len(gens)))
+    while live:
+        for g in list(live):
+            try:
+                next(gens[g])
+            except StopIteration as stop:
+                out[g] = stop.value
+                live.remove(g)
+    return out
+
+
+def _attention_step_gen(qs, caches, fp: FixedPointParams, ctxs, mpcs):
+    """The step of attention_step_heads; yields after enqueueing each client decryption."""
     _mark("step.start")
     H = len(qs)
     c0 = ctxs[0]
@@ -316,7 +350,9 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
     for ch, length in plan:
         ch.predraw([length])
     _mark("masks.predrawn")
-    shares = he_to_shares_wave(W.concat(parts), chans, lens) if parts else []
+    pend = he_to_shares_start(W.concat(parts), chans, lens) if parts else None
+    yield
+    shares = he_to_shares_finish(pend) if parts else []
     _mark("scores.decrypted")
     # ---- client: reassemble scores, softmax -------------------------------------
     rows, si = [], 0
@@ -411,7 +447,9 @@ def attention_step_heads(qs, caches, fp: FixedPointParams, ctxs, mpcs) -> list:
     _mark("values.enqueued")
     # ---- output: masked decrypt (d2 slots), truncate, re-encrypt -----------------
     d2s = [c.d2 for c in caches]
-    sh = he_to_shares_wave(ow, mpcs, d2s)
+    pend = he_to_shares_start(ow, mpcs, d2s)
+    yield
+    sh = he_to_shares_finish(pend)
     _mark("values.decrypted")
     tr = [_truncate(s, fp, ch) for s, ch in zip(sh, mpcs)]
     out = shares_to_he_wave(tr, ctxs, mpcs).handles()

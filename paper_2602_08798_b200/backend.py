@@ -666,6 +666,25 @@ class GpuContext:
         return wave.ctxs[0]._ring.decrypt(wave.aids)
 
     @staticmethod
+    def w_decrypt_start(wave: Wave):
+        """w_decrypt split at the client round trip: charges and enqueues now;
+        w_decrypt_finish(pending) waits for this batch only."""
+        if len(wave) == 0:
+            return ("empty", wave.ctxs[0].params.n_slots)
+        if wave.budgets.min() <= 0:
+            raise DecryptionFailure("noise budget exhausted: decryption would be incorrect")
+        GpuContext._charge(wave, "decrypt", n_emit=0)
+        ring = wave.ctxs[0]._ring
+        return (ring, ring.decrypt_start(wave.aids), wave)
+
+    @staticmethod
+    def w_decrypt_finish(pending) -> np.ndarray:
+        if pending[0] == "empty":
+            return np.zeros((0, pending[1]), np.int64)
+        ring, ticket, _ = pending
+        return ring.decrypt_finish(ticket)
+
+    @staticmethod
     def w_add(wa: Wave, wb: Wave) -> Wave:
         c0 = wa.ctxs[0]
         b = GpuContext._spend_all(np.minimum(wa.budgets, wb.budgets), c0.params.noise_costs.add)

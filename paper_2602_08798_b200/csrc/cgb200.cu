@@ -176,6 +176,7 @@ struct cgb_ring {
   u64 t;
   std::vector<u64> mods;  // Q | P | B | t
   std::vector<ModTab> h_mods;
+  std::vector<std::pair<size_t, u64 *>> dec_pool;  // pinned landing buffers of cgb_decrypt_start
   ModTab *d_mods = nullptr;
   u64 *d_tables = nullptr;
   u32 *d_slot_idx = nullptr;
@@ -808,6 +809,45 @@ struct MdEpi {
       }
     }
   }
+  // start the async copies of the epilogue operands of words pos .. pos + 3 of unit
+  // `unit` into stg[0..3] (input, rotate_add) and stg[16..19] (the 32-byte block of
+  // the automorphed c0 holding them)
+  __device__ void prefetch4(int item, int unit, u64 pos, u64 *stg) const {
+    const int pp = unit / L, l = unit - pp * L;
+    const u64 N = 1ull << logN;
+    if (add1) {
+      const u64 *b = add1[item] + (u64)unit * N + pos;
+      cp_async16(stg, b);
+      cp_async16(stg + 2, b + 2);
+    }
+    if (pp == 0 && (add0.items || add0.base)) {
+      const u64 *c;
+      if (add0.items) {
+        c = add0.items[item] + add0.off + ((u64)l << logN);
+        c += add0.g ? (perm_g((u32)pos, add0.g[item], logN) & ~3u) : pos;
+      } else {
+        c = add0.base + (u64)item * add0.stride + ((u64)l << logN) + pos;
+      }
+      cp_async16(stg + 16, c);
+      cp_async16(stg + 18, c + 2);
+    }
+  }
+  // combine4 with the operands prefetch4 staged (after cp_async_wait_all)
+  __device__ void combine4_staged(int item, int unit, u64 pos, const u64 *w, const u64 *av, const u64 *stg) const {
+    const int pp = unit / L, l = unit - pp * L;
+    const u64 N = 1ull << logN, q = mods[l].q, pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
+    const bool a0 = pp == 0 && (add0.items || add0.base);
+    const bool gal = a0 && add0.items && add0.g;
+    const u64 g = gal ? add0.g[item] : 1;
+    u64 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      v[k] = mul_shoup(sub_mod(av[k], w[k], q), pi, pis, q);
+      if (a0) v[k] = add_mod(v[k], stg[16 + (gal ? (perm_g((u32)(pos + k), g, logN) & 3u) : k)], q);
+      if (add1) v[k] = add_mod(v[k], stg[k], q);
+    }
+    st256(out[item] + (u64)unit * N + pos, v[0], v[1], v[2], v[3]);
+  }
   // words pos .. pos + 3 of unit `unit`: W's words w, the accumulator's words av
   __device__ void combine4(int item, int unit, u64 pos, const u64 *w, const u64 *av) const {
     const int pp = unit / L, l = unit - pp * L;
@@ -841,15 +881,21 @@ struct MdEpi {
 // so a sum of <= 4 digits is an exact integer < 11q < 2^53 and its canonical residue
 // equals the integer path's.  acc[item][p][l] is written
 // once; D's row-pass output never reaches memory.
-// k_ks_row's bulk-copy landing tile: rows of 2^LB words at a pitch of 2^LB + 8
-// (consecutive rows alternate between the two bank halves)
-__host__ __device__ constexpr int ksr_pitch(int LB) { return (1 << LB) + 8; }
-#ifndef CGB_KSROW_TMA
-#define CGB_KSROW_TMA 0  // D / W row tiles prefetched by bulk async copies (one tile ahead): measured slower
+#ifndef CGB_KSROW_GTW
+#define CGB_KSROW_GTW 0  // row twiddles read through L1 instead of staged: measured slower
+#endif
+#ifndef CGB_KSROW_EPF
+#define CGB_KSROW_EPF 0  // MODE 2: epilogue operands prefetched (cp.async) into the exchange tile: measured slower
 #endif
 #ifndef CGB_KSROW_G4
 #define CGB_KSROW_G4 0  // measured: the per-word own-digit loads are faster here (profiles/r02)
 #endif
+// words of k_ks_row's exchange tile: the padded row tile, or (EPF) 32 staging words per thread
+__host__ __device__ constexpr int ksr_data_words(int LB) {
+  return ((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1) > (CGB_KSROW_EPF ? 32 * (NTT2_TILE / 16) : 0)
+             ? ((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1)
+             : 32 * (NTT2_TILE / 16);
+}
 #ifndef CGB_KSROW_MINB
 #define CGB_KSROW_MINB 3  // <= 168 registers: 3 CTAs per SM (MODE 2 would otherwise take 208)
 #endif
@@ -877,8 +923,15 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   const double qd = Md.qd, qinv = Md.qinv;
   const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
   const u64 row0 = (u64)(first + g) << LM;  // word offset of this thread's row
+#if CGB_KSROW_GTW
+  // the row twiddles are read through L1 from the transposed global table (the
+  // freed shared memory stages MODE 2's epilogue operands)
+  constexpr bool GT = true;
+  const double2 *tw = reinterpret_cast<const double2 *>(Md.ftw1t) + row0;
+#else
   // the tile's row twiddles (same for every digit) staged once: rows of M + 1 pairs
-  double2 *tws = reinterpret_cast<double2 *>(sm3 + ((G * PADM + 1) & ~1));
+  constexpr bool GT = false;
+  double2 *tws = reinterpret_cast<double2 *>(sm3 + ksr_data_words(LM));
   auto stage_tw = [&](const u64 *table) {
     const double2 *gt = reinterpret_cast<const double2 *>(table) + ((u64)first << LM);
 #pragma unroll
@@ -888,6 +941,8 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     }
   };
   stage_tw(Md.ftw1t);
+  const double2 *tw = tws + g * (M + 1);
+#endif
   // row tiles this CTA reads, in order: D(j, l) for the digits j != l, then (MODE 2) W(0, l), W(1, l)
   constexpr int NT_MAX = L + 2;
   const int ntile = (l == L ? L : L - 1) + (MODE == 2 ? 2 : 0);
@@ -900,37 +955,6 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     return W + ((u64)item * 2 * L + (u64)(t - nd) * L + l) * N + ((u64)first << LM);
   };
   (void)NT_MAX;
-#if CGB_KSROW_TMA
-  constexpr int PITCH = ksr_pitch(LM);
-  u64 *land = sm3 + ((G * PADM + 1) & ~1) + 2 * (NTT2_TILE + G);  // after the twiddle rows
-  u64 *bar = land + G * PITCH;
-  auto issue = [&](int t) {  // one thread: the G rows of tile t
-    mbar_expect_tx(bar, (u32)(G * M * sizeof(u64)));
-    const u64 *src = tile_src(t);
-    for (int rr = 0; rr < G; rr++) bulk_g2s(land + rr * PITCH, src + ((u64)rr << LM), M * sizeof(u64), bar);
-  };
-  if (tid == 0) mbar_init(bar, 1);
-  __syncthreads();
-  pdl_start_dependents();
-  pdl_wait();
-  if (tid == 0 && ntile > 0) issue(0);
-  int tcur = 0;
-  // PA-phase words of the next tile: from the landing tile, then release it to the next copy
-  auto load_tile = [&](double *x) {
-    mbar_wait(bar, (u32)(tcur & 1));
-#pragma unroll
-    for (int k = 0; k < PA::K; k++) {
-      const u64 v = land[g * PITCH + PA::idx(tl, 0, k)];
-      x[k] = (raw & 1) ? r2d(v) : u2d(v);
-    }
-    __syncthreads();  // every thread has its words (and the previous tile's phase-B reads are done)
-    if (tid == 0 && tcur + 1 < ntile) {
-      fence_proxy_async();
-      issue(tcur + 1);
-    }
-    tcur++;
-  };
-#else
   pdl_start_dependents();
   pdl_wait();
   int tcur = 0;
@@ -944,8 +968,6 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
   };
-#endif
-  const double2 *tw = tws + g * (M + 1);
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
   const u64 *K = keys[item];
@@ -975,7 +997,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #endif
     } else {
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, false>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, true, E, false, GT>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
       __syncthreads();
@@ -983,7 +1005,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
-      phase_regs_fp<LM, RA, RB, true, E, true, false>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, true, E, true, GT>(x, tw, tl, qd, qinv);
     }
     const u64 *k0 = K + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = K + ((u64)(j * 2 + 1) * LP + l) * N + row0;
 #pragma unroll
@@ -1008,7 +1030,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     for (int pp = 0; pp < 2; pp++) {
       double x[E];
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, false>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, true, E, false, GT>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
       __syncthreads();
@@ -1016,7 +1038,22 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];
-      phase_regs_fp<LM, RA, RB, true, E, true, false>(x, tw, tl, qd, qinv);
+#if CGB_KSROW_EPF
+      // the exchange tile is free until the next pass: this pass's epilogue operands
+      // (c0 o sigma, the rotate_add input) stream into the thread's slots of it while
+      // phase B computes
+      u64 *stg = sm3 + 32 * tid;
+      __syncthreads();  // every thread has read its phase-B words
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k += 4) epi.prefetch4(item, pp * L + l, row0 + PB::idx(tl, u, k), stg + u * PB::K + k);
+      cp_async_commit();
+#endif
+      phase_regs_fp<LM, RA, RB, true, E, true, GT>(x, tw, tl, qd, qinv);
+#if CGB_KSROW_EPF
+      cp_async_wait_all();
+#endif
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
@@ -1027,23 +1064,31 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
             w[e] = fp_canon(x[u * PB::K + k + e], qd, qinv);
             av[e] = fp_canon(pp ? a1[u * PB::K + k + e] : a0[u * PB::K + k + e], qd, qinv);
           }
+#if CGB_KSROW_EPF
+          epi.combine4_staged(item, pp * L + l, row0 + PB::idx(tl, u, k), w, av, stg + u * PB::K + k);
+#else
           epi.combine4(item, pp * L + l, row0 + PB::idx(tl, u, k), w, av);
+#endif
         }
     }
     return;
   }
   u64 *o0 = acc + ((u64)item * 2 * LP + l) * N + row0, *o1 = acc + ((u64)item * 2 * LP + LP + l) * N + row0;
   if (l == L) {  // P limb: ModDown's inverse row pass runs here, on the accumulators
+#if CGB_KSROW_GTW
+    const double2 *itw = reinterpret_cast<const double2 *>(Md.fitw1t) + row0;
+#else
     __syncthreads();  // every thread is done with the forward twiddles
     stage_tw(Md.fitw1t);
     const double2 *itw = tw;
+#endif
 #pragma unroll 1
     for (int pp = 0; pp < 2; pp++) {
       double y[E];
 #pragma unroll
       for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
       __syncthreads();  // inverse twiddles staged / previous poly's reads done
-      phase_regs_fp<LM, RA, RB, false, E, true, false>(y, itw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, false, E, true, GT>(y, itw, tl, qd, qinv);
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
@@ -1052,7 +1097,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
-      phase_regs_fp<LM, 0, RA, false, E, false, false>(y, itw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, false, E, false, GT>(y, itw, tl, qd, qinv);
       u64 *o = pp ? o1 : o0;
 #pragma unroll
       for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (raw & 2) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
@@ -1218,10 +1263,8 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
 }
 
 template <int LA, int LB>
-static size_t ks_row_smem() {  // row-pass data tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
-  return sizeof(u64) * (size_t)((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1) +
-         16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)) +
-         (CGB_KSROW_TMA ? sizeof(u64) * ((size_t)(NTT2_TILE >> LB) * ksr_pitch(LB) + 2) : 0);
+static size_t ks_row_smem() {  // exchange tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
+  return sizeof(u64) * (size_t)ksr_data_words(LB) + (CGB_KSROW_GTW ? 0 : 16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)));
 }
 template <int LA, int LB, int L>
 static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in
@@ -2808,6 +2851,7 @@ void cgb_ring_destroy(cgb_ring *r) {
   cudaFree(r->d_s);
   cudaFree(r->d_c);
   cudaFreeHost(r->pin);
+  for (auto &b : r->dec_pool) cudaFreeHost(b.second);
   for (auto e : r->pin_left)
     if (e) cudaEventDestroy(e);
   if (r->own_stream) cudaStreamDestroy(r->stream);
@@ -3105,9 +3149,54 @@ int cgb_encrypt_batch(cgb_ring *r, int count, const uint64_t *slots, const uint3
   API_END
 }
 
+struct DecTicket {  // an enqueued decryption: pinned landing buffer + completion event
+  u64 *host;
+  size_t words, cap;
+  cudaEvent_t done;
+};
+static void decrypt_enqueue(cgb_ring *r, int count, const uint32_t *cts, u64 *dst_host);
+int cgb_decrypt_start(cgb_ring *r, int count, const uint32_t *cts, void **ticket_out) {
+  API_BEGIN
+  const size_t words = (size_t)(count > 0 ? count : 0) * r->n_slots;
+  auto *t = new DecTicket{nullptr, words, words, nullptr};
+  *ticket_out = t;
+  if (count <= 0) return CGB_OK;
+  for (size_t i = 0; i < r->dec_pool.size(); i++)
+    if (r->dec_pool[i].first >= words) {
+      t->host = r->dec_pool[i].second;
+      t->cap = r->dec_pool[i].first;
+      r->dec_pool.erase(r->dec_pool.begin() + i);
+      break;
+    }
+  if (!t->host) CK(cudaMallocHost(&t->host, sizeof(u64) * words));
+  decrypt_enqueue(r, count, cts, t->host);
+  CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->done, r->stream));
+  API_END
+}
+int cgb_decrypt_finish(cgb_ring *r, void *ticket, uint64_t *slots_out) {
+  API_BEGIN
+  (void)r;
+  auto *t = static_cast<DecTicket *>(ticket);
+  if (!t) FAIL(CGB_ERR_PARAM, "null decryption ticket");
+  if (t->words) {
+    CK(cudaEventSynchronize(t->done));
+    std::memcpy(slots_out, t->host, sizeof(u64) * t->words);
+    cudaEventDestroy(t->done);
+    r->dec_pool.push_back({t->cap, t->host});
+  }
+  delete t;
+  API_END
+}
 int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out) {
   API_BEGIN
   if (count <= 0) return CGB_OK;
+  decrypt_enqueue(r, count, cts, slots_out);
+  CK(cudaStreamSynchronize(r->stream));
+  API_END
+}
+// decryption kernels + the device->host copy of the slots, enqueued on the ring's stream
+static void decrypt_enqueue(cgb_ring *r, int count, const uint32_t *cts, u64 *slots_out) {
   Scratch S(r);
   auto pc = ct_ptrs(r, count, cts);
   u64 **dc = S.up(pc.data(), count);
@@ -3125,8 +3214,6 @@ int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out
   LAUNCH("gather_slots", BYTES_gather_slots, k_gather_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(so, m, r->d_slot_idx, r->n_slots,
                                                                                r->logN));
   CK(cudaMemcpyAsync(slots_out, so, sizeof(u64) * (size_t)count * r->n_slots, cudaMemcpyDeviceToHost, r->stream));
-  CK(cudaStreamSynchronize(r->stream));
-  API_END
 }
 
 int cgb_noise_budget(cgb_ring *r, int count, const uint32_t *cts, double *bits) {

@@ -191,6 +191,13 @@ __device__ __forceinline__ void mbar_wait(u64 *bar, u32 parity) {
       : "memory");
 }
 
+// 16-byte asynchronous global -> shared copies (no register staging)
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Aligned blocks of 2^b consecutive output words read an aligned block of 2^b
 // input words (the automorphism acts on the top bits of brev(k) by an affine map
 // and leaves the low bits' block fixed), so a gather of 4 consecutive outputs is

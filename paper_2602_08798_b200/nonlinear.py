@@ -23,7 +23,8 @@ import numpy as np
 from .backend import ParameterError
 from .fixedpoint import FixedPointParams, fp_truncate, from_signed, to_signed
 
-__all__ = ["MpcChannel", "SharePair", "he_to_shares", "he_to_shares_wave", "reconstruct", "share_vector",
+__all__ = ["MpcChannel", "SharePair", "he_to_shares", "he_to_shares_finish", "he_to_shares_start", "he_to_shares_wave",
+           "reconstruct", "share_vector",
            "shares_to_he", "shares_to_he_wave", "truncate"]
 
 
@@ -111,6 +112,12 @@ def truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel) -> SharePair:
 def he_to_shares_wave(wave, chans, lengths) -> list:
     """Server masks each ciphertext with a fresh r (n words from its channel),
     the client decrypts; returns one SharePair per item."""
+    return he_to_shares_finish(he_to_shares_start(wave, chans, lengths))
+
+
+def he_to_shares_start(wave, chans, lengths):
+    """he_to_shares_wave up to the client's decryption, which is enqueued, not
+    awaited: masks drawn and masked ciphertexts formed in the same order."""
     C = type(wave.ctxs[0])
     params = wave.ctxs[0].params
     n, p = params.n_slots, params.plain_modulus
@@ -122,7 +129,12 @@ def he_to_shares_wave(wave, chans, lengths) -> list:
     neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
     neg[neg == p] = 0
     masked = C.w_add_plain(wave, neg, one_shot=True)
-    client = C.w_decrypt(masked)
+    return C, C.w_decrypt_start(masked), r, list(chans), lengths, n, p
+
+
+def he_to_shares_finish(pending) -> list:
+    C, dec, r, chans, lengths, n, p = pending
+    client = C.w_decrypt_finish(dec)
     out = []
     for i, ch in enumerate(chans):
         ch.transfer("he_to_shares", n)

@@ -173,6 +173,22 @@ class Ring:
         self.d2h_bytes += out.nbytes
         return out.view(np.int64)  # residues < t < 2^63: the same values, no copy
 
+    def decrypt_start(self, ids):
+        """Enqueue a decryption (and its device->host copy); returns a ticket for
+        decrypt_finish.  Only that ticket is waited for."""
+        ids = _ids(ids)
+        t = ctypes.c_void_p()
+        nat.check(nat.lib().cgb_decrypt_start(self._h, ids.size, nat.u32ptr(ids), ctypes.byref(t)),
+                  "cgb_decrypt_start")
+        return t, ids.size
+
+    def decrypt_finish(self, ticket) -> np.ndarray:
+        t, n = ticket
+        out = np.zeros((n, self.n_slots), dtype=np.uint64)
+        nat.check(nat.lib().cgb_decrypt_finish(self._h, t, nat.u64ptr(out)), "cgb_decrypt_finish")
+        self.d2h_bytes += out.nbytes
+        return out.view(np.int64)
+
     def noise_budget(self, ids) -> np.ndarray:
         ids = _ids(ids)
         out = np.zeros(ids.size, dtype=np.float64)
