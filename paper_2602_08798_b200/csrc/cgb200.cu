@@ -160,6 +160,10 @@ struct Consts {
   u64 QhatInv_sh[MAXL], QhatModB_sh[MAXL][MAXL + 1], QmodB_sh[MAXL + 1];
   u64 QBhatInv_sh[MAXL], BQhatInv_sh[MAXL + 1], sc_omega_sh[MAXL][MAXL + 1], tBhat_sh[MAXL + 1];
   u64 BhatInv_sh[MAXL + 1], BhatModQ_sh[MAXL + 1][MAXL], BmodQ_sh[MAXL];
+  // FP64-pipe companions (w, w / modulus) of the same constants (rings of < 2^49 primes)
+  double2 fQhatInv[MAXL], fQhatModB[MAXL][MAXL + 1], fQmodB[MAXL + 1];
+  double2 fQBhatInv[MAXL], fBQhatInv[MAXL + 1], fsc_omega[MAXL][MAXL + 1], ftBhat[MAXL + 1];
+  double2 fBhatInv[MAXL + 1], fBhatModQ[MAXL + 1][MAXL], fBmodQ[MAXL];
 };
 
 static const u64 DOM_SK = 1, DOM_KSK_A = 2, DOM_KSK_E = 3, DOM_ENC_A = 4, DOM_ENC_E = 5;
@@ -356,6 +360,7 @@ static void launch_end(cgb_ring *r, const char *name, double bytes, double mm = 
 static int g_ntt2_e = 8;  // words per thread of the two-pass NTT (8 or 16; CGB_NTT_E)
 static int g_fp_regio = 3;  // FP64 NTT passes with register I/O: bit0 pass 0, bit1 pass 1 (CGB_FP_REGIO)
 static bool g_md_epi = true;  // ModDown combine fused into its NTT's row pass (CGB_MD_EPI=0 -> separate kernel)
+static bool g_fp_bconv = true;  // mult_cipher base conversions on the FP64 pipe (CGB_FP_BCONV)
 static bool g_ks_md = true;   // ModDown row pass + combine fused into the Q limbs' k_ks_row (CGB_KS_MD)
 static bool g_ks_row = true;  // ModUp row pass fused with the key inner product (CGB_KS_ROW=0 -> ks_inner)
 static bool g_col_fused = true;  // INTT column pass + lift + forward column passes in one kernel (CGB_COL_FUSED)
@@ -1617,6 +1622,96 @@ __global__ void k_lift_QB_t(u64 *dst, const u64 *coef, const ModTab *mods, const
     d[(u64)(L + k) * N + jn] = sub_mod(acc, mul_shoup(v, C->QmodB[k], C->QmodB_sh[k], q), q);
   }
 }
+// FP64-pipe forms of the two base conversions (every modulus < 2^49): the same
+// modular products as the integer kernels through fp_mulmod (exact, results in
+// (-2m, 2m)), lazy FP64 sums of <= 4 such products, canonical at the end -- so the
+// same residues; the double-precision overflow estimates and the 128-bit
+// fixed-point rounding are the integer kernels' operations unchanged.
+__device__ __forceinline__ double fpm(double a, double2 w, double m) { return fp_mulmod(a, w.x, w.y, m); }
+template <int L>
+__global__ void k_lift_QB_fp(u64 *dst, const u64 *coef, const ModTab *mods, const Consts *C, int iB0, int logN) {
+  constexpr int nB = L + 1;
+  const int item = blockIdx.y;
+  const u64 N = 1ull << logN;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 4 * N) return;
+  const u64 jn = i & (N - 1);
+  const int p = (int)(i >> logN);
+  const u64 *src = coef + ((u64)item * 4 + p) * L * N;
+  double yd[L];
+  double s = 0.0;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    const ModTab &M = mods[l];
+    const u64 y = fp_canon(fpm(u2d(src[(u64)l * N + jn]), C->fQhatInv[l], M.qd), M.qd, M.qinv);
+    yd[l] = u2d(y);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(y), C->invq[l]));
+  }
+  const double v = u2d((u64)__dadd_rn(s, 0.5));
+  u64 *d = dst + ((u64)item * 4 + p) * (L + nB) * N;
+#pragma unroll
+  for (int k = 0; k < nB; k++) {
+    const ModTab &M = mods[iB0 + k];
+    double acc = -fpm(v, C->fQmodB[k], M.qd);
+#pragma unroll
+    for (int l = 0; l < L; l++) {
+      acc += fpm(yd[l], C->fQhatModB[l][k], M.qd);
+      if ((l & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+    }
+    d[(u64)(L + k) * N + jn] = fp_canon(acc, M.qd, M.qinv);
+  }
+}
+template <int L>
+__global__ void k_scale_round_fp(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int iB0, int logN) {
+  constexpr int nB = L + 1, nt = L + nB;
+  const int item = blockIdx.y;
+  const u64 N = 1ull << logN;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * N) return;
+  const u64 jn = i & (N - 1);
+  const int p = (int)(i >> logN);
+  const u64 *cp = ten + ((u64)item * 3 + p) * nt * N;
+  double yd[L];
+  u128 S = 0;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    const ModTab &M = mods[l];
+    const u64 y = fp_canon(fpm(u2d(cp[(u64)l * N + jn]), C->fQBhatInv[l], M.qd), M.qd, M.qinv);
+    yd[l] = u2d(y);
+    S += (u128)y * C->sc_th_hi[l] + (u128)__umul64hi(y, C->sc_th_lo[l]);
+  }
+  const u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
+  double ykd[nB];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < nB; k++) {
+    const ModTab &M = mods[iB0 + k];
+    double acc = u2d(reduce4(R, M.q));
+#pragma unroll
+    for (int l = 0; l < L; l++) {
+      acc += fpm(yd[l], C->fsc_omega[l][k], M.qd);
+      if ((l & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+    }
+    const double z = fpm(u2d(cp[(u64)(L + k) * N + jn]), C->fBQhatInv[k], M.qd);
+    acc = fp_reduce(acc + fpm(z, C->ftBhat[k], M.qd), M.qd, M.qinv);
+    const u64 yk = fp_canon(fpm(acc, C->fBhatInv[k], M.qd), M.qd, M.qinv);
+    ykd[k] = u2d(yk);
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(yk), C->invb[k]));
+  }
+  const double v = u2d((u64)__dadd_rn(s, 0.5));
+  u64 *o = d + ((u64)item * 3 + p) * L * N;
+#pragma unroll
+  for (int l = 0; l < L; l++) {
+    const ModTab &M = mods[l];
+    double acc = -fpm(v, C->fBmodQ[l], M.qd);
+#pragma unroll
+    for (int k = 0; k < nB; k++) {
+      acc += fpm(ykd[k], C->fBhatModQ[k][l], M.qd);
+      if ((k & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+    }
+    o[(u64)l * N + jn] = fp_canon(acc, M.qd, M.qinv);
+  }
+}
 template <int L>
 __global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int iB0, int logN) {
   constexpr int nB = L + 1, nt = L + nB;
@@ -2727,6 +2822,23 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     C.tBhat_sh[k] = h_shoup(C.tBhat[k], b[k]);
     C.BhatInv_sh[k] = h_shoup(C.BhatInv[k], b[k]);
   }
+  auto fw = [](u64 w, u64 m) { return make_double2((double)w, (double)w / (double)m); };
+  for (int l = 0; l < L; l++) {
+    C.fQhatInv[l] = fw(C.QhatInv[l], q[l]);
+    C.fQBhatInv[l] = fw(C.QBhatInv[l], q[l]);
+    C.fBmodQ[l] = fw(C.BmodQ[l], q[l]);
+    for (int k = 0; k < nB; k++) {
+      C.fQhatModB[l][k] = fw(C.QhatModB[l][k], b[k]);
+      C.fsc_omega[l][k] = fw(C.sc_omega[l][k], b[k]);
+      C.fBhatModQ[k][l] = fw(C.BhatModQ[k][l], q[l]);
+    }
+  }
+  for (int k = 0; k < nB; k++) {
+    C.fQmodB[k] = fw(C.QmodB[k], b[k]);
+    C.fBQhatInv[k] = fw(C.BQhatInv[k], b[k]);
+    C.ftBhat[k] = fw(C.tBhat[k], b[k]);
+    C.fBhatInv[k] = fw(C.BhatInv[k], b[k]);
+  }
   CK(cudaMalloc((void **)&r->d_c, sizeof(Consts)));
   CK(cudaMemcpy(r->d_c, &C, sizeof(Consts), cudaMemcpyHostToDevice));
   // secret key: ternary from ChaCha20(key_seed, DOM_SK), word j -> (w mod 3) - 1
@@ -2822,6 +2934,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_MD")) g_ks_md = atoi(e) != 0;
+  if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
@@ -3374,6 +3487,7 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
   API_BEGIN
   if (count <= 0) return CGB_OK;
   const int L = r->L, nB = r->nB, nt = L + nB, N = r->N, logN = r->logN;
+  const bool fpbc = r->fp_ntt && g_fp_bconv;  // base conversions on the FP64 pipe (every modulus < 2^49)
   u64 *rk = get_key(r, 0);
   std::vector<int> qm, bm(nB), tm(nt);
   q_mod_idx(r, qm);
@@ -3414,7 +3528,11 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       const dim3 grid(GRID1(4ull * N, TPB).x, n);
       launch_begin(r);
       switch (L) {
-#define LQB(LL) case LL: k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); break;
+#define LQB(LL)                                                                                     \
+  case LL:                                                                                           \
+    if (fpbc) k_lift_QB_fp<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); \
+    else k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN);      \
+    break;
         LQB(1) LQB(2) LQB(3) LQB(4) LQB(5) LQB(6) LQB(7) LQB(8)
 #undef LQB
         default: k_lift_QB<<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0, logN);
@@ -3443,7 +3561,11 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       const dim3 grid(GRID1(3ull * N, TPB).x, n);
       launch_begin(r);
       switch (L) {
-#define LSR(LL) case LL: k_scale_round_t<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN); break;
+#define LSR(LL)                                                                                       \
+  case LL:                                                                                             \
+    if (fpbc) k_scale_round_fp<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN); \
+    else k_scale_round_t<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN);      \
+    break;
         LSR(1) LSR(2) LSR(3) LSR(4) LSR(5) LSR(6) LSR(7) LSR(8)
 #undef LSR
         default: k_scale_round<<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, L, nB, r->iB0, logN);
