@@ -164,6 +164,7 @@ struct Consts {
   double2 fQhatInv[MAXL], fQhatModB[MAXL][MAXL + 1], fQmodB[MAXL + 1];
   double2 fQBhatInv[MAXL], fBQhatInv[MAXL + 1], fsc_omega[MAXL][MAXL + 1], ftBhat[MAXL + 1];
   double2 fBhatInv[MAXL + 1], fBhatModQ[MAXL + 1][MAXL], fBmodQ[MAXL];
+  double2 fPinvq[MAXL];
 };
 
 static const u64 DOM_SK = 1, DOM_KSK_A = 2, DOM_KSK_E = 3, DOM_ENC_A = 4, DOM_ENC_E = 5;
@@ -853,6 +854,31 @@ struct MdEpi {
     }
     st256(out[item] + (u64)unit * N + pos, v[0], v[1], v[2], v[3]);
   }
+  // combine4 on the FP64 pipe, from the unreduced row-pass output xw (|xw| < 12q) and
+  // FP64 accumulator sums xa (|xa| < 11q): (xa - xw) P^-1 (+ c0) (+ add1), every
+  // intermediate an exact integer (|y| < 4.7q), canonical at the store -- the same
+  // residues as the integer combine
+  __device__ void combine4_fp(int item, int unit, u64 pos, const double *xw, const double *xa) const {
+    const int pp = unit / L, l = unit - pp * L;
+    const u64 N = 1ull << logN;
+    const ModTab &M = mods[l];
+    const double q = M.qd, qi = M.qinv;
+    const double2 pinv = C->fPinvq[l];
+    const bool a0 = pp == 0 && (add0.items || add0.base);
+    u64 bv[4], cv[4];
+    if (add1) ld256(add1[item] + (u64)unit * N + pos, bv);
+    if (a0) ks_src_block4(add0, item, l, (u32)pos, logN, cv);
+    u64 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      // |xa - reduce(xw)| < 11.5q: exact, inside fp_mulmod's analysed range (< 12q)
+      double y = fp_mulmod(xa[k] - fp_reduce(xw[k], q, qi), pinv.x, pinv.y, q);
+      if (a0) y += u2d(cv[k]);
+      if (add1) y += u2d(bv[k]);
+      v[k] = fp_canon(y, q, qi);
+    }
+    st256(out[item] + (u64)unit * N + pos, v[0], v[1], v[2], v[3]);
+  }
   // words pos .. pos + 3 of unit `unit`: W's words w, the accumulator's words av
   __device__ void combine4(int item, int unit, u64 pos, const u64 *w, const u64 *av) const {
     const int pp = unit / L, l = unit - pp * L;
@@ -891,6 +917,9 @@ struct MdEpi {
 #endif
 #ifndef CGB_KSROW_EPF
 #define CGB_KSROW_EPF 0  // MODE 2: epilogue operands prefetched (cp.async) into the exchange tile: measured slower
+#endif
+#ifndef CGB_KSROW_FPC
+#define CGB_KSROW_FPC 1  // MODE 2: the ModDown combine on the FP64 pipe
 #endif
 #ifndef CGB_KSROW_G4
 #define CGB_KSROW_G4 0  // measured: the per-word own-digit loads are faster here (profiles/r02)
@@ -1063,6 +1092,11 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k += 4) {
+#if CGB_KSROW_FPC
+          epi.combine4_fp(item, pp * L + l, row0 + PB::idx(tl, u, k), &x[u * PB::K + k],
+                          pp ? &a1[u * PB::K + k] : &a0[u * PB::K + k]);
+          continue;
+#endif
           u64 w[4], av[4];
 #pragma unroll
           for (int e = 0; e < 4; e++) {
@@ -2833,6 +2867,7 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
       C.fBhatModQ[k][l] = fw(C.BhatModQ[k][l], q[l]);
     }
   }
+  for (int l = 0; l < L; l++) C.fPinvq[l] = fw(C.Pinvq[l], q[l]);
   for (int k = 0; k < nB; k++) {
     C.fQmodB[k] = fw(C.QmodB[k], b[k]);
     C.fBQhatInv[k] = fw(C.BQhatInv[k], b[k]);
