@@ -297,18 +297,21 @@ def layer_cpu_baseline(args):
             "host": _cpu_model()}
 
 
+def _ncu(kernel: str):
+    """The committed ncu figures of a kernel (profiles/r01/ncu_kernels.json), or {}."""
+    f = ROOT / "profiles" / "r01" / "ncu_kernels.json"
+    return json.loads(f.read_text()).get(kernel, {}) if f.exists() else {}
+
+
 def _traffic(kernel: str, alg_bytes_per_launch: float):
     """DRAM bytes per launch of the dominant kernel: the algorithmic bytes scaled by
-    the dram/algorithmic ratio of its committed ncu --set full capture
-    (profiles/r01/ncu_traffic.json), or None when no capture is committed."""
-    f = ROOT / "profiles" / "r01" / "ncu_traffic.json"
-    if not f.exists():
+    the DRAM/algorithmic ratio of its committed ncu --set full capture, or None."""
+    cap = _ncu(kernel)
+    if "dram_over_algorithmic" not in cap:
         return None
-    cap = json.loads(f.read_text()).get(kernel)
-    if not cap:
-        return None
-    return {"bytes_per_launch": alg_bytes_per_launch * cap["ratio"], "dram_over_algorithmic": cap["ratio"],
-            "source": "profiles/r01/ncu_traffic.json (" + cap["kernel"] + ")"}
+    return {"bytes_per_launch": alg_bytes_per_launch * cap["dram_over_algorithmic"],
+            "dram_over_algorithmic": cap["dram_over_algorithmic"],
+            "source": "profiles/r01/ncu_kernels.json (" + cap["kernel"] + ")"}
 
 
 def run_ours(args):
@@ -431,7 +434,8 @@ def run_ours(args):
                      "pipe": {"name": "fp64" if ring.fp_ntt else "int64", "unit": "modmul/s",
                               "achieved": kmm / (kms * 1e-3) if kmm else None, "peak": peak_mm,
                               "frac": kmm / (kms * 1e-3) / peak_mm if kmm else None,
-                              "peak_source": "cgb_modmul_peak: measured chains of the same modular product"}},
+                              "peak_source": "cgb_modmul_peak: measured chains of the same modular product",
+                              "fp64_pipe_active_pct_ncu": _ncu(name).get("fp64_pipe_active")}},
         "arith_pipe": {"kernels": "every launch with modular-product work (NTT passes, fused key switch)",
                        "pipe": "fp64" if ring.fp_ntt else "int64",
                        "modmuls_per_s": ar_mm / (ar_ms * 1e-3) if ar_ms else None,
