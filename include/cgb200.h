@@ -138,6 +138,14 @@ int cgb_add_plain(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *
 int cgb_mult_plain(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out);
 /* Context.mult_cipher (backend.py:341-347): tensor, scale-and-round, relinearise */
 int cgb_mult_cipher(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out);
+/* mult_cipher with b's extension to the auxiliary base B kept resident: bx holds two
+   arena slots per item (b's polys 0 and 1, the nB B limbs in NTT form, as written by
+   cgb_extend_b); the result equals cgb_mult_cipher's word for word.  The encrypted KV
+   cache's parts are multiplied every decode step, so their extension is computed once
+   (the reference recomputes nothing -- it has no base extension: backend.py:341-347). */
+int cgb_extend_b(cgb_ring *ring, int count, const uint32_t *b, const uint32_t *bx);
+int cgb_mult_cipher_ext(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
+                        const uint32_t *out);
 /* Galois automorphism X -> X^g plus key switch; g = 1 copies.
  * Context.rotate (backend.py:349-355) is galois(5^k mod 2N) in the one-row layout. */
 int cgb_galois(cgb_ring *ring, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out);

@@ -275,7 +275,7 @@ class SlotContext:
                         SlotContext._charge(wave, "mult_plain"))
 
     @staticmethod
-    def w_mult_cipher(wa, wb):
+    def w_mult_cipher(wa, wb, resident_b=False):
         c = wa.ctxs[0]
         b = SlotContext._spend(np.minimum(wa.budgets, wb.budgets), c.params.noise_costs.mult_cipher)
         return SlotWave(wa.ctxs, wa.owner, (wa.vals * wb.vals) % c.params.plain_modulus, b,

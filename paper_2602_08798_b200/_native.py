@@ -93,6 +93,8 @@ SIGNATURES = {
     "cgb_add_plain": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),
     "cgb_mult_plain": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),
     "cgb_mult_cipher": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),
+    "cgb_extend_b": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p]),
+    "cgb_mult_cipher_ext": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p, _u32p]),
     "cgb_galois": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p, _u32p]),
     "cgb_rotate": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _i64p, _u32p]),
     "cgb_rotate_add": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _i64p, _u32p]),

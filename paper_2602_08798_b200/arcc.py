@@ -296,7 +296,7 @@ def _attention_step_gen(qs, caches, fp: FixedPointParams, ctxs, mpcs):
         js = np.concatenate([np.arange(d) for d in d2s])
         b = broadcast_wave(qw.take(src), js, n)
         kparts = [pt for h in pref_heads for pt in caches[h].prefill_K.parts]
-        prods = C.w_mult_cipher(b, C.wave_of(kparts, [ctxs[h] for h in src]))
+        prods = C.w_mult_cipher(b, C.wave_of(kparts, [ctxs[h] for h in src]), resident_b=True)
         bounds = np.concatenate([[0], np.cumsum(d2s)])
         pref_acc = C.w_sum(prods, [np.arange(bounds[i], bounds[i + 1]) for i in range(len(pref_heads))])
     # ---- scores: generated segment (inner-outer over compacted K) -------------
@@ -309,7 +309,7 @@ def _attention_step_gen(qs, caches, fp: FixedPointParams, ctxs, mpcs):
         nparts = [len(caches[h].auto_K.parts) for h in auto_heads]
         rep = np.repeat(np.arange(len(auto_heads)), nparts)
         kparts = [pt for h in auto_heads for pt in caches[h].auto_K.parts]
-        prods = C.w_mult_cipher(vt.take(rep), C.wave_of(kparts, [ctxs[auto_heads[i]] for i in rep]))
+        prods = C.w_mult_cipher(vt.take(rep), C.wave_of(kparts, [ctxs[auto_heads[i]] for i in rep]), resident_b=True)
         auto_sc = fold_wave(prods, d2)
     # masked decryption of every score ciphertext, per head in reference order
     order, chans, lens, ap = [], [], [], 0
@@ -402,7 +402,7 @@ def _attention_step_gen(qs, caches, fp: FixedPointParams, ctxs, mpcs):
         rep = np.repeat(np.asarray(a_idx), d2s)
         vparts = [pt for h in pref_heads for pt in caches[h].prefill_V.parts]
         src_heads = np.repeat(np.asarray(pref_heads), d2s)
-        prods = C.w_mult_cipher(enc.take(rep), C.wave_of(vparts, [ctxs[h] for h in src_heads]))
+        prods = C.w_mult_cipher(enc.take(rep), C.wave_of(vparts, [ctxs[h] for h in src_heads]), resident_b=True)
         tot = fold_wave(prods, n)
         cs = np.concatenate([np.arange(d) for d in d2s])
         pieces = C.w_mult_plain(tot, _onehots(n, cs))
@@ -413,7 +413,7 @@ def _attention_step_gen(qs, caches, fp: FixedPointParams, ctxs, mpcs):
         a_idx = [i for i, t in enumerate(s_tag) if t[0] == "a"]
         vparts = [pt for h in auto_heads for pt in caches[h].auto_V.parts]
         owners = [ctxs[h] for h in auto_heads for _ in caches[h].auto_V.parts]
-        prods = C.w_mult_cipher(enc.take(a_idx), C.wave_of(vparts, owners))
+        prods = C.w_mult_cipher(enc.take(a_idx), C.wave_of(vparts, owners), resident_b=True)
         nparts = [len(caches[h].auto_V.parts) for h in auto_heads]
         bounds = np.concatenate([[0], np.cumsum(nparts)])
         acc = C.w_sum(prods, [np.arange(bounds[i], bounds[i + 1]) for i in range(len(auto_heads))])

@@ -325,6 +325,9 @@ SlotCiphertext = GpuCiphertext
 # ----------------------------------------------------------------------------
 # waves: batches of ciphertexts processed by one launch sequence
 # ----------------------------------------------------------------------------
+EXT_B = os.environ.get("CGB_EXT_B", "1") != "0"  # resident base-B extensions of KV cache parts
+
+
 class Wave:
     """A batch of ciphertexts (arena ids + ledger budgets + owning contexts).
 
@@ -727,11 +730,18 @@ class GpuContext:
         return GpuContext._plain_op(wave, vecs, nat.CGB_PT_MUL, "mult_plain", one_shot)
 
     @staticmethod
-    def w_mult_cipher(wa: Wave, wb: Wave) -> Wave:
+    def w_mult_cipher(wa: Wave, wb: Wave, resident_b: bool = False) -> Wave:
+        """mult_cipher per item; ``resident_b``: wb's items are multiplied again
+        later (KV cache parts), so their base-B extension is computed once and kept
+        with the ciphertext (same words either way)."""
         c0 = wa.ctxs[0]
         b = GpuContext._spend_all(np.minimum(wa.budgets, wb.budgets), c0.params.noise_costs.mult_cipher)
         blk, ids = c0._new(len(wa))
-        c0._ring.mult_cipher(wa.aids, wb.aids, ids)
+        ring = c0._ring
+        if resident_b and EXT_B:
+            ring.mult_cipher_ext(wa.aids, wb.aids, ring.ext_B(wb.aids), ids)
+        else:
+            ring.mult_cipher(wa.aids, wb.aids, ids)
         return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "mult_cipher"))
 
     @staticmethod

@@ -1801,6 +1801,7 @@ __global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, cons
 // Q limbs straight from the operand ciphertexts (pa / pb: per-item [2][L][N]),
 // B limbs from the lifted buffer
 __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64 *const *pa, const u64 *const *pb,
+                         const u64 *const *pbx /*null, or b's B-limb extension: [item][2] slots of [nB][N]*/,
                          const ModTab *mods, int L, int nt, int iB0, int logN) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, P = (u64)nt * N, LN = (u64)L * N;
@@ -1812,6 +1813,8 @@ __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64
   u64 a0, a1, b0, b1;
   if (l < L) {
     a0 = pa[item][i], a1 = pa[item][LN + i], b0 = pb[item][i], b1 = pb[item][LN + i];
+  } else if (pbx) {
+    a0 = x[i], a1 = x[P + i], b0 = pbx[2 * item][i - LN], b1 = pbx[2 * item + 1][i - LN];
   } else {
     a0 = x[i], a1 = x[P + i], b0 = x[2 * P + i], b1 = x[3 * P + i];
   }
@@ -3518,9 +3521,100 @@ int cgb_prepare_galois(cgb_ring *r, int count, const uint64_t *g) {
   API_END
 }
 
+// INTT of the two polys of each item's operand (per-item pointers) into
+// coef[item][4][L][N] at poly offset `poff`
+static void intt_and_lift(cgb_ring *r, Scratch &S, int n, const std::vector<u64 *> &srcs, int poff, u64 *coef,
+                          u64 *, bool) {
+  const int L = r->L, N = r->N;
+  std::vector<int> qm;
+  q_mod_idx(r, qm);
+  {
+    std::vector<u64 *> dst(n);
+    for (int i = 0; i < n; i++) dst[i] = coef + (size_t)i * 4 * L * N + (size_t)poff * L * N;
+    NttJob job{};
+    job.items = S.up(dst.data(), n);
+    job.src_items = S.up(const_cast<u64 **>(srcs.data()), n);
+    int u = 0;
+    for (int p = 0; p < 2; p++)
+      for (int l = 0; l < L; l++) {
+        job.sub_off[u] = job.src_off[u] = (unsigned short)(p * L + l);
+        job.sub_mod[u] = (unsigned char)qm[l];
+        u++;
+      }
+    job.nsub = u;
+    launch_ntt(r, false, job, n);
+  }
+}
+static void lift_QB(cgb_ring *r, int n, int npoly, u64 *coef, u64 *in, bool fpbc) {
+  const int L = r->L, nB = r->nB, N = r->N, logN = r->logN;
+  const dim3 grid(GRID1((u64)npoly * N, TPB).x, n);
+  launch_begin(r);
+  switch (L) {
+#define LQB(LL)                                                                                     \
+  case LL:                                                                                           \
+    if (fpbc) k_lift_QB_fp<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); \
+    else k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN);      \
+    break;
+    LQB(1) LQB(2) LQB(3) LQB(4) LQB(5) LQB(6) LQB(7) LQB(8)
+#undef LQB
+    default: k_lift_QB<<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0, logN);
+  }
+  launch_end(r, "lift_QB", BYTES_lift_QB * npoly / 4.0);
+}
+
+// b's extension to the auxiliary base: polys 0 and 1 of each b item, B limbs in NTT
+// form, into two arena slots per item (slot words [nB][N]) -- what mult_cipher
+// derives from b every time, kept resident for operands that are multiplied again
+// (the encrypted KV cache's parts, every decode step)
+static void extend_B(cgb_ring *r, int count, const uint32_t *b, const uint32_t *bx) {
+  const int L = r->L, nB = r->nB, nt = L + nB, N = r->N;
+  if ((size_t)nB * N > r->ct_words) FAIL(CGB_ERR_PARAM, "B extension does not fit an arena slot");
+  const bool fpbc = r->fp_ntt && g_fp_bconv;
+  size_t CH = chunk_for(r, (size_t)N * (4 * nt + 4 * L));
+  for (int c0 = 0; c0 < count; c0 += (int)CH) {
+    const int n = std::min((int)CH, count - c0);
+    Scratch S(r);
+    auto pb = ct_ptrs(r, n, b + c0);
+    auto px = ct_ptrs(r, 2 * n, bx + 2 * (size_t)c0);
+    u64 *in = S.alloc<u64>((size_t)n * 4 * nt * N);
+    u64 *coef = S.alloc<u64>((size_t)n * 4 * L * N);
+    intt_and_lift(r, S, n, pb, 0, coef, in, fpbc);
+    lift_QB(r, n, 2, coef, in, fpbc);
+    std::vector<u64 *> src(2 * (size_t)n);
+    for (int i = 0; i < n; i++)
+      for (int p = 0; p < 2; p++) src[2 * i + p] = in + ((size_t)i * 4 + p) * nt * N + (size_t)L * N;
+    NttJob job{};
+    job.items = S.up(px.data(), 2 * n);
+    job.src_items = S.up(src.data(), 2 * n);
+    for (int k = 0; k < nB; k++) {
+      job.sub_off[k] = job.src_off[k] = (unsigned short)k;
+      job.sub_mod[k] = (unsigned char)(r->iB0 + k);
+    }
+    job.nsub = nB;
+    launch_ntt(r, true, job, 2 * n);
+  }
+}
+int cgb_extend_b(cgb_ring *r, int count, const uint32_t *b, const uint32_t *bx) {
+  API_BEGIN
+  if (count > 0) extend_B(r, count, b, bx);
+  API_END
+}
+
+static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
+                             const uint32_t *out);
 int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
   API_BEGIN
-  if (count <= 0) return CGB_OK;
+  if (count > 0) mult_cipher_impl(r, count, a, b, nullptr, out);
+  API_END
+}
+int cgb_mult_cipher_ext(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
+                        const uint32_t *out) {
+  API_BEGIN
+  if (count > 0) mult_cipher_impl(r, count, a, b, bx, out);
+  API_END
+}
+static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
+                             const uint32_t *out) {
   const int L = r->L, nB = r->nB, nt = L + nB, N = r->N, logN = r->logN;
   const bool fpbc = r->fp_ntt && g_fp_bconv;  // base conversions on the FP64 pipe (every modulus < 2^49)
   u64 *rk = get_key(r, 0);
@@ -3538,48 +3632,25 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     u64 *in = S.alloc<u64>((size_t)n * 4 * nt * N);
     u64 *coef = S.alloc<u64>((size_t)n * 4 * L * N);
     u64 **dpa = S.up(pa.data(), n), **dpb = S.up(pb.data(), n);
-    {  // INTT of both operands straight from the arena into coef: 2n items of 2L units
-      std::vector<u64 *> dst(2 * (size_t)n), src(2 * (size_t)n);
-      for (int i = 0; i < n; i++) {
-        dst[i] = coef + (size_t)i * 4 * L * N;
-        dst[n + i] = coef + (size_t)i * 4 * L * N + 2ull * L * N;
-        src[i] = pa[i];
-        src[n + i] = pb[i];
-      }
-      NttJob job{};
-      job.items = S.up(dst.data(), 2 * n);
-      job.src_items = S.up(src.data(), 2 * n);
-      int u = 0;
-      for (int p = 0; p < 2; p++)
-        for (int l = 0; l < L; l++) {
-          job.sub_off[u] = job.src_off[u] = (unsigned short)(p * L + l);
-          job.sub_mod[u] = (unsigned char)qm[l];
-          u++;
-        }
-      job.nsub = u;
-      launch_ntt(r, false, job, 2 * n);
+    // INTT of the operands straight from the arena into coef, lift Q -> B; with b's
+    // resident extension (bx) only a's two polys
+    const int npoly = bx ? 2 : 4;
+    u64 **dpx = nullptr;
+    if (bx) {
+      auto px = ct_ptrs(r, 2 * n, bx + 2 * (size_t)c0);
+      dpx = S.up(px.data(), 2 * n);
+      intt_and_lift(r, S, n, pa, 0, coef, in, fpbc);
+    } else {
+      intt_and_lift(r, S, n, pa, 0, coef, in, fpbc);
+      intt_and_lift(r, S, n, pb, 2, coef, in, fpbc);
     }
-    {
-      const dim3 grid(GRID1(4ull * N, TPB).x, n);
-      launch_begin(r);
-      switch (L) {
-#define LQB(LL)                                                                                     \
-  case LL:                                                                                           \
-    if (fpbc) k_lift_QB_fp<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); \
-    else k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN);      \
-    break;
-        LQB(1) LQB(2) LQB(3) LQB(4) LQB(5) LQB(6) LQB(7) LQB(8)
-#undef LQB
-        default: k_lift_QB<<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, L, nB, r->iB0, logN);
-      }
-      launch_end(r, "lift_QB", BYTES_lift_QB);
-    }
+    lift_QB(r, n, npoly, coef, in, fpbc);
     {
       NttJob job{};
       job.base = in;
       job.item_stride = 4ull * nt * N;
       int u = 0;
-      for (int p = 0; p < 4; p++)
+      for (int p = 0; p < npoly; p++)
         for (int k = 0; k < nB; k++) {
           job.sub_off[u] = (unsigned short)(p * nt + L + k);
           job.sub_mod[u] = (unsigned char)bm[k];
@@ -3589,7 +3660,7 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
       launch_ntt(r, true, job, n);
     }
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
-    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, r->d_mods, L, nt, r->iB0, logN));
+    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN));
     ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
     {
@@ -3618,7 +3689,6 @@ int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b
     KsSrc none{nullptr, 0, nullptr, 0, nullptr};
     keyswitch(r, S, xin, n, dk, dout, none, (const u64 *const *)dd01);
   }
-  API_END
 }
 
 }  // extern "C"

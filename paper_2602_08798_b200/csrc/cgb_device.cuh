@@ -206,12 +206,21 @@ __device__ __forceinline__ u64 sel4(const u64 w[4], u32 s) {
   const u64 lo = (s & 1) ? w[1] : w[0], hi = (s & 1) ? w[3] : w[2];
   return (s & 2) ? hi : lo;
 }
+#ifndef CGB_GATHER_NC
+#define CGB_GATHER_NC 1  // measured: the non-coherent path is marginally faster for the digit rows
+#endif
 // out[i] = src[perm_g(k0 + i)], i < 4, k0 a multiple of 4
 __device__ __forceinline__ void gather4(const u64 *src, u32 k0, u64 g, int logN, u64 out[4]) {
   const u32 p0 = perm_g(k0, g, logN);
   u64 w[4];
+#if CGB_GATHER_NC
   asm("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
-               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(src + (p0 & ~3u)));
+      : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(src + (p0 & ~3u)));
+#else  // the coherent L1 path: neighbouring threads' blocks stay cached
+  const ulonglong2 *b = reinterpret_cast<const ulonglong2 *>(src + (p0 & ~3u));
+  const ulonglong2 lo = b[0], hi = b[1];
+  w[0] = lo.x, w[1] = lo.y, w[2] = hi.x, w[3] = hi.y;
+#endif
   out[0] = sel4(w, p0 & 3);
 #pragma unroll
   for (int i = 1; i < 4; i++) out[i] = sel4(w, perm_g(k0 + i, g, logN) & 3);

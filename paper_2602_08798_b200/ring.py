@@ -37,6 +37,7 @@ class Ring:
         if arena_pts is None:
             arena_pts = max(64, min(65536, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
         self.arena_cts, self.arena_pts = int(arena_cts), int(arena_pts)
+        self._ext = {}  # arena id -> the two slots of its resident base-B extension (cgb_extend_b)
         self.h2d_bytes = 0  # host payload bytes moved to / from the device (slot vectors, raw words)
         self.d2h_bytes = 0
         ks = np.ascontiguousarray(np.asarray(key_seed, dtype=np.uint32).reshape(8))
@@ -107,7 +108,29 @@ class Ring:
     def free(self, ids):
         ids = _ids(ids)
         if ids.size and self._h:
+            if self._ext:  # a freed ciphertext's extension goes with it (ids are reused)
+                ext = [self._ext.pop(int(a)) for a in ids if int(a) in self._ext]
+                if ext:
+                    ids = np.concatenate([ids, np.concatenate(ext)]).astype(np.uint32)
             nat.check(nat.lib().cgb_ct_free(self._h, ids.size, nat.u32ptr(ids)), "cgb_ct_free")
+
+    def ext_B(self, b_ids) -> np.ndarray:
+        """Slot pairs of the base-B extensions of b_ids (2 per item), computing the
+        missing ones; they live as long as their ciphertext's arena id."""
+        b_ids = _ids(b_ids)
+        missing = np.array(sorted({int(a) for a in b_ids} - self._ext.keys()), dtype=np.uint32)
+        if missing.size:
+            slots = self.alloc(2 * missing.size)
+            nat.check(nat.lib().cgb_extend_b(self._h, missing.size, nat.u32ptr(missing), nat.u32ptr(slots)),
+                      "cgb_extend_b")
+            for k, a in enumerate(missing):
+                self._ext[int(a)] = slots[2 * k:2 * k + 2].copy()
+        return np.ascontiguousarray(np.concatenate([self._ext[int(a)] for a in b_ids]).astype(np.uint32))
+
+    def mult_cipher_ext(self, a, b, bx, out):
+        a, b, bx, out = _ids(a), _ids(b), _ids(bx), _ids(out)
+        nat.check(nat.lib().cgb_mult_cipher_ext(self._h, a.size, nat.u32ptr(a), nat.u32ptr(b), nat.u32ptr(bx),
+                                                nat.u32ptr(out)), "cgb_mult_cipher_ext")
 
     def alloc_pt(self, n: int) -> np.ndarray:
         ids = np.zeros(n, dtype=np.uint32)

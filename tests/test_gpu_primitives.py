@@ -95,6 +95,25 @@ def test_mult_cipher_bitexact(pair, rng):
     assert np.array_equal(g.decrypt(out)[0], (v * w) % o.t)
 
 
+def test_mult_cipher_resident_extension_bitexact(pair, rng):
+    """mult_cipher with b's base-B extension kept resident: the same words as
+    mult_cipher, the extension reused across calls and freed with b."""
+    g, o = pair
+    v, w = rng.integers(0, o.t, (2, o.n_slots))
+    a, ra = _enc(g, o, v, 11)
+    b, rb = _enc(g, o, w, 12)
+    ref = o.mult_cipher(ra, rb)
+    out = g.alloc(2)
+    bb = np.concatenate([b, b])
+    g.mult_cipher_ext(np.concatenate([a, a]), bb, g.ext_B(bb), out)
+    words = g.store(out)
+    assert np.array_equal(words[0], ref) and np.array_equal(words[1], ref)
+    assert int(b[0]) in g._ext
+    g.free(b)
+    assert int(b[0]) not in g._ext
+    g.free(np.concatenate([a, out]))
+
+
 def test_rings_of_different_sizes_coexist():
     """Kernel attributes are process-global: a smaller ring created later must not
     break a larger one created earlier (regression)."""
