@@ -402,6 +402,10 @@ def run_ours(args):
     gaps = {k: round(v[1], 3) for k, v in rep.items() if k.startswith("(gap")}
     for k in gaps:
         rep.pop(k)
+    trans = {k[7:-1]: [v[0], round(v[1], 3)] for k, v in rep.items() if k.startswith("(trans:")}
+    for k in list(rep):
+        if k.startswith("(trans:"):
+            rep.pop(k)
     peak_mm = ring.modmul_peak()
 
     ms, ms_e2e = max_over_ranks(ms, world), max_over_ranks(ms_e2e, world)
@@ -449,6 +453,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_idle_ms_per_step": round(idle_ms, 2),
         "gpu_idle_top_gaps_ms": gaps,
+        "gpu_idle_by_transition_ms": trans,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, samples=1)

@@ -3131,6 +3131,22 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
     agg.back().second.n = (long)gaps[k].second;
     agg.back().second.ms = gaps[k].first;
   }
+  // idle per (previous -> next) launch-name transition, largest totals first
+  {
+    std::vector<std::pair<std::string, Agg>> tr;
+    for (auto &gp : gaps) {
+      std::string k = std::string("(trans:") + r->recs[gp.second - 1].name + "->" + r->recs[gp.second].name + ")";
+      auto it = std::find_if(tr.begin(), tr.end(), [&](auto &kv) { return kv.first == k; });
+      if (it == tr.end()) {
+        tr.push_back({k, Agg{}});
+        it = tr.end() - 1;
+      }
+      it->second.n++;
+      it->second.ms += gp.first;
+    }
+    std::sort(tr.begin(), tr.end(), [](auto &x, auto &y) { return x.second.ms > y.second.ms; });
+    for (size_t k = 0; k < std::min<size_t>(10, tr.size()); k++) agg.push_back(tr[k]);
+  }
   std::string out;
   for (auto &kv : agg) {
     char line[256];
