@@ -2264,10 +2264,12 @@ template <int LA, int LB, int L>
 static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys,
                            u64 *const *d_out, const KsSrc &add0, const u64 *const *d_add1) {
   constexpr int LP = L + 1, N = 1 << (LA + LB), G0 = NTT2_TILE >> LA, G1 = NTT2_TILE >> LB;
-  u64 *xr = S.alloc<u64>((size_t)count * L * N);
-  u64 *D = S.alloc<u64>((size_t)count * L * LP * N);
-  u64 *acc = S.alloc<u64>((size_t)count * 2 * LP * N);
-  u64 *W = S.alloc<u64>((size_t)count * 2 * L * N);
+  // one scratch allocation for the four intermediates
+  const size_t nxr = (size_t)count * L * N, nD = (size_t)count * L * LP * N, nacc = (size_t)count * 2 * LP * N;
+  u64 *xr = S.alloc<u64>(nxr + nD + nacc + (size_t)count * 2 * L * N);
+  u64 *D = xr + nxr;
+  u64 *acc = D + nD;
+  u64 *W = acc + nacc;
   const dim3 rows_grid1((unsigned)((size_t)count * L * ((1 << LA) / G1)));
   {  // 1
     NttJob job{};
@@ -2561,8 +2563,18 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
       keys[k] = get_key(r, g[k]);
     }
     std::vector<u64 *> src = ct_ptrs(r, n, ia.data()), dst = ct_ptrs(r, n, io.data());
-    u64 **d_src = S.up(src.data(), n), **d_dst = S.up(dst.data(), n), **d_keys = S.up(keys.data(), n);
-    u64 *d_g = S.up(g.data(), n);
+    // the four per-item tables in ONE upload (host cost per wave is the critical path of small waves)
+    std::vector<u64> blob(4 * (size_t)n);
+    for (int k = 0; k < n; k++) {
+      blob[k] = (u64)src[k];
+      blob[n + k] = (u64)dst[k];
+      blob[2 * n + k] = (u64)keys[k];
+      blob[3 * n + k] = g[k];
+    }
+    u64 *d_blob = S.up(blob.data(), blob.size());
+    u64 **d_src = reinterpret_cast<u64 **>(d_blob), **d_dst = reinterpret_cast<u64 **>(d_blob + n),
+        **d_keys = reinterpret_cast<u64 **>(d_blob + 2 * n);
+    u64 *d_g = d_blob + 3 * n;
     // c1' = sigma_g(c1) is read through the automorphism by the key switch; c0' by its epilogue
     KsSrc xin{nullptr, 0, d_src, (u64)L * N, d_g};
     KsSrc c0p{nullptr, 0, d_src, 0, d_g};
