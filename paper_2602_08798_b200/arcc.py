@@ -518,7 +518,10 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
                 pieces.append(C.w_rotate(kcols.take(items_c[nz]), items_r[nz]))
             order = np.concatenate([z, nz])
             kr = type(kcols).concat(pieces).take(np.argsort(order))
-            prods = C.w_mult_cipher(Qw.take(items_c), kr)
+            # Q's columns recur for every row shift: the resident operand (mult_cipher is
+            # symmetric word for word -- (a0 b0, a0 b1 + a1 b0, a1 b1) -- and both operands
+            # belong to the head's context)
+            prods = C.w_mult_cipher(kr, Qw.take(items_c), resident_b=True)
             acc = C.w_sum(prods, [np.arange(i * d2, (i + 1) * d2) for i in range(rs.size)])
             diag_shares.extend(he_to_shares_wave(acc, [mpc] * rs.size, [m] * rs.size))
         # client: rebuild S from its diagonals, causal softmax per row
@@ -545,7 +548,7 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
             cs = np.arange(c0_, min(d2, c0_ + cols_per))
             it_c = np.repeat(cs, m)
             it_i = np.tile(np.arange(m), cs.size)
-            prods = C.w_mult_cipher(a_rows.take(it_i), Vw.take(it_c))
+            prods = C.w_mult_cipher(a_rows.take(it_i), Vw.take(it_c), resident_b=True)
             tot = fold_wave(prods, n)
             pieces = C.w_mult_plain(tot, _onehots(n, it_i))
             acc = C.w_sum(pieces, [np.arange(k * m, (k + 1) * m) for k in range(cs.size)])
