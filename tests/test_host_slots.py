@@ -72,3 +72,21 @@ def test_softmax_rows_equals_per_row():
                 S = rng.integers(-4 * scale, 4 * scale, (12, n))
                 ref = np.stack([attention_weights(S[h], 64, fp) for h in range(12)])
                 assert (attention_weights_rows(S, 64, fp) == ref).all()
+
+
+@pytest.mark.parametrize("groups", [2, 3])
+def test_interleaved_head_groups_equal_one_schedule(api, groups):
+    """attention_step_heads with the heads as interleaved groups (one group's client
+    round trip overlapping the next group's device work) charges and returns exactly
+    what the single schedule does: outputs, ids, budgets, counters, transcripts."""
+    from paper_2602_08798_b200 import arcc
+
+    def run(g):
+        root, fp, ctxs, caches, qs, chans = harness.attention_heads(api, slot_ctx, 64, harness.P64, 4, 6, 5, 6,
+                                                                    seed=3)
+        outs = arcc.attention_step_heads(qs, caches, fp, ctxs, chans, groups=g)
+        return ([np.asarray(o.slots).tolist() for o in outs], [o.id % harness.ID_BASE for o in outs], [o.noise_budget for o in outs],
+                [c.counter.as_dict() for c in ctxs], [ch.transcript for ch in chans],
+                [ch.sample_mask(4).tolist() for ch in chans])
+
+    assert run(1) == run(groups)
