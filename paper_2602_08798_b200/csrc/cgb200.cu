@@ -918,6 +918,9 @@ struct MdEpi {
 #ifndef CGB_KSROW_EPF
 #define CGB_KSROW_EPF 0  // MODE 2: epilogue operands prefetched (cp.async) into the exchange tile: measured slower
 #endif
+#ifndef CGB_KSROW_PF
+#define CGB_KSROW_PF 0  // L2 prefetch of the next tile / gathered blocks: measured slower
+#endif
 #ifndef CGB_KSROW_FPC
 #define CGB_KSROW_FPC 1  // MODE 2: the ModDown combine on the FP64 pipe
 #endif
@@ -1005,11 +1008,38 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
   const u64 *K = keys[item];
+  // L2 prefetch of what the NEXT step of this CTA reads (no registers held): the next
+  // digit's row tile (one 128-byte line per thread), the own digit's gathered blocks,
+  // or (MODE 2) the W tiles
+  auto prefetch_next = [&](int j) {  // called while digit j (or W tile j - L) is processed
+#if CGB_KSROW_PF
+    const int nd = l == L ? L : L - 1;
+    if (j + 1 < L && j + 1 == l) {
+      const u64 gi = xin.g ? xin.g[item] : 1;
+      const u64 *p = xin.items ? xin.items[item] + xin.off + ((u64)l << LOGN)
+                               : xin.base + (u64)item * xin.stride + ((u64)l << LOGN);
+#pragma unroll
+      for (int u = 0; u < PB::R; u++) {
+        const u32 k0 = (u32)(row0 + PB::idx(tl, u, 0));
+        prefetch_l2(p + (xin.items && xin.g ? (perm_g(k0, gi, LOGN) & ~7u) : k0));
+      }
+      return;
+    }
+    // index of the next tile in tile_src order
+    int t;
+    if (j + 1 < L) t = (l == L || j + 1 < l) ? j + 1 : j;  // digit j+1 (l skipped)
+    else t = nd + (j + 1 - L);                             // W tile
+    if (t < ntile) prefetch_l2(tile_src(t) + 16 * (u64)tid);
+#else
+    (void)j;
+#endif
+  };
   double a0[E], a1[E];
 #pragma unroll
   for (int i = 0; i < E; i++) a0[i] = a1[i] = 0.0;
 #pragma unroll 1
   for (int j = 0; j < L; j++) {
+    prefetch_next(j);
     double x[E];
     if (j == l) {  // the digit's own limb: the input itself, already in NTT form
 #if CGB_KSROW_G4
@@ -1062,6 +1092,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   if constexpr (MODE == 2) {  // ModDown: row pass of W[pp][l] (same forward twiddles), combine, store
 #pragma unroll 1
     for (int pp = 0; pp < 2; pp++) {
+      prefetch_next(L + pp);
       double x[E];
       load_tile(x);
       phase_regs_fp<LM, 0, RA, true, E, false, GT>(x, tw, tl, qd, qinv);

@@ -159,6 +159,8 @@ __device__ __forceinline__ u32 perm_g(u32 k, u64 g, int logN) {
   const u32 se = (u32)((e * g) & ((2ull << logN) - 1));
   return __brev((se - 1) >> 1) >> (32 - logN);
 }
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // Programmatic dependent launch: a kernel launched with the PDL attribute may
 // start while its predecessor drains; it stages constant tables (twiddles), then
 // waits for the predecessor's writes.  Without the attribute both are no-ops.
