@@ -27,7 +27,7 @@ import numpy as np
 
 from .backend import ParameterError, PlainBatch
 from .encodings import Encoding, EncodingKind, PackedMatrix, block_capacity, load_matrix, save_matrix
-from .nonlinear import MpcChannel
+from .nonlinear import MpcChannel, draw_masks
 
 __all__ = ["KVCache", "RefreshEvent", "append_token", "append_token_heads", "cache_stats", "init_cache",
            "load_cache", "maybe_refresh", "maybe_refresh_heads", "save_cache"]
@@ -208,9 +208,7 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     if not sel:
         return list(caches)
     # masks drawn per part in order from each head's channel
-    r = np.empty((len(sel), n), np.int64)
-    for k, (h, _, _, _) in enumerate(sel):
-        r[k] = chans[h].sample_mask(n)
+    r = draw_masks([chans[s[0]] for s in sel], n)
     owners = [ctxs[s[0]] for s in sel]
     start = {id(c): c._next_id for c in owners}
     wave = C.wave_of([s[3] for s in sel], owners)

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import collections
 import json
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -82,6 +83,36 @@ class MpcChannel:
         return json.dumps({"bytes_sent": self.bytes_sent, "rounds": self.rounds, "log": self.transcript}, indent=2)
 
 
+_POOL = None
+
+
+def draw_masks(chans, n: int) -> np.ndarray:
+    """rows[i] = chans[i].sample_mask(n), each channel's draws in item order (its
+    sequence is unchanged); distinct channels draw on parallel host threads (the
+    generator fill releases the GIL) when there is enough to draw."""
+    global _POOL
+    out = np.empty((len(chans), n), np.int64)
+    groups = {}
+    for i, ch in enumerate(chans):
+        groups.setdefault(id(ch), (ch, []))[1].append(i)
+
+    def fill(item):
+        ch, idx = item
+        for i in idx:
+            out[i] = ch.sample_mask(n)
+
+    if len(groups) > 1 and len(chans) * n >= (1 << 20):
+        if _POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            _POOL = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+        list(_POOL.map(fill, groups.values()))
+    else:
+        for item in groups.values():
+            fill(item)
+    return out
+
+
 def reconstruct(s: SharePair) -> np.ndarray:
     v = s.client + s.server
     if v.size and v.min() >= 0 and v.max() < 2 * s.p:  # both shares in [0, p): one conditional subtract
@@ -125,7 +156,7 @@ def he_to_shares_start(wave, chans, lengths):
     for L in lengths:
         if not 0 < L <= n:
             raise ParameterError(f"share length {L} out of range")
-    r = np.stack([ch.sample_mask(n) for ch in chans]) if len(chans) else np.zeros((0, n), np.int64)
+    r = draw_masks(chans, n)
     neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
     neg[neg == p] = 0
     masked = C.w_add_plain(wave, neg, one_shot=True)
