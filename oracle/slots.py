@@ -224,7 +224,7 @@ class SlotContext:
         return left
 
     @staticmethod
-    def w_encrypt(ctxs, vecs):
+    def w_encrypt(ctxs, vecs, canonical=False):
         uniq, owner = _owners(ctxs)
         p = uniq[0].params.plain_modulus
         w = SlotWave(uniq, owner, np.mod(np.asarray(vecs, np.int64), p),
@@ -255,7 +255,7 @@ class SlotContext:
                         SlotContext._charge(wa, "add"))
 
     @staticmethod
-    def w_add_plain(wave, vecs, one_shot=False):
+    def w_add_plain(wave, vecs, one_shot=False, canonical=False):
         if hasattr(vecs, "build"):
             vecs = vecs.build(vecs.keys)
         c = wave.ctxs[0]

@@ -639,10 +639,12 @@ class GpuContext:
         return Wave(wave.ctxs, wave.owner, aids, budgets, [block])
 
     @staticmethod
-    def w_encrypt(ctxs, vecs) -> Wave:
-        """Encrypt rows of ``vecs`` (item i by ctxs[i]); one nonce per item in order."""
+    def w_encrypt(ctxs, vecs, canonical: bool = False) -> Wave:
+        """Encrypt rows of ``vecs`` (item i by ctxs[i]); one nonce per item in order.
+        ``canonical``: the rows are residues in [0, t) by construction (shares,
+        decrypted slots), so the host range passes are skipped."""
         uniq, owner = _owners(ctxs)
-        vecs = np.ascontiguousarray(residues(vecs, uniq[0].params.plain_modulus))
+        vecs = np.ascontiguousarray(vecs if canonical else residues(vecs, uniq[0].params.plain_modulus))
         ring = uniq[0]._ring
         ids = ring.alloc(len(owner))
         blk = _Block(ring, ids)
@@ -654,7 +656,7 @@ class GpuContext:
             idx[sel] = c._enc_index + np.arange(sel.size, dtype=np.uint64)
             c._enc_index += sel.size
         keys = np.stack([np.asarray(c._enc_key, dtype=np.uint32).reshape(8) for c in uniq])[owner]
-        ring.encrypt_batch(vecs, keys, idx, ids)
+        ring.encrypt_batch(vecs, keys, idx, ids, canonical=True)
         w = Wave(uniq, owner, ids, np.full(len(owner), uniq[0].params.initial_noise_budget, np.int64), [blk])
         w.cids = GpuContext._charge(w, "encrypt")
         return w
@@ -696,12 +698,12 @@ class GpuContext:
         return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "add"))
 
     @staticmethod
-    def _plain_op(wave: Wave, vecs, kind, field_name, one_shot: bool = False):
+    def _plain_op(wave: Wave, vecs, kind, field_name, one_shot: bool = False, canonical: bool = False):
         c0 = wave.ctxs[0]
         cost = getattr(c0.params.noise_costs, field_name)
         b = GpuContext._spend_all(wave.budgets, cost)
         if not isinstance(vecs, PlainBatch):
-            vecs = residues(vecs, c0.params.plain_modulus)
+            vecs = np.asarray(vecs, dtype=np.int64) if canonical else residues(vecs, c0.params.plain_modulus)
             if vecs.ndim == 1:
                 vecs = np.broadcast_to(vecs, (len(wave), vecs.shape[0]))
         ring = c0._ring
@@ -712,7 +714,7 @@ class GpuContext:
             _pt_cache(ring).make_room(len(wave))
             pts = ring.alloc_pt(len(wave))
             try:
-                ring.encode_pt(vecs, kind, pts)
+                ring.encode_pt(vecs, kind, pts, canonical=True)
                 fn(wave.aids, pts, ids)
             finally:
                 ring.free_pt(pts)  # stream-ordered: later encodes run after this op
@@ -722,8 +724,8 @@ class GpuContext:
         return Wave(wave.ctxs, wave.owner, ids, b, [blk], GpuContext._charge(wave, field_name))
 
     @staticmethod
-    def w_add_plain(wave: Wave, vecs, one_shot: bool = False) -> Wave:
-        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain", one_shot)
+    def w_add_plain(wave: Wave, vecs, one_shot: bool = False, canonical: bool = False) -> Wave:
+        return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain", one_shot, canonical)
 
     @staticmethod
     def w_mult_plain(wave: Wave, vecs, one_shot: bool = False) -> Wave:

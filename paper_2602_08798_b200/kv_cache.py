@@ -214,13 +214,13 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     wave = C.wave_of([s[3] for s in sel], owners)
     neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
     neg[neg == p] = 0
-    masked = C.w_add_plain(wave, neg, one_shot=True)
+    masked = C.w_add_plain(wave, neg, one_shot=True, canonical=True)
     del neg
     view = C.w_decrypt(masked)
-    fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view)
+    fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view, canonical=True)
     for h, _, _, _ in sel:
         chans[h].transfer("refresh", n, trips=2)
-    restored = _retag(C.w_add_plain(fresh, r, one_shot=True).handles(), _chain_ids(owners, [3] * len(sel), start))
+    restored = _retag(C.w_add_plain(fresh, r, one_shot=True, canonical=True).handles(), _chain_ids(owners, [3] * len(sel), start))
     out = []
     for h, cache in enumerate(caches):
         mine = [(k, s) for k, s in enumerate(sel) if s[0] == h]

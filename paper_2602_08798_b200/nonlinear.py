@@ -159,7 +159,7 @@ def he_to_shares_start(wave, chans, lengths):
     r = draw_masks(chans, n)
     neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
     neg[neg == p] = 0
-    masked = C.w_add_plain(wave, neg, one_shot=True)
+    masked = C.w_add_plain(wave, neg, one_shot=True, canonical=True)
     return C, C.w_decrypt_start(masked), r, list(chans), lengths, n, p
 
 
@@ -188,8 +188,8 @@ def shares_to_he_wave(shares, ctxs, chans, record: bool = True):
             raise ParameterError("vector longer than slot count")
         client[i, : sh.client.shape[0]] = sh.client
         server[i, : sh.server.shape[0]] = sh.server
-    enc = C.w_encrypt(ctxs, client)
-    out = C.w_add_plain(enc, server, one_shot=True)
+    enc = C.w_encrypt(ctxs, client, canonical=True)
+    out = C.w_add_plain(enc, server, one_shot=True, canonical=True)
     if record:
         for ch in chans:
             ch.transfer("shares_to_he", n)

@@ -159,16 +159,18 @@ class Ring:
         nat.check(nat.lib().cgb_ct_load(self._h, ids.size, nat.u32ptr(ids), nat.u64ptr(w)), "cgb_ct_load")
 
     # plaintexts ------------------------------------------------------------
-    def _slots2d(self, slots) -> np.ndarray:
+    def _slots2d(self, slots, canonical: bool = False) -> np.ndarray:
         a = np.asarray(slots, dtype=np.int64)
         if a.ndim == 1:
             a = a.reshape(1, -1)
+        if canonical:  # the caller's residues are in [0, t) by construction: no range pass
+            return np.ascontiguousarray(a).view(np.uint64)
         if a.size and a.min() >= 0 and a.max() < self.t:  # already residues: zero-copy view
             return np.ascontiguousarray(a).view(np.uint64)
         return np.ascontiguousarray(np.mod(a, self.t).astype(np.uint64))
 
-    def encode_pt(self, slots, kind: int, ids):
-        s, ids = self._slots2d(slots), _ids(ids)
+    def encode_pt(self, slots, kind: int, ids, canonical: bool = False):
+        s, ids = self._slots2d(slots, canonical), _ids(ids)
         nat.check(nat.lib().cgb_pt_encode(self._h, ids.size, nat.u64ptr(s), kind, nat.u32ptr(ids)), "cgb_pt_encode")
         self.h2d_bytes += s.nbytes
 
@@ -180,9 +182,9 @@ class Ring:
                                         nat.u32ptr(ids)), "cgb_encrypt")
         self.h2d_bytes += s.nbytes
 
-    def encrypt_batch(self, slots, enc_keys, indices, ids):
+    def encrypt_batch(self, slots, enc_keys, indices, ids, canonical: bool = False):
         """Item i encrypted with key enc_keys[i] (8 words) at encryption index indices[i]."""
-        s, ids = self._slots2d(slots), _ids(ids)
+        s, ids = self._slots2d(slots, canonical), _ids(ids)
         k = np.ascontiguousarray(np.asarray(enc_keys, dtype=np.uint32).reshape(ids.size, 8))
         ix = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(ids.size))
         nat.check(nat.lib().cgb_encrypt_batch(self._h, ids.size, nat.u64ptr(s), nat.u32ptr(k), nat.u64ptr(ix),
