@@ -754,6 +754,13 @@ __global__ void k_key_shoup(u64 *dst, const u64 *src, const ModTab *mods, int L,
   u64 q = mods[l == L ? iP : l].q;
   dst[i] = (u64)((((unsigned __int128)src[i]) << 64) / q);
 }
+// the key's FP64 plane: every word as an exact double (k_ks_row's products read it
+// without a per-word integer -> double conversion)
+__global__ void k_key_fp(u64 *dst, const u64 *src, u64 words) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words) return;
+  dst[i] = (u64)__double_as_longlong(u2d(src[i]));
+}
 // ModDown lift: W[item][p][l][N] = centred(acc[item][p][L] (coeff, mod P)) mod q_l
 __global__ void k_moddown_lift(u64 *W, const u64 *acc, const ModTab *mods, int L, int iP, int logN) {
   int item = blockIdx.y;
@@ -1071,7 +1078,9 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
       phase_regs_fp<LM, RA, RB, true, E, true, GT>(x, tw, tl, qd, qinv);
     }
-    const u64 *k0 = K + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = K + ((u64)(j * 2 + 1) * LP + l) * N + row0;
+    // the key's FP64 plane (k_key_fp): exact doubles, no per-word conversion
+    const u64 *KF = K + 2 * (u64)L * 2 * LP * N;
+    const u64 *k0 = KF + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = KF + ((u64)(j * 2 + 1) * LP + l) * N + row0;
 #pragma unroll
     for (int u = 0; u < PB::R; u++)
 #pragma unroll
@@ -1083,7 +1092,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const double xv = x[u * PB::K + k + e];
-          const double d0 = u2d(w0[e]), d1 = u2d(w1[e]);
+          const double d0 = r2d(w0[e]), d1 = r2d(w1[e]);
           a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
           a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
         }
@@ -2639,7 +2648,7 @@ static u64 *get_key(cgb_ring *r, u64 g) {
   const int L = r->L, LP = L + 1, N = r->N;
   const u64 LPN = (u64)LP * N;
   u64 *key;
-  CK(cudaMalloc((void **)&key, 2 * sizeof(u64) * (size_t)L * 2 * LPN));  // values | Shoup companions
+  CK(cudaMalloc((void **)&key, 3 * sizeof(u64) * (size_t)L * 2 * LPN));  // values | Shoup companions | doubles
   Scratch S(r);
   std::vector<int> mi(LP);
   for (int l = 0; l < L; l++) mi[l] = l;
@@ -2668,6 +2677,7 @@ static u64 *get_key(cgb_ring *r, u64 g) {
   {
     const u64 words = (u64)L * 2 * LPN;
     LAUNCH("keygen", 0, k_key_shoup<<<GRID1(words, TPB), TPB, 0, r->stream>>>(key + words, key, r->d_mods, L, r->iP, r->logN, words));
+    LAUNCH("keygen", 0, k_key_fp<<<GRID1(words, TPB), TPB, 0, r->stream>>>(key + 2 * words, key, words));
   }
   r->keys[g] = key;
   return key;
