@@ -3381,14 +3381,20 @@ int cgb_decrypt_start(cgb_ring *r, int count, const uint32_t *cts, void **ticket
   auto *t = new DecTicket{nullptr, words, words, nullptr};
   *ticket_out = t;
   if (count <= 0) return CGB_OK;
+  size_t best = r->dec_pool.size();  // best fit: the smallest pooled buffer that holds the batch
   for (size_t i = 0; i < r->dec_pool.size(); i++)
-    if (r->dec_pool[i].first >= words) {
-      t->host = r->dec_pool[i].second;
-      t->cap = r->dec_pool[i].first;
-      r->dec_pool.erase(r->dec_pool.begin() + i);
-      break;
-    }
-  if (!t->host) CK(cudaMallocHost(&t->host, sizeof(u64) * words));
+    if (r->dec_pool[i].first >= words && (best == r->dec_pool.size() || r->dec_pool[i].first < r->dec_pool[best].first))
+      best = i;
+  if (best < r->dec_pool.size()) {
+    t->host = r->dec_pool[best].second;
+    t->cap = r->dec_pool[best].first;
+    r->dec_pool.erase(r->dec_pool.begin() + best);
+  } else {  // sizes rounded up to a power of two so buffers serve nearby batch sizes
+    size_t cap = 1;
+    while (cap < words) cap <<= 1;
+    CK(cudaMallocHost(&t->host, sizeof(u64) * cap));
+    t->cap = cap;
+  }
   decrypt_enqueue(r, count, cts, t->host);
   CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
   CK(cudaEventRecord(t->done, r->stream));
