@@ -925,6 +925,10 @@ struct MdEpi {
 #ifndef CGB_KSROW_EPF
 #define CGB_KSROW_EPF 0  // MODE 2: epilogue operands prefetched (cp.async) into the exchange tile: measured slower
 #endif
+#ifndef CGB_KSROW_TWW
+#define CGB_KSROW_TWW 0  // staged row twiddles as w only (w/q formed on use): half the shared memory
+#endif
+constexpr bool TWW = CGB_KSROW_TWW && !CGB_KSROW_GTW;
 #ifndef CGB_KSROW_PF
 #define CGB_KSROW_PF 0  // L2 prefetch of the next tile / gathered blocks: measured slower
 #endif
@@ -974,7 +978,21 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   const double2 *tw = reinterpret_cast<const double2 *>(Md.ftw1t) + row0;
 #else
   // the tile's row twiddles (same for every digit) staged once: rows of M + 1 pairs
+  // (TWW: rows of M + 1 doubles, the w/q halves formed on use -- half the shared memory)
   constexpr bool GT = false;
+#if CGB_KSROW_TWW
+  double *twd = reinterpret_cast<double *>(sm3 + ksr_data_words(LM));
+  auto stage_tw = [&](const u64 *table) {
+    const double2 *gt = reinterpret_cast<const double2 *>(table) + ((u64)first << LM);
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      const int e = tid + i * (NTT2_TILE / E);
+      twd[e + (e >> LM)] = __ldg(gt + e).x;
+    }
+  };
+  stage_tw(Md.ftw1t);
+  const double2 *tw = reinterpret_cast<const double2 *>(twd + g * (M + 1));
+#else
   double2 *tws = reinterpret_cast<double2 *>(sm3 + ksr_data_words(LM));
   auto stage_tw = [&](const u64 *table) {
     const double2 *gt = reinterpret_cast<const double2 *>(table) + ((u64)first << LM);
@@ -986,6 +1004,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   };
   stage_tw(Md.ftw1t);
   const double2 *tw = tws + g * (M + 1);
+#endif
 #endif
   // row tiles this CTA reads, in order: D(j, l) for the digits j != l, then (MODE 2) W(0, l), W(1, l)
   constexpr int NT_MAX = L + 2;
@@ -1068,7 +1087,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #endif
     } else {
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, GT>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
       __syncthreads();
@@ -1076,7 +1095,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
-      phase_regs_fp<LM, RA, RB, true, E, true, GT>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
     }
     // the key's FP64 plane (k_key_fp): exact doubles, no per-word conversion
     const u64 *KF = K + 2 * (u64)L * 2 * LP * N;
@@ -1104,7 +1123,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       prefetch_next(L + pp);
       double x[E];
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, GT>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
       __syncthreads();
@@ -1124,7 +1143,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
         for (int k = 0; k < PB::K; k += 4) epi.prefetch4(item, pp * L + l, row0 + PB::idx(tl, u, k), stg + u * PB::K + k);
       cp_async_commit();
 #endif
-      phase_regs_fp<LM, RA, RB, true, E, true, GT>(x, tw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
 #if CGB_KSROW_EPF
       cp_async_wait_all();
 #endif
@@ -1167,7 +1186,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
       for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
       __syncthreads();  // inverse twiddles staged / previous poly's reads done
-      phase_regs_fp<LM, RA, RB, false, E, true, GT>(y, itw, tl, qd, qinv);
+      phase_regs_fp<LM, RA, RB, false, E, true, GT, TWW>(y, itw, tl, qd, qinv);
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
@@ -1176,7 +1195,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
-      phase_regs_fp<LM, 0, RA, false, E, false, GT>(y, itw, tl, qd, qinv);
+      phase_regs_fp<LM, 0, RA, false, E, false, GT, TWW>(y, itw, tl, qd, qinv);
       u64 *o = pp ? o1 : o0;
 #pragma unroll
       for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (raw & 2) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
@@ -1343,7 +1362,8 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
 
 template <int LA, int LB>
 static size_t ks_row_smem() {  // exchange tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
-  return sizeof(u64) * (size_t)ksr_data_words(LB) + (CGB_KSROW_GTW ? 0 : 16 * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)));
+  return sizeof(u64) * (size_t)ksr_data_words(LB) +
+         (CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 8 : 16) * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)));
 }
 template <int LA, int LB, int L>
 static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in

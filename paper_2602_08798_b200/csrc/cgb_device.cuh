@@ -705,7 +705,8 @@ struct PhaseShape {
 // ([j][blk] instead of [blk][j], see k_ntt2_fpr) so threads on consecutive
 // blocks read consecutive entries.
 // GTW: tws is a global table (read through the read-only path) instead of shared memory
-template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false>
+// WQ: tws holds the twiddles' w only (doubles); w/q is formed by one DMUL per use
+template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false, bool WQ = false>
 __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, int tl, double q, double qinv) {
   using PS = PhaseShape<LM, S0, RP, E>;
   constexpr int K = PS::K, R = PS::R;
@@ -723,7 +724,12 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
         if ((k & ((1 << (RP - l)) - 1)) == 0) {
           const int ti = TRANS ? (1 << (S0 + l)) + ((k >> (RP - l)) << S0) + blk
                                : (1 << (S0 + l)) + (blk << l) + (k >> (RP - l));
-          W = GTW ? __ldg(tws + ti) : tws[ti];
+          if constexpr (WQ) {
+            const double w = reinterpret_cast<const double *>(tws)[ti];
+            W = make_double2(w, w * qinv);
+          } else {
+            W = GTW ? __ldg(tws + ti) : tws[ti];
+          }
         }
         double &X = x[u * K + k], &Y = x[u * K + k + half];
         if (FWD) {
