@@ -20,15 +20,24 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, "/root/reference/pkg/src")
 
-N, P = 64, 67109633  # harness.P64
-PROMPT = [5, 17, 3, 60, 22, 9]
-STEPS = 3
+# name -> (n_slots, plain modulus, model config or None for the toy config, prompt, steps)
+CASES = {
+    "layer_toy": (64, 67109633, None, [5, 17, 3, 60, 22, 9], 3),  # harness.P64
+    # the production ring (n = 8192, p = 536903681 -> N = 16384, FP64-pipe kernels)
+    "layer_n8192": (8192, 536903681, dict(layers=1, d1=128, heads=2, ffn_dim=256, vocab=512, max_seq=64, f=8),
+                    [7, 300, 41, 511, 2, 96, 180, 33], 2),
+}
 
 
 def main():
+    for name, case in CASES.items():
+        record(name, *case)
+
+
+def record(name, N, P, cfg_kw, PROMPT, STEPS):
     from cryptogen import backend, kv_cache, model as M
 
-    cfg = M.toy_config()
+    cfg = M.toy_config() if cfg_kw is None else M.ModelConfig(**cfg_kw)
     mdl = M.generate_toy_model(cfg, seed=0)
     ctx = backend.new_context(backend.BackendParams(n_slots=N, plain_modulus=P), 0)
     chans = M._channels(0, cfg.layers, cfg.heads, P)
@@ -47,8 +56,8 @@ def main():
     rec.update(config=json.dumps(cfg.as_dict()), prompt=np.array(PROMPT), tokens=np.array(tokens),
                logits=np.stack(logits), counters=json.dumps(ctx.counter.as_dict(), sort_keys=True),
                mpc_bytes=np.int64(sum(ch.bytes_sent for ch in chans.values())), n=N, p=P)
-    np.savez_compressed(HERE / "layer_toy.npz", **rec)
-    print("tokens", tokens, "counters", ctx.counter.as_dict())
+    np.savez_compressed(HERE / f"{name}.npz", **rec)
+    print(name, "tokens", tokens, "counters", ctx.counter.as_dict())
 
 
 if __name__ == "__main__":

@@ -1,7 +1,9 @@
 """Decoder-layer pipeline (paper_2602_08798_b200.model, BASELINE config 3) vs the
-reference's own encrypted pipeline: golden tests/golden/layer_toy.npz recorded
-by tests/golden/make_layer_golden.py (reference toy model, 2 layers, 4 heads,
-prompt 6, 3 greedy steps, every cache part force-refreshed before each step).
+reference's own encrypted pipeline: goldens recorded by
+tests/golden/make_layer_golden.py -- the reference's toy model (2 layers, 4
+heads, n = 64, prompt 6, 3 greedy steps) and a 1-layer model (d1 128, 2 heads,
+d_ff 256, vocab 512) on the production ring n = 8192 (prompt 8, 2 steps), every
+cache part force-refreshed before each step.
 Tokens, every step's logits, op counters and MPC byte totals must be equal."""
 import json
 from pathlib import Path
@@ -11,14 +13,15 @@ import pytest
 
 from conftest import gpu_available
 
-GOLD = Path(__file__).resolve().parent / "golden" / "layer_toy.npz"
+GOLDS = Path(__file__).resolve().parent / "golden"
+CASES = ["layer_toy", "layer_n8192"]  # n = 64 toy model; 1 layer on the production ring (n = 8192)
 
 
-def _run(make_ctx):
+def _run(make_ctx, case="layer_toy"):
     from paper_2602_08798_b200 import model as M
     from paper_2602_08798_b200.backend import BackendParams
 
-    g = np.load(GOLD)
+    g = np.load(GOLDS / f"{case}.npz")
     cfg = M.ModelConfig(**json.loads(str(g["config"])))
     mdl = M.Model(cfg, {k[2:]: g[k] for k in g.files if k.startswith("w_")})
     p = int(g["p"])
@@ -37,20 +40,22 @@ def _run(make_ctx):
     return ctx, state
 
 
-def test_layer_pipeline_on_slot_oracle():
+@pytest.mark.parametrize("case", CASES)
+def test_layer_pipeline_on_slot_oracle(case):
     from oracle.slots import SlotContext
 
-    _run(SlotContext)
+    _run(SlotContext, case)
 
 
 @pytest.mark.gpu
-def test_layer_pipeline_on_gpu():
+@pytest.mark.parametrize("case", CASES)
+def test_layer_pipeline_on_gpu(case):
     assert gpu_available()
     from paper_2602_08798_b200._native import build
     from paper_2602_08798_b200.backend import GpuContext
 
     build()
-    ctx, state = _run(GpuContext)
+    ctx, state = _run(GpuContext, case)
     assert all(c.noise_budget > 0 for cache in state.caches[0] for c in cache.prefill_K.parts)
 
 
