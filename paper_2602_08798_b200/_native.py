@@ -88,6 +88,7 @@ SIGNATURES = {
     "cgb_decrypt": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p]),
     "cgb_decrypt_start": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, ctypes.POINTER(_vp)]),
     "cgb_decrypt_finish": (ctypes.c_int, [_vp, _vp, _u64p]),
+    "cgb_decrypt_start_into": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p, ctypes.POINTER(_vp)]),
     "cgb_noise_budget": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _dblp]),
     "cgb_add": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),
     "cgb_add_plain": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p]),

@@ -3420,6 +3420,18 @@ int cgb_decrypt_start(cgb_ring *r, int count, const uint32_t *cts, void **ticket
   CK(cudaEventRecord(t->done, r->stream));
   API_END
 }
+// the same, landing straight in the caller's page-locked buffer (no copy at finish)
+int cgb_decrypt_start_into(cgb_ring *r, int count, const uint32_t *cts, uint64_t *pinned_dst, void **ticket_out) {
+  API_BEGIN
+  const size_t words = (size_t)(count > 0 ? count : 0) * r->n_slots;
+  auto *t = new DecTicket{pinned_dst, words, 0, nullptr};  // cap 0: not a pooled buffer
+  *ticket_out = t;
+  if (count <= 0) return CGB_OK;
+  decrypt_enqueue(r, count, cts, pinned_dst);
+  CK(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->done, r->stream));
+  API_END
+}
 int cgb_decrypt_finish(cgb_ring *r, void *ticket, uint64_t *slots_out) {
   API_BEGIN
   (void)r;
@@ -3427,9 +3439,9 @@ int cgb_decrypt_finish(cgb_ring *r, void *ticket, uint64_t *slots_out) {
   if (!t) FAIL(CGB_ERR_PARAM, "null decryption ticket");
   if (t->words) {
     CK(cudaEventSynchronize(t->done));
-    std::memcpy(slots_out, t->host, sizeof(u64) * t->words);
+    if (slots_out && slots_out != t->host) std::memcpy(slots_out, t->host, sizeof(u64) * t->words);
     cudaEventDestroy(t->done);
-    r->dec_pool.push_back({t->cap, t->host});
+    if (t->cap) r->dec_pool.push_back({t->cap, t->host});
   }
   delete t;
   API_END

@@ -27,7 +27,7 @@ import numpy as np
 
 from .backend import ParameterError, PlainBatch
 from .encodings import Encoding, EncodingKind, PackedMatrix, block_capacity, load_matrix, save_matrix
-from .nonlinear import MpcChannel, draw_masks
+from .nonlinear import MpcChannel, draw_masks, neg_mod
 
 __all__ = ["KVCache", "RefreshEvent", "append_token", "append_token_heads", "cache_stats", "init_cache",
            "load_cache", "maybe_refresh", "maybe_refresh_heads", "save_cache"]
@@ -212,10 +212,7 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     owners = [ctxs[s[0]] for s in sel]
     start = {id(c): c._next_id for c in owners}
     wave = C.wave_of([s[3] for s in sel], owners)
-    neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
-    neg[neg == p] = 0
-    masked = C.w_add_plain(wave, neg, one_shot=True, canonical=True)
-    del neg
+    masked = C.w_add_plain(wave, neg_mod(r, p), one_shot=True, canonical=True)
     view = C.w_decrypt(masked)
     fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view, canonical=True)
     for h, _, _, _ in sel:

@@ -84,6 +84,33 @@ class MpcChannel:
 
 
 _POOL = None
+_PINNED = None
+
+
+def host_buffer(shape) -> np.ndarray:
+    """An int64 host array, page-locked when a CUDA device is present (so its
+    upload is a DMA, not a driver-staged copy); plain numpy otherwise."""
+    global _PINNED
+    if _PINNED is None:
+        try:
+            import torch
+
+            _PINNED = bool(torch.cuda.is_available())
+        except Exception:  # pragma: no cover - torch is part of the image
+            _PINNED = False
+    if _PINNED and int(np.prod(shape)) >= (1 << 16):
+        import torch
+
+        return torch.empty(tuple(shape), dtype=torch.int64, pin_memory=True).numpy()
+    return np.empty(shape, np.int64)
+
+
+def neg_mod(r: np.ndarray, p: int) -> np.ndarray:
+    """(-r) mod p for r in [0, p), without an integer modulo, into a host buffer."""
+    out = host_buffer(r.shape)
+    np.subtract(p, r, out=out)
+    out[out == p] = 0
+    return out
 
 
 def draw_masks(chans, n: int) -> np.ndarray:
@@ -91,7 +118,7 @@ def draw_masks(chans, n: int) -> np.ndarray:
     sequence is unchanged); distinct channels draw on parallel host threads (the
     generator fill releases the GIL) when there is enough to draw."""
     global _POOL
-    out = np.empty((len(chans), n), np.int64)
+    out = host_buffer((len(chans), n))
     groups = {}
     for i, ch in enumerate(chans):
         groups.setdefault(id(ch), (ch, []))[1].append(i)
@@ -157,9 +184,7 @@ def he_to_shares_start(wave, chans, lengths):
         if not 0 < L <= n:
             raise ParameterError(f"share length {L} out of range")
     r = draw_masks(chans, n)
-    neg = p - r  # r in [0, p): (-r) mod p without an integer modulo
-    neg[neg == p] = 0
-    masked = C.w_add_plain(wave, neg, one_shot=True, canonical=True)
+    masked = C.w_add_plain(wave, neg_mod(r, p), one_shot=True, canonical=True)
     return C, C.w_decrypt_start(masked), r, list(chans), lengths, n, p
 
 

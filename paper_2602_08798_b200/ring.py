@@ -199,20 +199,24 @@ class Ring:
         return out.view(np.int64)  # residues < t < 2^63: the same values, no copy
 
     def decrypt_start(self, ids):
-        """Enqueue a decryption (and its device->host copy); returns a ticket for
-        decrypt_finish.  Only that ticket is waited for."""
+        """Enqueue a decryption (and its device->host copy straight into a
+        page-locked array); returns a ticket for decrypt_finish.  Only that ticket
+        is waited for."""
+        import torch  # page-locked host memory (torch's caching host allocator)
+
         ids = _ids(ids)
+        out = torch.empty((ids.size, self.n_slots), dtype=torch.int64, pin_memory=True).numpy()
         t = ctypes.c_void_p()
-        nat.check(nat.lib().cgb_decrypt_start(self._h, ids.size, nat.u32ptr(ids), ctypes.byref(t)),
-                  "cgb_decrypt_start")
-        return t, ids.size
+        nat.check(nat.lib().cgb_decrypt_start_into(self._h, ids.size, nat.u32ptr(ids),
+                                                   out.ctypes.data_as(nat._u64p), ctypes.byref(t)),
+                  "cgb_decrypt_start_into")
+        return t, out
 
     def decrypt_finish(self, ticket) -> np.ndarray:
-        t, n = ticket
-        out = np.zeros((n, self.n_slots), dtype=np.uint64)
-        nat.check(nat.lib().cgb_decrypt_finish(self._h, t, nat.u64ptr(out)), "cgb_decrypt_finish")
+        t, out = ticket
+        nat.check(nat.lib().cgb_decrypt_finish(self._h, t, None), "cgb_decrypt_finish")
         self.d2h_bytes += out.nbytes
-        return out.view(np.int64)
+        return out  # residues < t < 2^63 as int64, page-locked (later uploads are DMA)
 
     def noise_budget(self, ids) -> np.ndarray:
         ids = _ids(ids)
