@@ -126,8 +126,10 @@ int cgb_decrypt(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *slots_
    (Context.decrypt semantics per ciphertext are unchanged). */
 int cgb_decrypt_start(cgb_ring *ring, int count, const uint32_t *cts, void **ticket_out);
 int cgb_decrypt_finish(cgb_ring *ring, void *ticket, uint64_t *slots_out);
-/* cgb_decrypt_start landing in the caller's page-locked count x n_slots buffer, which
-   must stay valid until cgb_decrypt_finish(ring, ticket, NULL or that buffer) */
+/* cgb_decrypt_start landing in the caller's count x n_slots buffer, which must stay
+   valid until cgb_decrypt_finish(ring, ticket, NULL or that buffer); page-locked for
+   the copy to stay asynchronous (a pageable buffer works, the call then returns after
+   the copy) */
 int cgb_decrypt_start_into(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *pinned_dst, void **ticket_out);
 /* client-side diagnostic: invariant noise budget in bits of each ciphertext */
 int cgb_noise_budget(cgb_ring *ring, int count, const uint32_t *cts, double *bits_out);

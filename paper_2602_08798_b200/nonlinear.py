@@ -87,6 +87,13 @@ _POOL = None
 _PINNED = None
 
 
+# page-locked buffers up to 128 MB: the per-step round trips (a decode step's forced
+# refresh moves 100 MB each way) reuse them from torch's caching host allocator;
+# larger one-off batches (a prefill's 3072-column round trips) stay pageable, where
+# allocating fresh page-locked memory would cost more than the copies it saves
+PINNED_MAX_WORDS = 16 << 20
+
+
 def host_buffer(shape) -> np.ndarray:
     """An int64 host array, page-locked when a CUDA device is present (so its
     upload is a DMA, not a driver-staged copy); plain numpy otherwise."""
@@ -98,7 +105,7 @@ def host_buffer(shape) -> np.ndarray:
             _PINNED = bool(torch.cuda.is_available())
         except Exception:  # pragma: no cover - torch is part of the image
             _PINNED = False
-    if _PINNED and int(np.prod(shape)) >= (1 << 16):
+    if _PINNED and (1 << 16) <= int(np.prod(shape)) <= PINNED_MAX_WORDS:
         import torch
 
         return torch.empty(tuple(shape), dtype=torch.int64, pin_memory=True).numpy()

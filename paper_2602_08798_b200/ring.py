@@ -202,10 +202,10 @@ class Ring:
         """Enqueue a decryption (and its device->host copy straight into a
         page-locked array); returns a ticket for decrypt_finish.  Only that ticket
         is waited for."""
-        import torch  # page-locked host memory (torch's caching host allocator)
+        from .nonlinear import host_buffer  # page-locked up to 128 MB (torch's caching host allocator)
 
         ids = _ids(ids)
-        out = torch.empty((ids.size, self.n_slots), dtype=torch.int64, pin_memory=True).numpy()
+        out = host_buffer((ids.size, self.n_slots))
         t = ctypes.c_void_p()
         nat.check(nat.lib().cgb_decrypt_start_into(self._h, ids.size, nat.u32ptr(ids),
                                                    out.ctypes.data_as(nat._u64p), ctypes.byref(t)),
