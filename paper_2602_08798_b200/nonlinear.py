@@ -91,7 +91,7 @@ _PINNED = None
 # refresh moves 100 MB each way) reuse them from torch's caching host allocator;
 # larger one-off batches (a prefill's 3072-column round trips) stay pageable, where
 # allocating fresh page-locked memory would cost more than the copies it saves
-PINNED_MAX_WORDS = 16 << 20
+PINNED_MAX_WORDS = int(os.environ.get("CGB_PINNED_MAX_MB", "128")) << 17
 
 
 def host_buffer(shape) -> np.ndarray:
