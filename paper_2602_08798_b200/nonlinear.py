@@ -94,7 +94,7 @@ _PINNED = None
 PINNED_MAX_WORDS = int(os.environ.get("CGB_PINNED_MAX_MB", "128")) << 17
 
 
-def host_buffer(shape) -> np.ndarray:
+def host_buffer(shape, min_words: int = 1 << 16) -> np.ndarray:
     """An int64 host array, page-locked when a CUDA device is present (so its
     upload is a DMA, not a driver-staged copy); plain numpy otherwise."""
     global _PINNED
@@ -105,7 +105,7 @@ def host_buffer(shape) -> np.ndarray:
             _PINNED = bool(torch.cuda.is_available())
         except Exception:  # pragma: no cover - torch is part of the image
             _PINNED = False
-    if _PINNED and (1 << 16) <= int(np.prod(shape)) <= PINNED_MAX_WORDS:
+    if _PINNED and min_words <= int(np.prod(shape)) <= PINNED_MAX_WORDS:
         import torch
 
         return torch.empty(tuple(shape), dtype=torch.int64, pin_memory=True).numpy()

@@ -205,7 +205,9 @@ class Ring:
         from .nonlinear import host_buffer  # page-locked up to 128 MB (torch's caching host allocator)
 
         ids = _ids(ids)
-        out = host_buffer((ids.size, self.n_slots))
+        # always page-locked when it fits: a copy into pageable memory would make this
+        # call wait for everything queued before it
+        out = host_buffer((ids.size, self.n_slots), min_words=0)
         t = ctypes.c_void_p()
         nat.check(nat.lib().cgb_decrypt_start_into(self._h, ids.size, nat.u32ptr(ids),
                                                    out.ctypes.data_as(nat._u64p), ctypes.byref(t)),
