@@ -259,6 +259,13 @@ def run_layer(args):
     t_all = time.perf_counter() - t0
     pre_ms = ev[0].elapsed_time(ev[1])
     step_ms = [ev[i + 1].elapsed_time(ev[i + 2]) for i in range(args.steps)]
+    # one more step outside the timed ones with CUDA events around every launch
+    ring.timing(True)
+    M.decode_step(mdl, state, ctx, chans, force_refresh=True)
+    torch.cuda.synchronize()
+    rep = ring.timing_report()
+    ring.timing(False)
+    kern = {k: {"launches": v[0], "ms": round(v[1], 3)} for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])}
     line = {"metric": f"HE decoder-layer decode ms/token (GPT-2 small layer, prompt {args.L}, "
                       f"{args.steps} tokens, refresh each step)",
             "value": float(np.mean(step_ms)), "unit": "ms/token", "higher_is_better": False, "n_gpus": 1,
@@ -269,7 +276,8 @@ def run_layer(args):
             "prefill_ms": pre_ms, "decode_ms_per_token": step_ms,
             "wall_s": {"prefill": t_pre, "total": t_all},
             "gpu_launches": {"prefill": int(l1 - l0), "decode_per_token": int((ring.launches() - l1) / args.steps)},
-            "tokens": toks, "counters": ctx.counter.as_dict()}
+            "tokens": toks, "counters": ctx.counter.as_dict(),
+            "kernels_one_step": kern}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = layer_cpu_baseline(args)
     print(json.dumps(line), flush=True)

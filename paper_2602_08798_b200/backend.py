@@ -326,6 +326,15 @@ SlotCiphertext = GpuCiphertext
 # waves: batches of ciphertexts processed by one launch sequence
 # ----------------------------------------------------------------------------
 EXT_B = os.environ.get("CGB_EXT_B", "1") != "0"  # resident base-B extensions of KV cache parts
+_ROT_DEDUP = os.environ.get("CGB_ROT_DEDUP", "1") != "0"  # one key switch per (content class, step)
+
+
+_class_counter = itertools.count(1)
+
+
+def _fresh_classes(k: int) -> np.ndarray:
+    """k content classes never issued before (positive; wave_of's aid classes are negative)."""
+    return np.fromiter((next(_class_counter) for _ in range(k)), dtype=np.int64, count=k)
 
 
 class Wave:
@@ -337,18 +346,23 @@ class Wave:
     (``cids``) are charged to the owning context exactly as the per-op
     path would charge them."""
 
-    __slots__ = ("ctxs", "owner", "aids", "budgets", "blocks", "cids")
+    __slots__ = ("ctxs", "owner", "aids", "budgets", "blocks", "cids", "klass")
 
-    def __init__(self, ctxs, owner, aids, budgets, blocks, cids=None):
+    def __init__(self, ctxs, owner, aids, budgets, blocks, cids=None, klass=None):
         self.ctxs, self.owner, self.aids, self.budgets, self.blocks = ctxs, owner, aids, budgets, blocks
         self.cids = np.zeros(len(aids), np.int64) if cids is None else cids
+        # content classes: items with equal klass hold the same ciphertext words
+        # (copies of one input, or one rotation of such copies); None = all distinct.
+        # w_rotate computes one key switch per (class, step) and copies the rest.
+        self.klass = klass
 
     def __len__(self):
         return int(self.aids.size)
 
     def take(self, idx) -> "Wave":
         idx = np.asarray(idx, dtype=np.int64).reshape(-1)
-        return Wave(self.ctxs, self.owner[idx], self.aids[idx], self.budgets[idx], self.blocks, self.cids[idx])
+        return Wave(self.ctxs, self.owner[idx], self.aids[idx], self.budgets[idx], self.blocks, self.cids[idx],
+                    None if self.klass is None else self.klass[idx])
 
     @staticmethod
     def concat(waves: Sequence["Wave"]) -> "Wave":
@@ -358,8 +372,12 @@ class Wave:
             ctxs.extend(w.ctxs)
             owners.append(w.owner + base)
         blocks = [b for w in waves for b in w.blocks]
+        klass = None
+        if any(w.klass is not None for w in waves):
+            klass = np.concatenate([w.klass if w.klass is not None else _fresh_classes(len(w)) for w in waves])
         return Wave(ctxs, np.concatenate(owners), np.concatenate([w.aids for w in waves]),
-                    np.concatenate([w.budgets for w in waves]), blocks, np.concatenate([w.cids for w in waves]))
+                    np.concatenate([w.budgets for w in waves]), blocks, np.concatenate([w.cids for w in waves]),
+                    klass)
 
     def handles(self) -> list:
         keep = self.blocks[0] if len(self.blocks) == 1 else _Keep(self.blocks)
@@ -600,11 +618,13 @@ class GpuContext:
         aids = np.array([c._aid for c in cts], dtype=np.uint32)
         budgets = np.array([c.noise_budget for c in cts], dtype=np.int64)
         cids = np.array([c.id for c in cts], dtype=np.int64)
-        return Wave(ctxs, owner, aids, budgets, [c._block for c in cts], cids)
+        # one live arena id is one ciphertext: repeated handles share a content class
+        klass = -(aids.astype(np.int64) + 1) if len(set(aids.tolist())) < len(aids) else None
+        return Wave(ctxs, owner, aids, budgets, [c._block for c in cts], cids, klass)
 
     @staticmethod
     def bind(wave: Wave, ctx) -> Wave:
-        return Wave([ctx], np.zeros(len(wave), np.int64), wave.aids, wave.budgets, wave.blocks, wave.cids)
+        return Wave([ctx], np.zeros(len(wave), np.int64), wave.aids, wave.budgets, wave.blocks, wave.cids, wave.klass)
 
     # -- wave primitives: each charges counters/ids to the owning contexts exactly
     # -- as the equivalent sequence of per-op calls would
@@ -756,13 +776,32 @@ class GpuContext:
         rb = GpuContext._spend_all(wave.budgets, costs.rotate)
         b = GpuContext._spend_all(np.minimum(wave.budgets, rb), costs.add) if add_input else rb
         blk, ids = c0._new(len(wave))
-        _rotate_ids(c0._ring, c0.params, wave.aids, st, ids, add_input)
+        klass = None
+        if wave.klass is not None and _ROT_DEDUP:
+            # one key switch per distinct (content class, step); the other items are
+            # copies of its result -- the same words their own key switch would give
+            pairs = {}
+            lead = np.empty(len(wave), np.int64)
+            for i, key in enumerate(zip(wave.klass.tolist(), st.tolist())):
+                lead[i] = pairs.setdefault(key, i)
+            first = np.flatnonzero(lead == np.arange(len(wave)))
+            _rotate_ids(c0._ring, c0.params, wave.aids[first], st[first], ids[first], add_input)
+            dup = np.flatnonzero(lead != np.arange(len(wave)))
+            if dup.size:
+                c0._ring.copy(ids[lead[dup]], ids[dup])
+            fresh = _fresh_classes(first.size)
+            cls = np.empty(len(wave), np.int64)
+            cls[first] = fresh
+            cls[dup] = cls[lead[dup]]
+            klass = cls if dup.size else None
+        else:
+            _rotate_ids(c0._ring, c0.params, wave.aids, st, ids, add_input)
         if add_input:
             GpuContext._charge(wave, "rotate", n_emit=0)
             cids = GpuContext._charge(wave, "add", n_emit=2)
         else:
             cids = GpuContext._charge(wave, "rotate")
-        return Wave(wave.ctxs, wave.owner, ids, b, [blk], cids)
+        return Wave(wave.ctxs, wave.owner, ids, b, [blk], cids, klass)
 
     @staticmethod
     def w_sum(wave: Wave, groups) -> Wave:

@@ -2461,6 +2461,195 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
   return true;
 }
 
+// Hoisted key switch: several Galois elements applied to ONE source (the CPVM
+// projections rotate one activation by every diagonal step, linear_kernels.py:105-142).
+// sigma_g permutes the NTT evaluation points and commutes with the digit
+// decomposition and the centred base extension (centred(q - x) = -centred(x), q odd),
+// so digit j of ModUp(sigma_g(c1)) is word perm_g(k) of digit j of ModUp(c1): the
+// ModUp (inverse row pass, lift + column passes, forward row pass) runs once per
+// source, each item only gathers its digits through perm_g and takes the key inner
+// product.  Every word is the same residue the per-item path computes.
+static bool g_ks_hoist = true;  // CGB_KS_HOIST
+template <int L>
+__global__ void __launch_bounds__(256) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
+                                                        const u64 *const *keys, const ModTab *mods, int iP, int logN) {
+  constexpr int LP = L + 1;
+  const u64 N = 1ull << logN;
+  const int item = blockIdx.y;
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
+  if (i >= LP * N) return;
+  const int l = (int)(i >> logN);
+  const u32 k = (u32)(i & (N - 1));
+  const ModTab &Md = mods[l == L ? iP : l];
+  const double qd = Md.qd, qinv = Md.qinv;
+  const u32 kk = perm_g(k, xin.g[item], logN);
+  const u64 *Du = D + (u64)srcidx[item] * L * LP * N + kk;
+  const u64 *own = xin.items[item] + xin.off + kk;
+  const u64 *KF = keys[item] + 2 * (u64)L * 2 * LP * N + i;  // the key's FP64 plane (k_key_fp)
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < L; j++) {
+    const double xv = u2d(l == j ? own[(u64)j << logN] : Du[((u64)j * LP + l) * N]);
+    const double d0 = r2d(__ldcs(KF + (u64)(j * 2 + 0) * LP * N)), d1 = r2d(__ldcs(KF + (u64)(j * 2 + 1) * LP * N));
+    a0 += fp_mulmod(xv, d0, d0 * qinv, qd);
+    a1 += fp_mulmod(xv, d1, d1 * qinv, qd);
+  }
+  acc[((u64)item * 2 + 0) * LP * N + i] = fp_canon(a0, qd, qinv);
+  acc[((u64)item * 2 + 1) * LP * N + i] = fp_canon(a1, qd, qinv);
+}
+template <int LA, int LB, int L>
+static void keyswitch_hoisted_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, int nu, u64 *const *d_usrc,
+                                const u32 *d_srcidx, u64 *const *d_keys, u64 *const *d_out, const KsSrc &add0,
+                                const u64 *const *d_add1) {
+  constexpr int LP = L + 1, N = 1 << (LA + LB), G1 = NTT2_TILE >> LB;
+  constexpr int RT = (1 << LA) / G1;  // row tiles per limb-poly
+  const size_t nxr = (size_t)nu * L * N, nD = (size_t)nu * L * LP * N, nacc = (size_t)count * 2 * LP * N;
+  u64 *xr = S.alloc<u64>(nxr + nD + nacc + (size_t)count * 2 * L * N);
+  u64 *D = xr + nxr, *acc = D + nD, *W = acc + nacc;
+  const size_t f1 = fpr_smem_bytes<LA, LB>(1);
+  {  // 1: inverse row pass of each source's c1 (no automorphism)
+    NttJob job{};
+    job.base = xr;
+    job.item_stride = (u64)L * N;
+    job.src_items = d_usrc;
+    const int off = (int)(x.off / (u64)N);
+    for (int l = 0; l < L; l++) {
+      job.sub_off[l] = (unsigned short)l;
+      job.sub_mod[l] = (unsigned char)l;
+      job.src_off[l] = (unsigned short)(off + l);
+    }
+    job.nsub = L;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    job.out_raw = 1;
+    launch_begin(r);
+    launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1>, dim3((unsigned)((size_t)nu * L * RT)), NTT2_TILE / 16, f1, job, NoEpi{});
+    launch_end(r, "ks_digit_rows", 16.0 * (double)nu * L * N, (double)nu * L * (N / 2) * LB);
+  }
+  {  // 2: inverse column pass + centred lift + forward column passes into the other limbs
+    ColJob cj{};
+    cj.src = xr;
+    cj.src_stride = (u64)L * N;
+    cj.dst = D;
+    cj.dst_stride = (u64)L * LP * N;
+    cj.nsrc = L;
+    cj.in_raw = cj.out_raw = 1;
+    for (int j = 0; j < L; j++) {
+      cj.src_off[j] = (unsigned short)j;
+      cj.src_mod[j] = (unsigned char)j;
+      int t = 0;
+      for (int l = 0; l < LP; l++) {
+        if (l == j) continue;
+        cj.dst_off[j][t] = (unsigned short)(j * LP + l);
+        cj.dst_mod[j][t] = (unsigned char)(l == L ? r->iP : l);
+        t++;
+      }
+    }
+    col_fused(r, cj, nu, L, "ks_modup_cols");
+  }
+  {  // 3: forward row pass of the L x L extended digits, in place -> canonical NTT words
+    NttJob job{};
+    job.base = D;
+    job.item_stride = (u64)L * LP * N;
+    int n = 0;
+    for (int j = 0; j < L; j++)
+      for (int l = 0; l < LP; l++) {
+        if (l == j) continue;
+        job.sub_off[n] = (unsigned short)(j * LP + l);
+        job.sub_mod[n] = (unsigned char)(l == L ? r->iP : l);
+        n++;
+      }
+    job.nsub = n;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    job.in_raw = 1;
+    launch_begin(r);
+    launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1>, dim3((unsigned)((size_t)nu * n * RT)), NTT2_TILE / 16, f1, job, NoEpi{});
+    launch_end(r, "ks_hoist_rows", 16.0 * (double)nu * n * N, (double)nu * n * (N / 2) * LB);
+  }
+  {  // 4: per item: digits gathered through perm_g, key inner product over Q u P
+    launch_begin(r);
+    k_ks_inner_hoist<L><<<dim3(GRID1((u64)LP * N, 256).x, count), 256, 0, r->stream>>>(acc, D, d_srcidx, x, d_keys,
+                                                                                      r->d_mods, r->iP, LA + LB);
+    launch_end(r, "ks_hoist_inner", 8.0 * (double)count * LP * N * (L + 2.0 * L + 2.0), 2.0 * count * L * LP * (double)N);
+  }
+  {  // 5: ModDown's inverse row pass of the P limb (both polys), in place
+    NttJob job{};
+    job.base = acc;
+    job.item_stride = 2ull * LP * N;
+    job.sub_off[0] = (unsigned short)L;
+    job.sub_off[1] = (unsigned short)(LP + L);
+    job.sub_mod[0] = job.sub_mod[1] = (unsigned char)r->iP;
+    job.nsub = 2;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    job.out_raw = 1;
+    launch_begin(r);
+    launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1>, dim3((unsigned)((size_t)count * 2 * RT)), NTT2_TILE / 16, f1, job,
+               NoEpi{});
+    launch_end(r, "ks_hoist_prow", 16.0 * (double)count * 2 * N, (double)count * 2 * (N / 2) * LB);
+  }
+  {  // 6: inverse column pass of P, lift into Q, forward column passes
+    ColJob cj{};
+    cj.src = acc;
+    cj.src_stride = 2ull * LP * N;
+    cj.dst = W;
+    cj.dst_stride = 2ull * L * N;
+    cj.nsrc = 2;
+    cj.in_raw = cj.out_raw = 1;
+    for (int pp = 0; pp < 2; pp++) {
+      cj.src_off[pp] = (unsigned short)(pp * LP + L);
+      cj.src_mod[pp] = (unsigned char)r->iP;
+      for (int l = 0; l < L; l++) {
+        cj.dst_off[pp][l] = (unsigned short)(pp * L + l);
+        cj.dst_mod[pp][l] = (unsigned char)l;
+      }
+    }
+    col_fused(r, cj, count, L, "ks_moddown_cols");
+  }
+  {  // 7: forward row pass of W with the combine (acc_Q - W) P^-1 + sigma(c0) [+ input] as epilogue
+    const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
+    NttJob job{};
+    job.base = W;
+    job.item_stride = 2ull * L * N;
+    int n = 0;
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        job.sub_off[n] = (unsigned short)(pp * L + l);
+        job.sub_mod[n] = (unsigned char)l;
+        n++;
+      }
+    job.nsub = n;
+    job.mods = r->d_mods;
+    job.logN = LA + LB;
+    job.in_raw = 1;
+    launch_begin(r);
+    launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, dim3((unsigned)((size_t)count * n * RT)), NTT2_TILE / 16, f1, job,
+               epi);
+    launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)),
+               (double)count * n * ((N / 2) * LB + N));
+  }
+}
+static bool keyswitch_hoisted(cgb_ring *r, Scratch &S, const KsSrc &x, int count, int nu, u64 *const *d_usrc,
+                              const u32 *d_srcidx, u64 *const *d_keys, u64 *const *d_out, const KsSrc &add0,
+                              const u64 *const *d_add1) {
+  if (!(g_ks_hoist && col_fusable(r) && moddown_fusable(r)) || count <= 0 || !x.items || !x.g) return false;
+#define KHO(A, B)                                                                                              \
+  switch (r->L) {                                                                                              \
+    case 2: keyswitch_hoisted_t<A, B, 2>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    case 3: keyswitch_hoisted_t<A, B, 3>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    default: keyswitch_hoisted_t<A, B, 4>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+  }
+  switch (r->logN) {
+    case 13: KHO(6, 7) break;
+    case 14: KHO(7, 7) break;
+    case 15: KHO(7, 8) break;
+    default: KHO(8, 8) break;
+  }
+#undef KHO
+  return true;
+}
+
 static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *const *d_keys, u64 *const *d_out,
                       const KsSrc &add0, const u64 *const *d_add1) {
   if (keyswitch_fused(r, S, x, count, d_keys, d_out, add0, d_add1)) return;
@@ -2623,13 +2812,31 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
       keys[k] = get_key(r, g[k]);
     }
     std::vector<u64 *> src = ct_ptrs(r, n, ia.data()), dst = ct_ptrs(r, n, io.data());
-    // the four per-item tables in ONE upload (host cost per wave is the critical path of small waves)
-    std::vector<u64> blob(4 * (size_t)n);
+    // sources shared by several items (one activation rotated by many steps): one ModUp each
+    std::vector<u64> usrc;
+    std::vector<u32> sidx(n);
+    {
+      std::unordered_map<u64, u32> seen;
+      for (int k = 0; k < n; k++) {
+        auto it = seen.emplace((u64)src[k], (u32)usrc.size());
+        if (it.second) usrc.push_back((u64)src[k]);
+        sidx[k] = it.first->second;
+      }
+    }
+    const int nu = (int)usrc.size();
+    const bool hoist = g_ks_hoist && 2 * nu <= n;
+    // the per-item tables in ONE upload (host cost per wave is the critical path of small waves)
+    const size_t nb = 4 * (size_t)n + (hoist ? (size_t)nu + ((size_t)n + 1) / 2 : 0);
+    std::vector<u64> blob(nb);
     for (int k = 0; k < n; k++) {
       blob[k] = (u64)src[k];
       blob[n + k] = (u64)dst[k];
       blob[2 * n + k] = (u64)keys[k];
       blob[3 * n + k] = g[k];
+    }
+    if (hoist) {
+      std::copy(usrc.begin(), usrc.end(), blob.begin() + 4 * (size_t)n);
+      std::memcpy(blob.data() + 4 * (size_t)n + nu, sidx.data(), sizeof(u32) * (size_t)n);
     }
     u64 *d_blob = S.up(blob.data(), blob.size());
     u64 **d_src = reinterpret_cast<u64 **>(d_blob), **d_dst = reinterpret_cast<u64 **>(d_blob + n),
@@ -2638,7 +2845,12 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
     // c1' = sigma_g(c1) is read through the automorphism by the key switch; c0' by its epilogue
     KsSrc xin{nullptr, 0, d_src, (u64)L * N, d_g};
     KsSrc c0p{nullptr, 0, d_src, 0, d_g};
-    keyswitch(r, S, xin, n, d_keys, d_dst, c0p, add_input ? (const u64 *const *)d_src : nullptr);
+    const u64 *const *add1 = add_input ? (const u64 *const *)d_src : nullptr;
+    if (hoist && keyswitch_hoisted(r, S, xin, n, nu, reinterpret_cast<u64 **>(d_blob + 4 * (size_t)n),
+                                   reinterpret_cast<const u32 *>(d_blob + 4 * (size_t)n + nu), d_keys, d_dst, c0p,
+                                   add1))
+      continue;
+    keyswitch(r, S, xin, n, d_keys, d_dst, c0p, add1);
   }
 }
 
@@ -3045,6 +3257,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_FUSED")) g_ks_fused = atoi(e);
   if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_MD")) g_ks_md = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KS_HOIST")) g_ks_hoist = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;

@@ -105,3 +105,35 @@ def test_fused_append_refresh_equal_per_op(api):
     for a, b in zip(res["per_op"][0], res["fused"][0]):
         assert np.array_equal(a, b)
     assert res["per_op"][1:] == res["fused"][1:]
+
+
+def test_rotation_dedup_equals_per_item(api):
+    """Batched CPVM over copies of one input (the decode Q/K/V projections,
+    model.py:521-526): one key switch per (content class, step), copies for the
+    rest -- the same words, counters and ids as each item's own CPVM."""
+    from paper_2602_08798_b200 import backend as B
+    from paper_2602_08798_b200.linear_kernels import cpvm_inner_diagonal, cpvm_inner_diagonal_heads
+
+    n, p, d1, d2, H = 8192, harness.P8192, 128, 64, 4
+    params = api.BackendParams(n_slots=n, plain_modulus=p)
+    rng = np.random.default_rng(3)
+    xv = rng.integers(0, p, n)
+    Wm = [rng.integers(-300, 300, (d1, d2)) % p for _ in range(H)]
+    res = {}
+    for mode in ("per_item", "dedup"):
+        root = B.GpuContext(params, 11)
+        x = root.encrypt(root.plain_from_dense(xv))
+        ctxs = [root.fork() for _ in range(H)]
+        Ws = [api.encode(w, api.EncodingKind.DIAGONAL, c, encrypted=False) for w, c in zip(Wm, ctxs)]
+        if mode == "per_item":
+            outs = [cpvm_inner_diagonal(x, W, c) for W, c in zip(Ws, ctxs)]
+        else:
+            w = B.GpuContext.wave_of([x] * H, ctxs)
+            assert w.klass is not None and len(set(w.klass.tolist())) == 1
+            outs = cpvm_inner_diagonal_heads([x] * H, Ws, ctxs)
+        res[mode] = ([o.words() for o in outs], [c.counter.as_dict() for c in ctxs],
+                     [(o.id % 10**9, o.noise_budget) for o in outs], root.decrypt(outs[1]))
+    for a, b in zip(res["per_item"][0], res["dedup"][0]):
+        assert np.array_equal(a, b)
+    assert res["per_item"][1:3] == res["dedup"][1:3]
+    assert np.array_equal(res["per_item"][3], res["dedup"][3])

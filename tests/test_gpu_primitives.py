@@ -83,6 +83,29 @@ def test_rotate_bitexact(pair, rng):
             assert np.array_equal(g.decrypt(out)[0], np.roll(v, -k))
 
 
+def test_rotate_hoisted_bitexact(pair, rng):
+    """A wave of rotations of ONE source (the CPVM's diagonal steps) takes the
+    hoisted key switch (one ModUp, per-step gathers): same words as the oracle,
+    with and without the fused add of the input."""
+    g, o = pair
+    if not o.one_row:
+        pytest.skip("cgb_rotate needs the one-row layout")
+    v = rng.integers(0, o.t, o.n_slots)
+    a, ra = _enc(g, o, v, 4)
+    steps = np.array([1, 2, 5, o.n_slots - 1, 7, 3], np.int64)
+    src = np.repeat(a, steps.size)
+    for add in (False, True):
+        out = g.alloc(steps.size)
+        g.rotate(src, steps, out, add_input=add)
+        got = g.store(out)
+        for i, k in enumerate(steps):
+            want = o.galois(ra, pow(5, int(k) % o.n_slots, 2 * o.N))
+            if add:
+                want = o.add(want, ra)
+            assert np.array_equal(got[i], want), (add, k)
+        g.free(out)
+
+
 def test_mult_cipher_bitexact(pair, rng):
     g, o = pair
     v, w = rng.integers(0, o.t, (2, o.n_slots))

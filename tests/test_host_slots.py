@@ -90,3 +90,19 @@ def test_interleaved_head_groups_equal_one_schedule(api, groups):
                 [ch.sample_mask(4).tolist() for ch in chans])
 
     assert run(1) == run(groups)
+
+
+def test_wave_content_classes():
+    """Wave bookkeeping behind the rotation dedup: repeated handles share a class,
+    take() keeps classes, concat() gives class-less waves fresh distinct classes."""
+    from paper_2602_08798_b200.backend import Wave
+
+    aids = np.array([7, 7, 9], np.uint32)
+    w = Wave([None], np.zeros(3, np.int64), aids, np.zeros(3, np.int64), [], klass=-(aids.astype(np.int64) + 1))
+    t = w.take([2, 0, 1, 0])
+    assert t.klass.tolist() == [-10, -8, -8, -8]
+    plain = Wave([None], np.zeros(2, np.int64), np.array([1, 2], np.uint32), np.zeros(2, np.int64), [])
+    c = Wave.concat([t, plain])
+    assert c.klass[:4].tolist() == t.klass.tolist()
+    assert c.klass[4] != c.klass[5] and min(c.klass[4:]) > 0
+    assert Wave.concat([plain, plain]).klass is None
