@@ -112,11 +112,33 @@ def host_buffer(shape, min_words: int = 1 << 16) -> np.ndarray:
     return np.empty(shape, np.int64)
 
 
+def _pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _POOL
+
+
 def neg_mod(r: np.ndarray, p: int) -> np.ndarray:
-    """(-r) mod p for r in [0, p), without an integer modulo, into a host buffer."""
+    """(-r) mod p for r in [0, p), without an integer modulo, into a host buffer;
+    large batches (a forced refresh negates 1.5k x 8192 words) in row blocks on
+    the host threads (numpy releases the GIL)."""
     out = host_buffer(r.shape)
-    np.subtract(p, r, out=out)
-    out[out == p] = 0
+
+    def neg(sl):
+        o = out[sl]
+        np.subtract(p, r[sl], out=o)
+        hit = o == p
+        if hit.any():
+            o[hit] = 0
+
+    if r.ndim == 2 and r.shape[0] >= 16 and r.size >= (1 << 21):
+        step = -(-r.shape[0] // 8)
+        list(_pool().map(neg, [slice(i, i + step) for i in range(0, r.shape[0], step)]))
+    else:
+        neg(slice(None))
     return out
 
 
@@ -136,11 +158,7 @@ def draw_masks(chans, n: int) -> np.ndarray:
             out[i] = ch.sample_mask(n)
 
     if len(groups) > 1 and len(chans) * n >= (1 << 20):
-        if _POOL is None:
-            from concurrent.futures import ThreadPoolExecutor
-
-            _POOL = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
-        list(_POOL.map(fill, groups.values()))
+        list(_pool().map(fill, groups.values()))
     else:
         for item in groups.values():
             fill(item)
