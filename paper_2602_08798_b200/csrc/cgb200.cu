@@ -2472,31 +2472,92 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
 static bool g_ks_hoist = true;  // CGB_KS_HOIST
 template <int L>
 __global__ void __launch_bounds__(256) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
-                                                        const u64 *const *keys, const ModTab *mods, int iP, int logN) {
+                                                        const u64 *const *keys, const ModTab *mods, int iP, int logN,
+                                                        int lfirst) {
+  // 4 consecutive words per thread: the 4 gathered words of a digit sit in one aligned
+  // 32-byte block (gather4), the key words and the accumulators move as 256-bit accesses
   constexpr int LP = L + 1;
   const u64 N = 1ull << logN;
   const int item = blockIdx.y;
-  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;  // over [l][N]
+  const u64 i = ((u64)lfirst << logN) + 4 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);  // over [l][N]
   if (i >= LP * N) return;
   const int l = (int)(i >> logN);
-  const u32 k = (u32)(i & (N - 1));
+  const u32 k0 = (u32)(i & (N - 1));
   const ModTab &Md = mods[l == L ? iP : l];
   const double qd = Md.qd, qinv = Md.qinv;
-  const u32 kk = perm_g(k, xin.g[item], logN);
-  const u64 *Du = D + (u64)srcidx[item] * L * LP * N + kk;
-  const u64 *own = xin.items[item] + xin.off + kk;
+  const u64 g = xin.g[item];
+  const u64 *Du = D + (u64)srcidx[item] * L * LP * N;
+  const u64 *own = xin.items[item] + xin.off;
   const u64 *KF = keys[item] + 2 * (u64)L * 2 * LP * N + i;  // the key's FP64 plane (k_key_fp)
-  double a0 = 0.0, a1 = 0.0;
+  u64 dv[L][4], kv[L][2][4];
 #pragma unroll
   for (int j = 0; j < L; j++) {
-    const double xv = u2d(l == j ? own[(u64)j << logN] : Du[((u64)j * LP + l) * N]);
-    const double d0 = r2d(__ldcs(KF + (u64)(j * 2 + 0) * LP * N)), d1 = r2d(__ldcs(KF + (u64)(j * 2 + 1) * LP * N));
-    a0 += fp_mulmod(xv, d0, d0 * qinv, qd);
-    a1 += fp_mulmod(xv, d1, d1 * qinv, qd);
+    gather4(l == j ? own + ((u64)j << logN) : Du + ((u64)j * LP + l) * N, k0, g, logN, dv[j]);
+    ld256(KF + (u64)(j * 2 + 0) * LP * N, kv[j][0]);
+    ld256(KF + (u64)(j * 2 + 1) * LP * N, kv[j][1]);
   }
-  acc[((u64)item * 2 + 0) * LP * N + i] = fp_canon(a0, qd, qinv);
-  acc[((u64)item * 2 + 1) * LP * N + i] = fp_canon(a1, qd, qinv);
+  double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < L; j++)
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const double xv = u2d(dv[j][e]), d0 = r2d(kv[j][0][e]), d1 = r2d(kv[j][1][e]);
+      a0[e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+      a1[e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+    }
+  u64 *o0 = acc + ((u64)item * 2 + 0) * LP * N + i, *o1 = acc + ((u64)item * 2 + 1) * LP * N + i;
+  st256(o0, fp_canon(a0[0], qd, qinv), fp_canon(a0[1], qd, qinv), fp_canon(a0[2], qd, qinv), fp_canon(a0[3], qd, qinv));
+  st256(o1, fp_canon(a1[0], qd, qinv), fp_canon(a1[1], qd, qinv), fp_canon(a1[2], qd, qinv), fp_canon(a1[3], qd, qinv));
 }
+// ModDown's combine for the hoisted key switch: the Q limbs' accumulator words are
+// formed in the epilogue of W's row pass (gathered digits x key plane) and never
+// reach memory; only the P limb goes through k_ks_inner_hoist.
+static bool g_hoist_fuse = false;  // CGB_HOIST_FUSE: measured slower (2.12 vs 2.01 us/rotation), off
+struct MdEpiHoist : MdEpi {
+  const u64 *D;
+  const u32 *srcidx;
+  KsSrc xin;
+  const u64 *const *keys;
+  __device__ void store(int item, int unit, u64 pos, const u64 *w, int n) const {
+    const int pp = unit / L, l = unit - pp * L, LP = L + 1;
+    const u64 N = 1ull << logN;
+    const ModTab &M = mods[l];
+    const double qd = M.qd, qinv = M.qinv;
+    const u64 g = xin.g[item];
+    const u64 *Du = D + (u64)srcidx[item] * L * LP * N;
+    const u64 *KF = keys[item] + 2 * (u64)L * 2 * LP * N + ((u64)pp * LP + l) * N + pos;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < L; j++) {
+      const u64 *src = l == j ? xin.items[item] + xin.off + ((u64)j << logN) : Du + ((u64)j * LP + l) * N;
+      u64 dv[4], kv[4];
+      if (n == 4) {
+        gather4(src, (u32)pos, g, logN, dv);
+        ld256(KF + (u64)j * 2 * LP * N, kv);
+      } else {
+        dv[0] = src[perm_g((u32)pos, g, logN)];
+        kv[0] = KF[(u64)j * 2 * LP * N];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; e++)
+        if (e < n) {
+          const double d = r2d(kv[e]);
+          a[e] += fp_mulmod(u2d(dv[e]), d, d * qinv, qd);
+        }
+    }
+    u64 av[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) av[e] = fp_canon(a[e], qd, qinv);
+    if (n == 4) {
+      combine4(item, unit, pos, w, av);
+      return;
+    }
+    const u64 q = M.q, pi = C->Pinvq[l], pis = C->Pinvq_sh[l];
+    u64 v = mul_shoup(sub_mod(av[0], w[0], q), pi, pis, q);
+    if (pp == 0 && (add0.items || add0.base)) v = add_mod(v, ks_src_word(add0, item, l, (u32)pos, logN), q);
+    if (add1) v = add_mod(v, add1[item][(u64)unit * N + pos], q);
+    out[item][(u64)unit * N + pos] = v;
+  }
+};
 template <int LA, int LB, int L>
 static void keyswitch_hoisted_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, int nu, u64 *const *d_usrc,
                                 const u32 *d_srcidx, u64 *const *d_keys, u64 *const *d_out, const KsSrc &add0,
@@ -2569,9 +2630,11 @@ static void keyswitch_hoisted_t(cgb_ring *r, Scratch &S, const KsSrc &x, int cou
   }
   {  // 4: per item: digits gathered through perm_g, key inner product over Q u P
     launch_begin(r);
-    k_ks_inner_hoist<L><<<dim3(GRID1((u64)LP * N, 256).x, count), 256, 0, r->stream>>>(acc, D, d_srcidx, x, d_keys,
-                                                                                      r->d_mods, r->iP, LA + LB);
-    launch_end(r, "ks_hoist_inner", 8.0 * (double)count * LP * N * (L + 2.0 * L + 2.0), 2.0 * count * L * LP * (double)N);
+    const int lf = g_hoist_fuse ? L : 0, nl = LP - lf;  // fused: the Q limbs are formed in step 7's epilogue
+    k_ks_inner_hoist<L><<<dim3(GRID1((u64)nl * N / 4, 256).x, count), 256, 0, r->stream>>>(
+        acc, D, d_srcidx, x, d_keys, r->d_mods, r->iP, LA + LB, lf);
+    // key plane (2L words) + accumulators (2) per word; the gathered digits are L2-resident
+    launch_end(r, "ks_hoist_inner", 8.0 * (double)count * nl * N * (2.0 * L + 2.0), 2.0 * count * L * nl * (double)N);
   }
   {  // 5: ModDown's inverse row pass of the P limb (both polys), in place
     NttJob job{};
@@ -2623,11 +2686,25 @@ static void keyswitch_hoisted_t(cgb_ring *r, Scratch &S, const KsSrc &x, int cou
     job.mods = r->d_mods;
     job.logN = LA + LB;
     job.in_raw = 1;
+    const dim3 grid((unsigned)((size_t)count * n * RT));
     launch_begin(r);
-    launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, dim3((unsigned)((size_t)count * n * RT)), NTT2_TILE / 16, f1, job,
-               epi);
-    launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)),
-               (double)count * n * ((N / 2) * LB + N));
+    if (g_hoist_fuse) {
+      MdEpiHoist he;
+      static_cast<MdEpi &>(he) = epi;
+      he.D = D;
+      he.srcidx = d_srcidx;
+      he.xin = x;
+      he.keys = d_keys;
+      launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpiHoist>, grid, NTT2_TILE / 16, f1, job, he);
+      // W, sigma(c0), out, add1 + the key plane (2 words per digit) per word of the Q limbs
+      launch_end(r, "ks_hoist_md",
+                 8.0 * (double)count * n * N * (2 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0) + L),
+                 (double)count * n * ((N / 2) * LB + N + (double)L * N));
+    } else {
+      launch_pdl(r, k_ntt2_fpr<LA, LB, true, 1, MdEpi>, grid, NTT2_TILE / 16, f1, job, epi);
+      launch_end(r, "ks_moddown_rows", 8.0 * (double)count * n * N * (3 + (add0.items ? 0.5 : 0) + (d_add1 ? 1 : 0)),
+                 (double)count * n * ((N / 2) * LB + N));
+    }
   }
 }
 static bool keyswitch_hoisted(cgb_ring *r, Scratch &S, const KsSrc &x, int count, int nu, u64 *const *d_usrc,
@@ -3258,6 +3335,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_MD")) g_ks_md = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_HOIST")) g_ks_hoist = atoi(e) != 0;
+  if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
