@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--L", type=int, default=128, help="cached prefill length per head")
     ap.add_argument("--heads", type=int, default=HEADS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-vocab", action="store_true",
+                    help="layer workload: unembed all 50257 columns (7 slot blocks) instead of the first 8192")
     ap.add_argument("--profile-step", action="store_true",
                     help="warm up, run ONE step inside NVTX range 'timed_step', exit (for ncu)")
     return ap.parse_args()
@@ -215,7 +217,8 @@ def layer_model(args):
     from paper_2602_08798_b200 import model as M
 
     cfg = M.ModelConfig(layers=1, d1=HEADS * D2, heads=HEADS, ffn_dim=4 * HEADS * D2, vocab=GPT2_VOCAB,
-                        max_seq=args.L + args.steps + 1, f=F, unembed_vocab=N_SLOTS)
+                        max_seq=args.L + args.steps + 1, f=F,
+                        unembed_vocab=None if getattr(args, "full_vocab", False) else N_SLOTS)
     return M, M.gpt2_layer_model(cfg, seed=0)
 
 
@@ -224,8 +227,10 @@ def run_layer(args):
     N(0, 0.02) weights), a prompt of L token ids uniform over 50257, then
     `steps` greedy tokens, every cache part force-refreshed before each step.
     The unembedding covers the first 8192 vocabulary entries (n_slots)."""
-    os.environ.setdefault("CGB_ARENA_GIB", "64")  # the FFN prefill keeps ~20k ciphertexts live
-    os.environ.setdefault("CGB_PT_ARENA_GIB", "12")  # every decode-step weight diagonal stays resident
+    # the FFN prefill keeps ~20k ciphertexts live; every decode-step weight diagonal stays
+    # resident (a full-vocabulary unembedding: 7 x 8192 diagonals, 57k products per token)
+    os.environ.setdefault("CGB_ARENA_GIB", "56" if args.full_vocab else "64")
+    os.environ.setdefault("CGB_PT_ARENA_GIB", "34" if args.full_vocab else "12")
     import torch
 
     from paper_2602_08798_b200 import _native
@@ -271,7 +276,7 @@ def run_layer(args):
             "value": float(np.mean(step_ms)), "unit": "ms/token", "higher_is_better": False, "n_gpus": 1,
             "steps": args.steps, "dtype": "u64", "data": "synthetic (token ids uniform over 50257, N(0,0.02) weights)",
             "config": {"workload": f"gpt2_layer_prompt{args.L}_gen{args.steps}", "d_model": HEADS * D2,
-                       "heads": HEADS, "d_ff": 4 * HEADS * D2, "vocab": GPT2_VOCAB, "unembed_vocab": N_SLOTS,
+                       "heads": HEADS, "d_ff": 4 * HEADS * D2, "vocab": GPT2_VOCAB, "unembed_vocab": GPT2_VOCAB if args.full_vocab else N_SLOTS,
                        "n_slots": N_SLOTS, "plain_modulus": P, "ring": _ring_desc()},
             "prefill_ms": pre_ms, "decode_ms_per_token": step_ms,
             "wall_s": {"prefill": t_pre, "total": t_all},

@@ -775,26 +775,28 @@ class GpuContext:
         st = np.ascontiguousarray(np.broadcast_to(np.asarray(steps, dtype=np.int64), (len(wave),)))
         rb = GpuContext._spend_all(wave.budgets, costs.rotate)
         b = GpuContext._spend_all(np.minimum(wave.budgets, rb), costs.add) if add_input else rb
-        blk, ids = c0._new(len(wave))
         klass = None
         if wave.klass is not None and _ROT_DEDUP:
-            # one key switch per distinct (content class, step); the other items are
-            # copies of its result -- the same words their own key switch would give
-            pairs = {}
-            lead = np.empty(len(wave), np.int64)
-            for i, key in enumerate(zip(wave.klass.tolist(), st.tolist())):
-                lead[i] = pairs.setdefault(key, i)
+            # one key switch per distinct (content class, step); the other items share
+            # its arena id -- the same words their own key switch would give (handles
+            # are immutable and the block frees each id once)
+            _, fi, inv = np.unique(np.stack([wave.klass, st], axis=1), axis=0, return_index=True,
+                                   return_inverse=True)
+            lead = fi[inv.reshape(-1)].astype(np.int64)  # first item of each (class, step)
             first = np.flatnonzero(lead == np.arange(len(wave)))
-            _rotate_ids(c0._ring, c0.params, wave.aids[first], st[first], ids[first], add_input)
+            blk, uids = c0._new(first.size)
+            _rotate_ids(c0._ring, c0.params, wave.aids[first], st[first], uids, add_input)
+            ids = np.empty(len(wave), np.uint32)
+            ids[first] = uids
             dup = np.flatnonzero(lead != np.arange(len(wave)))
-            if dup.size:
-                c0._ring.copy(ids[lead[dup]], ids[dup])
+            ids[dup] = ids[lead[dup]]
             fresh = _fresh_classes(first.size)
             cls = np.empty(len(wave), np.int64)
             cls[first] = fresh
             cls[dup] = cls[lead[dup]]
             klass = cls if dup.size else None
         else:
+            blk, ids = c0._new(len(wave))
             _rotate_ids(c0._ring, c0.params, wave.aids, st, ids, add_input)
         if add_input:
             GpuContext._charge(wave, "rotate", n_emit=0)
@@ -817,11 +819,20 @@ class GpuContext:
         for gi, g in enumerate(groups):
             if g.size == 0:
                 raise ParameterError("empty sum")
-            acc = int(wave.budgets[g[0]])
-            for j in g[1:]:
-                acc = min(acc, int(wave.budgets[j])) - cost
-                if acc < 0:
-                    raise NoiseBudgetExhausted(f"operation needs {cost} bits but only {acc + cost} remain")
+            # the left fold acc <- min(acc, b_t) - cost in closed form: the final budget is
+            # min(b_0 - m cost, b_t - (m - t + 1) cost); the sequence strictly decreases,
+            # so only the final value can signal exhaustion (the loop then names the step)
+            bg = wave.budgets[g]
+            m = g.size - 1
+            coef = m + 1 - np.arange(g.size)
+            coef[0] = m
+            acc = int(np.min(bg - coef * cost))
+            if acc < 0:
+                acc = int(bg[0])
+                for b in bg[1:]:
+                    acc = min(acc, int(b)) - cost
+                    if acc < 0:
+                        raise NoiseBudgetExhausted(f"operation needs {cost} bits but only {acc + cost} remain")
             budgets[gi] = acc
             o = owner[gi] = wave.owner[g[0]]
             c = wave.ctxs[o]

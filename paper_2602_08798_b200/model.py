@@ -17,8 +17,9 @@ follow wave order (item by item per channel), which changes share values but
 not results: every conversion reconstructs exactly.
 
 Out of the reference: a vocab-50257 unembedding cannot be
-diagonal-packed at n = 8192, so ``unembed_vocab`` (<= n_slots) columns are
-unembedded while token embeddings keep the full vocabulary.
+diagonal-packed at n = 8192; here a vocabulary wider than n is unembedded in
+n-column blocks (``_logits``), and ``unembed_vocab`` can still cap the
+unembedded columns while token embeddings keep the full vocabulary.
 """
 
 from __future__ import annotations
@@ -174,10 +175,37 @@ def _matrix_roundtrip(parts, m, ctx, ch, fn):
 
 
 def _logits(model, x_ct, ctx, fp):
+    """model.py:487-495 / :548-556.  A vocabulary wider than the slot count (the
+    reference raises there) is unembedded in n-column blocks, one
+    CPVM per block over copies of the same activation: every block rotates it by
+    the same n - 1 steps, so the rotations are one hoisted key switch per step
+    (content classes, backend.Wave) and each block only adds its products."""
     c = model.config
-    p = ctx.params.plain_modulus
-    ct = cpvm_inner_diagonal(x_ct, model.diag("unembed", model.unembed(), ctx), ctx)
-    return fp_truncate(to_signed(ctx.decrypt(ct), p)[:c.out_vocab], fp.f)
+    p, n = ctx.params.plain_modulus, ctx.params.n_slots
+    V = c.out_vocab
+    if V <= n:
+        ct = cpvm_inner_diagonal(x_ct, model.diag("unembed", model.unembed(), ctx), ctx)
+        return fp_truncate(to_signed(ctx.decrypt(ct), p)[:V], fp.f)
+    nb = -(-V // n)
+    Ws = []
+    for b in range(nb):
+        W = model._diag.get((f"unembed.{b}", n, p))
+        if W is None:  # block b: columns b n .. (b + 1) n - 1, zero past the vocabulary
+            blk = np.zeros((c.d1, n), np.int64)
+            cols = model.unembed()[:, b * n:min(V, (b + 1) * n)]
+            blk[:, :cols.shape[1]] = cols
+            W = model.diag(f"unembed.{b}", blk, ctx)
+        Ws.append(W)
+    # UNEMBED_GROUP blocks per wave: their n x n products stay within the ciphertext arena
+    cts = []
+    for b0 in range(0, nb, UNEMBED_GROUP):
+        k = min(UNEMBED_GROUP, nb - b0)
+        cts += cpvm_inner_diagonal_heads([x_ct] * k, Ws[b0:b0 + k], [ctx] * k)
+    vals = np.concatenate([to_signed(ctx.decrypt(ct), p) for ct in cts])
+    return fp_truncate(vals[:V], fp.f)
+
+
+UNEMBED_GROUP = 4  # slot blocks of a wide unembedding per batched CPVM
 
 
 # ----------------------------------------------------------------------------

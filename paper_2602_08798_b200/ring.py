@@ -33,9 +33,9 @@ class Ring:
         self.fp_ntt = log_n >= 12 and self.q_bits <= 49 and not os.environ.get("CGB_INT_NTT")
         self.ct_words = 2 * self.L * self.N
         if arena_cts is None:
-            arena_cts = max(64, min(65536, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))
+            arena_cts = max(64, min(1 << 20, DEFAULT_ARENA_BYTES // (8 * self.ct_words)))
         if arena_pts is None:
-            arena_pts = max(64, min(65536, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
+            arena_pts = max(64, min(1 << 20, DEFAULT_PT_BYTES // (8 * self.L * self.N)))
         self.arena_cts, self.arena_pts = int(arena_cts), int(arena_pts)
         self._ext = {}  # arena id -> the two slots of its resident base-B extension (cgb_extend_b)
         self.h2d_bytes = 0  # host payload bytes moved to / from the device (slot vectors, raw words)

@@ -79,3 +79,43 @@ def test_cpmm_chunked_equals_unchunked():
     finally:
         LK.CPMM_CHUNK = old
     assert np.array_equal(full, chunked)
+
+
+def _wide_vocab_logits(make_ctx):
+    """Unembedding wider than the slot count (vocab 200 at n = 64: 4 blocks)
+    equals the plain fixed-point product x W, truncated."""
+    from paper_2602_08798_b200 import model as M
+    from paper_2602_08798_b200.backend import BackendParams
+    from paper_2602_08798_b200.fixedpoint import fp_truncate, to_signed
+
+    g = np.load(GOLDS / "layer_toy.npz")
+    p, n = int(g["p"]), int(g["n"])
+    cfg = M.ModelConfig(layers=1, d1=32, heads=4, ffn_dim=64, vocab=200, max_seq=8, f=8)
+    mdl = M.gpt2_layer_model(cfg, seed=3)
+    ctx = make_ctx(BackendParams(n_slots=n, plain_modulus=p), 0)
+    fp = mdl.fixed_point(ctx)
+    x = np.random.default_rng(1).integers(-300, 300, cfg.d1)
+    xv = np.zeros(n, np.int64)
+    xv[:cfg.d1] = np.mod(x, p)
+    x_ct = ctx.encrypt(ctx.plain_from_dense(xv))
+    got = M._logits(mdl, x_ct, ctx, fp)
+    want = fp_truncate(to_signed(np.mod(x @ mdl.unembed(), p), p), fp.f)
+    assert got.shape == (200,)
+    assert np.array_equal(got, want)
+    assert ctx.counter.rotate > 0
+
+
+def test_wide_vocab_unembedding_on_slot_oracle():
+    from oracle.slots import SlotContext
+
+    _wide_vocab_logits(SlotContext)
+
+
+@pytest.mark.gpu
+def test_wide_vocab_unembedding_on_gpu():
+    assert gpu_available()
+    from paper_2602_08798_b200._native import build
+    from paper_2602_08798_b200.backend import GpuContext
+
+    build()
+    _wide_vocab_logits(GpuContext)
