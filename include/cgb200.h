@@ -154,7 +154,10 @@ int cgb_mult_cipher_ext(cgb_ring *ring, int count, const uint32_t *a, const uint
 /* Galois automorphism X -> X^g plus key switch; g = 1 copies.
  * Context.rotate (backend.py:349-355) is galois(5^k mod 2N) in the one-row layout. */
 int cgb_galois(cgb_ring *ring, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out);
-/* Context.rotate: cyclic left shift by steps[i] (one-row layout only) */
+/* Context.rotate: cyclic left shift by steps[i] (one-row layout only).
+ * A batch in which ids repeat in a[] (one ciphertext rotated by many steps, e.g.
+ * the diagonal CPVM, linear_kernels.py:105-142) is key-switched hoisted: one
+ * ModUp per distinct source, same output words (CGB_KS_HOIST=0 disables). */
 int cgb_rotate(cgb_ring *ring, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out);
 /* out = a + rotate(a, step): one doubling/fold step of broadcast_slot
  * (arcc.py:90-93), tile_token (encodings.py:212-215) and fold_sum

@@ -24,6 +24,7 @@ unembedded columns while token embeddings keep the full vocabulary.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -205,7 +206,8 @@ def _logits(model, x_ct, ctx, fp):
     return fp_truncate(vals[:V], fp.f)
 
 
-UNEMBED_GROUP = 4  # slot blocks of a wide unembedding per batched CPVM
+# slot blocks of a wide unembedding per batched CPVM (their products share the arena)
+UNEMBED_GROUP = int(os.environ.get("CGB_UNEMBED_GROUP", "4"))
 
 
 # ----------------------------------------------------------------------------
