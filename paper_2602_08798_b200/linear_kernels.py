@@ -54,7 +54,7 @@ def cpvm_inner_diagonal(x, W: PackedMatrix, ctx):
     return cpvm_inner_diagonal_heads([x], [W], [ctx])[0]
 
 
-def cpvm_inner_diagonal_heads(xs, Ws, ctxs) -> list:
+def cpvm_inner_diagonal_heads(xs, Ws, ctxs, serial_products: bool = False) -> list:
     """``cpvm_inner_diagonal`` for B independent (x, W, ctx) triples of one
     shape (e.g. the 3 x 12 per-head decode projections, model.py:521-526):
     each rotation amount is one batched key switch over all B items; item i's
@@ -98,8 +98,17 @@ def cpvm_inner_diagonal_heads(xs, Ws, ctxs) -> list:
         groups = [np.concatenate([[b], B + b * (wd2 - 1) + np.arange(wd2 - 1)]) for b in range(B)]
     else:
         xs_w, keys, groups = xw, [key(b, 0) for b in range(B)], [np.array([b]) for b in range(B)]
-    prods = C.w_mult_plain(xs_w, PlainBatch(keys, build))
-    acc = C.w_sum(prods, groups)
+    if serial_products:
+        # one item's products at a time (same words; the rotations above stay one
+        # wave): a wide unembedding's 7 x 8192 products never coexist in the arena
+        accs = []
+        for g in groups:
+            prods = C.w_mult_plain(xs_w.take(g), PlainBatch([keys[i] for i in g], build))
+            accs.append(C.w_sum(prods, [np.arange(g.size)]))
+        acc = type(xw).concat(accs)
+    else:
+        prods = C.w_mult_plain(xs_w, PlainBatch(keys, build))
+        acc = C.w_sum(prods, groups)
     return (fold_wave(acc, wp // wd2, first_step=wd2) if wp > wd2 else acc).handles()
 
 

@@ -180,7 +180,8 @@ def _logits(model, x_ct, ctx, fp):
     reference raises there) is unembedded in n-column blocks, one
     CPVM per block over copies of the same activation: every block rotates it by
     the same n - 1 steps, so the rotations are one hoisted key switch per step
-    (content classes, backend.Wave) and each block only adds its products."""
+    (content classes, backend.Wave) and each block only adds its products,
+    block by block (serial_products) so they fit the ciphertext arena."""
     c = model.config
     p, n = ctx.params.plain_modulus, ctx.params.n_slots
     V = c.out_vocab
@@ -197,17 +198,17 @@ def _logits(model, x_ct, ctx, fp):
             blk[:, :cols.shape[1]] = cols
             W = model.diag(f"unembed.{b}", blk, ctx)
         Ws.append(W)
-    # UNEMBED_GROUP blocks per wave: their n x n products stay within the ciphertext arena
+    # UNEMBED_GROUP blocks share one rotation wave; their products run block by block
     cts = []
     for b0 in range(0, nb, UNEMBED_GROUP):
         k = min(UNEMBED_GROUP, nb - b0)
-        cts += cpvm_inner_diagonal_heads([x_ct] * k, Ws[b0:b0 + k], [ctx] * k)
+        cts += cpvm_inner_diagonal_heads([x_ct] * k, Ws[b0:b0 + k], [ctx] * k, serial_products=True)
     vals = np.concatenate([to_signed(ctx.decrypt(ct), p) for ct in cts])
     return fp_truncate(vals[:V], fp.f)
 
 
 # slot blocks of a wide unembedding per batched CPVM (their products share the arena)
-UNEMBED_GROUP = int(os.environ.get("CGB_UNEMBED_GROUP", "4"))
+UNEMBED_GROUP = int(os.environ.get("CGB_UNEMBED_GROUP", "8"))
 
 
 # ----------------------------------------------------------------------------
