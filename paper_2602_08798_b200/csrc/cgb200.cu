@@ -2470,8 +2470,11 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
 // source, each item only gathers its digits through perm_g and takes the key inner
 // product.  Every word is the same residue the per-item path computes.
 static bool g_ks_hoist = true;  // CGB_KS_HOIST
+#ifndef CGB_HOIST_MINB
+#define CGB_HOIST_MINB 4  // 4 CTAs of 256 per SM (<= 64 registers)
+#endif
 template <int L>
-__global__ void __launch_bounds__(256) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
+__global__ void __launch_bounds__(256, CGB_HOIST_MINB) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
                                                         const u64 *const *keys, const ModTab *mods, int iP, int logN,
                                                         int lfirst) {
   // 4 consecutive words per thread: the 4 gathered words of a digit sit in one aligned
