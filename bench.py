@@ -75,9 +75,10 @@ def _ring_desc():
 
 
 def workload(args):
+    """The config dict, identical in both arms (the GPU ring is reported beside it)."""
     return {"workload": f"decode_attention_{args.heads}h_L{args.L}", "heads": args.heads, "d_head": D2,
             "n_slots": N_SLOTS, "plain_modulus": P, "cached_len": args.L, "steps_appended": 1,
-            "ring": _ring_desc(), "l2": "working set >1.5 GB per step (> 126 MB L2)"}
+            "l2": "working set >1.5 GB per step (> 126 MB L2)", "parallelism": f"replicas{args.gpus}"}
 
 
 # ----------------------------------------------------------------------------
@@ -311,21 +312,19 @@ def layer_cpu_baseline(args):
             "host": _cpu_model()}
 
 
-def _ncu(kernel: str):
-    """The committed ncu figures of a kernel (profiles/r01/ncu_kernels.json), or {}."""
-    f = ROOT / "profiles" / "r01" / "ncu_kernels.json"
-    return json.loads(f.read_text()).get(kernel, {}) if f.exists() else {}
-
-
-def _traffic(kernel: str, alg_bytes_per_launch: float):
-    """DRAM bytes per launch of the dominant kernel: the algorithmic bytes scaled by
-    the DRAM/algorithmic ratio of its committed ncu --set full capture, or None."""
-    cap = _ncu(kernel)
-    if "dram_over_algorithmic" not in cap:
+def _traffic_ks(alg_bytes_per_launch: float, ring):
+    """DRAM bytes per batched key switch from the committed ncu --set full capture of
+    its five kernels (profiles/r02/ncu_keyswitch.json: DRAM bytes per key-switched
+    item), scaled to this bench's average batch; None without a capture."""
+    f = ROOT / "profiles" / "r02" / "ncu_keyswitch.json"
+    if not f.exists():
         return None
-    return {"bytes_per_launch": alg_bytes_per_launch * cap["dram_over_algorithmic"],
-            "dram_over_algorithmic": cap["dram_over_algorithmic"],
-            "source": "profiles/r01/ncu_kernels.json (" + cap["kernel"] + ")"}
+    cap = json.loads(f.read_text())
+    per_item, alg_item = cap.get("dram_bytes_per_item"), cap.get("algorithmic_bytes_per_item")
+    if not per_item or not alg_item:
+        return None
+    return {"bytes_per_launch": alg_bytes_per_launch * per_item / alg_item,
+            "dram_over_algorithmic": per_item / alg_item, "source": "profiles/r02/ncu_keyswitch.json"}
 
 
 def run_ours(args):
@@ -421,11 +420,20 @@ def run_ours(args):
     ms_e2e = ev0.elapsed_time(ev1)
     h2d = (ring.h2d_bytes - h0) / args.steps
     d2h = (ring.d2h_bytes - d0) / args.steps
-    # per-kernel live timing pass (CUDA events around every launch)
-    ring.timing(True)
+    # live timing passes, one step each: (1) CUDA events around every launch (PDL off:
+    # the per-kernel table); (2) events around every multi-launch operation -- a whole
+    # batched key switch, a whole mult_cipher -- with PDL on inside it (the 8(d) units
+    # the roofline is computed on)
+    ring.timing(1)
     one_step(dev_tokens[args.warmup])
     rep = ring.timing_report()
-    ring.timing(False)
+    ring.timing(2)
+    ev0.record(stream)
+    one_step(dev_tokens[args.warmup])
+    ev1.record(stream)
+    units = ring.timing_report()
+    ring.timing(0)
+    unit_step_ms = ev0.elapsed_time(ev1)
     idle_ms = rep.pop("(idle)", (0, 0.0, 0.0))[1]
     gaps = {k: round(v[1], 3) for k, v in rep.items() if k.startswith("(gap")}
     for k in gaps:
@@ -444,30 +452,45 @@ def run_ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     step_kernel_ms = sum(v[1] for v in rep.values())
-    top = max(rep.items(), key=lambda kv: kv[1][1])
-    name, (nl, kms, kbytes, kmm) = top
+    # the dominant unit: the batched key switch (five fused launches, or the hoisted
+    # variant), bytes = inputs + outputs once + each distinct key once
+    ks = [units[k] for k in ("keyswitch", "keyswitch_hoisted") if k in units]
+    nl, kms = sum(v[0] for v in ks), sum(v[1] for v in ks)
+    kbytes, kmm = sum(v[2] for v in ks), sum(v[3] for v in ks)
     achieved = kbytes / (kms * 1e-3) / 1e9
+    mc = [units[k] for k in ("mult_cipher", "mult_cipher_ext") if k in units]
     # arithmetic pipe (FP64 exact products for rings of < 2^49 primes, else 64-bit Shoup):
     # algorithmic modular products (butterflies + key / constant products) per second
     arith = [v for v in rep.values() if v[3] > 0]
     ar_ms, ar_mm = sum(v[1] for v in arith), sum(v[3] for v in arith)
     line = {
-        "metric": metric_name(args.L), "value": ms_step / world, "unit": "ms/token", "n_gpus": world,
+        # value: per-token latency of the job; N > 1 runs N independent replicas,
+        # each producing one token per step, timed as the max over ranks
+        "metric": metric_name(args.L), "value": ms_step, "unit": "ms/token", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform [-1,1], f=8)",
-        "config": dict(workload(args), parallelism=f"replicas{world}"),
-        "e2e": {"value": ms_e2e / args.steps / world, "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
+        "config": workload(args), "ring": _ring_desc(),
+        "e2e": {"value": ms_e2e / args.steps, "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": _traffic(name, kbytes / nl), "launches_per_step": nl,
-                     "share_of_step": kms / step_kernel_ms if step_kernel_ms else None,
+        "roofline": {"bound": "hbm", "kernel": "keyswitch (batched hybrid key switch as one unit: 5 fused "
+                                               "launches, or the hoisted variant)",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": _traffic_ks(kbytes / nl if nl else 0.0, ring), "launches_per_step": nl,
+                     "bytes_per_launch": kbytes / nl if nl else None,
+                     "bytes_def": "per batch: (input ct + output ct) x items + 2 dnum (L+1) N x 8 B per distinct key",
+                     "share_of_step": kms / unit_step_ms if unit_step_ms else None,
+                     "timing": "CUDA events around each whole batched key switch, PDL on inside (cgb_timing_enable 2)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
                      "pipe": {"name": "fp64" if ring.fp_ntt else "int64", "unit": "modmul/s",
                               "achieved": kmm / (kms * 1e-3) if kmm else None, "peak": peak_mm,
                               "frac": kmm / (kms * 1e-3) / peak_mm if kmm else None,
-                              "peak_source": "cgb_modmul_peak: measured chains of the same modular product",
-                              "fp64_pipe_active_pct_ncu": _ncu(name).get("fp64_pipe_active")}},
+                              "peak_source": "cgb_modmul_peak: measured chains of the same modular product"}},
+        "units": {k: {"calls": v[0], "ms": round(v[1], 3), "GBps": round(v[2] / (v[1] * 1e-3) / 1e9, 1) if v[1] else None,
+                      "Gmodmul_s": round(v[3] / (v[1] * 1e-3) / 1e9, 1) if v[1] and v[3] else None}
+                  for k, v in sorted(units.items(), key=lambda kv: -kv[1][1]) if not k.startswith("(")},
+        "mult_cipher_unit": {"ms": sum(v[1] for v in mc), "GBps": sum(v[2] for v in mc) / (sum(v[1] for v in mc) * 1e-3) / 1e9
+                             if mc else None},
         "arith_pipe": {"kernels": "every launch with modular-product work (NTT passes, fused key switch)",
                        "pipe": "fp64" if ring.fp_ntt else "int64",
                        "modmuls_per_s": ar_mm / (ar_ms * 1e-3) if ar_ms else None,
@@ -484,7 +507,7 @@ def run_ours(args):
         "gpu_idle_by_transition_ms": trans,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, samples=1)
+        line["cpu_baseline"] = cpu_baseline(args, samples=3)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -552,7 +575,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": metric_name(args.L), "value": ms, "unit": "ms/token", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64 (Z_p slot emulation)", "data": "synthetic",
-            "config": dict(workload(args), parallelism="cpu"),
+            "config": workload(args),
             "cpu_baseline": {"value": ms, "unit": "ms/token", "cores": 1, "kind": "port",
                              "sample": f"{args.steps} decode steps x {args.heads} heads at L={args.L}",
                              "host": _cpu_model()},

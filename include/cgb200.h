@@ -75,7 +75,10 @@ int cgb_set_stream(cgb_ring *ring, void *cuda_stream);
 int cgb_sync(cgb_ring *ring);
 /* number of device kernel launches issued by this ring so far */
 uint64_t cgb_launch_count(const cgb_ring *ring);
-/* per-launch CUDA-event timing: enable (clears earlier records) / disable */
+/* CUDA-event timing (clears earlier records): on = 1 times every launch (programmatic
+ * dependent launch off); on = 2 times every multi-launch operation as one record
+ * ("keyswitch", "keyswitch_hoisted", "mult_cipher[_ext]" with SURVEY 8(d)
+ * algorithmic bytes; PDL stays on inside it) and every other launch; 0 = off */
 int cgb_timing_enable(cgb_ring *ring, int on);
 /* aggregate of the recorded launches, one line per kernel:
  * "<name> <launches> <total ms> <algorithmic bytes> <algorithmic modular products>\n" */

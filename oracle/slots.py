@@ -9,7 +9,7 @@ code of the hot path (arcc / kv_cache / linear_kernels / encodings) can be
 checked on the CPU against golden vectors recorded from the reference
 (tests/golden/, made by tests/golden/make_golden.py).
 
-Pinned: tests/test_oracle_slots.py replays the reference's own
+Pinned: tests/test_host_slots.py replays the reference's own
 known-answer cases (tests/test_backend.py:63-110 examples, the 200-op
 random program) and compares with golden values recorded from the
 reference itself.

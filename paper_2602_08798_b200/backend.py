@@ -599,6 +599,25 @@ class GpuContext:
         blk, ids = self._encrypt_slots(slots.reshape(1, -1), hook=True)
         return self._emit(blk, ids[0], budget)
 
+    def load_ciphertext_words(self, words, budget: int, cid: int | None = None) -> GpuCiphertext:
+        """Rehydrate a ciphertext-level snapshot (kv_cache.save_cache_ct): raw
+        NTT-domain words uint64[2][L][N] of this context's ring, loaded without
+        decryption; not counted.  ``cid`` restores the snapshot's ciphertext id
+        (the same ciphertext), else a fresh id is issued as load_ciphertext does
+        (backend.py:362-364)."""
+        r = self._ring
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+        if w.shape != (2, r.L, r.N):
+            raise ParameterError(f"ciphertext words of shape {w.shape}, this ring needs {(2, r.L, r.N)}")
+        mods = np.asarray(r.moduli[: r.L], dtype=np.uint64).reshape(1, r.L, 1)
+        if (w >= mods).any():
+            raise ParameterError("ciphertext words are not residues of this ring's moduli")
+        blk, ids = self._new(1)
+        r.load(ids, w.reshape(1, 2, r.L, r.N))
+        if cid is None:
+            return self._emit(blk, ids[0], budget)
+        return GpuCiphertext(blk, ids[0], budget, int(cid), self.params, r)
+
     # -- diagnostics -------------------------------------------------------------------
     def noise_budget_bits(self, ct) -> float:
         """Real invariant noise budget (bits) of a ciphertext; client-side."""

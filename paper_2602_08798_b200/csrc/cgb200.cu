@@ -208,8 +208,14 @@ struct cgb_ring {
   cudaEvent_t pin_left[2] = {nullptr, nullptr};
   u64 launches = 0;
   std::mutex mu;
-  // per-launch timing (cgb_timing_enable): events around every kernel
+  // timing (cgb_timing_enable): mode 1 = events around every kernel (PDL off);
+  // mode 2 = events around every timing GROUP (a whole key switch, a whole
+  // mult_cipher: PDL stays on inside it) and around launches outside groups
   bool timing = false;
+  int timing_mode = 0;
+  int group_depth = 0;
+  cudaEvent_t group_a = nullptr;
+  double group_mm = 0;
   struct Rec {
     const char *name;
     double bytes;
@@ -237,8 +243,22 @@ static T *stage_to_device(cgb_ring *r, const T *host, size_t n, std::vector<void
   CK(cudaMallocAsync((void **)&dev, bytes, r->stream));
   frees.push_back(dev);
   const size_t half = r->pin_cap / 2;
-  if (bytes > half) {  // large payload: staged by the driver
+  if (bytes > half) {  // large payload: straight from the caller's buffer
     CK(cudaMemcpyAsync(dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
+    // A pageable source is staged by the driver before the call returns.  A
+    // page-locked one is DMA'd later, and the caller may free or rewrite it as
+    // soon as we return (torch's caching host allocator hands blocks out again):
+    // wait for the transfer itself before returning.
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, r->stream));
+      CK(cudaEventSynchronize(e));
+      CK(cudaEventDestroy(e));
+    } else {
+      cudaGetLastError();  // unregistered pageable memory may leave an error code behind
+    }
     return dev;
   }
   if (r->pin_off + bytes > half) {  // switch halves
@@ -296,15 +316,30 @@ static void launch_pdl(cgb_ring *r, void (*k)(KP...), dim3 grid, dim3 block, siz
   cfg.stream = r->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = (g_pdl && !r->timing) ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = (g_pdl && r->timing_mode != 1) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, ((KP)args)...);
 }
 static void launch_begin(cgb_ring *r) {
-  if (!r->timing) return;
+  if (!r->timing || r->group_depth) return;
   r->pending = take_event(r);
   CK(cudaEventRecord(r->pending, r->stream));
+}
+// timing groups (mode 2): one record for a whole multi-launch operation, named by
+// the operation, with its algorithmic bytes (SURVEY 8(d) units) and the modular
+// products its launches report
+static void group_begin(cgb_ring *r) {
+  if (r->timing_mode != 2 || r->group_depth++) return;
+  r->group_a = take_event(r);
+  r->group_mm = 0;
+  CK(cudaEventRecord(r->group_a, r->stream));
+}
+static void group_end(cgb_ring *r, const char *name, double bytes) {
+  if (r->timing_mode != 2 || --r->group_depth) return;
+  cudaEvent_t b = take_event(r);
+  CK(cudaEventRecord(b, r->stream));
+  r->recs.push_back({name, bytes, r->group_mm, r->group_a, b});
 }
 // bytes: algorithmic HBM bytes; mm: algorithmic modular products (NTT butterflies,
 // key and constant products) for the arithmetic-pipe roofline
@@ -315,6 +350,10 @@ static void launch_end(cgb_ring *r, const char *name, double bytes, double mm = 
     if (e != cudaSuccess) FAIL(CGB_ERR_CUDA, "launch of %s (N=%d, L=%d): %s", name, r->N, r->L, cudaGetErrorString(e));
   }
   if (!r->timing) return;
+  if (r->group_depth) {
+    r->group_mm += mm;
+    return;
+  }
   cudaEvent_t b = take_event(r);
   CK(cudaEventRecord(b, r->stream));
   r->recs.push_back({name, bytes, mm, r->pending, b});
@@ -497,7 +536,8 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
     }
 #undef LN2
     r->launches++;  // two kernels per transform (launch_end counts the other)
-    launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", 2.0 * bytes, (double)count * job.nsub * (r->N / 2) * r->logN);
+    // algorithmic bytes: each limb-poly read and written once (16 B/word), whatever the passes
+    launch_end(r, fwd ? "ntt_fwd" : "ntt_inv", bytes, (double)count * job.nsub * (r->N / 2) * r->logN);
     return;
   }
   int E = r->ntt_E(), T = r->ntt_threads();
@@ -2471,10 +2511,13 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
 // product.  Every word is the same residue the per-item path computes.
 static bool g_ks_hoist = true;  // CGB_KS_HOIST
 #ifndef CGB_HOIST_MINB
-#define CGB_HOIST_MINB 4  // 4 CTAs of 256 per SM (<= 64 registers)
+#define CGB_HOIST_MINB 4  // 4 CTAs of 256 per SM (<= 64 registers) at L <= 3
 #endif
+// The 64-register cap was measured at L = 3 only (0.189 -> 0.179 ms per 256
+// rotations, profiles/r01/hoist_micro.json; it already spills 72 bytes there).
+// At L = 4 the digit and key arrays alone hold 48 u64, so wider rings keep 2 CTAs.
 template <int L>
-__global__ void __launch_bounds__(256, CGB_HOIST_MINB) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
+__global__ void __launch_bounds__(256, (L <= 3 ? CGB_HOIST_MINB : 2)) k_ks_inner_hoist(u64 *acc, const u64 *D, const u32 *srcidx, KsSrc xin,
                                                         const u64 *const *keys, const ModTab *mods, int iP, int logN,
                                                         int lfirst) {
   // 4 consecutive words per thread: the 4 gathered words of a digit sit in one aligned
@@ -2926,11 +2969,21 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
     KsSrc xin{nullptr, 0, d_src, (u64)L * N, d_g};
     KsSrc c0p{nullptr, 0, d_src, 0, d_g};
     const u64 *const *add1 = add_input ? (const u64 *const *)d_src : nullptr;
-    if (hoist && keyswitch_hoisted(r, S, xin, n, nu, reinterpret_cast<u64 **>(d_blob + 4 * (size_t)n),
-                                   reinterpret_cast<const u32 *>(d_blob + 4 * (size_t)n + nu), d_keys, d_dst, c0p,
-                                   add1))
-      continue;
-    keyswitch(r, S, xin, n, d_keys, d_dst, c0p, add1);
+    // SURVEY 8(d) unit of a batched key switch: each input read once, each output
+    // written once, each distinct evaluation key 2 dnum (L+K) N words read once
+    double key_bytes = 0;
+    if (r->timing_mode == 2) {
+      std::vector<u64> gu(g);
+      std::sort(gu.begin(), gu.end());
+      key_bytes = (double)(std::unique(gu.begin(), gu.end()) - gu.begin()) * 8.0 * 2.0 * L * (L + 1.0) * N;
+    }
+    group_begin(r);
+    const bool hoisted = hoist && keyswitch_hoisted(r, S, xin, n, nu, reinterpret_cast<u64 **>(d_blob + 4 * (size_t)n),
+                                                    reinterpret_cast<const u32 *>(d_blob + 4 * (size_t)n + nu),
+                                                    d_keys, d_dst, c0p, add1);
+    if (!hoisted) keyswitch(r, S, xin, n, d_keys, d_dst, c0p, add1);
+    group_end(r, hoisted ? "keyswitch_hoisted" : "keyswitch",
+              8.0 * (double)ctw * ((hoisted ? nu : n) + n) + key_bytes);
   }
 }
 
@@ -3452,6 +3505,8 @@ int cgb_timing_enable(cgb_ring *r, int on) {
   }
   r->recs.clear();
   r->timing = on != 0;
+  r->timing_mode = on;
+  r->group_depth = 0;
   API_END
 }
 
@@ -4028,6 +4083,9 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
   for (int c0 = 0; c0 < count; c0 += (int)CH) {
     int n = std::min((int)CH, count - c0);
     Scratch S(r);
+    // 8(d) unit: two input and one output ciphertext per item, the relinearisation key once
+    group_begin(r);
+    const double mc_bytes = 8.0 * (double)r->ct_words * 3.0 * n + 8.0 * 2.0 * L * (L + 1.0) * N;
     auto pa = ct_ptrs(r, n, a + c0), pb = ct_ptrs(r, n, b + c0), po = ct_ptrs(r, n, out + c0);
     // inputs: in[item][4][nt][N] with Q limbs = NTT copies; coef[item][4][L][N]
     u64 *in = S.alloc<u64>((size_t)n * 4 * nt * N);
@@ -4089,6 +4147,7 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
     KsSrc xin{d + 2ull * L * N, 3ull * L * N, nullptr, 0, nullptr};
     KsSrc none{nullptr, 0, nullptr, 0, nullptr};
     keyswitch(r, S, xin, n, dk, dout, none, (const u64 *const *)dd01);
+    group_end(r, bx ? "mult_cipher_ext" : "mult_cipher", mc_bytes);
   }
 }
 

@@ -30,7 +30,7 @@ from .encodings import Encoding, EncodingKind, PackedMatrix, block_capacity, loa
 from .nonlinear import MpcChannel, draw_masks, neg_mod
 
 __all__ = ["KVCache", "RefreshEvent", "append_token", "append_token_heads", "cache_stats", "init_cache",
-           "load_cache", "maybe_refresh", "maybe_refresh_heads", "save_cache"]
+           "load_cache", "load_cache_ct", "maybe_refresh", "maybe_refresh_heads", "save_cache", "save_cache_ct"]
 
 SEGMENTS = ("prefill_K", "prefill_V", "auto_K", "auto_V")
 
@@ -285,16 +285,22 @@ def load_cache(path, ctx) -> KVCache:
         raise ParameterError("cache snapshot was taken under different parameters")
     d2, B = man["d2"], man["B"]
     ct_format = man.get("format") == "ciphertext"
+    if ct_format:
+        ring = ctx.ring
+        want = {"N": ring.N, "L": ring.L, "moduli": [int(q) for q in ring.moduli]}
+        if man.get("ring") != want:
+            raise ParameterError("ciphertext snapshot was taken on a different ring (N, L or moduli differ)")
 
     def seg(name, kind, block):
         meta = man["segments"].get(name)
         if meta is None:
             return None
         parts = []
+        ids = meta.get("ids") or [None] * len(meta["budgets"])
         for i, budget in enumerate(meta["budgets"]):
             if ct_format:
                 words = np.load(path / f"{name}_{i}.npy")
-                parts.append(ctx.load_ciphertext_words(words, budget))
+                parts.append(ctx.load_ciphertext_words(words, budget, ids[i]))
             else:
                 vals, _ = load_matrix(path / f"{name}_{i}.bin")
                 parts.append(ctx.load_ciphertext(vals[0], budget))
@@ -316,10 +322,23 @@ def save_cache_ct(cache: KVCache, path, ctx) -> None:
     path = Path(path)
     path.mkdir(parents=True, exist_ok=True)
     man = _manifest(cache, ctx, "ciphertext")
-    man["ring"] = {"N": ctx.ring.N, "L": ctx.ring.L, "moduli": ctx.ring.moduli}
+    ring = ctx.ring
+    man["ring"] = {"N": ring.N, "L": ring.L, "moduli": [int(q) for q in ring.moduli]}
     for name, seg in cache.segments():
-        for i, part in enumerate(seg.parts):
-            np.save(path / f"{name}_{i}.npy", part.words())
+        words = ring.store([pt._aid for pt in seg.parts]) if seg.parts else []
+        for i in range(len(seg.parts)):
+            np.save(path / f"{name}_{i}.npy", words[i])
         man["segments"][name] = {"rows": seg.encoding.rows, "parts": len(seg.parts),
-                                 "budgets": [pt.noise_budget for pt in seg.parts], "slot_period": seg.slot_period}
+                                 "budgets": [pt.noise_budget for pt in seg.parts], "slot_period": seg.slot_period,
+                                 "ids": [int(pt.id) for pt in seg.parts]}
     (path / "manifest.json").write_text(json.dumps(man, indent=2))
+
+
+def load_cache_ct(path, ctx) -> KVCache:
+    """Load a ciphertext-level snapshot (save_cache_ct): the same words, budgets
+    and ids; the manifest's ring must equal ctx's ring.  load_cache reads both
+    formats; this name only insists on the ciphertext one."""
+    man = json.loads((Path(path) / "manifest.json").read_text())
+    if man.get("format") != "ciphertext":
+        raise ParameterError("not a ciphertext-level snapshot")
+    return load_cache(path, ctx)

@@ -69,7 +69,8 @@ class Ring:
     def launches(self) -> int:
         return int(nat.lib().cgb_launch_count(self._h))
 
-    def timing(self, on: bool):
+    def timing(self, on: int):
+        """0 off, 1 every launch (PDL off), 2 every multi-launch operation as one record."""
         nat.check(nat.lib().cgb_timing_enable(self._h, int(on)), "cgb_timing_enable")
 
     def timing_report(self) -> dict:

@@ -15,6 +15,11 @@ CASES = [
     (14, 536903681, 4, 8192, True, 60),   # integer-pipe NTT
     (14, 536903681, 4, 8192, True, 49),   # FP64-pipe NTT
     (13, 536903681, 3, 4096, True, 49),
+    (14, 536903681, 3, 8192, True, 49),   # the benchmarked ring (bench.py decode step)
+    (14, 536903681, 2, 8192, True, 49),
+    (15, 537133057, 4, 16384, True, 49),  # config 5: N = 2^15 (p = 1 mod 2^16)
+    (16, 537133057, 3, 32768, True, 49),  # config 5: N = 2^16 (p = 1 mod 2^17)
+    (13, 536903681, 8, 4096, True, 49),   # config 5: 8 primes
 ]
 
 
