@@ -172,43 +172,108 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def prefill_state(api, new_ctx, args, seed=0):
+    params = api.BackendParams()
+    root = new_ctx(params, seed)
+    fp = api.FixedPointParams(F, P)
+    rng = np.random.default_rng(seed)
+    ctxs = [root.fork() for _ in range(args.heads)]
+    host = [[fp_tokens(rng, args.L, D2) for _ in range(3)] for _ in ctxs]
+    return root, fp, ctxs, host
+
+
+def prefill_config(args):
+    return {"workload": f"prefill_attention_{args.heads}h_L{args.L}", "heads": args.heads, "d_head": D2,
+            "n_slots": N_SLOTS, "plain_modulus": P, "prompt_len": args.L,
+            "l2": "working set > 126 MB L2 (1.5k+ ciphertexts of 768 KiB per wave)",
+            "parallelism": f"replicas{args.gpus}"}
+
+
 def run_prefill(args):
-    """Config 2: encrypted prefill Q.K^T and P.V for `heads` heads at prompt length L."""
+    """Config 2: encrypted prefill Q.K^T and P.V for `heads` heads at prompt length L
+    (arcc.prefill_attention_heads: all heads swept together)."""
     import torch
 
     import paper_2602_08798_b200 as api
     from paper_2602_08798_b200 import _native
     from paper_2602_08798_b200.backend import GpuContext
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     _native.build()
-    params = api.BackendParams()
-    root = GpuContext(params, 0)
-    fp = api.FixedPointParams(F, P)
-    rng = np.random.default_rng(0)
-    ctxs = [root.fork() for _ in range(args.heads)]
-    mats = [[api.encode(fp_tokens(rng, args.L, D2), api.EncodingKind.OUTER, c) for _ in range(3)] for c in ctxs]
-    chans = [api.MpcChannel(P, seed=2000 + h) for h in range(args.heads)]
+    root, fp, ctxs, host = prefill_state(api, GpuContext, args)
     ring = root.ring
     stream = torch.cuda.current_stream()
     ring.set_stream(stream.cuda_stream)
-    run = lambda: api.prefill_attention_heads([m[0] for m in mats], [m[1] for m in mats], [m[2] for m in mats], fp,
-                                              ctxs, chans)
-    run()  # warm-up (key generation)
+    chan_seed = [0]
+
+    def chans():
+        chan_seed[0] += 1
+        return [api.MpcChannel(P, seed=2000 + 100 * chan_seed[0] + h) for h in range(args.heads)]
+
+    def encrypt_all():
+        return [[api.encode(x, api.EncodingKind.OUTER, c) for x in hq] for hq, c in zip(host, ctxs)]
+
+    def run(mats):
+        return api.prefill_attention_heads([m[0] for m in mats], [m[1] for m in mats], [m[2] for m in mats], fp,
+                                           ctxs, chans())
+
+    mats = encrypt_all()
+    run(mats)  # warm-up (key generation)
+    gc.collect()
+    gc.freeze()
     torch.cuda.synchronize()
     l0 = ring.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run(mats)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = ring.launches() - l0
+    # e2e: host plaintext Q, K, V -> client encryption -> prefill -> client decryption of the outputs
+    h0, d0 = ring.h2d_bytes, ring.d2h_bytes
+    torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
-        run()
+        outs = run(encrypt_all())
+        [api.decode(o, c) for o, c in zip(outs, ctxs)]
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    print(json.dumps({"metric": f"HE prefill attention ms (Q.K^T and P.V, {args.heads} heads, L={args.L})",
-                      "value": ms, "unit": "ms", "higher_is_better": False, "steps": args.steps,
-                      "config": {"workload": f"prefill_attention_{args.heads}h_L{args.L}", "heads": args.heads,
-                                 "d_head": D2, "n_slots": N_SLOTS},
-                      "gpu_launches": int((ring.launches() - l0) / args.steps)}), flush=True)
+    ms_e2e = ev0.elapsed_time(ev1) / args.steps
+    h2d, d2h = (ring.h2d_bytes - h0) / args.steps, (ring.d2h_bytes - d0) / args.steps
+    roof, table, _ = unit_roofline(ring, lambda: run(mats), stream, _peaks(), ring.modmul_peak())
+    line = {"metric": f"HE prefill attention ms (Q.K^T and P.V, {args.heads} heads, L={args.L})", "value": ms,
+            "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": 1, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded uniform [-1,1], f=8)", "config": prefill_config(args), "ring": _ring_desc(),
+            "e2e": {"value": ms_e2e, "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches), "roofline": roof, "units": table, "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = prefill_cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+
+
+def prefill_cpu_baseline(args):
+    """ONE head of the same prefill on the reference's CPU path (per-op
+    restatement oracle/reference_path.prefill_attention over the slot emulation),
+    scaled to all heads (heads are independent and identical in op count)."""
+    from oracle import reference_path as ref
+    from oracle.slots import SlotContext
+    import paper_2602_08798_b200 as api
+
+    root, fp, ctxs, host = prefill_state(api, SlotContext, args)
+    mats = [api.encode(x, api.EncodingKind.OUTER, ctxs[0]) for x in host[0]]
+    t0 = time.perf_counter()
+    ref.prefill_attention(*mats, fp, ctxs[0], api.MpcChannel(P, seed=2000))
+    dt = time.perf_counter() - t0
+    return {"value": dt * 1e3 * args.heads, "unit": "ms", "cores": 1, "kind": "port",
+            "sample": f"1 of {args.heads} heads at L={args.L} timed ({dt:.1f} s), x{args.heads}; sequential per-op "
+                      "slot emulation (oracle/reference_path.prefill_attention + oracle/slots.py)",
+            "host": _cpu_model()}
 
 
 GPT2_VOCAB = 50257
@@ -256,13 +321,18 @@ def run_layer(args):
     torch.cuda.synchronize()
     t_pre = time.perf_counter() - t0
     l1 = ring.launches()
+    gc.collect()
+    gc.freeze()
     toks = []
-    for i in range(args.steps):
-        tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
-        toks.append(tok)
-        ev[i + 2].record(stream)
-    torch.cuda.synchronize()
+    h0, d0 = ring.h2d_bytes, ring.d2h_bytes
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for i in range(args.steps):
+            tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
+            toks.append(tok)
+            ev[i + 2].record(stream)
+        torch.cuda.synchronize()
     t_all = time.perf_counter() - t0
+    h2d, d2h = (ring.h2d_bytes - h0) / args.steps, (ring.d2h_bytes - d0) / args.steps
     pre_ms = ev[0].elapsed_time(ev[1])
     step_ms = [ev[i + 1].elapsed_time(ev[i + 2]) for i in range(args.steps)]
     # one more step outside the timed ones with CUDA events around every launch
@@ -272,9 +342,19 @@ def run_layer(args):
     rep = ring.timing_report()
     ring.timing(False)
     kern = {k: {"launches": v[0], "ms": round(v[1], 3)} for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])}
+    roof, table, _ = unit_roofline(ring, lambda: M.decode_step(mdl, state, ctx, chans, force_refresh=True), stream,
+                                   _peaks(), ring.modmul_peak())
+    steady = step_ms[1:] if len(step_ms) > 1 else step_ms
     line = {"metric": f"HE decoder-layer decode ms/token (GPT-2 small layer, prompt {args.L}, "
                       f"{args.steps} tokens, refresh each step)",
+            # value: mean decode ms/token over the timed tokens; the first token also builds the
+            # decode-side weight diagonals once (steady_state_ms_per_token excludes it)
             "value": float(np.mean(step_ms)), "unit": "ms/token", "higher_is_better": False, "n_gpus": 1,
+            "steady_state_ms_per_token": float(np.mean(steady)),
+            "e2e": {"value": float(np.mean(step_ms)), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "note": "decode_step is end to end: host token id in, client-decrypted logits out"},
+            "roofline": roof, "units": table, "clocks": clk.summary(),
             "steps": args.steps, "dtype": "u64", "data": "synthetic (token ids uniform over 50257, N(0,0.02) weights)",
             "config": {"workload": f"gpt2_layer_prompt{args.L}_gen{args.steps}", "d_model": HEADS * D2,
                        "heads": HEADS, "d_ff": 4 * HEADS * D2, "vocab": GPT2_VOCAB, "unembed_vocab": GPT2_VOCAB if args.full_vocab else N_SLOTS,
@@ -310,6 +390,48 @@ def layer_cpu_baseline(args):
     return {"value": dt * 1e3, "unit": "ms/token", "cores": 1, "kind": "port",
             "sample": f"one decode step of the layer at cached length {args.L} (caches by encode), slot emulation",
             "host": _cpu_model()}
+
+
+def unit_roofline(ring, step, stream, hbm_peak: float, peak_mm: float):
+    """Run `step` once with every multi-launch operation timed as one unit
+    (cgb_timing_enable 2, PDL on inside) and return (roofline dict of the batched
+    key switch per SURVEY 8(d), units table, timed step ms)."""
+    import torch
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ring.timing(2)
+    ev0.record(stream)
+    step()
+    ev1.record(stream)
+    units = ring.timing_report()
+    ring.timing(0)
+    unit_step_ms = ev0.elapsed_time(ev1)
+    ks = [units[k] for k in ("keyswitch", "keyswitch_hoisted") if k in units]
+    nl, kms = sum(v[0] for v in ks), sum(v[1] for v in ks)
+    kbytes, kmm = sum(v[2] for v in ks), sum(v[3] for v in ks)
+    achieved = kbytes / (kms * 1e-3) / 1e9 if kms else 0.0
+    roof = {"bound": "hbm", "kernel": "keyswitch (batched hybrid key switch as one unit: 5 fused launches, "
+                                      "or the hoisted variant)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": _traffic_ks(kbytes / nl if nl else 0.0, ring), "launches_per_step": nl,
+            "bytes_per_launch": kbytes / nl if nl else None,
+            "bytes_def": "per batch: (input ct + output ct) x items + 2 dnum (L+1) N x 8 B per distinct key",
+            "share_of_step": kms / unit_step_ms if unit_step_ms else None,
+            "timing": "CUDA events around each whole batched key switch, PDL on inside (cgb_timing_enable 2)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+            "pipe": {"name": "fp64" if ring.fp_ntt else "int64", "unit": "modmul/s",
+                     "achieved": kmm / (kms * 1e-3) if kmm else None, "peak": peak_mm,
+                     "frac": kmm / (kms * 1e-3) / peak_mm if kmm else None,
+                     "peak_source": "cgb_modmul_peak: measured chains of the same modular product"}}
+    table = {k: {"calls": v[0], "ms": round(v[1], 3), "GBps": round(v[2] / (v[1] * 1e-3) / 1e9, 1) if v[1] else None,
+                 "Gmodmul_s": round(v[3] / (v[1] * 1e-3) / 1e9, 1) if v[1] and v[3] else None}
+             for k, v in sorted(units.items(), key=lambda kv: -kv[1][1]) if not k.startswith("(")}
+    return roof, table, unit_step_ms
+
+
+def _peaks():
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    return peaks.get("hbm_gbs", 6650.0)
 
 
 def _traffic_ks(alg_bytes_per_launch: float, ring):

@@ -109,6 +109,18 @@ int cgb_pt_free(cgb_ring *ring, int count, const uint32_t *ids);
 int cgb_pt_encode(cgb_ring *ring, int count, const uint64_t *slots, int kind,
                   const uint32_t *pt_ids);
 
+/* Device-side server masks: MpcChannel.sample_mask(n_slots) (nonlinear.py:86-87,
+ * rng.integers(0, t, n) on numpy's PCG64 -- its 32-bit half-word buffer and Lemire
+ * rejection included) for `count` items, item i drawn from channel chan[i] (a
+ * channel's items in draw order).  st holds 6 words per channel -- state_hi,
+ * state_lo, inc_hi, inc_lo, has_uint32, uinteger (numpy's PCG64 state) -- and is
+ * advanced in place past the draws.  Each mask r_i is encoded as an add_plain
+ * plaintext into pt_pos[i] and t - r_i into pt_neg[i] (either may be NULL);
+ * masks_out (optional, host count x n_slots) receives r.  Replaces the host draws
+ * and uploads of _refresh_part (kv_cache.py:146-153). */
+int cgb_mask_pcg64(cgb_ring *ring, int count, int nchan, const int32_t *chan, uint64_t *st,
+                   const uint32_t *pt_neg, const uint32_t *pt_pos, uint64_t *masks_out);
+
 /* ---- client role ----------------------------------------------------------
  * Context.encrypt (backend.py:307-310): symmetric RLWE encryption; the
  * randomness of ciphertext i is ChaCha20(enc_key, first_index + i). */

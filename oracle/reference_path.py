@@ -10,6 +10,7 @@ does it:
                           fold_sum linear_kernels.py:27-42)
   _dot_into_slot          arcc.py:222-231
   attention_step          arcc.py:320-379
+  prefill_attention       arcc.py:248-317 (_column_period :234-245)
   _append_one/append      kv_cache.py:114-143
   _refresh_part/refresh   kv_cache.py:146-196
   he_to_shares etc.       nonlinear.py:101-144
@@ -179,3 +180,51 @@ def maybe_refresh(cache, ctx, ch, force=False):
     return replace(cache, prefill_K=new.get("prefill_K", cache.prefill_K),
                    prefill_V=new.get("prefill_V", cache.prefill_V), auto_K=new.get("auto_K", cache.auto_K),
                    auto_V=new.get("auto_V", cache.auto_V), refresh_log=cache.refresh_log + tuple(events))
+
+
+def _column_period(P, idx, period, ctx):
+    col = P.parts[idx]
+    if P.slot_period == period:
+        return col
+    return tile_token(col, period, ctx.params.n_slots // period, ctx)
+
+
+def prefill_attention(Q, K, V, fp, ctx, mpc, causal=True):
+    """arcc.py:248-317 op by op (score diagonals from rotated key columns,
+    client softmax, value sweep by _dot_into_slot arcc.py:222-231)."""
+    from paper_2602_08798_b200.encodings import next_pow2
+    from paper_2602_08798_b200.fixedpoint import attention_weights, causal_attention_weights
+
+    m, d2 = Q.encoding.rows, Q.encoding.cols
+    n = ctx.params.n_slots
+    w = next_pow2(m)
+    k_cols = [_column_period(K, c, w, ctx) for c in range(d2)]
+    diag_shares = []
+    for r in range(w):
+        acc = None
+        for c in range(d2):
+            kr = ctx.rotate(k_cols[c], r) if r else k_cols[c]
+            prod = ctx.mult_cipher(Q.parts[c], kr)
+            acc = prod if acc is None else ctx.add(acc, prod)
+        diag_shares.append(he_to_shares(acc, ctx, mpc, length=m))
+    S = np.zeros((m, m), dtype=np.int64)
+    for r, sp in enumerate(diag_shares):
+        vals = reconstruct(sp)
+        for i in range(m):
+            j = (i + r) % w
+            if j < m:
+                S[i, j] = vals[i]
+    A = np.stack([causal_attention_weights(S[i], i, d2, fp) if causal else attention_weights(S[i], d2, fp)
+                  for i in range(m)])
+    mpc.transfer("prefill_softmax", m * m, trips=3 + fp.reciprocal_iters)
+    a_rows = [shares_to_he(share_vector(A[i], mpc), ctx, mpc) for i in range(m)]
+    out_parts = []
+    for c in range(d2):
+        acc = None
+        for i in range(m):
+            prod = ctx.mult_cipher(a_rows[i], V.parts[c])
+            piece = ctx.mult_plain(fold_sum(prod, n, ctx), _one_hot(n, i))
+            acc = piece if acc is None else ctx.add(acc, piece)
+        sp = truncate(he_to_shares(acc, ctx, mpc, length=m), fp, mpc)
+        out_parts.append(shares_to_he(sp, ctx, mpc))
+    return PackedMatrix(Q.encoding, out_parts, encrypted=True, slot_period=None)

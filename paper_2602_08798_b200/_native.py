@@ -17,7 +17,8 @@ import numpy as np
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SO_PATH = PKG / "libcgb200.so"
-SOURCES = [PKG / "csrc" / "cgb200.cu", PKG / "csrc" / "cgb_device.cuh", ROOT / "include" / "cgb200.h"]
+SOURCES = [PKG / "csrc" / "cgb200.cu", PKG / "csrc" / "cgb_device.cuh", PKG / "csrc" / "cgb_masks.cuh",
+           ROOT / "include" / "cgb200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -83,6 +84,8 @@ SIGNATURES = {
     "cgb_pt_alloc": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_pt_free": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_pt_encode": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, ctypes.c_int, _u32p]),
+    "cgb_mask_pcg64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), _u64p, _u32p,
+                                      _u32p, _u64p]),
     "cgb_encrypt": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, _u32p, ctypes.c_uint64, _u32p]),
     "cgb_encrypt_batch": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, _u32p, _u64p, _u32p]),
     "cgb_decrypt": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p]),

@@ -470,7 +470,7 @@ def _truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel, mask=None) -> 
 # ----------------------------------------------------------------------------
 # prefill attention (outer-outer score diagonals), batched over heads
 # ----------------------------------------------------------------------------
-PREFILL_CHUNK = 1024  # ciphertexts per wave in the diagonal / value sweeps
+PREFILL_CHUNK = int(os.environ.get("CGB_PREFILL_CHUNK", "3072"))  # ciphertexts per wave of the sweeps
 
 
 def prefill_attention(Q, K, V, fp: FixedPointParams, ctx, mpc: MpcChannel, causal: bool = True) -> PackedMatrix:
@@ -479,6 +479,14 @@ def prefill_attention(Q, K, V, fp: FixedPointParams, ctx, mpc: MpcChannel, causa
 
 
 def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal: bool = True) -> list:
+    """``prefill_attention`` (arcc.py:248-317) for H independent heads, swept
+    together: every score-diagonal shift r is ONE batched key switch over all
+    heads' K columns (one Galois key for H x d2 ciphertexts), and the value
+    sweep's products, folds and one-hot selections run over all heads' columns
+    in the same waves.  Head h uses ctxs[h] and mpcs[h] exactly as its own
+    prefill_attention call would: its masks are drawn and its transcript
+    written in the reference's order, so outputs, ids, counters and transcripts
+    equal H sequential calls (tests/test_gpu_hotpath.py)."""
     H = len(Qs)
     c0 = ctxs[0]
     C = _C(c0)
@@ -489,45 +497,60 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
                 raise ParameterError(f"{name} must be an encrypted outer packing")
         if not (Q.encoding == K.encoding == V.encoding):
             raise ParameterError("Q, K, V disagree on dimensions")
-    results = []
-    for h in range(H):  # heads share no state; per head, sweep in chunks
-        Q, K, V, ctx, mpc = Qs[h], Ks[h], Vs[h], ctxs[h], mpcs[h]
-        m, d2 = Q.encoding.rows, Q.encoding.cols
-        w = next_pow2(m)
-        Kw = C.wave_of(K.parts, [ctx] * d2)
-        if K.slot_period == w:
-            kcols = Kw
-        elif K.slot_period is None:
-            kcols = tile_wave(Kw, w, n // w)
-        else:
-            raise ParameterError(f"column padding period {K.slot_period} incompatible with {w}")
-        Qw = C.wave_of(Q.parts, [ctx] * d2)
-        # score diagonals r = 0..w-1: acc_r = sum_c Q_c * rot(K_c, r)
-        diag_shares = []
-        rs_per = max(1, PREFILL_CHUNK // d2)
-        for r0 in range(0, w, rs_per):
-            rs = np.arange(r0, min(w, r0 + rs_per))
-            items_r = np.repeat(rs, d2)
-            items_c = np.tile(np.arange(d2), rs.size)
-            nz = np.nonzero(items_r > 0)[0]
-            z = np.nonzero(items_r == 0)[0]
-            pieces = []
-            if z.size:
-                pieces.append(kcols.take(items_c[z]))
-            if nz.size:
-                pieces.append(C.w_rotate(kcols.take(items_c[nz]), items_r[nz]))
-            order = np.concatenate([z, nz])
-            kr = type(kcols).concat(pieces).take(np.argsort(order))
-            # Q's columns recur for every row shift: the resident operand (mult_cipher is
-            # symmetric word for word -- (a0 b0, a0 b1 + a1 b0, a1 b1) -- and both operands
-            # belong to the head's context)
-            prods = C.w_mult_cipher(kr, Qw.take(items_c), resident_b=True)
-            acc = C.w_sum(prods, [np.arange(i * d2, (i + 1) * d2) for i in range(rs.size)])
-            diag_shares.extend(he_to_shares_wave(acc, [mpc] * rs.size, [m] * rs.size))
-        # client: rebuild S from its diagonals, causal softmax per row
+    shapes = {(Q.encoding.rows, Q.encoding.cols, K.slot_period) for Q, K in zip(Qs, Ks)}
+    if len(shapes) > 1 or len({id(c) for c in ctxs}) < H:
+        # heads of different shapes, or sharing a context (whose draws would interleave):
+        # one head at a time
+        return [prefill_attention_heads([Qs[h]], [Ks[h]], [Vs[h]], fp, [ctxs[h]], [mpcs[h]], causal)[0]
+                for h in range(H)]
+    m, d2 = Qs[0].encoding.rows, Qs[0].encoding.cols
+    w = next_pow2(m)
+    Kw = type(C.wave_of(Ks[0].parts, [ctxs[0]] * d2)).concat(
+        [C.wave_of(Ks[h].parts, [ctxs[h]] * d2) for h in range(H)])
+    period = Ks[0].slot_period
+    if period == w:
+        kcols = Kw
+    elif period is None:
+        kcols = tile_wave(Kw, w, n // w)  # item h d2 + c
+    else:
+        raise ParameterError(f"column padding period {period} incompatible with {w}")
+    Qw = type(Kw).concat([C.wave_of(Qs[h].parts, [ctxs[h]] * d2) for h in range(H)])
+    # ---- score diagonals r = 0..w-1: acc_{h,r} = sum_c Q_{h,c} * rot(K_{h,c}, r) ----
+    diag_shares = [[] for _ in range(H)]
+    rs_per = max(1, PREFILL_CHUNK // (d2 * H))
+    for r0 in range(0, w, rs_per):
+        rs = np.arange(r0, min(w, r0 + rs_per))
+        # items (r, h, c): one shift's H x d2 columns together, one key
+        it_r = np.repeat(rs, H * d2)
+        it_hc = np.tile(np.arange(H * d2), rs.size)
+        nz = np.nonzero(it_r > 0)[0]
+        z = np.nonzero(it_r == 0)[0]
+        pieces = []
+        if z.size:
+            pieces.append(kcols.take(it_hc[z]))
+        if nz.size:
+            pieces.append(C.w_rotate(kcols.take(it_hc[nz]), it_r[nz]))
+        order = np.concatenate([z, nz])
+        kr = type(kcols).concat(pieces).take(np.argsort(order))
+        # Q's columns recur for every row shift: the resident operand (mult_cipher is
+        # symmetric word for word -- (a0 b0, a0 b1 + a1 b0, a1 b1) -- and both operands
+        # belong to the head's context)
+        prods = C.w_mult_cipher(kr, Qw.take(it_hc), resident_b=True)
+        groups = [np.arange(g * d2, (g + 1) * d2) for g in range(rs.size * H)]  # group (r, h)
+        acc = C.w_sum(prods, groups)
+        # he_to_shares per head in r order (each head's channel draws its diagonals in order)
+        g_h = np.tile(np.arange(H), rs.size)
+        by_head = np.argsort(g_h, kind="stable")  # (h, r) order
+        sh = he_to_shares_wave(acc.take(by_head), [mpcs[h] for h in g_h[by_head]], [m] * by_head.size)
+        for k, gi in enumerate(by_head):
+            diag_shares[g_h[gi]].append(sh[k])
+    # ---- client: S from its diagonals, causal softmax per row; rows back encrypted ----
+    a_rows, plans = [], []
+    i = np.arange(m)
+    for h in range(H):
+        mpc, ctx = mpcs[h], ctxs[h]
         S = np.zeros((m, m), dtype=np.int64)
-        i = np.arange(m)
-        for r, sp in enumerate(diag_shares):
+        for r, sp in enumerate(diag_shares[h]):
             vals = reconstruct(sp)
             j = (i + r) % w
             ok = j < m
@@ -536,37 +559,41 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
                       for k in range(m)])
         mpc.transfer("prefill_softmax", m * m, trips=3 + fp.reciprocal_iters)
         rows_sp = [share_vector(A[k], mpc) for k in range(m)]
-        a_rows = shares_to_he_wave(rows_sp, [ctx] * m, [mpc] * m)
-        # values: column c gets sum_i dot_into_slot(a_row_i, V_c, i).  The
-        # reference draws (he_to_shares: n words, truncate: m words) column by
-        # column; the chunked sweep pre-draws them in that order.
-        plan = [(mpc.sample_mask(n), mpc.sample_mask(m)) for _ in range(d2)]
-        Vw = C.wave_of(V.parts, [ctx] * d2)
-        cols_per = max(1, PREFILL_CHUNK // m)
-        out_parts = [None] * d2
-        for c0_ in range(0, d2, cols_per):
-            cs = np.arange(c0_, min(d2, c0_ + cols_per))
-            it_c = np.repeat(cs, m)
-            it_i = np.tile(np.arange(m), cs.size)
-            prods = C.w_mult_cipher(a_rows.take(it_i), Vw.take(it_c), resident_b=True)
-            tot = fold_wave(prods, n)
-            pieces = C.w_mult_plain(tot, _onehots(n, it_i))
-            acc = C.w_sum(pieces, [np.arange(k * m, (k + 1) * m) for k in range(cs.size)])
-            # he_to_shares with the planned masks, then truncate / re-encrypt
-            r = np.stack([plan[c][0] for c in cs])
-            masked = C.w_add_plain(acc, (p - r) % p, one_shot=True)
-            client = C.w_decrypt(masked)
-            trs = []
-            for k, c in enumerate(cs):
-                mpc.transfer("he_to_shares", n)
-                sp = SharePair(client[k, :m].copy(), r[k, :m].copy(), p, m)
-                trs.append(_truncate(sp, fp, mpc, mask=plan[c][1]))
-            hs = shares_to_he_wave(trs, [ctx] * cs.size, [mpc] * cs.size, record=False).handles()
-            for k, c in enumerate(cs):
-                out_parts[c] = hs[k]
-            _reorder_transcript(mpc, cs.size, n)
-        results.append(PackedMatrix(Q.encoding, out_parts, encrypted=True, slot_period=None))
-    return results
+        a_rows.append(shares_to_he_wave(rows_sp, [ctx] * m, [mpc] * m))
+        # values: column c gets sum_i dot_into_slot(a_row_i, V_c, i).  The reference
+        # draws (he_to_shares: n words, truncate: m words) column by column; the
+        # batched sweep pre-draws them in that order
+        plans.append([(mpc.sample_mask(n), mpc.sample_mask(m)) for _ in range(d2)])
+    Aw = type(a_rows[0]).concat(a_rows)  # item h m + i
+    Vw = type(Kw).concat([C.wave_of(Vs[h].parts, [ctxs[h]] * d2) for h in range(H)])  # item h d2 + c
+    out_parts = [[None] * d2 for _ in range(H)]
+    cols_per = max(1, PREFILL_CHUNK // (m * H))
+    for c0_ in range(0, d2, cols_per):
+        cs = np.arange(c0_, min(d2, c0_ + cols_per))
+        # items (h, c, i), group (h, c)
+        hc = [(h, c) for h in range(H) for c in cs]
+        it_a = np.concatenate([h * m + np.arange(m) for h, c in hc])
+        it_v = np.repeat([h * d2 + c for h, c in hc], m)
+        it_i = np.tile(np.arange(m), len(hc))
+        prods = C.w_mult_cipher(Aw.take(it_a), Vw.take(it_v), resident_b=True)
+        tot = fold_wave(prods, n)
+        pieces = C.w_mult_plain(tot, _onehots(n, it_i))
+        acc = C.w_sum(pieces, [np.arange(k * m, (k + 1) * m) for k in range(len(hc))])
+        # he_to_shares with the planned masks, then truncate / re-encrypt
+        r = np.stack([plans[h][c][0] for h, c in hc])
+        masked = C.w_add_plain(acc, (p - r) % p, one_shot=True)
+        client = C.w_decrypt(masked)
+        trs = []
+        for k, (h, c) in enumerate(hc):
+            mpcs[h].transfer("he_to_shares", n)
+            sp = SharePair(client[k, :m].copy(), r[k, :m].copy(), p, m)
+            trs.append(_truncate(sp, fp, mpcs[h], mask=plans[h][c][1]))
+        hs = shares_to_he_wave(trs, [ctxs[h] for h, _ in hc], [mpcs[h] for h, _ in hc], record=False).handles()
+        for k, (h, c) in enumerate(hc):
+            out_parts[h][c] = hs[k]
+        for h in range(H):
+            _reorder_transcript(mpcs[h], cs.size, n)
+    return [PackedMatrix(Qs[h].encoding, out_parts[h], encrypted=True, slot_period=None) for h in range(H)]
 
 
 def _reorder_transcript(mpc: MpcChannel, k: int, n: int):

@@ -767,6 +767,16 @@ class GpuContext:
         return GpuContext._plain_op(wave, vecs, nat.CGB_PT_ADD, "add_plain", one_shot, canonical)
 
     @staticmethod
+    def w_add_plain_ids(wave: Wave, pts) -> Wave:
+        """add_plain per item with already-encoded plaintexts (arena ids of kind
+        CGB_PT_ADD, e.g. device-drawn masks); charged like w_add_plain."""
+        c0 = wave.ctxs[0]
+        b = GpuContext._spend_all(wave.budgets, c0.params.noise_costs.add_plain)
+        blk, ids = c0._new(len(wave))
+        c0._ring.add_plain(wave.aids, pts, ids)
+        return Wave(wave.ctxs, wave.owner, ids, b, [blk], GpuContext._charge(wave, "add_plain"))
+
+    @staticmethod
     def w_mult_plain(wave: Wave, vecs, one_shot: bool = False) -> Wave:
         return GpuContext._plain_op(wave, vecs, nat.CGB_PT_MUL, "mult_plain", one_shot)
 

@@ -20,6 +20,7 @@
 
 #include "../../include/cgb200.h"
 #include "cgb_device.cuh"
+#include "cgb_masks.cuh"
 
 using namespace cgb;
 typedef unsigned __int128 u128;
@@ -984,6 +985,12 @@ __host__ __device__ constexpr int ksr_data_words(int LB) {
              ? ((((NTT2_TILE >> LB) * fpr_padm(LB, 1)) + 1) & ~1)
              : 32 * (NTT2_TILE / 16);
 }
+#ifndef CGB_KSROW_KSTAGE
+#define CGB_KSROW_KSTAGE 0  // key words cp.async-staged in shared memory during the row pass: measured slower
+                                  // (28.8 -> 42.6 ms ks_row_md per decode step; 36.6 with TWW, profiles/r02/ab_kstage.log)
+#endif
+// bytes of k_ks_row's key staging area: 2 polys x 16 words per thread x 128 threads
+constexpr int KSTAGE_BYTES = CGB_KSROW_KSTAGE ? 2 * 16 * 8 * (NTT2_TILE / 16) : 0;
 #ifndef CGB_KSROW_MINB
 #define CGB_KSROW_MINB 3  // <= 168 registers: 3 CTAs per SM (MODE 2 would otherwise take 208)
 #endif
@@ -1103,9 +1110,33 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   double a0[E], a1[E];
 #pragma unroll
   for (int i = 0; i < E; i++) a0[i] = a1[i] = 0.0;
+#if CGB_KSROW_KSTAGE
+  // digit j's key words (both polys) for this thread's 16 output positions, staged by
+  // cp.async while the digit's tile loads and its row pass runs; chunk c (16 bytes) of
+  // thread t at [c][t] (conflict-free 128-bit reads), 8 chunks per poly
+  constexpr int T_ = NTT2_TILE / 16;
+  double2 *kst = reinterpret_cast<double2 *>(sm3 + ksr_data_words(LM) +
+                                              (CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 1 : 2) * (NTT2_TILE + (NTT2_TILE >> LB))));
+  auto stage_keys = [&](int j) {
+    const u64 *KF = K + 2 * (u64)L * 2 * LP * N;
+    const u64 *k0 = KF + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = KF + ((u64)(j * 2 + 1) * LP + l) * N + row0;
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k += 2) {
+        const int c = (u * PB::K + k) / 2, o = PB::idx(tl, u, k);
+        cp_async16(&kst[c * T_ + tid], k0 + o);
+        cp_async16(&kst[(8 + c) * T_ + tid], k1 + o);
+      }
+    cp_async_commit();
+  };
+#endif
 #pragma unroll 1
   for (int j = 0; j < L; j++) {
     prefetch_next(j);
+#if CGB_KSROW_KSTAGE
+    stage_keys(j);
+#endif
     double x[E];
     if (j == l) {  // the digit's own limb: the input itself, already in NTT form
 #if CGB_KSROW_G4
@@ -1138,6 +1169,27 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
     }
     // the key's FP64 plane (k_key_fp): exact doubles, no per-word conversion
+#if CGB_KSROW_KSTAGE
+    cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k += 4) {
+        const int c = (u * PB::K + k) / 2;
+        const double2 p0 = kst[c * T_ + tid], p1 = kst[(c + 1) * T_ + tid];
+        const double2 q0 = kst[(8 + c) * T_ + tid], q1 = kst[(9 + c) * T_ + tid];
+        const double w0d[4] = {p0.x, p0.y, p1.x, p1.y}, w1d[4] = {q0.x, q0.y, q1.x, q1.y};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const double xv = x[u * PB::K + k + e];
+          const double d0 = w0d[e], d1 = w1d[e];
+          a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+          a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+        }
+      }
+    if (false)
+#endif
+    {
     const u64 *KF = K + 2 * (u64)L * 2 * LP * N;
     const u64 *k0 = KF + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = KF + ((u64)(j * 2 + 1) * LP + l) * N + row0;
 #pragma unroll
@@ -1156,6 +1208,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
           a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
         }
       }
+    }
   }
   if constexpr (MODE == 2) {  // ModDown: row pass of W[pp][l] (same forward twiddles), combine, store
 #pragma unroll 1
@@ -1401,9 +1454,9 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
 }
 
 template <int LA, int LB>
-static size_t ks_row_smem() {  // exchange tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
+__host__ __device__ constexpr size_t ks_row_smem() {  // exchange tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
   return sizeof(u64) * (size_t)ksr_data_words(LB) +
-         (CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 8 : 16) * (size_t)(NTT2_TILE + (NTT2_TILE >> LB)));
+         (CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 8 : 16) * (size_t)(NTT2_TILE + (NTT2_TILE >> LB))) + KSTAGE_BYTES;
 }
 template <int LA, int LB, int L>
 static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in
@@ -3671,6 +3724,15 @@ int cgb_ct_load(cgb_ring *r, int count, const uint32_t *ids, const uint64_t *hos
   API_END
 }
 
+// plaintext polys m[count][N] (coefficient form mod t) -> encoded plaintexts of `kind`
+static void pt_from_coeffs(cgb_ring *r, Scratch &S, const u64 *m, int count, int kind, const uint32_t *pt_ids) {
+  auto pp = pt_ptrs(r, count, pt_ids);
+  u64 **dp = S.up(pp.data(), count);
+  u64 words = (u64)r->L * r->N;
+  LAUNCH("pt_lift", BYTES_pt_lift, k_pt_lift<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dp, m, r->d_mods, r->d_c, r->L, r->logN, kind));
+  std::vector<int> qm;
+  ntt_items(r, true, nullptr, dp, 0, count, 1, r->L, q_mod_idx(r, qm));
+}
 int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const uint32_t *pt_ids) {
   API_BEGIN
   if (count <= 0) return CGB_OK;
@@ -3678,12 +3740,116 @@ int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const
   Scratch S(r);
   u64 *m = S.alloc<u64>((size_t)count * r->N);
   encode_slots(r, S, slots, count, m);
-  auto pp = pt_ptrs(r, count, pt_ids);
-  u64 **dp = S.up(pp.data(), count);
-  u64 words = (u64)r->L * r->N;
-  LAUNCH("pt_lift", BYTES_pt_lift, k_pt_lift<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(dp, m, r->d_mods, r->d_c, r->L, r->logN, kind));
-  std::vector<int> qm;
-  ntt_items(r, true, nullptr, dp, 0, count, 1, r->L, q_mod_idx(r, qm));
+  pt_from_coeffs(r, S, m, count, kind, pt_ids);
+  API_END
+}
+
+// device slot vectors (residues mod t) -> coefficient-form plaintext polys; neg: (t - s) mod t
+__global__ void k_scatter_slots_dev(u64 *m, const u64 *slots, const u32 *slot_idx, int n, u64 t, int logN, int neg) {
+  int item = blockIdx.y;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 v = slots[(u64)item * n + i];
+  m[((u64)item << logN) + slot_idx[i]] = neg ? (v ? t - v : 0) : v;
+}
+
+int cgb_mask_pcg64(cgb_ring *r, int count, int nchan, const int32_t *chan, uint64_t *st, const uint32_t *pt_neg,
+                   const uint32_t *pt_pos, uint64_t *masks_out) {
+  API_BEGIN
+  using namespace cgbmask;
+  if (count <= 0) return CGB_OK;
+  if (nchan <= 0 || r->t >= (1ull << 32)) FAIL(CGB_ERR_PARAM, "mask stream: %d channels, bound %llu", nchan,
+                                               (unsigned long long)r->t);
+  const int n = r->n_slots;
+  const u32 p = (u32)r->t, thr = (u32)((0x100000000ull - p) % p);
+  std::vector<std::vector<u32>> per(nchan);
+  for (int i = 0; i < count; i++) {
+    if (chan[i] < 0 || chan[i] >= nchan) FAIL(CGB_ERR_PARAM, "item %d: channel %d out of range", i, chan[i]);
+    per[chan[i]].push_back((u32)i);
+  }
+  std::vector<u32> items;
+  std::vector<Chan> C(nchan);
+  for (int c = 0; c < nchan; c++) {
+    C[c].state = {st[6 * c + 0], st[6 * c + 1]};
+    C[c].inc = {st[6 * c + 2], st[6 * c + 3]};
+    C[c].has_u32 = (u32)st[6 * c + 4];
+    C[c].uinteger = (u32)st[6 * c + 5];
+    C[c].item0 = items.size();
+    C[c].need = (u64)per[c].size() * n;
+    items.insert(items.end(), per[c].begin(), per[c].end());
+  }
+  Scratch S(r);
+  u64 *slots = S.alloc<u64>((size_t)count * n);
+  u32 *d_items = S.up(items.data(), items.size());
+  std::vector<long long> last(nchan);
+  // the stream is cut with a margin over the expected 1/(1 - 2^-3) draws per accepted
+  // value (rejection rate (2^32 mod p) / 2^32 < 1/8 for p > 2^29); cut again, longer,
+  // in the (never observed) case it falls short
+  for (double margin = 1.25;; margin *= 1.5) {
+    std::vector<u64> tb(nchan + 1, 0);
+    u64 total = 0;
+    for (int c = 0; c < nchan; c++) {
+      const u64 outs = ((u64)((double)C[c].need * margin / 2.0) + 1024 + GEN_CHUNK - 1) / GEN_CHUNK * GEN_CHUNK;
+      C[c].base = total;
+      C[c].halves = C[c].has_u32 + 2 * outs;
+      total += C[c].halves;
+      tb[c + 1] = tb[c] + outs / GEN_CHUNK;
+    }
+    Chan *d_ch = S.up(C.data(), C.size());
+    u64 *d_tb = S.up(tb.data(), tb.size());
+    u32 *val = S.alloc<u32>(total), *flag = S.alloc<u32>(total), *idx = S.alloc<u32>(total);
+    long long *d_last = S.alloc<long long>(nchan);
+    CK(cudaMemsetAsync(d_last, 0xff, sizeof(long long) * nchan, r->stream));
+    LAUNCH("mask_gen", 8.0 * (double)total,
+           k_pcg_gen<<<(unsigned)((tb[nchan] + 127) / 128), 128, 0, r->stream>>>(d_ch, nchan, d_tb, val, flag, p, thr));
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, idx, (int)total, r->stream));
+    void *tmp = S.alloc<char>(tmp_bytes);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, (int)total, r->stream));
+    LAUNCH("mask_scatter", 12.0 * (double)total + 8.0 * count * n,
+           k_pcg_scatter<<<(unsigned)((total + 255) / 256), 256, 0, r->stream>>>(d_ch, nchan, idx, val, flag, total, d_items, n, slots, d_last));
+    CK(cudaMemcpyAsync(last.data(), d_last, sizeof(long long) * nchan, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaStreamSynchronize(r->stream));
+    bool ok = true;
+    for (int c = 0; c < nchan; c++) ok = ok && (C[c].need == 0 || last[c] >= 0);
+    if (ok) break;
+    if (margin > 8) FAIL(CGB_ERR_STATE, "mask stream too short");
+  }
+  // the channels' generator states after the draws (numpy's PCG64 state layout)
+  for (int c = 0; c < nchan; c++) {
+    if (C[c].need == 0) continue;
+    const long long lh = last[c];
+    // numpy keeps the high half of the last split output in `uinteger` (buffered when
+    // its low half was the last word consumed, stale but kept otherwise)
+    u64 steps = 0, has = 0, uint = st[6 * c + 5];
+    if (!(C[c].has_u32 && lh == 0)) {
+      const u64 k = (u64)lh - C[c].has_u32;  // index among the 64-bit outputs' halves
+      steps = k / 2 + 1;
+      has = (k & 1) ? 0 : 1;
+      uint = pcg_output(pcg_advance(C[c].state, C[c].inc, steps)) >> 32;
+    }
+    const U128 ns = pcg_advance(C[c].state, C[c].inc, steps);
+    st[6 * c + 0] = ns.hi;
+    st[6 * c + 1] = ns.lo;
+    st[6 * c + 4] = has;
+    st[6 * c + 5] = uint;
+  }
+  u64 *m = S.alloc<u64>((size_t)count * r->N);
+  for (int neg = 0; neg < 2; neg++) {
+    const uint32_t *ids = neg ? pt_neg : pt_pos;
+    if (!ids) continue;
+    CK(cudaMemsetAsync(m, 0, sizeof(u64) * (size_t)count * r->N, r->stream));
+    LAUNCH("scatter_slots", BYTES_scatter_slots,
+           k_scatter_slots_dev<<<dim3(GRID1(n, TPB).x, count), TPB, 0, r->stream>>>(m, slots, r->d_slot_idx, n, r->t,
+                                                                                   r->logN, neg));
+    int mi = r->iT;
+    ntt_items(r, false, m, nullptr, r->N, count, 1, 1, &mi);
+    pt_from_coeffs(r, S, m, count, CGB_PT_ADD, ids);
+  }
+  if (masks_out) {
+    CK(cudaMemcpyAsync(masks_out, slots, sizeof(u64) * (size_t)count * n, cudaMemcpyDeviceToHost, r->stream));
+    CK(cudaStreamSynchronize(r->stream));
+  }
   API_END
 }
 

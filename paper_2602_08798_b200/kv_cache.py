@@ -25,9 +25,9 @@ from pathlib import Path
 
 import numpy as np
 
-from .backend import ParameterError, PlainBatch
+from .backend import ParameterError, PlainBatch, _pt_cache
 from .encodings import Encoding, EncodingKind, PackedMatrix, block_capacity, load_matrix, save_matrix
-from .nonlinear import MpcChannel, draw_masks, neg_mod
+from .nonlinear import MpcChannel, device_masks, device_masks_ok, draw_masks, neg_mod
 
 __all__ = ["KVCache", "RefreshEvent", "append_token", "append_token_heads", "cache_stats", "init_cache",
            "load_cache", "load_cache_ct", "maybe_refresh", "maybe_refresh_heads", "save_cache", "save_cache_ct"]
@@ -207,17 +207,32 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
                     sel.append((h, name, i, part))
     if not sel:
         return list(caches)
-    # masks drawn per part in order from each head's channel
-    r = draw_masks([chans[s[0]] for s in sel], n)
+    # masks drawn per part in order from each head's channel: on the device when the
+    # backend can (numpy's PCG64 stream reproduced bit-exactly, nonlinear.device_masks),
+    # else on the host
+    item_chans = [chans[s[0]] for s in sel]
     owners = [ctxs[s[0]] for s in sel]
     start = {id(c): c._next_id for c in owners}
     wave = C.wave_of([s[3] for s in sel], owners)
-    masked = C.w_add_plain(wave, neg_mod(r, p), one_shot=True, canonical=True)
+    on_device = hasattr(C, "w_add_plain_ids") and device_masks_ok(item_chans)
+    if on_device:
+        ring = c0.ring
+        _pt_cache(ring).make_room(2 * len(sel))
+        pt_neg, pt_pos, _ = device_masks(ring, item_chans)
+        masked = C.w_add_plain_ids(wave, pt_neg)
+    else:
+        r = draw_masks(item_chans, n)
+        masked = C.w_add_plain(wave, neg_mod(r, p), one_shot=True, canonical=True)
     view = C.w_decrypt(masked)
     fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view, canonical=True)
     for h, _, _, _ in sel:
         chans[h].transfer("refresh", n, trips=2)
-    restored = _retag(C.w_add_plain(fresh, r, one_shot=True, canonical=True).handles(), _chain_ids(owners, [3] * len(sel), start))
+    if on_device:
+        restored = C.w_add_plain_ids(fresh, pt_pos)
+        ring.free_pt(np.concatenate([pt_neg, pt_pos]))  # stream-ordered after their last use
+    else:
+        restored = C.w_add_plain(fresh, r, one_shot=True, canonical=True)
+    restored = _retag(restored.handles(), _chain_ids(owners, [3] * len(sel), start))
     out = []
     for h, cache in enumerate(caches):
         mine = [(k, s) for k, s in enumerate(sel) if s[0] == h]

@@ -13,8 +13,9 @@ ledger budgets), the channels (one per (layer, head) plus "common", seeded
 as model.py:388-398), the client-side fixed-point arithmetic (truncation,
 GELU, LayerNorm, softmax) and hence every decrypted value: the generated
 tokens and logits equal the reference's.  Mask draws and transcript entries
-follow wave order (item by item per channel), which changes share values but
-not results: every conversion reconstructs exactly.
+follow the reference's per-op order within every channel (``_trunc_wave``
+draws and records item by item), so share values, masks and transcripts equal
+the reference's too (tests/test_layer.py pins them).
 
 Out of the reference: a vocab-50257 unembedding cannot be
 diagonal-packed at n = 8192; here a vocabulary wider than n is unembedded in
@@ -35,7 +36,8 @@ from .encodings import EncodingKind, PackedMatrix, encode
 from .fixedpoint import FixedPointParams, fp_gelu, fp_layernorm_rows, fp_truncate, to_signed
 from .kv_cache import append_token_heads, init_cache, maybe_refresh_heads
 from .linear_kernels import cpmm_outer_diagonal, cpvm_inner_diagonal, cpvm_inner_diagonal_heads
-from .nonlinear import MpcChannel, he_to_shares_wave, reconstruct, share_vector, shares_to_he_wave, truncate
+from .nonlinear import (MpcChannel, SharePair, _pool, he_to_shares_wave, host_buffer, neg_mod, reconstruct, share_vector,
+                        shares_to_he_wave)
 
 __all__ = ["GenerationState", "Model", "ModelConfig", "decode_step", "generate", "gpt2_layer_model", "prefill"]
 
@@ -153,9 +155,57 @@ def _C(ctx):
 
 
 def _trunc_wave(wave, lengths, fp, ctxs, chans):
-    """Per item: he_to_shares -> truncate -> shares_to_he (model.py:372-377)."""
-    sp = he_to_shares_wave(wave, chans, lengths)
-    return shares_to_he_wave([truncate(s, fp, ch) for s, ch in zip(sp, chans)], ctxs, chans)
+    """Per item: he_to_shares -> truncate -> shares_to_he (model.py:370-375,
+    :526-531), as one wave.  The reference runs the three steps item by item, so
+    each channel draws (n words for the masked decryption, then `length` words
+    for the truncation's re-share) and records (he_to_shares, truncate,
+    shares_to_he) per item; the masks are drawn and the transcript written in
+    exactly that order here, so every share, mask and transcript entry equals
+    the per-op code's."""
+    C = type(wave.ctxs[0])
+    params = wave.ctxs[0].params
+    n, p = params.n_slots, params.plain_modulus
+    lengths = [int(x) for x in lengths]
+    r_dec, r_tr = _draw_in_order(chans, [(n, L) for L in lengths])
+    masked = C.w_add_plain(wave, neg_mod(r_dec, p), one_shot=True, canonical=True)
+    client = C.w_decrypt(masked)
+    shares = []
+    for i, (ch, L) in enumerate(zip(chans, lengths)):
+        v = client[i, :L] + r_dec[i, :L]  # reconstruct: both shares in [0, p)
+        v = np.where(v >= p, v - p, v)
+        out = np.mod(fp_truncate(to_signed(v, p), fp.f), p)
+        d = out - r_tr[i]
+        d[d < 0] += p
+        shares.append(SharePair(d, r_tr[i], p, L))
+        ch.transfer("he_to_shares", n)
+        ch.transfer("truncate", L, trips=3)
+        ch.transfer("shares_to_he", n)
+    return shares_to_he_wave(shares, ctxs, chans, record=False)
+
+
+def _draw_in_order(chans, plan):
+    """Item i draws plan[i] = (a, b): a words, then b words, from chans[i]; each
+    channel's items in list order (its sequence of per-op draws), distinct
+    channels on parallel host threads.  Returns (rows of a words, list of b-word arrays)."""
+    a = plan[0][0] if plan else 0
+    first = host_buffer((len(chans), a))
+    second = [None] * len(chans)
+    groups = {}
+    for i, ch in enumerate(chans):
+        groups.setdefault(id(ch), (ch, []))[1].append(i)
+
+    def fill(item):
+        ch, idx = item
+        for i in idx:
+            first[i] = ch.sample_mask(plan[i][0])
+            second[i] = ch.sample_mask(plan[i][1])
+
+    if len(groups) > 1 and len(chans) * a >= (1 << 20):
+        list(_pool().map(fill, groups.values()))
+    else:
+        for item in groups.values():
+            fill(item)
+    return first, second
 
 
 def _vector_roundtrips(wave, lengths, ctxs, chans, fns):

@@ -165,6 +165,51 @@ def draw_masks(chans, n: int) -> np.ndarray:
     return out
 
 
+DEVICE_MASKS = os.environ.get("CGB_DEVICE_MASKS", "1") != "0"
+_M64 = (1 << 64) - 1
+
+
+def _pcg_state_words(ch: "MpcChannel") -> list:
+    st = ch.rng.bit_generator.state
+    if st["bit_generator"] != "PCG64":
+        raise ParameterError("device masks reproduce numpy's PCG64 only")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    return [s >> 64, s & _M64, inc >> 64, inc & _M64, int(st["has_uint32"]), int(st["uinteger"])]
+
+
+def device_masks_ok(chans) -> bool:
+    """Whether these channels' next masks can be drawn on the device: numpy PCG64
+    generators with no masks pre-drawn on the host (those come first)."""
+    return DEVICE_MASKS and all(not ch._pre and type(ch.rng.bit_generator).__name__ == "PCG64" for ch in chans)
+
+
+def device_masks(ring, chans, want_neg: bool = True, want_pos: bool = True, want_masks: bool = False):
+    """Item i's mask = chans[i].sample_mask(n_slots), drawn on the device
+    (cgb_mask_pcg64: numpy's PCG64 + bounded-integer sampling, bit-exact) and
+    encoded as add_plain plaintexts of t - r (neg) and r (pos); each channel's
+    generator continues exactly where the host draws would have left it.
+    Returns (pt_neg, pt_pos, masks or None); the caller frees the plaintexts."""
+    uniq, idx = [], {}
+    chan_of = np.empty(len(chans), np.int32)
+    for i, ch in enumerate(chans):
+        k = idx.get(id(ch))
+        if k is None:
+            k = idx[id(ch)] = len(uniq)
+            uniq.append(ch)
+        chan_of[i] = k
+    st = np.array([_pcg_state_words(ch) for ch in uniq], dtype=np.uint64)
+    neg = ring.alloc_pt(len(chans)) if want_neg else None
+    pos = ring.alloc_pt(len(chans)) if want_pos else None
+    masks = ring.mask_pcg64(chan_of, st, neg, pos, want_masks)
+    for ch, w in zip(uniq, st.tolist()):
+        bg = ch.rng.bit_generator
+        s = bg.state
+        s["state"]["state"] = (int(w[0]) << 64) | int(w[1])
+        s["has_uint32"], s["uinteger"] = int(w[4]), int(w[5])
+        bg.state = s
+    return neg, pos, masks
+
+
 def reconstruct(s: SharePair) -> np.ndarray:
     v = s.client + s.server
     if v.size and v.min() >= 0 and v.max() < 2 * s.p:  # both shares in [0, p): one conditional subtract

@@ -175,6 +175,21 @@ class Ring:
         nat.check(nat.lib().cgb_pt_encode(self._h, ids.size, nat.u64ptr(s), kind, nat.u32ptr(ids)), "cgb_pt_encode")
         self.h2d_bytes += s.nbytes
 
+    def mask_pcg64(self, chan_of_item, states, pt_neg=None, pt_pos=None, want_masks: bool = False):
+        """Server masks drawn on the device (cgb_mask_pcg64): item i takes the next
+        n_slots words of channel chan_of_item[i]'s numpy PCG64 stream; ``states``
+        (uint64[nchan][6]) is advanced in place.  Returns the masks when asked."""
+        ch = np.ascontiguousarray(np.asarray(chan_of_item, dtype=np.int32))
+        st = states
+        assert st.dtype == np.uint64 and st.flags.c_contiguous and st.shape[1] == 6
+        out = np.zeros((ch.size, self.n_slots), np.uint64) if want_masks else None
+        nat.check(nat.lib().cgb_mask_pcg64(self._h, ch.size, st.shape[0],
+                                           ch.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), nat.u64ptr(st),
+                                           None if pt_neg is None else nat.u32ptr(_ids(pt_neg)),
+                                           None if pt_pos is None else nat.u32ptr(_ids(pt_pos)),
+                                           None if out is None else nat.u64ptr(out)), "cgb_mask_pcg64")
+        return None if out is None else out.view(np.int64)
+
     # client role -----------------------------------------------------------
     def encrypt(self, slots, enc_key, first_index: int, ids):
         s, ids = self._slots2d(slots), _ids(ids)

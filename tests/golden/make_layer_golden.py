@@ -8,8 +8,8 @@ model (model.py:95-99 config, generate_toy_model weights), runs its
 ``prefill`` and ``decode_step`` (model.py:425-566) on the slot emulation with
 every cache part force-refreshed before each step (config 3's "noise refresh
 each step", kv_cache.py:156 force=True), and writes tests/golden/layer_toy.npz:
-weights, prompt, generated tokens, every step's logits, op counters and MPC
-byte totals.  /root/reference is never read at test time.
+weights, prompt, generated tokens, every step's logits, op counters, MPC
+byte totals, every channel's transcript and its next mask draws.  /root/reference is never read at test time.
 """
 import json
 import sys
@@ -55,7 +55,9 @@ def record(name, N, P, cfg_kw, PROMPT, STEPS):
     rec = {f"w_{k}": v for k, v in mdl.weights.items()}
     rec.update(config=json.dumps(cfg.as_dict()), prompt=np.array(PROMPT), tokens=np.array(tokens),
                logits=np.stack(logits), counters=json.dumps(ctx.counter.as_dict(), sort_keys=True),
-               mpc_bytes=np.int64(sum(ch.bytes_sent for ch in chans.values())), n=N, p=P)
+               mpc_bytes=np.int64(sum(ch.bytes_sent for ch in chans.values())), n=N, p=P,
+               transcripts=json.dumps({str(k): ch.transcript for k, ch in chans.items()}, sort_keys=True),
+               next_masks=json.dumps({str(k): ch.sample_mask(4).tolist() for k, ch in chans.items()}, sort_keys=True))
     np.savez_compressed(HERE / f"{name}.npz", **rec)
     print(name, "tokens", tokens, "counters", ctx.counter.as_dict())
 

@@ -137,3 +137,21 @@ def test_rotation_dedup_equals_per_item(api):
         assert np.array_equal(a, b)
     assert res["per_item"][1:3] == res["dedup"][1:3]
     assert np.array_equal(res["per_item"][3], res["dedup"][3])
+
+
+def test_prefill_heads_batched_words_equal_per_head(api):
+    """Head-batched prefill (one key switch per shift over every head's columns)
+    == one prefill_attention per head on the production ring: every output
+    ciphertext word, budget, counter and transcript entry."""
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_host_slots import _prefill_heads
+
+    res = {}
+    for batched in (False, True):
+        outs, ctxs, chans = _prefill_heads(api, gpu_ctx, 8192, harness.P8192, 8, 4, 3, batched)
+        res[batched] = ([pt.words() for o in outs for pt in o.parts],
+                        [[pt.noise_budget for pt in o.parts] for o in outs],
+                        [c.counter.as_dict() for c in ctxs], [ch.transcript for ch in chans])
+    for a, b in zip(res[False][0], res[True][0]):
+        assert np.array_equal(a, b)
+    assert res[False][1:] == res[True][1:]

@@ -202,3 +202,58 @@ def test_attention_step_words_equal_reference_sequence(oracle_mod):
         assert res[h].noise_budget == out.noise_budget
         assert np.array_equal(ctxs[h].decrypt(res[h]), oracle_mod.OracleRing(*spec[:5], kseed, q_bits=spec[5])
                               .decrypt(out.words()))
+
+
+def test_prefill_words_equal_reference_sequence(oracle_mod):
+    """Encrypted prefill attention (2 heads, n = 8192, m = 3, d2 = 2) on the
+    production ring: the head-batched B200 sweep against the reference's op
+    sequence (arcc.py:248-317) executed op by op on the CPU RNS-BFV oracle --
+    every output ciphertext word, counter and transcript entry."""
+    from dataclasses import replace  # noqa: F401
+
+    import harness
+    from hostapi import repo_api
+    from oracle import reference_path as ref
+    from oracle.rns_context import OracleContext
+    from paper_2602_08798_b200 import backend as B
+    from paper_2602_08798_b200._native import build
+
+    build()
+    api = repo_api()
+    n, p, m, d2, H = 8192, harness.P8192, 3, 2, 2
+    params = api.BackendParams(n_slots=n, plain_modulus=p)
+    root = B.GpuContext(params, 31)
+    fp = api.FixedPointParams(8, p)
+    rng = np.random.default_rng(31)
+    ctxs = [root.fork() for _ in range(H)]
+    mats = [[api.encode(np.mod(api.fp_encode(rng.uniform(-1, 1, (m, d2)), fp), p), api.EncodingKind.OUTER, c)
+             for _ in range(3)] for c in ctxs]
+    ring = ctxs[0].ring
+    kseed = np.random.SeedSequence([0xB200_4B45, B._KEY_SEED]).generate_state(8, dtype=np.uint32)
+    spec = (ring.log_n, ring.t, ring.L, ring.n_slots, ring.one_row, ring.q_bits)
+    inputs = [([[(pt.words(), pt.noise_budget) for pt in P.parts] for P in mats[h]], ctxs[h]._enc_key.copy(),
+               ctxs[h]._enc_index) for h in range(H)]
+
+    def oracle_head(h):
+        parts, key, idx = inputs[h]
+        oc = OracleContext(params, oracle_mod.OracleRing(*spec[:5], kseed, q_bits=spec[5]), key, idx)
+        Q, K, V = (api.PackedMatrix(mats[h][k].encoding, [oc.wrap(w, b) for w, b in parts[k]], encrypted=True)
+                   for k in range(3))
+        ch = api.MpcChannel(p, seed=70 + h)
+        out = ref.prefill_attention(Q, K, V, fp, oc, ch)
+        return out, oc.counter.as_dict(), ch.transcript
+
+    chans = [api.MpcChannel(p, seed=70 + h) for h in range(H)]
+    with cf.ThreadPoolExecutor(H) as ex:
+        futs = [ex.submit(oracle_head, h) for h in range(H)]
+        snaps = [c.counter.snapshot() for c in ctxs]
+        res = api.prefill_attention_heads([x[0] for x in mats], [x[1] for x in mats], [x[2] for x in mats], fp, ctxs,
+                                          chans)
+        want = [f.result() for f in futs]
+    for h in range(H):
+        out, counts, transcript = want[h]
+        for a, b in zip(res[h].parts, out.parts):
+            assert np.array_equal(a.words(), b.words()), f"head {h}: output words differ"
+            assert a.noise_budget == b.noise_budget
+        assert ctxs[h].counter.delta(snaps[h]) == counts
+        assert chans[h].transcript == transcript

@@ -106,3 +106,36 @@ def test_wave_content_classes():
     assert c.klass[:4].tolist() == t.klass.tolist()
     assert c.klass[4] != c.klass[5] and min(c.klass[4:]) > 0
     assert Wave.concat([plain, plain]).klass is None
+
+
+def _prefill_heads(api, new_ctx, n, p, m, d2, H, batched, seed=3):
+    params = api.BackendParams(n_slots=n, plain_modulus=p)
+    root = new_ctx(params, seed)
+    fp = api.FixedPointParams(8, p)
+    rng = np.random.default_rng(seed)
+    ctxs = [root.fork() for _ in range(H)]
+    mats = [[api.encode(np.mod(api.fp_encode(rng.uniform(-1, 1, (m, d2)), fp), p), api.EncodingKind.OUTER, c)
+             for _ in range(3)] for c in ctxs]
+    chans = [api.MpcChannel(p, seed=50 + h) for h in range(H)]
+    if batched:
+        outs = api.prefill_attention_heads([x[0] for x in mats], [x[1] for x in mats], [x[2] for x in mats], fp, ctxs,
+                                           chans)
+    else:
+        outs = [api.prefill_attention(x[0], x[1], x[2], fp, c, ch) for x, c, ch in zip(mats, ctxs, chans)]
+    return outs, ctxs, chans
+
+
+def test_prefill_heads_batched_equals_per_head(api):
+    """prefill_attention_heads (all heads swept together: one key per shift for
+    every head's columns) == one prefill_attention per head: outputs, budgets,
+    counters, transcripts, next masks (arcc.py:248-317)."""
+    from oracle.slots import SlotContext
+
+    res = {}
+    for batched in (False, True):
+        outs, ctxs, chans = _prefill_heads(api, SlotContext, 64, harness.P64, 5, 4, 3, batched)
+        res[batched] = ([api.decode(o, c).tolist() for o, c in zip(outs, ctxs)],
+                        [[pt.noise_budget for pt in o.parts] for o in outs],
+                        [c.counter.as_dict() for c in ctxs], [ch.transcript for ch in chans],
+                        [ch.sample_mask(4).tolist() for ch in chans])
+    assert res[False] == res[True]

@@ -4,7 +4,8 @@ tests/golden/make_layer_golden.py -- the reference's toy model (2 layers, 4
 heads, n = 64, prompt 6, 3 greedy steps) and a 1-layer model (d1 128, 2 heads,
 d_ff 256, vocab 512) on the production ring n = 8192 (prompt 8, 2 steps), every
 cache part force-refreshed before each step.
-Tokens, every step's logits, op counters and MPC byte totals must be equal."""
+Tokens, every step's logits, op counters, MPC byte totals, every channel's
+transcript and next mask draws must be equal."""
 import json
 from pathlib import Path
 
@@ -37,6 +38,11 @@ def _run(make_ctx, case="layer_toy"):
     assert np.array_equal(np.stack(logits), g["logits"])
     assert ctx.counter.as_dict() == json.loads(str(g["counters"]))
     assert sum(ch.bytes_sent for ch in chans.values()) == int(g["mpc_bytes"])
+    # every channel's transcript in the reference's order, and its generator at the same
+    # point of its stream (the masks, hence every share, were drawn in the same order)
+    assert json.dumps({str(k): ch.transcript for k, ch in chans.items()}, sort_keys=True) == str(g["transcripts"])
+    assert json.dumps({str(k): ch.sample_mask(4).tolist() for k, ch in chans.items()},
+                      sort_keys=True) == str(g["next_masks"])
     return ctx, state
 
 
