@@ -1209,6 +1209,15 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
         }
       }
     }
+    if constexpr (L > 4) {  // every 4 digits: back to [-q/2, q/2] (4 products add < 10.8 q)
+      if ((j & 3) == 3 && j + 1 < L) {
+#pragma unroll
+        for (int i = 0; i < E; i++) {
+          a0[i] = fp_reduce(a0[i], qd, qinv);
+          a1[i] = fp_reduce(a1[i], qd, qinv);
+        }
+      }
+    }
   }
   if constexpr (MODE == 2) {  // ModDown: row pass of W[pp][l] (same forward twiddles), combine, store
 #pragma unroll 1
@@ -1424,6 +1433,18 @@ static void col_fused_t(cgb_ring *r, const ColJob &job, int count, int nt) {
     case 2: launch_pdl(r, k_col_fused<LA, LB, 2>, grid, NTT2_TILE / 16, sm, job); break;
     case 3: launch_pdl(r, k_col_fused<LA, LB, 3>, grid, NTT2_TILE / 16, sm, job); break;
     case 4: launch_pdl(r, k_col_fused<LA, LB, 4>, grid, NTT2_TILE / 16, sm, job); break;
+#define CFW(NT)                                                                                        \
+  case NT: {                                                                                           \
+    static std::once_flag once; /* > 48 KB of tables at 2^15 / 2^16 with many targets */              \
+    std::call_once(once, [&] {                                                                         \
+      CK(cudaFuncSetAttribute(k_col_fused<LA, LB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                              (int)col_fused_smem<LA, LB>(NT)));                                        \
+    });                                                                                                \
+    launch_pdl(r, k_col_fused<LA, LB, NT>, grid, NTT2_TILE / 16, sm, job);                            \
+    break;                                                                                             \
+  }
+      CFW(5) CFW(6) CFW(7) CFW(8)
+#undef CFW
     default: launch_pdl(r, k_col_fused<LA, LB, 1>, grid, NTT2_TILE / 16, sm, job); break;
   }
 }
@@ -1435,7 +1456,7 @@ static bool col_fusable(const cgb_ring *r) {
     hi = q > hi ? q : hi;
   }
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_col_fused && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
-         r->L <= 4 && hi < 2 * lo;
+         r->L <= 8 && hi < 2 * lo;
 }
 // inverse column pass of job.nsrc source units + lift + forward column passes into nt targets
 static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *name) {
@@ -1487,8 +1508,10 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
              r->iP, count, (const u64 *)nullptr, MdEpi{}, 0);
 }
 static bool ks_row_fusable(const cgb_ring *r) {
+  // the FP64 inner-product sum is reduced after every 4 digits (|sum| < 11.3 q < 2^53), so
+  // any digit count up to the 8 limbs of BASELINE config 5 stays exact
   return r->fp_ntt && (g_fp_regio & 3) == 3 && g_ks_row && r->logN >= 13 && r->logN <= 16 && r->L >= 2 &&
-         r->L <= 4;  // <= 4 digits: the FP64 inner-product sum stays below 2^53
+         r->L <= 8;
 }
 static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u64 *D, const KsSrc &x,
                          u64 *const *d_keys) {
@@ -2542,7 +2565,11 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
   switch (r->L) {                                                                      \
     case 2: keyswitch_fp_t<A, B, 2>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
     case 3: keyswitch_fp_t<A, B, 3>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
-    default: keyswitch_fp_t<A, B, 4>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    case 4: keyswitch_fp_t<A, B, 4>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    case 5: keyswitch_fp_t<A, B, 5>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    case 6: keyswitch_fp_t<A, B, 6>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    case 7: keyswitch_fp_t<A, B, 7>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
+    default: keyswitch_fp_t<A, B, 8>(r, S, x, count, d_keys, d_out, add0, d_add1); break; \
   }
   switch (r->logN) {
     case 13: KFP(6, 7) break;
@@ -2588,16 +2615,41 @@ __global__ void __launch_bounds__(256, (L <= 3 ? CGB_HOIST_MINB : 2)) k_ks_inner
   const u64 *Du = D + (u64)srcidx[item] * L * LP * N;
   const u64 *own = xin.items[item] + xin.off;
   const u64 *KF = keys[item] + 2 * (u64)L * 2 * LP * N + i;  // the key's FP64 plane (k_key_fp)
-  u64 dv[L][4], kv[L][2][4];
+  if constexpr (L > 4) {  // wide rings: digit by digit, the sum reduced after every 4 digits
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int j = 0; j < L; j++) {
+      u64 dv[4], k0v[4], k1v[4];
+      gather4(l == j ? own + ((u64)j << logN) : Du + ((u64)j * LP + l) * N, k0, g, logN, dv);
+      ld256(KF + (u64)(j * 2 + 0) * LP * N, k0v);
+      ld256(KF + (u64)(j * 2 + 1) * LP * N, k1v);
 #pragma unroll
-  for (int j = 0; j < L; j++) {
+      for (int e = 0; e < 4; e++) {
+        const double xv = u2d(dv[e]), d0 = r2d(k0v[e]), d1 = r2d(k1v[e]);
+        a0[e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+        a1[e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+        if ((j & 3) == 3) {
+          a0[e] = fp_reduce(a0[e], qd, qinv);
+          a1[e] = fp_reduce(a1[e], qd, qinv);
+        }
+      }
+    }
+    u64 *o0 = acc + ((u64)item * 2 + 0) * LP * N + i, *o1 = acc + ((u64)item * 2 + 1) * LP * N + i;
+    st256(o0, fp_canon(a0[0], qd, qinv), fp_canon(a0[1], qd, qinv), fp_canon(a0[2], qd, qinv), fp_canon(a0[3], qd, qinv));
+    st256(o1, fp_canon(a1[0], qd, qinv), fp_canon(a1[1], qd, qinv), fp_canon(a1[2], qd, qinv), fp_canon(a1[3], qd, qinv));
+    return;
+  }
+  constexpr int LD = L > 4 ? 1 : L;  // (the branch above returned for wider rings)
+  u64 dv[LD][4], kv[LD][2][4];
+#pragma unroll
+  for (int j = 0; j < LD; j++) {
     gather4(l == j ? own + ((u64)j << logN) : Du + ((u64)j * LP + l) * N, k0, g, logN, dv[j]);
     ld256(KF + (u64)(j * 2 + 0) * LP * N, kv[j][0]);
     ld256(KF + (u64)(j * 2 + 1) * LP * N, kv[j][1]);
   }
   double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int j = 0; j < L; j++)
+  for (int j = 0; j < LD; j++)
 #pragma unroll
     for (int e = 0; e < 4; e++) {
       const double xv = u2d(dv[j][e]), d0 = r2d(kv[j][0][e]), d1 = r2d(kv[j][1][e]);
@@ -2641,6 +2693,7 @@ struct MdEpiHoist : MdEpi {
         if (e < n) {
           const double d = r2d(kv[e]);
           a[e] += fp_mulmod(u2d(dv[e]), d, d * qinv, qd);
+          if ((j & 3) == 3) a[e] = fp_reduce(a[e], qd, qinv);  // > 4 digits stay exact
         }
     }
     u64 av[4];
@@ -2814,7 +2867,11 @@ static bool keyswitch_hoisted(cgb_ring *r, Scratch &S, const KsSrc &x, int count
   switch (r->L) {                                                                                              \
     case 2: keyswitch_hoisted_t<A, B, 2>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
     case 3: keyswitch_hoisted_t<A, B, 3>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
-    default: keyswitch_hoisted_t<A, B, 4>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    case 4: keyswitch_hoisted_t<A, B, 4>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    case 5: keyswitch_hoisted_t<A, B, 5>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    case 6: keyswitch_hoisted_t<A, B, 6>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    case 7: keyswitch_hoisted_t<A, B, 7>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
+    default: keyswitch_hoisted_t<A, B, 8>(r, S, x, count, nu, d_usrc, d_srcidx, d_keys, d_out, add0, d_add1); break; \
   }
   switch (r->logN) {
     case 13: KHO(6, 7) break;

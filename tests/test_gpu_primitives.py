@@ -20,6 +20,8 @@ CASES = [
     (15, 537133057, 4, 16384, True, 49),  # config 5: N = 2^15 (p = 1 mod 2^16)
     (16, 537133057, 3, 32768, True, 49),  # config 5: N = 2^16 (p = 1 mod 2^17)
     (13, 536903681, 8, 4096, True, 49),   # config 5: 8 primes
+    (14, 536903681, 6, 8192, True, 49),   # config 5: fused key switch with > 4 digits
+    (16, 537133057, 8, 32768, True, 49),  # config 5: the widest ring
 ]
 
 
