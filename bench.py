@@ -37,6 +37,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+os.environ.setdefault("CGB_KEY_SEED", "0")  # a reproducible keyring for the measurement
 
 P = 536903681
 N_SLOTS = 8192

@@ -166,6 +166,13 @@ int cgb_mult_cipher(cgb_ring *ring, int count, const uint32_t *a, const uint32_t
 int cgb_extend_b(cgb_ring *ring, int count, const uint32_t *b, const uint32_t *bx);
 int cgb_mult_cipher_ext(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
                         const uint32_t *out);
+/* mult_cipher with BOTH operands' base-B extensions resident (ax, bx: two arena slots
+   per item each, from cgb_extend_b; ax may be NULL = cgb_mult_cipher_ext): an operand
+   multiplied by many others (the decode step's encrypted attention weights against
+   every V column, arcc.py:358-361; the prefill's weight rows, arcc.py:307-314) is
+   extended once.  Same words as cgb_mult_cipher. */
+int cgb_mult_cipher_ext2(cgb_ring *ring, int count, const uint32_t *a, const uint32_t *ax, const uint32_t *b,
+                         const uint32_t *bx, const uint32_t *out);
 /* Galois automorphism X -> X^g plus key switch; g = 1 copies.
  * Context.rotate (backend.py:349-355) is galois(5^k mod 2N) in the one-row layout. */
 int cgb_galois(cgb_ring *ring, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out);

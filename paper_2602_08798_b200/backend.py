@@ -47,7 +47,7 @@ from . import _native as nat
 __all__ = [
     "BackendParams", "Context", "DecryptionFailure", "GpuCiphertext", "GpuContext", "NoiseBudgetExhausted",
     "NoiseCosts", "OpCounter", "ParameterError", "PlainVector", "SlotCiphertext", "PlainBatch", "Wave", "default_plain_modulus", "onehot_batch",
-    "is_prime", "new_context", "ring_for",
+    "is_prime", "key_seed", "new_context", "ring_for", "set_key_seed",
 ]
 
 PlainVector = np.ndarray
@@ -207,8 +207,28 @@ def _params_key(params) -> tuple:
 # ----------------------------------------------------------------------------
 # rings: one per (n_slots, p, limbs, key seed), shared by all contexts
 # ----------------------------------------------------------------------------
-_KEY_SEED = int(os.environ.get("CGB_KEY_SEED", "0"))
+def _default_key_seed() -> int:
+    """The keyring seed: CGB_KEY_SEED when set (reproducible runs: tests, benches),
+    else a per-process secret from the OS CSPRNG -- the secret and evaluation keys
+    are never a function of a public constant."""
+    env = os.environ.get("CGB_KEY_SEED")
+    return int(env) if env is not None else int.from_bytes(os.urandom(8), "little")
+
+
+_KEY_SEED = _default_key_seed()
 _rings: dict = {}
+
+
+def set_key_seed(seed: int) -> None:
+    """Explicit keyring: contexts created from now on use keys derived from
+    ``seed`` (contexts with equal params and the same keyring interoperate, as
+    the reference's contexts do, backend.py:290; earlier contexts keep theirs)."""
+    global _KEY_SEED
+    _KEY_SEED = int(seed)
+
+
+def key_seed() -> int:
+    return _KEY_SEED
 _rings_lock = threading.Lock()
 
 
@@ -326,6 +346,7 @@ SlotCiphertext = GpuCiphertext
 # waves: batches of ciphertexts processed by one launch sequence
 # ----------------------------------------------------------------------------
 EXT_B = os.environ.get("CGB_EXT_B", "1") != "0"  # resident base-B extensions of KV cache parts
+EXT_A = os.environ.get("CGB_EXT_A", "1") != "0"  # ... and of an a-operand repeated across a mult_cipher wave
 _ROT_DEDUP = os.environ.get("CGB_ROT_DEDUP", "1") != "0"  # one key switch per (content class, step)
 
 
@@ -790,7 +811,12 @@ class GpuContext:
         blk, ids = c0._new(len(wa))
         ring = c0._ring
         if resident_b and EXT_B:
-            ring.mult_cipher_ext(wa.aids, wb.aids, ring.ext_B(wb.aids), ids)
+            bx = ring.ext_B(wb.aids)
+            if EXT_A and len(wa) >= 8 and 4 * np.unique(wa.aids).size <= len(wa):
+                # a repeats (one ciphertext times many): extend each distinct a once
+                ring.mult_cipher_ext2(wa.aids, ring.ext_B(wa.aids), wb.aids, bx, ids)
+            else:
+                ring.mult_cipher_ext(wa.aids, wb.aids, bx, ids)
         else:
             ring.mult_cipher(wa.aids, wb.aids, ids)
         return Wave(wa.ctxs, wa.owner, ids, b, [blk], GpuContext._charge(wa, "mult_cipher"))

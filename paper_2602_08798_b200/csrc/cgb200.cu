@@ -1838,8 +1838,58 @@ __global__ void k_lift_QB_t(u64 *dst, const u64 *coef, const ModTab *mods, const
 // same residues; the double-precision overflow estimates and the 128-bit
 // fixed-point rounding are the integer kernels' operations unchanged.
 __device__ __forceinline__ double fpm(double a, double2 w, double m) { return fp_mulmod(a, w.x, w.y, m); }
+// The FP64 base conversions' constants as a kernel parameter (the constant bank:
+// uniform reads without a load per thread -- they were ~60 L1 loads per element
+// through a Consts pointer), built once per ring from Consts / the modulus table.
 template <int L>
-__global__ void k_lift_QB_fp(u64 *dst, const u64 *coef, const ModTab *mods, const Consts *C, int iB0, int logN) {
+struct BConv {
+  static constexpr int nB = L + 1;
+  double qd[L + nB], qinv[L + nB];  // Q limbs, then B limbs
+  u64 qB[nB];
+  double2 QhatInv[L], QmodB[nB], QhatModB[L][nB];
+  double invq[L];
+  double2 QBhatInv[L];
+  u64 th_hi[L], th_lo[L];
+  double2 omega[L][nB], BQhatInv[nB], tBhat[nB], BhatInv[nB];
+  double invb[nB];
+  double2 BmodQ[L], BhatModQ[nB][L];
+};
+template <int L>
+static BConv<L> make_bconv(const cgb_ring *r) {
+  constexpr int nB = L + 1;
+  const Consts &C = r->h_c;
+  BConv<L> K{};
+  for (int l = 0; l < L + nB; l++) {
+    const ModTab &M = r->h_mods[l < L ? l : r->iB0 + (l - L)];
+    K.qd[l] = M.qd;
+    K.qinv[l] = M.qinv;
+  }
+  for (int k = 0; k < nB; k++) {
+    K.qB[k] = r->h_mods[r->iB0 + k].q;
+    K.QmodB[k] = C.fQmodB[k];
+    K.BQhatInv[k] = C.fBQhatInv[k];
+    K.tBhat[k] = C.ftBhat[k];
+    K.BhatInv[k] = C.fBhatInv[k];
+    K.invb[k] = C.invb[k];
+    for (int l = 0; l < L; l++) K.BhatModQ[k][l] = C.fBhatModQ[k][l];
+  }
+  for (int l = 0; l < L; l++) {
+    K.QhatInv[l] = C.fQhatInv[l];
+    K.invq[l] = C.invq[l];
+    K.QBhatInv[l] = C.fQBhatInv[l];
+    K.th_hi[l] = C.sc_th_hi[l];
+    K.th_lo[l] = C.sc_th_lo[l];
+    K.BmodQ[l] = C.fBmodQ[l];
+    for (int k = 0; k < nB; k++) {
+      K.QhatModB[l][k] = C.fQhatModB[l][k];
+      K.omega[l][k] = C.fsc_omega[l][k];
+    }
+  }
+  return K;
+}
+// FP64 Q -> B base conversion (HPS lift, same residues as k_lift_QB_t)
+template <int L>
+__global__ void k_lift_QB_fp(u64 *dst, const u64 *coef, const __grid_constant__ BConv<L> K, int logN) {
   constexpr int nB = L + 1;
   const int item = blockIdx.y;
   const u64 N = 1ull << logN;
@@ -1852,27 +1902,26 @@ __global__ void k_lift_QB_fp(u64 *dst, const u64 *coef, const ModTab *mods, cons
   double s = 0.0;
 #pragma unroll
   for (int l = 0; l < L; l++) {
-    const ModTab &M = mods[l];
-    const u64 y = fp_canon(fpm(u2d(src[(u64)l * N + jn]), C->fQhatInv[l], M.qd), M.qd, M.qinv);
+    const u64 y = fp_canon(fpm(u2d(src[(u64)l * N + jn]), K.QhatInv[l], K.qd[l]), K.qd[l], K.qinv[l]);
     yd[l] = u2d(y);
-    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(y), C->invq[l]));
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(y), K.invq[l]));
   }
   const double v = u2d((u64)__dadd_rn(s, 0.5));
   u64 *d = dst + ((u64)item * 4 + p) * (L + nB) * N;
 #pragma unroll
   for (int k = 0; k < nB; k++) {
-    const ModTab &M = mods[iB0 + k];
-    double acc = -fpm(v, C->fQmodB[k], M.qd);
+    const double qd = K.qd[L + k], qinv = K.qinv[L + k];
+    double acc = -fpm(v, K.QmodB[k], qd);
 #pragma unroll
     for (int l = 0; l < L; l++) {
-      acc += fpm(yd[l], C->fQhatModB[l][k], M.qd);
-      if ((l & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+      acc += fpm(yd[l], K.QhatModB[l][k], qd);
+      if ((l & 3) == 2) acc = fp_reduce(acc, qd, qinv);
     }
-    d[(u64)(L + k) * N + jn] = fp_canon(acc, M.qd, M.qinv);
+    d[(u64)(L + k) * N + jn] = fp_canon(acc, qd, qinv);
   }
 }
 template <int L>
-__global__ void k_scale_round_fp(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int iB0, int logN) {
+__global__ void k_scale_round_fp(u64 *d, const u64 *ten, const __grid_constant__ BConv<L> K, int logN) {
   constexpr int nB = L + 1, nt = L + nB;
   const int item = blockIdx.y;
   const u64 N = 1ull << logN;
@@ -1885,41 +1934,40 @@ __global__ void k_scale_round_fp(u64 *d, const u64 *ten, const ModTab *mods, con
   u128 S = 0;
 #pragma unroll
   for (int l = 0; l < L; l++) {
-    const ModTab &M = mods[l];
-    const u64 y = fp_canon(fpm(u2d(cp[(u64)l * N + jn]), C->fQBhatInv[l], M.qd), M.qd, M.qinv);
+    const u64 y = fp_canon(fpm(u2d(cp[(u64)l * N + jn]), K.QBhatInv[l], K.qd[l]), K.qd[l], K.qinv[l]);
     yd[l] = u2d(y);
-    S += (u128)y * C->sc_th_hi[l] + (u128)__umul64hi(y, C->sc_th_lo[l]);
+    S += (u128)y * K.th_hi[l] + (u128)__umul64hi(y, K.th_lo[l]);
   }
   const u64 R = (u64)((S + ((u128)1 << 63)) >> 64);
   double ykd[nB];
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < nB; k++) {
-    const ModTab &M = mods[iB0 + k];
-    double acc = u2d(reduce4(R, M.q));
+    const double qd = K.qd[L + k], qinv = K.qinv[L + k];
+    double acc = u2d(reduce4(R, K.qB[k]));
 #pragma unroll
     for (int l = 0; l < L; l++) {
-      acc += fpm(yd[l], C->fsc_omega[l][k], M.qd);
-      if ((l & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+      acc += fpm(yd[l], K.omega[l][k], qd);
+      if ((l & 3) == 2) acc = fp_reduce(acc, qd, qinv);
     }
-    const double z = fpm(u2d(cp[(u64)(L + k) * N + jn]), C->fBQhatInv[k], M.qd);
-    acc = fp_reduce(acc + fpm(z, C->ftBhat[k], M.qd), M.qd, M.qinv);
-    const u64 yk = fp_canon(fpm(acc, C->fBhatInv[k], M.qd), M.qd, M.qinv);
+    const double z = fpm(u2d(cp[(u64)(L + k) * N + jn]), K.BQhatInv[k], qd);
+    acc = fp_reduce(acc + fpm(z, K.tBhat[k], qd), qd, qinv);
+    const u64 yk = fp_canon(fpm(acc, K.BhatInv[k], qd), qd, qinv);
     ykd[k] = u2d(yk);
-    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(yk), C->invb[k]));
+    s = __dadd_rn(s, __dmul_rn(__ull2double_rn(yk), K.invb[k]));
   }
   const double v = u2d((u64)__dadd_rn(s, 0.5));
   u64 *o = d + ((u64)item * 3 + p) * L * N;
 #pragma unroll
   for (int l = 0; l < L; l++) {
-    const ModTab &M = mods[l];
-    double acc = -fpm(v, C->fBmodQ[l], M.qd);
+    const double qd = K.qd[l], qinv = K.qinv[l];
+    double acc = -fpm(v, K.BmodQ[l], qd);
 #pragma unroll
     for (int k = 0; k < nB; k++) {
-      acc += fpm(ykd[k], C->fBhatModQ[k][l], M.qd);
-      if ((k & 3) == 2) acc = fp_reduce(acc, M.qd, M.qinv);
+      acc += fpm(ykd[k], K.BhatModQ[k][l], qd);
+      if ((k & 3) == 2) acc = fp_reduce(acc, qd, qinv);
     }
-    o[(u64)l * N + jn] = fp_canon(acc, M.qd, M.qinv);
+    o[(u64)l * N + jn] = fp_canon(acc, qd, qinv);
   }
 }
 template <int L>
@@ -1978,7 +2026,8 @@ __global__ void k_scale_round_t(u64 *d, const u64 *ten, const ModTab *mods, cons
 // B limbs from the lifted buffer
 __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64 *const *pa, const u64 *const *pb,
                          const u64 *const *pbx /*null, or b's B-limb extension: [item][2] slots of [nB][N]*/,
-                         const ModTab *mods, int L, int nt, int iB0, int logN) {
+                         const ModTab *mods, int L, int nt, int iB0, int logN,
+                         const u64 *const *pax = nullptr /*null, or a's B-limb extension (then pbx too)*/) {
   int item = blockIdx.y;
   u64 N = 1ull << logN, P = (u64)nt * N, LN = (u64)L * N;
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1989,6 +2038,9 @@ __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64
   u64 a0, a1, b0, b1;
   if (l < L) {
     a0 = pa[item][i], a1 = pa[item][LN + i], b0 = pb[item][i], b1 = pb[item][LN + i];
+  } else if (pax) {
+    a0 = pax[2 * item][i - LN], a1 = pax[2 * item + 1][i - LN], b0 = pbx[2 * item][i - LN],
+    b1 = pbx[2 * item + 1][i - LN];
   } else if (pbx) {
     a0 = x[i], a1 = x[P + i], b0 = pbx[2 * item][i - LN], b1 = pbx[2 * item + 1][i - LN];
   } else {
@@ -4231,7 +4283,7 @@ static void lift_QB(cgb_ring *r, int n, int npoly, u64 *coef, u64 *in, bool fpbc
   switch (L) {
 #define LQB(LL)                                                                                     \
   case LL:                                                                                           \
-    if (fpbc) k_lift_QB_fp<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN); \
+    if (fpbc) k_lift_QB_fp<LL><<<grid, TPB, 0, r->stream>>>(in, coef, make_bconv<LL>(r), logN);          \
     else k_lift_QB_t<LL><<<grid, TPB, 0, r->stream>>>(in, coef, r->d_mods, r->d_c, r->iB0, logN);      \
     break;
     LQB(1) LQB(2) LQB(3) LQB(4) LQB(5) LQB(6) LQB(7) LQB(8)
@@ -4280,7 +4332,7 @@ int cgb_extend_b(cgb_ring *r, int count, const uint32_t *b, const uint32_t *bx) 
 }
 
 static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
-                             const uint32_t *out);
+                             const uint32_t *out, const uint32_t *ax = nullptr);
 int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
   API_BEGIN
   if (count > 0) mult_cipher_impl(r, count, a, b, nullptr, out);
@@ -4292,8 +4344,15 @@ int cgb_mult_cipher_ext(cgb_ring *r, int count, const uint32_t *a, const uint32_
   if (count > 0) mult_cipher_impl(r, count, a, b, bx, out);
   API_END
 }
+int cgb_mult_cipher_ext2(cgb_ring *r, int count, const uint32_t *a, const uint32_t *ax, const uint32_t *b,
+                         const uint32_t *bx, const uint32_t *out) {
+  API_BEGIN
+  if (ax && !bx) FAIL(CGB_ERR_PARAM, "mult_cipher_ext2: a resident a-extension needs b's too (swap the operands)");
+  if (count > 0) mult_cipher_impl(r, count, a, b, bx, out, ax);
+  API_END
+}
 static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
-                             const uint32_t *out) {
+                             const uint32_t *out, const uint32_t *ax) {
   const int L = r->L, nB = r->nB, nt = L + nB, N = r->N, logN = r->logN;
   const bool fpbc = r->fp_ntt && g_fp_bconv;  // base conversions on the FP64 pipe (every modulus < 2^49)
   u64 *rk = get_key(r, 0);
@@ -4316,9 +4375,15 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
     u64 **dpa = S.up(pa.data(), n), **dpb = S.up(pb.data(), n);
     // INTT of the operands straight from the arena into coef, lift Q -> B; with b's
     // resident extension (bx) only a's two polys
-    const int npoly = bx ? 2 : 4;
-    u64 **dpx = nullptr;
-    if (bx) {
+    // (ax too: both extensions resident -- an operand multiplied by many others, e.g. the
+    // decode step's encrypted weights a_pref against every V column, arcc.py:358-361)
+    const int npoly = ax ? 0 : bx ? 2 : 4;
+    u64 **dpx = nullptr, **dpax = nullptr;
+    if (ax) {
+      auto px = ct_ptrs(r, 2 * n, bx + 2 * (size_t)c0), pxa = ct_ptrs(r, 2 * n, ax + 2 * (size_t)c0);
+      dpx = S.up(px.data(), 2 * n);
+      dpax = S.up(pxa.data(), 2 * n);
+    } else if (bx) {
       auto px = ct_ptrs(r, 2 * n, bx + 2 * (size_t)c0);
       dpx = S.up(px.data(), 2 * n);
       intt_and_lift(r, S, n, pa, 0, coef, in, fpbc);
@@ -4326,8 +4391,8 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
       intt_and_lift(r, S, n, pa, 0, coef, in, fpbc);
       intt_and_lift(r, S, n, pb, 2, coef, in, fpbc);
     }
-    lift_QB(r, n, npoly, coef, in, fpbc);
-    {
+    if (npoly) lift_QB(r, n, npoly, coef, in, fpbc);
+    if (npoly) {
       NttJob job{};
       job.base = in;
       job.item_stride = 4ull * nt * N;
@@ -4342,7 +4407,7 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
       launch_ntt(r, true, job, n);
     }
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
-    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN));
+    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
     ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
     {
@@ -4351,7 +4416,7 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
       switch (L) {
 #define LSR(LL)                                                                                       \
   case LL:                                                                                             \
-    if (fpbc) k_scale_round_fp<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN); \
+    if (fpbc) k_scale_round_fp<LL><<<grid, TPB, 0, r->stream>>>(d, ten, make_bconv<LL>(r), logN);         \
     else k_scale_round_t<LL><<<grid, TPB, 0, r->stream>>>(d, ten, r->d_mods, r->d_c, r->iB0, logN);      \
     break;
         LSR(1) LSR(2) LSR(3) LSR(4) LSR(5) LSR(6) LSR(7) LSR(8)
@@ -4370,7 +4435,7 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
     KsSrc xin{d + 2ull * L * N, 3ull * L * N, nullptr, 0, nullptr};
     KsSrc none{nullptr, 0, nullptr, 0, nullptr};
     keyswitch(r, S, xin, n, dk, dout, none, (const u64 *const *)dd01);
-    group_end(r, bx ? "mult_cipher_ext" : "mult_cipher", mc_bytes);
+    group_end(r, ax ? "mult_cipher_ext2" : bx ? "mult_cipher_ext" : "mult_cipher", mc_bytes);
   }
 }
 

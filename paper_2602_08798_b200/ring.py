@@ -133,6 +133,12 @@ class Ring:
         nat.check(nat.lib().cgb_mult_cipher_ext(self._h, a.size, nat.u32ptr(a), nat.u32ptr(b), nat.u32ptr(bx),
                                                 nat.u32ptr(out)), "cgb_mult_cipher_ext")
 
+    def mult_cipher_ext2(self, a, ax, b, bx, out):
+        """mult_cipher with both operands' base-B extensions resident (cgb_mult_cipher_ext2)."""
+        a, ax, b, bx, out = _ids(a), _ids(ax), _ids(b), _ids(bx), _ids(out)
+        nat.check(nat.lib().cgb_mult_cipher_ext2(self._h, a.size, nat.u32ptr(a), nat.u32ptr(ax), nat.u32ptr(b),
+                                                 nat.u32ptr(bx), nat.u32ptr(out)), "cgb_mult_cipher_ext2")
+
     def alloc_pt(self, n: int) -> np.ndarray:
         ids = np.zeros(n, dtype=np.uint32)
         if n:

@@ -7,6 +7,8 @@ import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
+# reproducible keyring for the parity tests (the product default is a per-process secret)
+os.environ.setdefault("CGB_KEY_SEED", "0")
 
 
 def pytest_configure(config):

@@ -167,7 +167,7 @@ def test_attention_step_words_equal_reference_sequence(oracle_mod):
     n, p, d2, m, t, H, seed = 8192, harness.P8192, 4, 5, 3, 2, 21
     root, fp, ctxs, caches, qs, chans = harness.attention_heads(api, B.GpuContext, n, p, d2, m, t, H, seed=seed)
     ring = ctxs[0].ring
-    kseed = np.random.SeedSequence([0xB200_4B45, B._KEY_SEED]).generate_state(8, dtype=np.uint32)
+    kseed = np.random.SeedSequence([0xB200_4B45, B.key_seed()]).generate_state(8, dtype=np.uint32)
     spec = (ring.log_n, ring.t, ring.L, ring.n_slots, ring.one_row, ring.q_bits)
 
     # the oracle side starts from the same ciphertext words, encryption streams and channel seeds
@@ -229,7 +229,7 @@ def test_prefill_words_equal_reference_sequence(oracle_mod):
     mats = [[api.encode(np.mod(api.fp_encode(rng.uniform(-1, 1, (m, d2)), fp), p), api.EncodingKind.OUTER, c)
              for _ in range(3)] for c in ctxs]
     ring = ctxs[0].ring
-    kseed = np.random.SeedSequence([0xB200_4B45, B._KEY_SEED]).generate_state(8, dtype=np.uint32)
+    kseed = np.random.SeedSequence([0xB200_4B45, B.key_seed()]).generate_state(8, dtype=np.uint32)
     spec = (ring.log_n, ring.t, ring.L, ring.n_slots, ring.one_row, ring.q_bits)
     inputs = [([[(pt.words(), pt.noise_budget) for pt in P.parts] for P in mats[h]], ctxs[h]._enc_key.copy(),
                ctxs[h]._enc_index) for h in range(H)]
@@ -257,3 +257,19 @@ def test_prefill_words_equal_reference_sequence(oracle_mod):
             assert a.noise_budget == b.noise_budget
         assert ctxs[h].counter.delta(snaps[h]) == counts
         assert chans[h].transcript == transcript
+
+
+def test_batched_mult_cipher_both_resident_bitexact(bench):
+    """16 a-operands each multiplied by 16 b's (the decode step's a_pref x V
+    columns pattern) with BOTH base-B extensions resident (cgb_mult_cipher_ext2,
+    the path w_mult_cipher takes when a repeats): the oracle's words."""
+    g, pool, vals, ids, words = bench
+    ai = np.repeat(np.arange(16), 16)
+    bi = (np.arange(256) * 7 + 3) % COUNT
+    out = g.alloc(256)
+    g.mult_cipher_ext2(ids[ai], g.ext_B(ids[ai]), ids[bi], g.ext_B(ids[bi]), out)
+    got = g.store(out)
+    want = pool.map(lambda o, i, j: o.mult_cipher(words[i], words[j]), ai, bi)
+    bad = [i for i in range(256) if not np.array_equal(got[i], want[i])]
+    assert not bad, f"{len(bad)} items differ, first {bad[:8]}"
+    g.free(out)
