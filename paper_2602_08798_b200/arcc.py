@@ -471,6 +471,7 @@ def _truncate(s: SharePair, fp: FixedPointParams, ch: MpcChannel, mask=None) -> 
 # prefill attention (outer-outer score diagonals), batched over heads
 # ----------------------------------------------------------------------------
 PREFILL_CHUNK = int(os.environ.get("CGB_PREFILL_CHUNK", "3072"))  # ciphertexts per wave of the sweeps
+EXT_A_SWEEP = os.environ.get("CGB_EXT_A", "1") != "0"
 
 
 def prefill_attention(Q, K, V, fp: FixedPointParams, ctx, mpc: MpcChannel, causal: bool = True) -> PackedMatrix:
@@ -566,6 +567,10 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
         plans.append([(mpc.sample_mask(n), mpc.sample_mask(m)) for _ in range(d2)])
     Aw = type(a_rows[0]).concat(a_rows)  # item h m + i
     Vw = type(Kw).concat([C.wave_of(Vs[h].parts, [ctxs[h]] * d2) for h in range(H)])  # item h d2 + c
+    # every weight row meets all d2 V columns, over several waves: its base-B extension is
+    # computed once here and kept with it (mult_cipher_ext2; same words)
+    if hasattr(c0, "ring") and EXT_A_SWEEP:
+        c0.ring.ext_B(Aw.aids)
     out_parts = [[None] * d2 for _ in range(H)]
     cols_per = max(1, PREFILL_CHUNK // (m * H))
     for c0_ in range(0, d2, cols_per):

@@ -812,8 +812,9 @@ class GpuContext:
         ring = c0._ring
         if resident_b and EXT_B:
             bx = ring.ext_B(wb.aids)
-            if EXT_A and len(wa) >= 8 and 4 * np.unique(wa.aids).size <= len(wa):
-                # a repeats (one ciphertext times many): extend each distinct a once
+            if EXT_A and (ring.has_ext(wa.aids) or (len(wa) >= 8 and 4 * np.unique(wa.aids).size <= len(wa))):
+                # a repeats (one ciphertext times many), or already has a resident extension
+                # (a sweep's operand extended once for all its waves): no per-item extension
                 ring.mult_cipher_ext2(wa.aids, ring.ext_B(wa.aids), wb.aids, bx, ids)
             else:
                 ring.mult_cipher_ext(wa.aids, wb.aids, bx, ids)

@@ -128,6 +128,10 @@ class Ring:
                 self._ext[int(a)] = slots[2 * k:2 * k + 2].copy()
         return np.ascontiguousarray(np.concatenate([self._ext[int(a)] for a in b_ids]).astype(np.uint32))
 
+    def has_ext(self, ids) -> bool:
+        """Whether every id already has a resident base-B extension."""
+        return bool(self._ext) and all(int(a) in self._ext for a in _ids(ids))
+
     def mult_cipher_ext(self, a, b, bx, out):
         a, b, bx, out = _ids(a), _ids(b), _ids(bx), _ids(out)
         nat.check(nat.lib().cgb_mult_cipher_ext(self._h, a.size, nat.u32ptr(a), nat.u32ptr(b), nat.u32ptr(bx),
