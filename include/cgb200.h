@@ -102,6 +102,8 @@ int cgb_ct_copy(cgb_ring *ring, int count, const uint32_t *src, const uint32_t *
 int cgb_ct_store(cgb_ring *ring, int count, const uint32_t *ids, uint64_t *host_words);
 int cgb_ct_load(cgb_ring *ring, int count, const uint32_t *ids, const uint64_t *host_words);
 uint64_t *cgb_ct_device_ptr(cgb_ring *ring, uint32_t id);
+/* free ciphertext slots of the arena (headroom checks of optional resident data) */
+int64_t cgb_ct_free_count(cgb_ring *ring);
 int cgb_pt_alloc(cgb_ring *ring, int count, uint32_t *ids_out);
 int cgb_pt_free(cgb_ring *ring, int count, const uint32_t *ids);
 /* encode host slot vectors into plaintexts; kind CGB_PT_MUL / CGB_PT_ADD.

@@ -570,7 +570,10 @@ def prefill_attention_heads(Qs, Ks, Vs, fp: FixedPointParams, ctxs, mpcs, causal
     # every weight row meets all d2 V columns, over several waves: its base-B extension is
     # computed once here and kept with it (mult_cipher_ext2; same words)
     if hasattr(c0, "ring") and EXT_A_SWEEP:
-        c0.ring.ext_B(Aw.aids)
+        ring = c0.ring
+        # only with headroom: the sweep's own waves need ~3 PREFILL_CHUNK slots at a time
+        if ring.free_slots() > 2 * len(Aw) + 8 * PREFILL_CHUNK:
+            ring.ext_B(Aw.aids)
     out_parts = [[None] * d2 for _ in range(H)]
     cols_per = max(1, PREFILL_CHUNK // (m * H))
     for c0_ in range(0, d2, cols_per):

@@ -991,8 +991,15 @@ __host__ __device__ constexpr int ksr_data_words(int LB) {
 #endif
 // bytes of k_ks_row's key staging area: 2 polys x 16 words per thread x 128 threads
 constexpr int KSTAGE_BYTES = CGB_KSROW_KSTAGE ? 2 * 16 * 8 * (NTT2_TILE / 16) : 0;
+#ifndef CGB_KSROW_RPF
+#define CGB_KSROW_RPF 0  // next row tile prefetched into registers during the current tile's work
+#endif
 #ifndef CGB_KSROW_MINB
+#if CGB_KSROW_RPF
+#define CGB_KSROW_MINB 2
+#else
 #define CGB_KSROW_MINB 3  // <= 168 registers: 3 CTAs per SM (MODE 2 would otherwise take 208)
+#endif
 #endif
 #define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_KSROW_MINB)
 // MODE 0: every limb of Q u P; 1: the P limb only; 2: the Q limbs, followed by
@@ -1068,6 +1075,26 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   pdl_start_dependents();
   pdl_wait();
   int tcur = 0;
+#if CGB_KSROW_RPF
+  // software pipelining: the NEXT row tile's words are loaded into registers while
+  // this tile's row pass and key products run (loads in flight across the compute)
+  u64 nv[PA::K];
+  auto issue_tile = [&](int t) {
+    if (t < ntile) {
+      const u64 *src = tile_src(t) + ((u64)g << LM);
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) nv[k] = __ldcs(src + PA::idx(tl, 0, k));
+    }
+  };
+  issue_tile(0);
+  auto load_tile = [&](double *x) {
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) x[k] = (raw & 1) ? r2d(nv[k]) : u2d(nv[k]);
+    issue_tile(tcur + 1);
+    __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
+    tcur++;
+  };
+#else
   auto load_tile = [&](double *x) {
     const u64 *src = tile_src(tcur) + ((u64)g << LM);
 #pragma unroll
@@ -1078,6 +1105,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
   };
+#endif
   double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
   auto spad = [](int i) { return i + (i >> PSH); };
   const u64 *K = keys[item];
@@ -2051,6 +2079,49 @@ __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64
   o[P + i] = add_mod(mul_mod(a0, b1, M), mul_mod(a1, b0, M), M.q);
   o[2 * P + i] = mul_mod(a1, b1, M);
 }
+// The tensor product fed straight into the first (row) pass of its inverse NTT:
+// unit (k, l) of item i is d_k in limb l of Q u B -- (a0 b0, a0 b1 + a1 b0, a1 b1)
+// mod q_l, from the operands' NTT words (the same residues k_tensor writes).  The
+// 3 (L + nB) tensor limb-polys never make the HBM round trip (mult_cipher).
+struct TensorLoad {
+  static constexpr bool active = false;  // stores: the plain transform's
+  static constexpr bool loads = true;
+  const u64 *const *pa, *const *pb;      // arena items: the Q limbs of a, b (NTT form)
+  const u64 *in;                         // [item][4][nt][N]: the B limbs of a (polys 0,1), b (2,3)
+  const u64 *const *pbx, *const *pax;    // resident B extensions ([2 item + p] -> [nB][N]) or null
+  const ModTab *mods;
+  int L, nt, iB0, logN;
+  __device__ void store(int, int, u64, const u64 *, int) const {}
+  __device__ void load4(int item, int sub, u64 pos, u64 out[4]) const {
+    const int k = sub / nt, l = sub - k * nt;
+    const u64 N = 1ull << logN, P = (u64)nt * N, LN = (u64)L * N;
+    const ModTab &M = mods[l < L ? l : iB0 + (l - L)];
+    const u64 i = (u64)l * N + pos;
+    const u64 *x = in + (u64)item * 4 * P;
+    const u64 *a0p, *a1p, *b0p, *b1p;
+    if (l < L) {
+      a0p = pa[item] + i, a1p = pa[item] + LN + i, b0p = pb[item] + i, b1p = pb[item] + LN + i;
+    } else if (pax) {
+      a0p = pax[2 * item] + (i - LN), a1p = pax[2 * item + 1] + (i - LN);
+      b0p = pbx[2 * item] + (i - LN), b1p = pbx[2 * item + 1] + (i - LN);
+    } else if (pbx) {
+      a0p = x + i, a1p = x + P + i, b0p = pbx[2 * item] + (i - LN), b1p = pbx[2 * item + 1] + (i - LN);
+    } else {
+      a0p = x + i, a1p = x + P + i, b0p = x + 2 * P + i, b1p = x + 3 * P + i;
+    }
+    u64 a0[4], a1[4], b0[4], b1[4];
+    if (k != 2) ld256(a0p, a0);
+    if (k != 0) ld256(a1p, a1);
+    if (k != 2) ld256(b0p, b0);
+    if (k != 0) ld256(b1p, b1);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      if (k == 0) out[e] = mul_mod(a0[e], b0[e], M);
+      else if (k == 2) out[e] = mul_mod(a1[e], b1[e], M);
+      else out[e] = add_mod(mul_mod(a0[e], b1[e], M), mul_mod(a1[e], b0[e], M), M.q);
+    }
+  }
+};
 // scale by t/Q and round into B, then centred B -> Q: d[item][3][L][N]
 __global__ void k_scale_round(u64 *d, const u64 *ten, const ModTab *mods, const Consts *C, int L, int nB, int iB0,
                               int logN) {
@@ -3052,6 +3123,10 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
              d_out, acc, W, add0, d_add1, r->d_mods, r->d_c, L, logN));
 }
 
+// items per batched key switch (CGB_KS_CHUNK; 0 = as many as the workspace budget
+// allows): smaller chunks keep a chunk's intermediates (xr, D, acc_P, W) L2-resident
+// between the five launches
+static int g_ks_chunk = 0;
 static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
   size_t budget = (size_t)3 << 30;  // bytes of workspace per chunk
   size_t c = budget / std::max<size_t>(words_per_item * 8, 1);
@@ -3084,6 +3159,10 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
   }
   size_t per_item = ctw * 2 + (size_t)L * N * (1 + L * (L + 1) + 2 * (L + 1) + 2 * L);
   size_t CH = chunk_for(r, per_item);
+  if (g_ks_chunk > 0) {  // at most g_ks_chunk items per batched key switch; equal-sized chunks
+    const size_t nch = (idx.size() + (size_t)g_ks_chunk - 1) / (size_t)g_ks_chunk;
+    CH = std::min(CH, std::max<size_t>(1, (idx.size() + nch - 1) / std::max<size_t>(nch, 1)));
+  }
   for (size_t c0 = 0; c0 < idx.size(); c0 += CH) {
     int n = (int)std::min(CH, idx.size() - c0);
     Scratch S(r);
@@ -3482,6 +3561,58 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
 // ============================================================================
 // C ABI
 // ============================================================================
+// the tensor product and its inverse NTT in two launches: the row pass computes the
+// products in its load (TensorLoad), the column pass finishes the transform into ten
+// measured slower: tensor_intt 6.46 ms against tensor 2.43 + its inverse transform
+// 3.71 ms per decode step (the integer products in the row pass's load sit on its
+// critical path); off (CGB_TENSOR_FUSE=1 turns it on)
+static bool g_tensor_fuse = false;
+template <int LA, int LB>
+static void tensor_intt_t(cgb_ring *r, int n, u64 *ten, const TensorLoad &tl, const int *mod_of_limb) {
+  const int nt = tl.nt;
+  NttJob job{};
+  job.base = ten;
+  job.item_stride = 3ull * nt * r->N;
+  int u = 0;
+  for (int k = 0; k < 3; k++)
+    for (int l = 0; l < nt; l++) {
+      job.sub_off[u] = (unsigned short)(k * nt + l);
+      job.sub_mod[u] = (unsigned char)mod_of_limb[l];
+      u++;
+    }
+  job.nsub = u;
+  job.mods = r->d_mods;
+  job.logN = r->logN;
+  auto grid = [&](int lm) {
+    int nsubs = 1 << (LA + LB - lm), G = NTT2_TILE / (1 << lm);
+    return dim3((unsigned)((size_t)n * job.nsub * (nsubs / G)));
+  };
+  static std::once_flag once;
+  std::call_once(once, [] {
+    CK(cudaFuncSetAttribute(k_ntt2_fpr<LA, LB, false, 1, TensorLoad>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)fpr_smem_bytes<LA, LB>(1)));
+  });
+  NttJob first = job, second = job;
+  first.out_raw = 1;  // the words between the passes stay reduced doubles
+  second.in_raw = 1;
+  launch_begin(r);
+  launch_pdl(r, k_ntt2_fpr<LA, LB, false, 1, TensorLoad>, grid(LB), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(1), first, tl);
+  launch_pdl(r, k_ntt2_fpr<LA, LB, false, 0>, grid(LA), NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), second, NoEpi{});
+  r->launches++;  // two kernels (launch_end counts the other)
+  const double words = (double)n * job.nsub * r->N;
+  // operands read (4 limb-polys of a and b per limb), the tensor's transform written once
+  launch_end(r, "tensor_intt", 8.0 * (double)n * nt * r->N * 4.0 + 8.0 * words, words / 2.0 * r->logN);
+}
+static bool tensor_intt_fused(cgb_ring *r, int n, u64 *ten, const TensorLoad &tl, const int *mod_of_limb) {
+  if (!(g_tensor_fuse && r->fp_ntt && (g_fp_regio & 3) == 3 && r->logN >= 13 && r->logN <= 16)) return false;
+  switch (r->logN) {
+    case 13: tensor_intt_t<6, 7>(r, n, ten, tl, mod_of_limb); break;
+    case 14: tensor_intt_t<7, 7>(r, n, ten, tl, mod_of_limb); break;
+    case 15: tensor_intt_t<7, 8>(r, n, ten, tl, mod_of_limb); break;
+    default: tensor_intt_t<8, 8>(r, n, ten, tl, mod_of_limb); break;
+  }
+  return true;
+}
 extern "C" {
 
 const char *cgb_last_error(void) { return g_err.c_str(); }
@@ -3553,6 +3684,8 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_PDL")) g_pdl = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_MD")) g_ks_md = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_HOIST")) g_ks_hoist = atoi(e) != 0;
+  if (const char *e = getenv("CGB_TENSOR_FUSE")) g_tensor_fuse = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
@@ -3780,6 +3913,10 @@ int cgb_ct_free(cgb_ring *r, int count, const uint32_t *ids) {
   API_END
 }
 uint64_t *cgb_ct_device_ptr(cgb_ring *r, uint32_t id) { return r->arena + (size_t)id * r->ct_words; }
+int64_t cgb_ct_free_count(cgb_ring *r) {
+  std::lock_guard<std::mutex> g(r->mu);
+  return (int64_t)r->ct_free.size();
+}
 
 int cgb_pt_alloc(cgb_ring *r, int count, uint32_t *ids) {
   API_BEGIN
@@ -4407,8 +4544,11 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
       launch_ntt(r, true, job, n);
     }
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
-    LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
-    ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
+    const TensorLoad tl{dpa, dpb, in, dpx, dpax, r->d_mods, L, nt, r->iB0, logN};
+    if (!tensor_intt_fused(r, n, ten, tl, tm.data())) {
+      LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
+      ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
+    }
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
     {
       const dim3 grid(GRID1(3ull * N, TPB).x, n);

@@ -7,6 +7,7 @@
 // bit-identical to the CPU restatement in oracle/rnsbfv.c.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace cgb {
@@ -753,6 +754,17 @@ struct NoEpi {
   static constexpr bool active = false;
   __device__ void store(int, int, u64, const u64 *, int) const {}
 };
+// an EPI may also feed the first pass of a row-first transform: `loads` = true and
+// load4(item, unit, pos, out) supplies the 4 canonical words at pos (e.g. a tensor
+// product computed from its operands on the fly, cgb200.cu TensorLoad)
+template <class E, class = void>
+struct EpiLoads {
+  static constexpr bool value = false;
+};
+template <class E>
+struct EpiLoads<E, std::void_t<decltype(E::loads)>> {
+  static constexpr bool value = E::loads;
+};
 
 // LM-point sub-NTT in two register phases (RA stages then LM - RA), E = 16
 #ifdef CGB_FPR_MINB
@@ -808,7 +820,13 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   double x[E];
   {
     u64 v[E];
-    if (PASS == 1 && PA::ST == 1 && PA::K % 4 == 0 && gal == 1) {  // K consecutive words: full-sector loads
+    if constexpr (EpiLoads<EPI>::value) {  // the source words computed by the epilogue object
+      static_assert(PASS == 1 && PA::ST == 1 && PA::K % 4 == 0, "fused loads feed a row pass in 4-word runs");
+#pragma unroll
+      for (int u = 0; u < PA::R; u++)
+#pragma unroll
+        for (int k = 0; k < PA::K; k += 4) epi.load4(item, sub, gaddr(PA::idx(tl, u, k)), &v[u * PA::K + k]);
+    } else if (PASS == 1 && PA::ST == 1 && PA::K % 4 == 0 && gal == 1) {  // K consecutive words: full-sector loads
 #pragma unroll
       for (int u = 0; u < PA::R; u++)
 #pragma unroll

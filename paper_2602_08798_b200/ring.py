@@ -128,6 +128,9 @@ class Ring:
                 self._ext[int(a)] = slots[2 * k:2 * k + 2].copy()
         return np.ascontiguousarray(np.concatenate([self._ext[int(a)] for a in b_ids]).astype(np.uint32))
 
+    def free_slots(self) -> int:
+        return int(nat.lib().cgb_ct_free_count(self._h))
+
     def has_ext(self, ids) -> bool:
         """Whether every id already has a resident base-B extension."""
         return bool(self._ext) and all(int(a) in self._ext for a in _ids(ids))
