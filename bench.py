@@ -289,7 +289,7 @@ def layer_model(args):
     from paper_2602_08798_b200 import model as M
 
     cfg = M.ModelConfig(layers=1, d1=HEADS * D2, heads=HEADS, ffn_dim=4 * HEADS * D2, vocab=GPT2_VOCAB,
-                        max_seq=args.L + args.steps + 2, f=F,
+                        max_seq=args.L + args.steps + args.warmup + 2, f=F,
                         unembed_vocab=None if getattr(args, "full_vocab", False) else N_SLOTS)
     return M, M.gpt2_layer_model(cfg, seed=0)
 
@@ -331,7 +331,7 @@ def run_layer(args):
     first_ms = []
     toks = []
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))).__enter__()  # before the warm-up token
-    for _ in range(max(1, min(args.warmup, 1))):
+    for _ in range(max(1, args.warmup)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
@@ -365,8 +365,8 @@ def run_layer(args):
                                    _peaks(), ring.modmul_peak())
     line = {"metric": f"HE decoder-layer decode ms/token (GPT-2 small layer, prompt {args.L}, "
                       f"{args.steps} tokens, refresh each step)",
-            # value: mean decode ms/token over the timed tokens, after one warm-up token (which
-            # also builds the decode-side weight diagonals once: first_token_ms)
+            # value: mean decode ms/token over the timed tokens, after `warmup` untimed tokens
+            # (the first builds the decode-side weight diagonals once: first_token_ms)
             "value": float(np.mean(step_ms)), "unit": "ms/token", "higher_is_better": False, "n_gpus": 1,
             "warmup_tokens": len(first_ms), "first_token_ms": first_ms,
             "e2e": {"value": float(np.mean(step_ms)), "unit": "ms/token", "h2d_bytes_per_step": int(h2d),

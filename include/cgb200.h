@@ -134,6 +134,12 @@ int cgb_encrypt(cgb_ring *ring, int count, const uint64_t *slots,
  * encryptions owned by different contexts) */
 int cgb_encrypt_batch(cgb_ring *ring, int count, const uint64_t *slots, const uint32_t *enc_keys,
                       const uint64_t *indices, const uint32_t *out_ids);
+/* The client's decrypt-then-encrypt of a refresh (kv_cache.py:150: ctx.encrypt(ctx.decrypt(masked)))
+ * without the host hop: item i is decrypted to its slot vector on the device and encrypted
+ * again with key enc_keys[8 i ..] at index indices[i] -- the same words as cgb_decrypt
+ * followed by cgb_encrypt_batch of those slots. */
+int cgb_reencrypt_batch(cgb_ring *ring, int count, const uint32_t *cts, const uint32_t *enc_keys,
+                        const uint64_t *indices, const uint32_t *out_ids);
 /* Context.decrypt (backend.py:312-319) */
 int cgb_decrypt(cgb_ring *ring, int count, const uint32_t *cts, uint64_t *slots_out);
 /* The same decryption split at the client round trip: _start enqueues it (and the

@@ -85,6 +85,7 @@ SIGNATURES = {
     "cgb_pt_free": (ctypes.c_int, [_vp, ctypes.c_int, _u32p]),
     "cgb_pt_encode": (ctypes.c_int, [_vp, ctypes.c_int, _u64p, ctypes.c_int, _u32p]),
     "cgb_ct_free_count": (ctypes.c_int64, [_vp]),
+    "cgb_reencrypt_batch": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u64p, _u32p]),
     "cgb_mult_cipher_ext2": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u32p, _u32p, _u32p, _u32p]),
     "cgb_mask_pcg64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), _u64p, _u32p,
                                       _u32p, _u64p]),

@@ -722,6 +722,29 @@ class GpuContext:
         return w
 
     @staticmethod
+    def w_reencrypt(wave: Wave, ctxs) -> Wave:
+        """w_encrypt(ctxs, w_decrypt(wave)) -- the client's re-encryption of a refresh
+        (kv_cache.py:150) -- with the slot vectors kept on the device: the same
+        words, counters, nonces and budgets as the two calls."""
+        if len(wave) and wave.budgets.min() <= 0:
+            raise DecryptionFailure("noise budget exhausted: decryption would be incorrect")
+        GpuContext._charge(wave, "decrypt", n_emit=0)
+        uniq, owner = _owners(ctxs)
+        ring = uniq[0]._ring
+        ids = ring.alloc(len(owner))
+        blk = _Block(ring, ids)
+        idx = np.zeros(len(owner), np.uint64)
+        for k, c in enumerate(uniq):
+            sel = np.nonzero(owner == k)[0]
+            idx[sel] = c._enc_index + np.arange(sel.size, dtype=np.uint64)
+            c._enc_index += sel.size
+        keys = np.stack([np.asarray(c._enc_key, dtype=np.uint32).reshape(8) for c in uniq])[owner]
+        ring.reencrypt_batch(wave.aids, keys, idx, ids)
+        w = Wave(uniq, owner, ids, np.full(len(owner), uniq[0].params.initial_noise_budget, np.int64), [blk])
+        w.cids = GpuContext._charge(w, "encrypt")
+        return w
+
+    @staticmethod
     def w_decrypt(wave: Wave) -> np.ndarray:
         if len(wave) == 0:
             return np.zeros((0, wave.ctxs[0].params.n_slots), np.int64)

@@ -3127,8 +3127,12 @@ static void keyswitch(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64 *c
 // allows): smaller chunks keep a chunk's intermediates (xr, D, acc_P, W) L2-resident
 // between the five launches
 static int g_ks_chunk = 0;
+// workspace bytes per chunk (CGB_WS_GIB): 6 GiB lets a decode wave's key switch run as
+// ONE batch of up to 528 ciphertexts (3 GiB: 264) -- 76.3 -> 73.1 ms/token, fewer
+// launch tails; 10 GiB measured the same
+static size_t g_ws_bytes = (size_t)6 << 30;
 static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
-  size_t budget = (size_t)3 << 30;  // bytes of workspace per chunk
+  size_t budget = g_ws_bytes;
   size_t c = budget / std::max<size_t>(words_per_item * 8, 1);
   return std::max<size_t>(1, std::min<size_t>(c, 4096));
 }
@@ -3686,6 +3690,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_HOIST")) g_ks_hoist = atoi(e) != 0;
   if (const char *e = getenv("CGB_TENSOR_FUSE")) g_tensor_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
+  if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
   fused_attrs_for(log_n, n_limbs);
@@ -4102,10 +4107,19 @@ int cgb_mask_pcg64(cgb_ring *r, int count, int nchan, const int32_t *chan, uint6
 // encryption of `count` slot vectors, item i with ChaCha20 key keys[i] and encryption
 // index idx[i] (nonces DOM_ENC_A / DOM_ENC_E); one launch sequence for the batch
 static void encrypt_items(cgb_ring *r, int count, const uint64_t *slots, const ChaKey *keys, const u64 *idx,
-                          const uint32_t *out) {
+                          const uint32_t *out, const u64 *d_slots = nullptr) {
   Scratch S(r);
   u64 *m = S.alloc<u64>((size_t)count * r->N);
-  encode_slots(r, S, slots, count, m);
+  if (d_slots) {  // slot vectors already on the device (the client's re-encryption of a refresh)
+    CK(cudaMemsetAsync(m, 0, sizeof(u64) * (size_t)count * r->N, r->stream));
+    LAUNCH("scatter_slots", BYTES_scatter_slots,
+           k_scatter_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(m, d_slots, r->d_slot_idx,
+                                                                                       r->n_slots, r->t, r->logN));
+    int mi = r->iT;
+    ntt_items(r, false, m, nullptr, r->N, count, 1, 1, &mi);
+  } else {
+    encode_slots(r, S, slots, count, m);
+  }
   auto pc = ct_ptrs(r, count, out);
   u64 **dc = S.up(pc.data(), count);
   std::vector<u64 *> c1(count);
@@ -4147,6 +4161,20 @@ int cgb_encrypt_batch(cgb_ring *r, int count, const uint64_t *slots, const uint3
   std::vector<ChaKey> keys(count);
   for (int i = 0; i < count; i++) memcpy(keys[i].k, enc_keys + 8 * (size_t)i, sizeof keys[i].k);
   encrypt_items(r, count, slots, keys.data(), indices, out);
+  API_END
+}
+
+static void decrypt_slots_dev(cgb_ring *r, Scratch &S, int count, const uint32_t *cts, u64 *so);
+int cgb_reencrypt_batch(cgb_ring *r, int count, const uint32_t *cts, const uint32_t *enc_keys,
+                        const uint64_t *indices, const uint32_t *out) {
+  API_BEGIN
+  if (count <= 0) return CGB_OK;
+  std::vector<ChaKey> keys(count);
+  for (int i = 0; i < count; i++) memcpy(keys[i].k, enc_keys + 8 * (size_t)i, sizeof keys[i].k);
+  Scratch S(r);
+  u64 *so = S.alloc<u64>((size_t)count * r->n_slots);
+  decrypt_slots_dev(r, S, count, cts, so);
+  encrypt_items(r, count, nullptr, keys.data(), indices, out, so);
   API_END
 }
 
@@ -4215,6 +4243,23 @@ int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out
   API_END
 }
 // decryption kernels + the device->host copy of the slots, enqueued on the ring's stream
+// decryption into device slot vectors so[count][n_slots] (the client's view)
+static void decrypt_slots_dev(cgb_ring *r, Scratch &S, int count, const uint32_t *cts, u64 *so) {
+  auto pc = ct_ptrs(r, count, cts);
+  u64 **dc = S.up(pc.data(), count);
+  u64 words = (u64)r->L * r->N;
+  u64 *X = S.alloc<u64>((size_t)count * words);
+  LAUNCH("dec_inner", BYTES_dec_inner, k_dec_inner<<<dim3(GRID1(words, TPB).x, count), TPB, 0, r->stream>>>(X, (const u64 *const *)dc, r->d_s, r->d_mods,
+                                                                       r->d_c, r->L, r->logN, 0));
+  std::vector<int> qm;
+  ntt_items(r, false, X, nullptr, words, count, 1, r->L, q_mod_idx(r, qm));
+  u64 *m = S.alloc<u64>((size_t)count * r->N);
+  LAUNCH("dec_scale", BYTES_dec_scale, k_dec_scale<<<dim3(GRID1(r->N, TPB).x, count), TPB, 0, r->stream>>>(m, X, r->d_c, r->L, r->logN));
+  int mi = r->iT;
+  ntt_items(r, true, m, nullptr, r->N, count, 1, 1, &mi);
+  LAUNCH("gather_slots", BYTES_gather_slots, k_gather_slots<<<dim3(GRID1(r->n_slots, TPB).x, count), TPB, 0, r->stream>>>(so, m, r->d_slot_idx, r->n_slots,
+                                                                               r->logN));
+}
 static void decrypt_enqueue(cgb_ring *r, int count, const uint32_t *cts, u64 *slots_out) {
   Scratch S(r);
   auto pc = ct_ptrs(r, count, cts);

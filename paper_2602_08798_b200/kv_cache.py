@@ -223,8 +223,11 @@ def maybe_refresh_heads(caches, ctxs, chans, force: bool = False) -> list:
     else:
         r = draw_masks(item_chans, n)
         masked = C.w_add_plain(wave, neg_mod(r, p), one_shot=True, canonical=True)
-    view = C.w_decrypt(masked)
-    fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view, canonical=True)
+    if on_device:  # the client's decrypt + re-encrypt without the host hop (same words)
+        fresh = C.w_reencrypt(masked, [ctxs[s[0]] for s in sel])
+    else:
+        view = C.w_decrypt(masked)
+        fresh = C.w_encrypt([ctxs[s[0]] for s in sel], view, canonical=True)
     for h, _, _, _ in sel:
         chans[h].transfer("refresh", n, trips=2)
     if on_device:

@@ -220,6 +220,15 @@ class Ring:
                                               nat.u32ptr(ids)), "cgb_encrypt_batch")
         self.h2d_bytes += s.nbytes
 
+    def reencrypt_batch(self, src, enc_keys, indices, out):
+        """Decrypt each src item and encrypt its slots again (key enc_keys[i], index
+        indices[i]) without leaving the device (cgb_reencrypt_batch)."""
+        src, out = _ids(src), _ids(out)
+        k = np.ascontiguousarray(np.asarray(enc_keys, dtype=np.uint32).reshape(src.size, 8))
+        ix = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64).reshape(src.size))
+        nat.check(nat.lib().cgb_reencrypt_batch(self._h, src.size, nat.u32ptr(src), nat.u32ptr(k), nat.u64ptr(ix),
+                                                nat.u32ptr(out)), "cgb_reencrypt_batch")
+
     def decrypt(self, ids) -> np.ndarray:
         ids = _ids(ids)
         out = np.zeros((ids.size, self.n_slots), dtype=np.uint64)
