@@ -301,8 +301,11 @@ def run_layer(args):
     The unembedding covers the first 8192 vocabulary entries (n_slots)."""
     # the FFN prefill keeps ~20k ciphertexts live; every decode-step weight diagonal stays
     # resident (a full-vocabulary unembedding: 7 x 8192 diagonals, 57k products per token)
+    # plaintext arena: every decode-side weight diagonal (~33k: 36 head projections x 768,
+    # wo, w1, w2, the unembedding) stays resident next to the forced refresh's 3.1k mask
+    # plaintexts per token; at 12 GiB the masks evicted diagonals (a 1.4 s re-encode token)
     os.environ.setdefault("CGB_ARENA_GIB", "56" if args.full_vocab else "64")
-    os.environ.setdefault("CGB_PT_ARENA_GIB", "34" if args.full_vocab else "12")
+    os.environ.setdefault("CGB_PT_ARENA_GIB", "40")
     import torch
 
     from paper_2602_08798_b200 import _native

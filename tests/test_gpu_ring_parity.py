@@ -273,3 +273,19 @@ def test_batched_mult_cipher_both_resident_bitexact(bench):
     bad = [i for i in range(256) if not np.array_equal(got[i], want[i])]
     assert not bad, f"{len(bad)} items differ, first {bad[:8]}"
     g.free(out)
+
+
+def test_reencrypt_equals_decrypt_then_encrypt(bench):
+    """The client's re-encryption of a refresh on the device (cgb_reencrypt_batch)
+    == decrypt to host slots, then encrypt them (kv_cache.py:150): every word."""
+    g, pool, vals, ids, words = bench
+    src = ids[:16]
+    keys = np.stack([ENC + 7 * i for i in range(16)]).astype(np.uint32)
+    idx = np.arange(100, 116, dtype=np.uint64)
+    a = g.alloc(16)
+    g.reencrypt_batch(src, keys, idx, a)
+    b = g.alloc(16)
+    g.encrypt_batch(g.decrypt(src), keys, idx, b)
+    assert np.array_equal(g.store(a), g.store(b))
+    assert np.array_equal(g.decrypt(a), vals[:16])
+    g.free(np.concatenate([a, b]))
