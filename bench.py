@@ -304,8 +304,9 @@ def run_layer(args):
     # plaintext arena: every decode-side weight diagonal (~33k: 36 head projections x 768,
     # wo, w1, w2, the unembedding) stays resident next to the forced refresh's 3.1k mask
     # plaintexts per token; at 12 GiB the masks evicted diagonals (a 1.4 s re-encode token)
-    os.environ.setdefault("CGB_ARENA_GIB", "56" if args.full_vocab else "64")
-    os.environ.setdefault("CGB_PT_ARENA_GIB", "40")
+    # (~8k rotation keys of 6 MiB stay resident too: arenas + keys + workspace < 180 GB)
+    os.environ.setdefault("CGB_ARENA_GIB", "48")
+    os.environ.setdefault("CGB_PT_ARENA_GIB", "34" if args.full_vocab else "24")
     import torch
 
     from paper_2602_08798_b200 import _native
@@ -329,6 +330,7 @@ def run_layer(args):
     ev[1].record(stream)
     torch.cuda.synchronize()
     t_pre = time.perf_counter() - t0
+    pre_ms = ev[0].elapsed_time(ev[1])
     # warm-up decode token(s): the first builds the decode-side weight diagonals (a
     # one-time model setup) and every rotation key of the step; timed separately
     first_ms = []
@@ -346,6 +348,8 @@ def run_layer(args):
     gc.collect()
     gc.freeze()
     h0, d0 = ring.h2d_bytes, ring.d2h_bytes
+    torch.cuda.synchronize()
+    ev[1].record(stream)  # the timed tokens start here (after the warm-up tokens)
     if True:
         for i in range(args.steps):
             tok, state = M.decode_step(mdl, state, ctx, chans, force_refresh=True)
@@ -355,7 +359,6 @@ def run_layer(args):
     clk.__exit__(None, None, None)
     t_all = time.perf_counter() - t0
     h2d, d2h = (ring.h2d_bytes - h0) / args.steps, (ring.d2h_bytes - d0) / args.steps
-    pre_ms = ev[0].elapsed_time(ev[1])
     step_ms = [ev[i + 1].elapsed_time(ev[i + 2]) for i in range(args.steps)]
     # one more step outside the timed ones with CUDA events around every launch
     ring.timing(True)
