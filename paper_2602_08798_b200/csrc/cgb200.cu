@@ -46,6 +46,7 @@ struct CgbError {
   } while (0)
 
 #define API_BEGIN try {
+#define RING_LOCK(r) std::lock_guard<std::recursive_mutex> _ring_lock((r)->api)
 #define API_END                                                                       \
   {                                                                                   \
     cudaError_t _le = cudaGetLastError();                                             \
@@ -209,6 +210,10 @@ struct cgb_ring {
   cudaEvent_t pin_left[2] = {nullptr, nullptr};
   u64 launches = 0;
   std::mutex mu;
+  // every entry point taking the ring holds this while it enqueues: the reference runs
+  // heads on threads with forked contexts (model.py:395-400), which share one ring here,
+  // and the ring's staging buffers, scratch and key cache are per-ring state
+  std::recursive_mutex api;
   // timing (cgb_timing_enable): mode 1 = events around every kernel (PDL off);
   // mode 2 = events around every timing GROUP (a whole key switch, a whole
   // mult_cipher: PDL stays on inside it) and around launches outside groups
@@ -1344,6 +1349,144 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
             fp_canon(y1[3], qd, qinv));
     }
 }
+
+// k_ks_row's MODE 2 (Q limbs' key inner product + ModDown row pass of W + combine)
+// with 8 words per thread: 256 threads per 2048-word row tile, the 7-stage row pass
+// in three register phases (1 + 3 + 3 stages, two shared-memory exchanges), half the
+// per-thread accumulators -- aimed at 128 registers (2 CTAs = 16 warps per SM against
+// 12 at 16 words per thread).  LB = 7 (N = 2^14) only; same words.  CGB_KSROW8.
+template <int LA, int LB, int L>
+__global__ void __launch_bounds__(NTT2_TILE / 8, 2)
+    k_ks_row8(const u64 *D, KsSrc xin, const u64 *const *keys, const ModTab *mods, const u64 *W, MdEpi epi, int raw) {
+  extern __shared__ u64 sm3[];
+  constexpr int E = 8, T = NTT2_TILE / E, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
+  constexpr int G = NTT2_TILE / M, TPS = M / E, TILES = (1 << LA) / G;
+  constexpr int PSH = fpr_psh(LM, 1), PADM = fpr_padm(LM, 1);
+  static_assert(LM == 7, "three row phases of 1 + 3 + 3 stages");
+  using PA = PhaseShape<LM, 0, 1, E>;
+  using PB = PhaseShape<LM, 1, 3, E>;
+  using PC = PhaseShape<LM, 4, 3, E>;
+  static_assert(PC::ST == 1 && PC::K % 4 == 0, "row-pass output: runs of >= 4 consecutive words");
+  const u64 N = 1ull << LOGN;
+  const int tile = blockIdx.x % TILES, rest = blockIdx.x / TILES;
+  const int l = rest % L, item = rest / L;
+  const ModTab &Md = mods[l];
+  const double qd = Md.qd, qinv = Md.qinv;
+  const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
+  const u64 row0 = (u64)(first + g) << LM;
+  double2 *tws = reinterpret_cast<double2 *>(sm3 + ksr_data_words(LM));
+  {
+    const double2 *gt = reinterpret_cast<const double2 *>(Md.ftw1t) + ((u64)first << LM);
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      const int e = tid + i * T;
+      tws[e + (e >> LM)] = __ldg(gt + e);
+    }
+  }
+  const double2 *tw = tws + g * (M + 1);
+  auto tile_src = [&](int t) -> const u64 * {
+    if (t < L - 1) {
+      const int j = t < l ? t : t + 1;
+      return D + ((u64)item * L * LP + (u64)j * LP + l) * N + ((u64)first << LM);
+    }
+    return W + ((u64)item * 2 * L + (u64)(t - (L - 1)) * L + l) * N + ((u64)first << LM);
+  };
+  pdl_start_dependents();
+  pdl_wait();
+  double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
+  auto spad = [](int i) { return i + (i >> PSH); };
+  // forward row pass of tile t: x ends in PC layout (8 consecutive words per thread)
+  auto row_pass = [&](double *x, int t) {
+    const u64 *src = tile_src(t) + ((u64)g << LM);
+#pragma unroll
+    for (int u = 0; u < PA::R; u++)
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) {
+        const u64 v = __ldcs(src + PA::idx(tl, u, k));
+        x[u * PA::K + k] = (raw & 1) ? r2d(v) : u2d(v);
+      }
+    __syncthreads();  // twiddles staged; the previous pass's reads of the tile are done
+    phase_regs_fp<LM, 0, 1, true, E, false>(x, tw, tl, qd, qinv);
+#pragma unroll
+    for (int u = 0; u < PA::R; u++)
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, u, k))] = x[u * PA::K + k];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];
+    phase_regs_fp<LM, 1, 3, true, E, false>(x, tw, tl, qd, qinv);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k++) sd[spad(PB::idx(tl, u, k))] = x[u * PB::K + k];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PC::R; u++)
+#pragma unroll
+      for (int k = 0; k < PC::K; k++) x[u * PC::K + k] = sd[spad(PC::idx(tl, u, k))];  // forward: unreduced
+    phase_regs_fp<LM, 4, 3, true, E, true>(x, tw, tl, qd, qinv);
+  };
+  const u64 *K = keys[item];
+  const u64 *KF = K + 2 * (u64)L * 2 * LP * N;  // the key's FP64 plane
+  double a0[E], a1[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) a0[i] = a1[i] = 0.0;
+  int tcur = 0;
+#pragma unroll 1
+  for (int j = 0; j < L; j++) {
+    double x[E];
+    if (j == l) {  // the digit's own limb: the input itself, already in NTT form
+#pragma unroll
+      for (int u = 0; u < PC::R; u++)
+#pragma unroll
+        for (int k = 0; k < PC::K; k++)
+          x[u * PC::K + k] = u2d(ks_src_word(xin, item, j, (u32)(row0 + PC::idx(tl, u, k)), LOGN));
+    } else {
+      row_pass(x, tcur++);
+    }
+    const u64 *k0 = KF + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = KF + ((u64)(j * 2 + 1) * LP + l) * N + row0;
+#pragma unroll
+    for (int u = 0; u < PC::R; u++)
+#pragma unroll
+      for (int k = 0; k < PC::K; k += 4) {
+        const int o = PC::idx(tl, u, k);
+        u64 w0[4], w1[4];
+        ld256(k0 + o, w0);
+        ld256(k1 + o, w1);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const double xv = x[u * PC::K + k + e];
+          const double d0 = r2d(w0[e]), d1 = r2d(w1[e]);
+          a0[u * PC::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+          a1[u * PC::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+        }
+      }
+    if constexpr (L > 4) {
+      if ((j & 3) == 3 && j + 1 < L) {
+#pragma unroll
+        for (int i = 0; i < E; i++) {
+          a0[i] = fp_reduce(a0[i], qd, qinv);
+          a1[i] = fp_reduce(a1[i], qd, qinv);
+        }
+      }
+    }
+  }
+#pragma unroll 1
+  for (int pp = 0; pp < 2; pp++) {  // ModDown: row pass of W[pp][l], combine, store
+    double x[E];
+    row_pass(x, tcur++);
+#pragma unroll
+    for (int u = 0; u < PC::R; u++)
+#pragma unroll
+      for (int k = 0; k < PC::K; k += 4)
+        epi.combine4_fp(item, pp * L + l, row0 + PC::idx(tl, u, k), &x[u * PC::K + k],
+                        pp ? &a1[u * PC::K + k] : &a0[u * PC::K + k]);
+  }
+}
+static bool g_ksrow8 = false;  // CGB_KSROW8
 
 // Column-pass fusion: inverse column pass of a source limb-poly (its row pass already
 // done) followed, in the same CTA, by the centred lift into NT target moduli and each
@@ -2650,8 +2793,23 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   }
   if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
     launch_begin(r);
-    launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
+    if constexpr (LB == 7) {
+      if (g_ksrow8) {
+        static std::once_flag once8;
+        std::call_once(once8, [] {
+          CK(cudaFuncSetAttribute(k_ks_row8<LA, LB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ks_row_smem<LA, LB>()));
+        });
+        launch_pdl(r, k_ks_row8<LA, LB, L>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 8,
+                   ks_row_smem<LA, LB>(), (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, (const u64 *)W, epi, 3);
+      } else {
+        launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
+                   ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
+      }
+    } else {
+      launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
+                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
+    }
     // D (L-1 digits) + own digit + W (2) + out (2) per limb, c0 / add1 when present; keys once
     launch_end(r, "ks_row_md",
                8.0 * (double)count * N * L * (L + 4.0 + (add0.items || add0.base ? 1 : 0) + (d_add1 ? 2 : 0)) +
@@ -3690,6 +3848,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_HOIST")) g_ks_hoist = atoi(e) != 0;
   if (const char *e = getenv("CGB_TENSOR_FUSE")) g_tensor_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
+  if (const char *e = getenv("CGB_KSROW8")) g_ksrow8 = atoi(e) != 0;
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
@@ -3739,6 +3898,7 @@ uint64_t cgb_launch_count(const cgb_ring *r) { return r->launches; }
 
 int cgb_modmul_peak(cgb_ring *r, double *modmuls_per_s) {
   API_BEGIN
+  RING_LOCK(r);
   u64 q = r->mods[0], w = r->mods[0] / 3 + 7, wsh = h_shoup(w, q);
   u64 *sink;
   CK(cudaMallocAsync((void **)&sink, 8, r->stream));
@@ -3774,6 +3934,7 @@ int cgb_modmul_peak(cgb_ring *r, double *modmuls_per_s) {
 // each) on scratch data; returns the average milliseconds per batch.
 int cgb_bench_ntt(cgb_ring *r, int count, int fwd, int iters, double *ms_out) {
   API_BEGIN
+  RING_LOCK(r);
   const int L = r->L, N = r->N;
   Scratch S(r);
   u64 *buf = S.alloc<u64>((size_t)count * 2 * L * N);
@@ -3798,6 +3959,7 @@ int cgb_bench_ntt(cgb_ring *r, int count, int fwd, int iters, double *ms_out) {
 
 int cgb_timing_enable(cgb_ring *r, int on) {
   API_BEGIN
+  RING_LOCK(r);
   CK(cudaStreamSynchronize(r->stream));
   for (auto &rc : r->recs) {
     r->event_pool.push_back(rc.a);
@@ -3812,6 +3974,7 @@ int cgb_timing_enable(cgb_ring *r, int on) {
 
 int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
   API_BEGIN
+  RING_LOCK(r);
   CK(cudaStreamSynchronize(r->stream));
   struct Agg {
     long n = 0;
@@ -3883,6 +4046,7 @@ int cgb_timing_report(cgb_ring *r, char *buf, size_t cap) {
 
 int cgb_set_stream(cgb_ring *r, void *s) {
   API_BEGIN
+  RING_LOCK(r);
   CK(cudaStreamSynchronize(r->stream));
   if (r->own_stream) cudaStreamDestroy(r->stream);
   r->stream = (cudaStream_t)s;
@@ -3891,12 +4055,14 @@ int cgb_set_stream(cgb_ring *r, void *s) {
 }
 int cgb_sync(cgb_ring *r) {
   API_BEGIN
+  RING_LOCK(r);
   CK(cudaStreamSynchronize(r->stream));
   API_END
 }
 
 int cgb_ct_alloc(cgb_ring *r, int count, uint32_t *ids) {
   API_BEGIN
+  RING_LOCK(r);
   std::lock_guard<std::mutex> g(r->mu);
   if ((size_t)count > r->ct_free.size())
     FAIL(CGB_ERR_NOMEM, "ciphertext arena exhausted (%zu slots)", r->arena_cap);
@@ -3909,6 +4075,7 @@ int cgb_ct_alloc(cgb_ring *r, int count, uint32_t *ids) {
 }
 int cgb_ct_free(cgb_ring *r, int count, const uint32_t *ids) {
   API_BEGIN
+  RING_LOCK(r);
   std::lock_guard<std::mutex> g(r->mu);
   for (int i = 0; i < count; i++) {
     if (ids[i] >= r->arena_cap || !r->ct_used[ids[i]]) FAIL(CGB_ERR_PARAM, "double free of ciphertext %u", ids[i]);
@@ -3925,6 +4092,7 @@ int64_t cgb_ct_free_count(cgb_ring *r) {
 
 int cgb_pt_alloc(cgb_ring *r, int count, uint32_t *ids) {
   API_BEGIN
+  RING_LOCK(r);
   std::lock_guard<std::mutex> g(r->mu);
   if ((size_t)count > r->pt_free.size()) FAIL(CGB_ERR_NOMEM, "plaintext arena exhausted (%zu slots)", r->pt_cap);
   for (int i = 0; i < count; i++) {
@@ -3936,6 +4104,7 @@ int cgb_pt_alloc(cgb_ring *r, int count, uint32_t *ids) {
 }
 int cgb_pt_free(cgb_ring *r, int count, const uint32_t *ids) {
   API_BEGIN
+  RING_LOCK(r);
   std::lock_guard<std::mutex> g(r->mu);
   for (int i = 0; i < count; i++) {
     if (ids[i] >= r->pt_cap || !r->pt_used[ids[i]]) FAIL(CGB_ERR_PARAM, "double free of plaintext %u", ids[i]);
@@ -3947,6 +4116,7 @@ int cgb_pt_free(cgb_ring *r, int count, const uint32_t *ids) {
 
 int cgb_ct_copy(cgb_ring *r, int count, const uint32_t *src, const uint32_t *dst) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   Scratch S(r);
   auto ps = ct_ptrs(r, count, src), pd = ct_ptrs(r, count, dst);
@@ -3956,6 +4126,7 @@ int cgb_ct_copy(cgb_ring *r, int count, const uint32_t *src, const uint32_t *dst
 }
 int cgb_ct_store(cgb_ring *r, int count, const uint32_t *ids, uint64_t *host) {
   API_BEGIN
+  RING_LOCK(r);
   for (int i = 0; i < count; i++) {
     auto p = ct_ptrs(r, 1, &ids[i]);
     CK(cudaMemcpyAsync(host + (size_t)i * r->ct_words, p[0], sizeof(u64) * r->ct_words, cudaMemcpyDeviceToHost,
@@ -3966,6 +4137,7 @@ int cgb_ct_store(cgb_ring *r, int count, const uint32_t *ids, uint64_t *host) {
 }
 int cgb_ct_load(cgb_ring *r, int count, const uint32_t *ids, const uint64_t *host) {
   API_BEGIN
+  RING_LOCK(r);
   for (int i = 0; i < count; i++) {
     auto p = ct_ptrs(r, 1, &ids[i]);
     CK(cudaMemcpyAsync(p[0], host + (size_t)i * r->ct_words, sizeof(u64) * r->ct_words, cudaMemcpyHostToDevice,
@@ -3986,6 +4158,7 @@ static void pt_from_coeffs(cgb_ring *r, Scratch &S, const u64 *m, int count, int
 }
 int cgb_pt_encode(cgb_ring *r, int count, const uint64_t *slots, int kind, const uint32_t *pt_ids) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   if (kind != CGB_PT_MUL && kind != CGB_PT_ADD) FAIL(CGB_ERR_PARAM, "unknown plaintext kind %d", kind);
   Scratch S(r);
@@ -4007,6 +4180,7 @@ __global__ void k_scatter_slots_dev(u64 *m, const u64 *slots, const u32 *slot_id
 int cgb_mask_pcg64(cgb_ring *r, int count, int nchan, const int32_t *chan, uint64_t *st, const uint32_t *pt_neg,
                    const uint32_t *pt_pos, uint64_t *masks_out) {
   API_BEGIN
+  RING_LOCK(r);
   using namespace cgbmask;
   if (count <= 0) return CGB_OK;
   if (nchan <= 0 || r->t >= (1ull << 32)) FAIL(CGB_ERR_PARAM, "mask stream: %d channels, bound %llu", nchan,
@@ -4144,6 +4318,7 @@ static void encrypt_items(cgb_ring *r, int count, const uint64_t *slots, const C
 int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t enc_key[8], uint64_t first_index,
                 const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   ChaKey key;
   memcpy(key.k, enc_key, sizeof key.k);
@@ -4157,6 +4332,7 @@ int cgb_encrypt(cgb_ring *r, int count, const uint64_t *slots, const uint32_t en
 int cgb_encrypt_batch(cgb_ring *r, int count, const uint64_t *slots, const uint32_t *enc_keys,
                       const uint64_t *indices, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   std::vector<ChaKey> keys(count);
   for (int i = 0; i < count; i++) memcpy(keys[i].k, enc_keys + 8 * (size_t)i, sizeof keys[i].k);
@@ -4168,6 +4344,7 @@ static void decrypt_slots_dev(cgb_ring *r, Scratch &S, int count, const uint32_t
 int cgb_reencrypt_batch(cgb_ring *r, int count, const uint32_t *cts, const uint32_t *enc_keys,
                         const uint64_t *indices, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   std::vector<ChaKey> keys(count);
   for (int i = 0; i < count; i++) memcpy(keys[i].k, enc_keys + 8 * (size_t)i, sizeof keys[i].k);
@@ -4186,6 +4363,7 @@ struct DecTicket {  // an enqueued decryption: pinned landing buffer + completio
 static void decrypt_enqueue(cgb_ring *r, int count, const uint32_t *cts, u64 *dst_host);
 int cgb_decrypt_start(cgb_ring *r, int count, const uint32_t *cts, void **ticket_out) {
   API_BEGIN
+  RING_LOCK(r);
   const size_t words = (size_t)(count > 0 ? count : 0) * r->n_slots;
   auto *t = new DecTicket{nullptr, words, words, nullptr};
   *ticket_out = t;
@@ -4212,6 +4390,7 @@ int cgb_decrypt_start(cgb_ring *r, int count, const uint32_t *cts, void **ticket
 // the same, landing straight in the caller's page-locked buffer (no copy at finish)
 int cgb_decrypt_start_into(cgb_ring *r, int count, const uint32_t *cts, uint64_t *pinned_dst, void **ticket_out) {
   API_BEGIN
+  RING_LOCK(r);
   const size_t words = (size_t)(count > 0 ? count : 0) * r->n_slots;
   auto *t = new DecTicket{pinned_dst, words, 0, nullptr};  // cap 0: not a pooled buffer
   *ticket_out = t;
@@ -4223,6 +4402,7 @@ int cgb_decrypt_start_into(cgb_ring *r, int count, const uint32_t *cts, uint64_t
 }
 int cgb_decrypt_finish(cgb_ring *r, void *ticket, uint64_t *slots_out) {
   API_BEGIN
+  RING_LOCK(r);
   (void)r;
   auto *t = static_cast<DecTicket *>(ticket);
   if (!t) FAIL(CGB_ERR_PARAM, "null decryption ticket");
@@ -4237,6 +4417,7 @@ int cgb_decrypt_finish(cgb_ring *r, void *ticket, uint64_t *slots_out) {
 }
 int cgb_decrypt(cgb_ring *r, int count, const uint32_t *cts, uint64_t *slots_out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   decrypt_enqueue(r, count, cts, slots_out);
   CK(cudaStreamSynchronize(r->stream));
@@ -4282,6 +4463,7 @@ static void decrypt_enqueue(cgb_ring *r, int count, const uint32_t *cts, u64 *sl
 
 int cgb_noise_budget(cgb_ring *r, int count, const uint32_t *cts, double *bits) {
   API_BEGIN
+  RING_LOCK(r);
   const int L = r->L, N = r->N;
   u64 words = (u64)L * N;
   std::vector<u64> host(words);
@@ -4354,6 +4536,7 @@ int cgb_noise_budget(cgb_ring *r, int count, const uint32_t *cts, double *bits) 
 
 int cgb_add(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pb = ct_ptrs(r, count, b), po = ct_ptrs(r, count, out);
@@ -4365,6 +4548,7 @@ int cgb_add(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const 
 }
 int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
@@ -4375,6 +4559,7 @@ int cgb_add_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt,
 }
 int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), pp = pt_ptrs(r, count, pt), po = ct_ptrs(r, count, out);
@@ -4385,6 +4570,7 @@ int cgb_mult_plain(cgb_ring *r, int count, const uint32_t *a, const uint32_t *pt
 }
 int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) FAIL(CGB_ERR_PARAM, "empty sum");
   Scratch S(r);
   auto pa = ct_ptrs(r, count, a), po = ct_ptrs(r, 1, &out);
@@ -4396,6 +4582,7 @@ int cgb_sum(cgb_ring *r, int count, const uint32_t *a, uint32_t out) {
 
 int cgb_galois(cgb_ring *r, int count, const uint32_t *a, const uint64_t *g, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   galois_batch(r, count, a, g, out, false);
   API_END
@@ -4413,6 +4600,7 @@ static std::vector<u64> steps_to_g(cgb_ring *r, int count, const int64_t *steps)
 }
 int cgb_rotate(cgb_ring *r, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   auto g = steps_to_g(r, count, steps);
   galois_batch(r, count, a, g.data(), out, false);
@@ -4420,6 +4608,7 @@ int cgb_rotate(cgb_ring *r, int count, const uint32_t *a, const int64_t *steps, 
 }
 int cgb_rotate_add(cgb_ring *r, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count <= 0) return CGB_OK;
   auto g = steps_to_g(r, count, steps);
   galois_batch(r, count, a, g.data(), out, true);
@@ -4427,6 +4616,7 @@ int cgb_rotate_add(cgb_ring *r, int count, const uint32_t *a, const int64_t *ste
 }
 int cgb_prepare_galois(cgb_ring *r, int count, const uint64_t *g) {
   API_BEGIN
+  RING_LOCK(r);
   for (int i = 0; i < count; i++) {
     u64 gg = g[i] % (2ull * r->N);
     if (gg != 1) get_key(r, gg);
@@ -4509,6 +4699,7 @@ static void extend_B(cgb_ring *r, int count, const uint32_t *b, const uint32_t *
 }
 int cgb_extend_b(cgb_ring *r, int count, const uint32_t *b, const uint32_t *bx) {
   API_BEGIN
+  RING_LOCK(r);
   if (count > 0) extend_B(r, count, b, bx);
   API_END
 }
@@ -4517,18 +4708,21 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
                              const uint32_t *out, const uint32_t *ax = nullptr);
 int cgb_mult_cipher(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count > 0) mult_cipher_impl(r, count, a, b, nullptr, out);
   API_END
 }
 int cgb_mult_cipher_ext(cgb_ring *r, int count, const uint32_t *a, const uint32_t *b, const uint32_t *bx,
                         const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (count > 0) mult_cipher_impl(r, count, a, b, bx, out);
   API_END
 }
 int cgb_mult_cipher_ext2(cgb_ring *r, int count, const uint32_t *a, const uint32_t *ax, const uint32_t *b,
                          const uint32_t *bx, const uint32_t *out) {
   API_BEGIN
+  RING_LOCK(r);
   if (ax && !bx) FAIL(CGB_ERR_PARAM, "mult_cipher_ext2: a resident a-extension needs b's too (swap the operands)");
   if (count > 0) mult_cipher_impl(r, count, a, b, bx, out, ax);
   API_END
