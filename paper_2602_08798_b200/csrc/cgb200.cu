@@ -839,6 +839,9 @@ __global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W,
 // ModDown combine as the store epilogue of the forward row pass that produces
 // W = NTT_l(lift_P(INTT_P(acc_P))): out = (acc_l - W) P^-1 (+ add0 on poly 0)
 // (+ add1), the same words as k_moddown_combine without W's round trip.
+#ifndef CGB_ABLATE
+#define CGB_ABLATE 0  // timing experiments only (wrong results): which loads / phases bound k_ks_row
+#endif
 struct MdEpi {
   static constexpr bool active = true;
   u64 *const *out;
@@ -919,8 +922,13 @@ struct MdEpi {
     const double2 pinv = C->fPinvq[l];
     const bool a0 = pp == 0 && (add0.items || add0.base);
     u64 bv[4], cv[4];
-    if (add1) ld256(add1[item] + (u64)unit * N + pos, bv);
-    if (a0) ks_src_block4(add0, item, l, (u32)pos, logN, cv);
+    if (CGB_ABLATE & 8) {
+#pragma unroll
+      for (int k = 0; k < 4; k++) bv[k] = pos + k, cv[k] = pos + 2 * k;
+    } else {
+      if (add1) ld256(add1[item] + (u64)unit * N + pos, bv);
+      if (a0) ks_src_block4(add0, item, l, (u32)pos, logN, cv);
+    }
     u64 v[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -972,7 +980,9 @@ struct MdEpi {
 #define CGB_KSROW_EPF 0  // MODE 2: epilogue operands prefetched (cp.async) into the exchange tile: measured slower
 #endif
 #ifndef CGB_KSROW_TWW
-#define CGB_KSROW_TWW 0  // staged row twiddles as w only (w/q formed on use): half the shared memory
+#define CGB_KSROW_TWW 1  // staged row twiddles as w only (w/q formed by one DMUL on use): half the shared
+                        // memory and half the twiddle LDS traffic of the LSU-bound row kernels (0.94 -> 0.90 ms
+                        // per 768 key switches in ks_row_md)
 #endif
 constexpr bool TWW = CGB_KSROW_TWW && !CGB_KSROW_GTW;
 #ifndef CGB_KSROW_PF
@@ -999,6 +1009,18 @@ constexpr int KSTAGE_BYTES = CGB_KSROW_KSTAGE ? 2 * 16 * 8 * (NTT2_TILE / 16) : 
 #ifndef CGB_KSROW_RPF
 #define CGB_KSROW_RPF 0  // next row tile prefetched into registers during the current tile's work
 #endif
+#ifndef CGB_KSROW_CPF
+#define CGB_KSROW_CPF 1  // next row tile prefetched by cp.async into a warp-private staging buffer
+                        // (in the shared memory TWW frees: 3 CTAs per SM as before): 0.90 -> 0.86 ms
+#endif
+// bytes of k_ks_row's staged row twiddles
+__host__ __device__ constexpr size_t ksr_tw_bytes(int LB) {
+  return CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 8 : 16) * (size_t)(NTT2_TILE + (NTT2_TILE >> LB));
+}
+// bytes of the cp.async staging buffer: the tile's rows at a pitch of 2^LB + 8 words
+__host__ __device__ constexpr size_t ksr_pf_bytes(int LB) {
+  return CGB_KSROW_CPF ? 8 * (size_t)(NTT2_TILE >> LB) * ((1 << LB) + 8) : 0;
+}
 #ifndef CGB_KSROW_MINB
 #if CGB_KSROW_RPF
 #define CGB_KSROW_MINB 2
@@ -1006,7 +1028,15 @@ constexpr int KSTAGE_BYTES = CGB_KSROW_KSTAGE ? 2 * 16 * 8 * (NTT2_TILE / 16) : 
 #define CGB_KSROW_MINB 3  // <= 168 registers: 3 CTAs per SM (MODE 2 would otherwise take 208)
 #endif
 #endif
+#if CGB_KSROW_PF >= 2  // 2: the next tile into L1; 3: and the next digit's key rows
+#define KSROW_PREFETCH(p) prefetch_l1(p)
+#else
+#define KSROW_PREFETCH(p) prefetch_l2(p)
+#endif
 #define KSROW_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_KSROW_MINB)
+// A row of the tile belongs to M / E <= 16 consecutive threads of ONE warp, so the
+// exchange between the two register phases of a row pass only needs a warp-level
+// barrier (ROW_SYNC, cgb_device.cuh): the CTA's warps run their rows independently.
 // MODE 0: every limb of Q u P; 1: the P limb only; 2: the Q limbs, followed by
 // ModDown's forward row pass of W (the column-pass output of lift(INTT(acc_P)))
 // with the combine as its epilogue -- the Q limbs' accumulators never reach memory.
@@ -1061,7 +1091,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       tws[e + (e >> LM)] = __ldg(gt + e);
     }
   };
-  stage_tw(Md.ftw1t);
+  if (!(CGB_ABLATE & 32)) stage_tw(Md.ftw1t);
   const double2 *tw = tws + g * (M + 1);
 #endif
 #endif
@@ -1096,7 +1126,42 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
     for (int k = 0; k < PA::K; k++) x[k] = (raw & 1) ? r2d(nv[k]) : u2d(nv[k]);
     issue_tile(tcur + 1);
-    __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
+    if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
+    tcur++;
+  };
+#elif CGB_KSROW_CPF
+  // The NEXT row tile streams into shared memory by 16-byte asynchronous copies while
+  // this tile's row pass and key products run: no registers are held and no warp
+  // waits on the tile's global loads.  A warp copies exactly the rows it consumes
+  // (its 32 / TPS rows are contiguous in the tile), so the hand-over is warp-local.
+  constexpr int PFP = M + 8;  // row pitch: the rows a half-warp reads in phase A fall in different bank halves
+  u64 *pfb = sm3 + ksr_data_words(LM) + (ksr_tw_bytes(LB) + KSTAGE_BYTES) / 8;
+  const int lane = tid & 31, wrow0 = (tid >> 5) * (32 / TPS);
+  auto issue_tile = [&](int t) {
+    if (t < ntile) {
+      constexpr int CH = (32 / TPS) * (M / 2);  // 16-byte chunks of the warp's rows
+      const u64 *src = tile_src(t) + ((u64)wrow0 << LM);
+#pragma unroll
+      for (int i = 0; i < CH / 32; i++) {
+        const int c = lane + 32 * i, r = c / (M / 2), cc = c % (M / 2);
+        cp_async16(pfb + (wrow0 + r) * PFP + 2 * cc, src + 2 * c);
+      }
+    }
+    cp_async_commit();
+  };
+  issue_tile(0);
+  auto load_tile = [&](double *x) {
+    cp_async_wait_all();
+    __syncwarp();
+    const u64 *src = pfb + g * PFP;
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) {
+      const u64 v = src[PA::idx(tl, 0, k)];
+      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+    }
+    __syncwarp();  // every lane has read the staged tile
+    issue_tile(tcur + 1);
+    if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
   };
 #else
@@ -1104,10 +1169,10 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     const u64 *src = tile_src(tcur) + ((u64)g << LM);
 #pragma unroll
     for (int k = 0; k < PA::K; k++) {
-      const u64 v = __ldcs(src + PA::idx(tl, 0, k));
-      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+      const u64 v = (CGB_ABLATE & 4) ? (u64)(tid * 977 + k + tcur) : __ldcs(src + PA::idx(tl, 0, k));
+      x[k] = ((raw & 1) && !(CGB_ABLATE & 4)) ? r2d(v) : u2d(v);
     }
-    __syncthreads();  // twiddles staged; the previous tile's phase-B reads are done
+    if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
   };
 #endif
@@ -1127,7 +1192,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
       for (int u = 0; u < PB::R; u++) {
         const u32 k0 = (u32)(row0 + PB::idx(tl, u, 0));
-        prefetch_l2(p + (xin.items && xin.g ? (perm_g(k0, gi, LOGN) & ~7u) : k0));
+        KSROW_PREFETCH(p + (xin.items && xin.g ? (perm_g(k0, gi, LOGN) & ~7u) : k0));
       }
       return;
     }
@@ -1135,7 +1200,14 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     int t;
     if (j + 1 < L) t = (l == L || j + 1 < l) ? j + 1 : j;  // digit j+1 (l skipped)
     else t = nd + (j + 1 - L);                             // W tile
-    if (t < ntile) prefetch_l2(tile_src(t) + 16 * (u64)tid);
+    if (t < ntile) KSROW_PREFETCH(tile_src(t) + 16 * (u64)tid);
+#if CGB_KSROW_PF >= 3  // also the next digit's key rows (both polys), one line per thread each
+    if (j + 1 < L) {
+      const u64 *KFp = K + 2 * (u64)L * 2 * LP * N;
+      KSROW_PREFETCH(KFp + ((u64)((j + 1) * 2 + 0) * LP + l) * N + ((u64)first << LM) + 16 * (u64)tid);
+      KSROW_PREFETCH(KFp + ((u64)((j + 1) * 2 + 1) * LP + l) * N + ((u64)first << LM) + 16 * (u64)tid);
+    }
+#endif
 #else
     (void)j;
 #endif
@@ -1182,6 +1254,19 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
           for (int e = 0; e < 4; e++) x[u * PB::K + k + e] = u2d(w[e]);
         }
+#elif (CGB_ABLATE & 1)
+      {
+        const u64 *p_ = xin.items[item] + xin.off + ((u64)j << LOGN) + row0;
+#pragma unroll
+        for (int u = 0; u < PB::R; u++)
+#pragma unroll
+          for (int k = 0; k < PB::K; k += 4) {
+            u64 w[4];
+            ld256(p_ + PB::idx(tl, u, k), w);
+#pragma unroll
+            for (int e = 0; e < 4; e++) x[u * PB::K + k + e] = u2d(w[e] & 0xFFFFFFFFFFFFull);
+          }
+      }
 #else
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
@@ -1191,15 +1276,15 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #endif
     } else {
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
+      if (!(CGB_ABLATE & 16)) phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
-      __syncthreads();
+      ROW_SYNC();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];  // no reduction in a forward pass
-      phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
+      if (!(CGB_ABLATE & 16)) phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
     }
     // the key's FP64 plane (k_key_fp): exact doubles, no per-word conversion
 #if CGB_KSROW_KSTAGE
@@ -1231,8 +1316,16 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       for (int k = 0; k < PB::K; k += 4) {
         const int o = PB::idx(tl, u, k);
         u64 w0[4], w1[4];
-        ld256(k0 + o, w0);
-        ld256(k1 + o, w1);
+        if (CGB_ABLATE & 2) {
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            w0[e] = (u64)__double_as_longlong((double)(o + e + j * 7 + 12345));
+            w1[e] = (u64)__double_as_longlong((double)(o + e + j * 5 + 54321));
+          }
+        } else {
+          ld256(k0 + o, w0);
+          ld256(k1 + o, w1);
+        }
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const double xv = x[u * PB::K + k + e];
@@ -1258,10 +1351,10 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       prefetch_next(L + pp);
       double x[E];
       load_tile(x);
-      phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
+      if (!(CGB_ABLATE & 16)) phase_regs_fp<LM, 0, RA, true, E, false, GT, TWW>(x, tw, tl, qd, qinv);
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
-      __syncthreads();
+      ROW_SYNC();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
@@ -1278,7 +1371,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
         for (int k = 0; k < PB::K; k += 4) epi.prefetch4(item, pp * L + l, row0 + PB::idx(tl, u, k), stg + u * PB::K + k);
       cp_async_commit();
 #endif
-      phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
+      if (!(CGB_ABLATE & 16)) phase_regs_fp<LM, RA, RB, true, E, true, GT, TWW>(x, tw, tl, qd, qinv);
 #if CGB_KSROW_EPF
       cp_async_wait_all();
 #endif
@@ -1320,14 +1413,14 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
       double y[E];
 #pragma unroll
       for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
-      __syncthreads();  // inverse twiddles staged / previous poly's reads done
+      if (pp == 0) __syncthreads(); else ROW_SYNC();  // inverse twiddles staged / previous poly's reads done
       phase_regs_fp<LM, RA, RB, false, E, true, GT, TWW>(y, itw, tl, qd, qinv);
-      __syncthreads();
+      ROW_SYNC();
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
         for (int k = 0; k < PB::K; k++) sd[spad(PB::idx(tl, u, k))] = y[u * PB::K + k];
-      __syncthreads();
+      ROW_SYNC();
 #pragma unroll
       for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
       phase_regs_fp<LM, 0, RA, false, E, false, GT, TWW>(y, itw, tl, qd, qinv);
@@ -1355,8 +1448,11 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 // in three register phases (1 + 3 + 3 stages, two shared-memory exchanges), half the
 // per-thread accumulators -- aimed at 128 registers (2 CTAs = 16 warps per SM against
 // 12 at 16 words per thread).  LB = 7 (N = 2^14) only; same words.  CGB_KSROW8.
+#ifndef CGB_KSROW8_MINB
+#define CGB_KSROW8_MINB 2
+#endif
 template <int LA, int LB, int L>
-__global__ void __launch_bounds__(NTT2_TILE / 8, 2)
+__global__ void __launch_bounds__(NTT2_TILE / 8, CGB_KSROW8_MINB)
     k_ks_row8(const u64 *D, KsSrc xin, const u64 *const *keys, const ModTab *mods, const u64 *W, MdEpi epi, int raw) {
   extern __shared__ u64 sm3[];
   constexpr int E = 8, T = NTT2_TILE / E, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
@@ -1405,24 +1501,24 @@ __global__ void __launch_bounds__(NTT2_TILE / 8, 2)
         const u64 v = __ldcs(src + PA::idx(tl, u, k));
         x[u * PA::K + k] = (raw & 1) ? r2d(v) : u2d(v);
       }
-    __syncthreads();  // twiddles staged; the previous pass's reads of the tile are done
+    if (t == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous pass's reads of the tile are done
     phase_regs_fp<LM, 0, 1, true, E, false>(x, tw, tl, qd, qinv);
 #pragma unroll
     for (int u = 0; u < PA::R; u++)
 #pragma unroll
       for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, u, k))] = x[u * PA::K + k];
-    __syncthreads();
+    ROW_SYNC();
 #pragma unroll
     for (int u = 0; u < PB::R; u++)
 #pragma unroll
       for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];
     phase_regs_fp<LM, 1, 3, true, E, false>(x, tw, tl, qd, qinv);
-    __syncthreads();
+    ROW_SYNC();
 #pragma unroll
     for (int u = 0; u < PB::R; u++)
 #pragma unroll
       for (int k = 0; k < PB::K; k++) sd[spad(PB::idx(tl, u, k))] = x[u * PB::K + k];
-    __syncthreads();
+    ROW_SYNC();
 #pragma unroll
     for (int u = 0; u < PC::R; u++)
 #pragma unroll
@@ -1647,8 +1743,7 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
 
 template <int LA, int LB>
 __host__ __device__ constexpr size_t ks_row_smem() {  // exchange tile + the tile's row twiddles (rows of 2^LB + 1 pairs)
-  return sizeof(u64) * (size_t)ksr_data_words(LB) +
-         (CGB_KSROW_GTW ? 0 : (CGB_KSROW_TWW ? 8 : 16) * (size_t)(NTT2_TILE + (NTT2_TILE >> LB))) + KSTAGE_BYTES;
+  return sizeof(u64) * (size_t)ksr_data_words(LB) + ksr_tw_bytes(LB) + KSTAGE_BYTES + ksr_pf_bytes(LB);
 }
 template <int LA, int LB, int L>
 static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-in

@@ -161,6 +161,7 @@ __device__ __forceinline__ u32 perm_g(u32 k, u64 g, int logN) {
   return __brev((se - 1) >> 1) >> (32 - logN);
 }
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // Programmatic dependent launch: a kernel launched with the PDL attribute may
 // start while its predecessor drains; it stages constant tables (twiddles), then
@@ -666,9 +667,17 @@ __global__ void __launch_bounds__(NTT2_TILE / E) k_ntt2_fp(NttJob job) {
 // to consecutive words of a row, which keeps both ends coalesced.
 // ---------------------------------------------------------------------------
 // 256-bit global accesses (one full 32-byte sector per thread; sm_100 LDG/STG.256)
+#ifndef CGB_LD256_SPLIT
+#define CGB_LD256_SPLIT 0  // experiment: 256-bit loads as two 128-bit loads
+#endif
 __device__ __forceinline__ void ld256(const u64 *p, u64 *v) {
+#if CGB_LD256_SPLIT
+  asm volatile("ld.global.cs.v2.b64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
+  asm volatile("ld.global.cs.v2.b64 {%0, %1}, [%2];" : "=l"(v[2]), "=l"(v[3]) : "l"(p + 2));
+#else
   asm volatile("ld.global.cs.v4.b64 {%0, %1, %2, %3}, [%4];"
                : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+#endif
 }
 __device__ __forceinline__ void st256(u64 *p, u64 a, u64 b, u64 c, u64 d) {
   asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
@@ -766,6 +775,16 @@ struct EpiLoads<E, std::void_t<decltype(E::loads)>> {
   static constexpr bool value = E::loads;
 };
 
+// Row passes (PASS 1) give each row to M / E <= 16 consecutive threads of one warp, so
+// the exchange between a row pass's register phases needs only a warp-level barrier.
+#ifndef CGB_ROW_WSYNC
+#define CGB_ROW_WSYNC 1
+#endif
+#if CGB_ROW_WSYNC
+#define ROW_SYNC() __syncwarp()
+#else
+#define ROW_SYNC() __syncthreads()
+#endif
 // LM-point sub-NTT in two register phases (RA stages then LM - RA), E = 16
 #ifdef CGB_FPR_MINB
 #define FPR_BOUNDS __launch_bounds__(NTT2_TILE / 16, CGB_FPR_MINB)
@@ -851,7 +870,7 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
       if (!FWD && RPA == 4) x[i] = fp_reduce(x[i], qd, qinv);  // a 4-stage inverse phase starts reduced
     }
   }
-  __syncthreads();  // twiddles staged
+  if (PASS == 0 || !CGB_ROW_WSYNC) __syncthreads();  // twiddles staged (row passes read theirs from global)
   const double2 *tw_g = PASS == 0 ? tws : gtw + ((u64)(first + g) << LM);
   phase_regs_fp<LM, S0A, RPA, FWD, E, PASS == 1 && S0A == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
   double *sd = data + g * PADM;
@@ -859,7 +878,8 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   for (int u = 0; u < PA::R; u++)
 #pragma unroll
     for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, u, k))] = x[u * PA::K + k];
-  __syncthreads();
+  if (PASS == 0) __syncthreads();
+  else ROW_SYNC();
 #pragma unroll
   for (int u = 0; u < PB::R; u++)
 #pragma unroll
