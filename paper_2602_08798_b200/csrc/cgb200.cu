@@ -166,7 +166,7 @@ struct Consts {
   double2 fQhatInv[MAXL], fQhatModB[MAXL][MAXL + 1], fQmodB[MAXL + 1];
   double2 fQBhatInv[MAXL], fBQhatInv[MAXL + 1], fsc_omega[MAXL][MAXL + 1], ftBhat[MAXL + 1];
   double2 fBhatInv[MAXL + 1], fBhatModQ[MAXL + 1][MAXL], fBmodQ[MAXL];
-  double2 fPinvq[MAXL];
+  double2 fPinvq[MAXL], fPmodq[MAXL];
 };
 
 static const u64 DOM_SK = 1, DOM_KSK_A = 2, DOM_KSK_E = 3, DOM_ENC_A = 4, DOM_ENC_E = 5;
@@ -1076,7 +1076,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
     for (int i = 0; i < E; i++) {
       const int e = tid + i * (NTT2_TILE / E);
-      twd[e + (e >> LM)] = __ldg(gt + e).x;
+      twd[e + (e >> LM)] = __ldg(reinterpret_cast<const double *>(table == Md.ftw1t ? Md.ftw1tw : Md.fitw1tw) + ((u64)first << LM) + e);
     }
   };
   stage_tw(Md.ftw1t);
@@ -1583,6 +1583,346 @@ __global__ void __launch_bounds__(NTT2_TILE / 8, CGB_KSROW8_MINB)
   }
 }
 static bool g_ksrow8 = false;  // CGB_KSROW8
+
+// ---------------------------------------------------------------------------
+// k_ks_row2: the key switch's two row kernels (MD = false: the P limb's inner product
+// and ModDown's inverse row pass, k_ks_row MODE 1; MD = true: the Q limbs' inner
+// product, ModDown's forward row pass of W and the combine, MODE 2) with EVERY operand
+// tile except the keys streamed through a two-slot cp.async ring in shared memory.
+//
+// ncu shows the row kernels bound by the L1 / LSU data pipe and by exposed load
+// latency, not by HBM or the FP64 pipe (profiles/r02/ncu_ks_row_lsu.md): each warp
+// used to load a tile, wait, compute, load the next.  Here a warp owns the 32 / TPS
+// rows it transforms (contiguous in the tile), copies exactly those rows two entries
+// ahead with 16-byte cp.async (no registers held, no warp waits on the copy), and
+// hands over with warp-level barriers only -- the kernel has no CTA barrier at all.
+// Entries, in consumption order:
+//   MD = false:  D(0, P) ... D(L-1, P)
+//   MD = true:   per digit j:  j != l: D(j, l);  j == l: the input's own limb read
+//                through the automorphism (its 2^LB-word source rows are contiguous:
+//                perm_g maps aligned blocks to aligned blocks), then c0 o sigma, which
+//                is folded into the accumulator as P c0 (out0 = (acc0 + P c0 - W0) / P:
+//                the same residue as adding c0 after the division);
+//                then W(0, l), [the rotate_add input, poly 0], W(1, l), [poly 1].
+// Tiles consumed pointwise (the rotate_add input) are stored with the 16-byte chunk
+// index XOR-swizzled so the 64- / 128-byte-strided lanes of a row read distinct banks.
+// Same words as k_ks_row (tests/test_gpu_ring_parity.py, test_gpu_primitives.py).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int LB>
+__host__ __device__ constexpr size_t ks_row2_smem() {
+  return 8 * ((size_t)ksr_data_words(LB) + (size_t)(NTT2_TILE >> LB) * ((1 << LB) + 1) +
+              2 * (size_t)(NTT2_TILE >> LB) * ((1 << LB) + 8));
+}
+#ifndef CGB_KSROW2_MINB
+#define CGB_KSROW2_MINB 3
+#endif
+#ifndef CGB_R2_OWN
+#define CGB_R2_OWN 0   // own limb / c0 through the ring (0: direct gathered loads, c0 in the epilogue): the
+                       // scattered shared-memory reads cost more than the gathers (ks_row_md 0.88 -> 0.95 ms)
+#endif
+#ifndef CGB_R2_ADD1
+#define CGB_R2_ADD1 1  // the rotate_add input through the ring (0: direct 256-bit loads in the epilogue)
+#endif
+template <int LA, int LB, int L, bool MD>
+__global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
+    k_ks_row2(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *keys, const ModTab *mods, int iP, const u64 *W,
+              MdEpi epi, int raw) {
+  extern __shared__ u64 sm3[];
+  constexpr int E = 16, LM = LB, M = 1 << LM, LOGN = LA + LB, LP = L + 1;
+  constexpr int G = NTT2_TILE / M, TPS = M / E, TILES = (1 << LA) / G, RW = 32 / TPS;
+  constexpr int PSH = fpr_psh(LM, 1), PADM = fpr_padm(LM, 1);
+  constexpr int RA = 4, RB = LM - 4;
+  using PA = PhaseShape<LM, 0, RA, E>;
+  using PB = PhaseShape<LM, RA, RB, E>;
+  static_assert(PB::ST == 1 && PB::K % 4 == 0, "row-pass output: runs of >= 4 consecutive words");
+  constexpr int PFP = M + 8, PFW = G * PFP;  // ring slot: the tile's rows at a pitch of M + 8 words
+  constexpr int CH = RW * (M / 2);           // 16-byte chunks of a warp's rows
+  const u64 N = 1ull << LOGN;
+  const int tile = blockIdx.x % TILES, rest = blockIdx.x / TILES;
+  const int l = MD ? rest % L : L, item = MD ? rest / L : rest;
+  const ModTab &Md = mods[l == L ? iP : l];
+  const double qd = Md.qd, qinv = Md.qinv;
+  const int tid = threadIdx.x, g = tid / TPS, tl = tid % TPS, first = tile * G;
+  const int lane = tid & 31, wrow0 = (tid >> 5) * RW;
+  const u64 row0 = (u64)(first + g) << LM;  // word offset of this thread's row
+  double *sd = reinterpret_cast<double *>(sm3) + g * PADM;
+  double *twd = reinterpret_cast<double *>(sm3 + ksr_data_words(LM));
+  u64 *ring = sm3 + ksr_data_words(LM) + G * (M + 1);
+  auto spad = [](int i) { return i + (i >> PSH); };
+  // the warp's rows' twiddles (w only; w / q is formed by one DMUL on use), staged by the warp itself
+  auto stage_tw = [&](const u64 *table) {  // the w-only table (ftw1tw / fitw1tw)
+    const double *gw = reinterpret_cast<const double *>(table) + ((u64)first << LM);
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      const int e = wrow0 * M + lane + 32 * i;
+      twd[e + (e >> LM)] = __ldg(gw + e);
+    }
+  };
+  stage_tw(Md.ftw1tw);
+  const double2 *tw = reinterpret_cast<const double2 *>(twd + g * (M + 1));
+  const bool any_c0 = MD && (epi.add0.items || epi.add0.base);
+  const bool any_add1 = MD && epi.add1 != nullptr;
+  const bool has_c0 = CGB_R2_OWN && any_c0;      // ... as ring entries
+  const bool has_add1 = CGB_R2_ADD1 && any_add1;
+  const int c0n = has_c0 ? 1 : 0;
+  const int NE = MD ? L - (CGB_R2_OWN ? 0 : 1) + c0n + 2 + (has_add1 ? 2 : 0) : L;
+  // the own limb / c0 as (limb-poly pointer, Galois element)
+  const u64 *own_p = nullptr, *c0_p = nullptr;
+  u64 own_g = 1, c0_g = 1;
+  if (MD) {
+    if (xin.items) {
+      own_p = xin.items[item] + xin.off + ((u64)l << LOGN);
+      own_g = xin.g ? xin.g[item] : 1;
+    } else {
+      own_p = xin.base + (u64)item * xin.stride + ((u64)l << LOGN);
+    }
+    if (has_c0) {
+      if (epi.add0.items) {
+        c0_p = epi.add0.items[item] + epi.add0.off + ((u64)l << LOGN);
+        c0_g = epi.add0.g ? epi.add0.g[item] : 1;
+      } else {
+        c0_p = epi.add0.base + (u64)item * epi.add0.stride + ((u64)l << LOGN);
+      }
+    }
+  }
+  pdl_start_dependents();
+  pdl_wait();
+  // start the copy of entry e into slot e & 1 (a group is committed even past the end,
+  // so "all but the newest group" always means "entry e has landed")
+  auto issue = [&](int e) {
+    if (e < NE) {
+      u64 *dst = ring + (e & 1) * PFW + wrow0 * PFP;
+      const u64 *src = nullptr, *gbase = nullptr;  // contiguous tile rows | gathered source rows
+      u64 gg = 1;
+      bool swz = false;
+      if (!MD) {
+        src = D + ((u64)item * L * LP + (u64)e * LP + L) * N;
+      } else if (!CGB_R2_OWN && e < L - 1) {
+        src = D + ((u64)item * L * LP + (u64)(e < l ? e : e + 1) * LP + l) * N;
+      } else if (!CGB_R2_OWN) {
+        const int t = e - (L - 1);
+        const int pp = has_add1 ? t >> 1 : t;
+        if (has_add1 && (t & 1)) {
+          src = epi.add1[item] + ((u64)pp * L + l) * N;
+          swz = true;
+        } else {
+          src = W + ((u64)item * 2 * L + (u64)pp * L + l) * N;
+        }
+      } else if (e < l) {
+        src = D + ((u64)item * L * LP + (u64)e * LP + l) * N;
+      } else if (e == l) {
+        gbase = own_p, gg = own_g;
+      } else if (e == l + 1 && has_c0) {
+        gbase = c0_p, gg = c0_g;
+      } else if (e < L + c0n) {
+        src = D + ((u64)item * L * LP + (u64)(e - c0n) * LP + l) * N;
+      } else {
+        const int t = e - (L + c0n);
+        const int pp = has_add1 ? t >> 1 : t;
+        if (has_add1 && (t & 1)) {
+          src = epi.add1[item] + ((u64)pp * L + l) * N;
+          swz = true;
+        } else {
+          src = W + ((u64)item * 2 * L + (u64)pp * L + l) * N;
+        }
+      }
+      if (gbase) {
+#pragma unroll
+        for (int i = 0; i < CH / 32; i++) {
+          const int c = lane + 32 * i, r = c / (M / 2), cc = c % (M / 2);
+          const u32 orow = (u32)(first + wrow0 + r);
+          const u32 srow = gg == 1 ? orow : perm_g(orow << LM, gg, LOGN) >> LM;
+          cp_async16(dst + r * PFP + 2 * cc, gbase + ((u64)srow << LM) + 2 * cc);
+        }
+      } else {
+        src += (u64)(first + wrow0) << LM;
+#pragma unroll
+        for (int i = 0; i < CH / 32; i++) {
+          const int c = lane + 32 * i, r = c / (M / 2), cc = c % (M / 2);
+          const int pc = swz ? (cc ^ ((cc >> 3) & 7)) : cc;
+          cp_async16(dst + r * PFP + 2 * pc, src + 2 * c);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  int ecur = 0;
+  auto slot = [&]() -> const u64 * { return ring + (ecur & 1) * PFW + g * PFP; };
+  auto arrive = [&]() {  // entry ecur has landed and is visible to the warp
+    cp_async_wait_1();
+    __syncwarp();
+  };
+  auto release = [&]() {  // every lane has read entry ecur: refill its slot with entry ecur + 2
+    __syncwarp();
+    issue(ecur + 2);
+    ecur++;
+  };
+  // forward row pass of the tile in the ring: x ends in PB layout, unreduced (|x| < 12 q)
+  auto row_pass = [&](double *x) {
+    arrive();
+    const u64 *b = slot();
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) {
+      const u64 v = b[PA::idx(tl, 0, k)];
+      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+    }
+    release();
+    phase_regs_fp<LM, 0, RA, true, E, false, false, true>(x, tw, tl, qd, qinv);
+#pragma unroll
+    for (int k = 0; k < PA::K; k++) sd[spad(PA::idx(tl, 0, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < PB::R; u++)
+#pragma unroll
+      for (int k = 0; k < PB::K; k++) x[u * PB::K + k] = sd[spad(PB::idx(tl, u, k))];
+    __syncwarp();  // the exchange rows are free for the next pass
+    phase_regs_fp<LM, RA, RB, true, E, true, false, true>(x, tw, tl, qd, qinv);
+  };
+  const u64 *K = keys[item];
+  const u64 *KF = K + 2 * (u64)L * 2 * LP * N;  // the key's FP64 plane
+  double a0[E], a1[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) a0[i] = a1[i] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < L; j++) {
+    double x[E];
+    if (MD && j == l && !CGB_R2_OWN) {
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++)
+          x[u * PB::K + k] = u2d(ks_src_word(xin, item, j, (u32)(row0 + PB::idx(tl, u, k)), LOGN));
+    } else if (MD && j == l) {  // the digit's own limb: the input itself, read through the automorphism
+      arrive();
+      const u64 *b = slot();
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++) {
+          const int i = PB::idx(tl, u, k);
+          const int si = own_g == 1 ? i : (int)(perm_g((u32)(row0 + i), own_g, LOGN) & (M - 1));
+          x[u * PB::K + k] = u2d(b[si]);
+        }
+      release();
+      if (has_c0) {  // P c0 o sigma joins poly 0's accumulator
+        const double2 pq = epi.C->fPmodq[l];
+        arrive();
+        const u64 *c = slot();
+#pragma unroll
+        for (int u = 0; u < PB::R; u++)
+#pragma unroll
+          for (int k = 0; k < PB::K; k++) {
+            const int i = PB::idx(tl, u, k);
+            const int si = c0_g == 1 ? i : (int)(perm_g((u32)(row0 + i), c0_g, LOGN) & (M - 1));
+            a0[u * PB::K + k] += fp_mulmod(u2d(c[si]), pq.x, pq.y, qd);
+          }
+        release();
+        if constexpr (L >= 4) {  // one term more than the digits: back to [-q/2, q/2]
+#pragma unroll
+          for (int i = 0; i < E; i++) a0[i] = fp_reduce(a0[i], qd, qinv);
+        }
+      }
+    } else {
+      row_pass(x);
+    }
+    {
+      const u64 *k0 = KF + ((u64)(j * 2 + 0) * LP + l) * N + row0, *k1 = KF + ((u64)(j * 2 + 1) * LP + l) * N + row0;
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k += 4) {
+          const int o = PB::idx(tl, u, k);
+          u64 w0[4], w1[4];
+          ld256(k0 + o, w0);
+          ld256(k1 + o, w1);
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const double xv = x[u * PB::K + k + e];
+            const double d0 = r2d(w0[e]), d1 = r2d(w1[e]);
+            a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
+            a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+          }
+        }
+    }
+    if constexpr (L > 4) {  // every 4 digits: back to [-q/2, q/2] (4 products add < 10.8 q)
+      if ((j & 3) == 3 && j + 1 < L) {
+#pragma unroll
+        for (int i = 0; i < E; i++) {
+          a0[i] = fp_reduce(a0[i], qd, qinv);
+          a1[i] = fp_reduce(a1[i], qd, qinv);
+        }
+      }
+    }
+  }
+  if constexpr (MD) {  // ModDown: forward row pass of W[pp][l], out = (acc - W) P^-1 (+ the rotate_add input)
+    const double2 pinv = epi.C->fPinvq[l];
+#pragma unroll 1
+    for (int pp = 0; pp < 2; pp++) {
+      double x[E];
+      row_pass(x);
+      if (has_add1) arrive();
+      const u64 *b = slot();
+      u64 *o = epi.out[item] + ((u64)pp * L + l) * N + row0;
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k += 4) {
+          const int i = PB::idx(tl, u, k);
+          u64 bv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
+          if (!CGB_R2_ADD1 && any_add1) ld256(epi.add1[item] + ((u64)pp * L + l) * N + row0 + i, bv);
+          if (!CGB_R2_OWN && any_c0 && pp == 0) ks_src_block4(epi.add0, item, l, (u32)(row0 + i), LOGN, cv);
+          if (has_add1) {
+            const int c0i = i >> 1, c1i = c0i + 1;
+            const ulonglong2 lo = *reinterpret_cast<const ulonglong2 *>(b + 2 * (c0i ^ ((c0i >> 3) & 7)));
+            const ulonglong2 hi = *reinterpret_cast<const ulonglong2 *>(b + 2 * (c1i ^ ((c1i >> 3) & 7)));
+            bv[0] = lo.x, bv[1] = lo.y, bv[2] = hi.x, bv[3] = hi.y;
+          }
+          u64 v[4];
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const double xa = pp ? a1[u * PB::K + k + e] : a0[u * PB::K + k + e];
+            // |xa - reduce(xw)| < 11.8 q: exact, inside fp_mulmod's analysed range (< 12 q)
+            double y = fp_mulmod(xa - fp_reduce(x[u * PB::K + k + e], qd, qinv), pinv.x, pinv.y, qd);
+            if (any_add1) y += u2d(bv[e]);
+            if (!CGB_R2_OWN && any_c0 && pp == 0) y += u2d(cv[e]);
+            v[e] = fp_canon(y, qd, qinv);
+          }
+          st256(o + i, v[0], v[1], v[2], v[3]);
+        }
+      if (has_add1) release();
+    }
+    return;
+  } else {  // P limb: ModDown's inverse row pass runs here, on the accumulators
+    u64 *o0 = acc + ((u64)item * 2 * LP + L) * N + row0, *o1 = o0 + (u64)LP * N;
+    __syncwarp();  // every lane is done with the forward twiddles
+    stage_tw(Md.fitw1tw);
+    __syncwarp();
+#pragma unroll 1
+    for (int pp = 0; pp < 2; pp++) {
+      double y[E];
+#pragma unroll
+      for (int i = 0; i < E; i++) y[i] = fp_reduce(pp ? a1[i] : a0[i], qd, qinv);
+      phase_regs_fp<LM, RA, RB, false, E, true, false, true>(y, tw, tl, qd, qinv);
+#pragma unroll
+      for (int u = 0; u < PB::R; u++)
+#pragma unroll
+        for (int k = 0; k < PB::K; k++) sd[spad(PB::idx(tl, u, k))] = y[u * PB::K + k];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) y[k] = fp_reduce(sd[spad(PA::idx(tl, 0, k))], qd, qinv);
+      __syncwarp();
+      phase_regs_fp<LM, 0, RA, false, E, false, false, true>(y, tw, tl, qd, qinv);
+      u64 *o = pp ? o1 : o0;
+#pragma unroll
+      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (raw & 2) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
+    }
+  }
+}
+static int g_ksrow2 = 1;  // CGB_KSROW2: 1 = the Q-limb kernel (ks_row_md), 2 = the P-limb kernel too, 0 = k_ks_row
+
 
 // Column-pass fusion: inverse column pass of a source limb-poly (its row pass already
 // done) followed, in the same CTA, by the centred lift into NT target moduli and each
@@ -2854,8 +3194,22 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   const MdEpi epi{d_out, acc, add0, d_add1, r->d_mods, r->d_c, L, LA + LB};
   const int TILES = (1 << LA) / G1;
   ks_row_attrs<LA, LB, L>();
+  if (g_ks_md && g_ksrow2) {
+    static std::once_flag once2;
+    std::call_once(once2, [] {
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
+    });
+  }
   if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
+    if (g_ksrow2 >= 2)
+      launch_pdl(r, k_ks_row2<LA, LB, L, false>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
+                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
+                 (const u64 *)nullptr, epi, 3);
+    else
     launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, 3);
     launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
@@ -2888,6 +3242,11 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   }
   if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
     launch_begin(r);
+    if (g_ksrow2) {
+      launch_pdl(r, k_ks_row2<LA, LB, L, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
+                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
+                 epi, 3);
+    } else
     if constexpr (LB == 7) {
       if (g_ksrow8) {
         static std::once_flag once8;
@@ -3605,7 +3964,7 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
   // twiddle tables
   // tw | itw | tw1 | itw1 (u64 (w, w') pairs) | the same four as (w, w/q) doubles | ftw1 / fitw1 with
   // each row's levels >= 4 transposed ([j][blk]) for the register-I/O FP64 kernel (k_ntt2_fpr)
-  size_t per = 20ull * N;
+  size_t per = 22ull * N;  // + the w halves of the two transposed row tables
   CK(cudaMalloc((void **)&r->d_tables, sizeof(u64) * per * r->nmod));
   std::vector<u64> tab(per);
   r->h_mods.resize(r->nmod);
@@ -3660,6 +4019,8 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
             tab[to + 1] = tab[from + 1];
           }
     }
+    for (int o = 0; o < 2; o++)
+      for (int k = 0; k < N; k++) tab[20ull * N + (size_t)o * N + k] = tab[16ull * N + (size_t)o * 2 * N + 2ull * k];
     u64 *dt = r->d_tables + per * i;
     CK(cudaMemcpy(dt, tab.data(), sizeof(u64) * per, cudaMemcpyHostToDevice));
     ModTab &M = r->h_mods[i];
@@ -3682,6 +4043,8 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.fitw1 = dt + 14 * N;
     M.ftw1t = dt + 16 * N;
     M.fitw1t = dt + 18 * N;
+    M.ftw1tw = dt + 20 * N;
+    M.fitw1tw = dt + 21 * N;
     M.qd = (double)q;
     M.qinv = 1.0 / (double)q;
     M.ninv_fp = (double)M.ninv;
@@ -3787,6 +4150,7 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     }
   }
   for (int l = 0; l < L; l++) C.fPinvq[l] = fw(C.Pinvq[l], q[l]);
+  for (int l = 0; l < L; l++) C.fPmodq[l] = fw(C.Pmodq[l], q[l]);
   for (int k = 0; k < nB; k++) {
     C.fQmodB[k] = fw(C.QmodB[k], b[k]);
     C.fBQhatInv[k] = fw(C.BQhatInv[k], b[k]);
@@ -3944,6 +4308,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_TENSOR_FUSE")) g_tensor_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
   if (const char *e = getenv("CGB_KSROW8")) g_ksrow8 = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KSROW2")) g_ksrow2 = atoi(e);
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;

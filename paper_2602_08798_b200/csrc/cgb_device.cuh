@@ -28,6 +28,7 @@ struct ModTab {
   const u64 *tw1, *itw1;                 // the same pairs in two-pass row-tile order (see k_ntt2)
   const u64 *ftw, *fitw, *ftw1, *fitw1;  // FP64 twiddles (w, w/q) as double pairs, same orders
   const u64 *ftw1t, *fitw1t;             // ftw1 / fitw1, levels >= 4 of each row transposed
+  const u64 *ftw1tw, *fitw1tw;           // the w halves of ftw1t / fitw1t alone (w / q is one DMUL on use)
   double qd, qinv;                       // q and 1/q as doubles (FP64 NTT)
   double ninv_fp, ninv_fpq;              // N^-1 and N^-1 / q as doubles
   int bits;
@@ -735,7 +736,7 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
           const int ti = TRANS ? (1 << (S0 + l)) + ((k >> (RP - l)) << S0) + blk
                                : (1 << (S0 + l)) + (blk << l) + (k >> (RP - l));
           if constexpr (WQ) {
-            const double w = reinterpret_cast<const double *>(tws)[ti];
+            const double w = GTW ? __ldg(reinterpret_cast<const double *>(tws) + ti) : reinterpret_cast<const double *>(tws)[ti];
             W = make_double2(w, w * qinv);
           } else {
             W = GTW ? __ldg(tws + ti) : tws[ti];
@@ -777,6 +778,9 @@ struct EpiLoads<E, std::void_t<decltype(E::loads)>> {
 
 // Row passes (PASS 1) give each row to M / E <= 16 consecutive threads of one warp, so
 // the exchange between a row pass's register phases needs only a warp-level barrier.
+#ifndef CGB_FPR_WQ
+#define CGB_FPR_WQ 1
+#endif
 #ifndef CGB_ROW_WSYNC
 #define CGB_ROW_WSYNC 1
 #endif
@@ -811,8 +815,11 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
   const int tid = threadIdx.x;
   double *data = reinterpret_cast<double *>(sm2);
   double2 *tws = reinterpret_cast<double2 *>(sm2 + ((G * PADM + 1) & ~1));
+  // row passes read their row's twiddles from global memory through L1: the w-only table
+  // (8 bytes per twiddle) halves that traffic of the LSU-bound row pass (CGB_FPR_WQ)
+  constexpr bool RWQ = CGB_FPR_WQ && PASS == 1;
   const double2 *gtw = reinterpret_cast<const double2 *>(
-      PASS == 0 ? (FWD ? Md.ftw : Md.fitw) : (FWD ? Md.ftw1t : Md.fitw1t));
+      PASS == 0 ? (FWD ? Md.ftw : Md.fitw) : RWQ ? (FWD ? Md.ftw1tw : Md.fitw1tw) : (FWD ? Md.ftw1t : Md.fitw1t));
   const int first = tile * G;
   // thread -> (sub-NTT g, thread-in-sub tl): columns fast in pass 0, words fast in pass 1
   const int g = PASS == 0 ? (tid % G) : (tid / TPS);
@@ -871,8 +878,10 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
     }
   }
   if (PASS == 0 || !CGB_ROW_WSYNC) __syncthreads();  // twiddles staged (row passes read theirs from global)
-  const double2 *tw_g = PASS == 0 ? tws : gtw + ((u64)(first + g) << LM);
-  phase_regs_fp<LM, S0A, RPA, FWD, E, PASS == 1 && S0A == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
+  const double2 *tw_g = PASS == 0 ? tws
+                        : RWQ     ? reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(gtw) + ((u64)(first + g) << LM))
+                                  : gtw + ((u64)(first + g) << LM);
+  phase_regs_fp<LM, S0A, RPA, FWD, E, PASS == 1 && S0A == 4, PASS == 1, RWQ>(x, tw_g, tl, qd, qinv);
   double *sd = data + g * PADM;
 #pragma unroll
   for (int u = 0; u < PA::R; u++)
@@ -888,7 +897,7 @@ __global__ void FPR_BOUNDS k_ntt2_fpr(NttJob job, EPI epi) {
       const double v = sd[spad(PB::idx(tl, u, k))];
       x[u * PB::K + k] = FWD ? v : fp_reduce(v, qd, qinv);
     }
-  phase_regs_fp<LM, S0B, RPB, FWD, E, PASS == 1 && S0B == 4, PASS == 1>(x, tw_g, tl, qd, qinv);
+  phase_regs_fp<LM, S0B, RPB, FWD, E, PASS == 1 && S0B == 4, PASS == 1, RWQ>(x, tw_g, tl, qd, qinv);
   const bool last = FWD ? (PASS == 1) : (PASS == 0);
   const double ni = Md.ninv_fp, niq = Md.ninv_fpq;
 #pragma unroll
