@@ -28,6 +28,12 @@ typedef unsigned __int128 u128;
 // ============================================================================
 // error plumbing
 // ============================================================================
+// two-pass split of the 2^14-point transform: 2^A14 strided column sub-transforms x 2^(14 - A14)
+// contiguous row sub-transforms (the other sizes split evenly: 6+7, 7+8, 8+8)
+#ifndef CGB_A14
+#define CGB_A14 7
+#endif
+static inline int split_a(int logN) { return logN == 14 ? CGB_A14 : logN / 2; }
 static thread_local std::string g_err;
 struct CgbError {
   int code;
@@ -536,7 +542,7 @@ static void launch_ntt(cgb_ring *r, bool fwd, NttJob &job, int count) {
     switch (r->logN) {
       case 12: LN2(6, 6); break;
       case 13: LN2(6, 7); break;
-      case 14: LN2(7, 7); break;
+      case 14: LN2(CGB_A14, 14 - CGB_A14); break;
       case 15: LN2(7, 8); break;
       default: LN2(8, 8); break;
     }
@@ -1663,10 +1669,10 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
   const double2 *tw = reinterpret_cast<const double2 *>(twd + g * (M + 1));
   const bool any_c0 = MD && (epi.add0.items || epi.add0.base);
   const bool any_add1 = MD && epi.add1 != nullptr;
-  const bool has_c0 = CGB_R2_OWN && any_c0;      // ... as ring entries
+  const bool has_c0 = CGB_R2_OWN == 1 && any_c0;      // ... as ring entries
   const bool has_add1 = CGB_R2_ADD1 && any_add1;
   const int c0n = has_c0 ? 1 : 0;
-  const int NE = MD ? L - (CGB_R2_OWN ? 0 : 1) + c0n + 2 + (has_add1 ? 2 : 0) : L;
+  const int NE = MD ? L - (CGB_R2_OWN >= 1 ? 0 : 1) + c0n + 2 + (has_add1 ? 2 : 0) : L;
   // the own limb / c0 as (limb-poly pointer, Galois element)
   const u64 *own_p = nullptr, *c0_p = nullptr;
   u64 own_g = 1, c0_g = 1;
@@ -1698,9 +1704,9 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
       bool swz = false;
       if (!MD) {
         src = D + ((u64)item * L * LP + (u64)e * LP + L) * N;
-      } else if (!CGB_R2_OWN && e < L - 1) {
+      } else if (CGB_R2_OWN < 1 && e < L - 1) {
         src = D + ((u64)item * L * LP + (u64)(e < l ? e : e + 1) * LP + l) * N;
-      } else if (!CGB_R2_OWN) {
+      } else if (CGB_R2_OWN < 1) {
         const int t = e - (L - 1);
         const int pp = has_add1 ? t >> 1 : t;
         if (has_add1 && (t & 1)) {
@@ -1789,7 +1795,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
 #pragma unroll 1
   for (int j = 0; j < L; j++) {
     double x[E];
-    if (MD && j == l && !CGB_R2_OWN) {
+    if (MD && j == l && CGB_R2_OWN < 1) {
 #pragma unroll
       for (int u = 0; u < PB::R; u++)
 #pragma unroll
@@ -1873,7 +1879,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
           const int i = PB::idx(tl, u, k);
           u64 bv[4] = {0, 0, 0, 0}, cv[4] = {0, 0, 0, 0};
           if (!CGB_R2_ADD1 && any_add1) ld256(epi.add1[item] + ((u64)pp * L + l) * N + row0 + i, bv);
-          if (!CGB_R2_OWN && any_c0 && pp == 0) ks_src_block4(epi.add0, item, l, (u32)(row0 + i), LOGN, cv);
+          if (CGB_R2_OWN != 1 && any_c0 && pp == 0) ks_src_block4(epi.add0, item, l, (u32)(row0 + i), LOGN, cv);
           if (has_add1) {
             const int c0i = i >> 1, c1i = c0i + 1;
             const ulonglong2 lo = *reinterpret_cast<const ulonglong2 *>(b + 2 * (c0i ^ ((c0i >> 3) & 7)));
@@ -1887,7 +1893,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
             // |xa - reduce(xw)| < 11.8 q: exact, inside fp_mulmod's analysed range (< 12 q)
             double y = fp_mulmod(xa - fp_reduce(x[u * PB::K + k + e], qd, qinv), pinv.x, pinv.y, qd);
             if (any_add1) y += u2d(bv[e]);
-            if (!CGB_R2_OWN && any_c0 && pp == 0) y += u2d(cv[e]);
+            if (CGB_R2_OWN != 1 && any_c0 && pp == 0) y += u2d(cv[e]);
             v[e] = fp_canon(y, qd, qinv);
           }
           st256(o + i, v[0], v[1], v[2], v[3]);
@@ -2071,12 +2077,12 @@ static void col_fused(cgb_ring *r, ColJob &job, int count, int nt, const char *n
   launch_begin(r);
   switch (r->logN) {
     case 13: col_fused_t<6, 7>(r, job, count, nt); break;
-    case 14: col_fused_t<7, 7>(r, job, count, nt); break;
+    case 14: col_fused_t<CGB_A14, 14 - CGB_A14>(r, job, count, nt); break;
     case 15: col_fused_t<7, 8>(r, job, count, nt); break;
     default: col_fused_t<8, 8>(r, job, count, nt); break;
   }
   // butterflies of the inverse column pass and nt forward column passes, plus the N^-1 scaling
-  const int LA = r->logN / 2;  // column pass length (col_fused_t<LA, LB>)
+  const int LA = split_a(r->logN);  // column pass length (col_fused_t<LA, LB>)
   launch_end(r, name, 8.0 * (double)count * job.nsrc * r->N * (1 + nt),
              (double)count * job.nsrc * ((r->N / 2.0) * LA * (1 + nt) + r->N));
 }
@@ -2131,7 +2137,7 @@ static void modup_ks_row(cgb_ring *r, NttJob &job, int count, u64 *acc, const u6
   }
   switch (r->logN) {
     case 13: MKR(6, 7) break;
-    case 14: MKR(7, 7) break;
+    case 14: MKR(CGB_A14, 14 - CGB_A14) break;
     case 15: MKR(7, 8) break;
     default: MKR(8, 8) break;
   }
@@ -2151,12 +2157,12 @@ static void ntt_inv_col(cgb_ring *r, NttJob &job, int count) {
   launch_begin(r);
   switch (r->logN) {
     case 13: ntt_inv_col_t<6, 7>(r, job, count); break;
-    case 14: ntt_inv_col_t<7, 7>(r, job, count); break;
+    case 14: ntt_inv_col_t<CGB_A14, 14 - CGB_A14>(r, job, count); break;
     case 15: ntt_inv_col_t<7, 8>(r, job, count); break;
     default: ntt_inv_col_t<8, 8>(r, job, count); break;
   }
   launch_end(r, "ntt_inv_col", 16.0 * (double)count * job.nsub * r->N,
-             (double)count * job.nsub * ((r->N / 2) * (r->logN - r->logN / 2) + r->N));
+             (double)count * job.nsub * ((r->N / 2) * (r->logN - split_a(r->logN)) + r->N));
 }
 
 // ModDown's forward NTT with the combine fused into its row pass (FP64 register-I/O
@@ -2185,7 +2191,7 @@ static bool moddown_ntt_fused(cgb_ring *r, NttJob &job, int count, const MdEpi &
   switch (r->logN) {
     case 12: moddown_ntt_fused_t<6, 6>(r, job, count, epi); break;
     case 13: moddown_ntt_fused_t<6, 7>(r, job, count, epi); break;
-    case 14: moddown_ntt_fused_t<7, 7>(r, job, count, epi); break;
+    case 14: moddown_ntt_fused_t<CGB_A14, 14 - CGB_A14>(r, job, count, epi); break;
     case 15: moddown_ntt_fused_t<7, 8>(r, job, count, epi); break;
     case 16: moddown_ntt_fused_t<8, 8>(r, job, count, epi); break;
     default: return false;
@@ -3308,7 +3314,7 @@ static bool keyswitch_fp(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u64
   }
   switch (r->logN) {
     case 13: KFP(6, 7) break;
-    case 14: KFP(7, 7) break;
+    case 14: KFP(CGB_A14, 14 - CGB_A14) break;
     case 15: KFP(7, 8) break;
     default: KFP(8, 8) break;
   }
@@ -3610,7 +3616,7 @@ static bool keyswitch_hoisted(cgb_ring *r, Scratch &S, const KsSrc &x, int count
   }
   switch (r->logN) {
     case 13: KHO(6, 7) break;
-    case 14: KHO(7, 7) break;
+    case 14: KHO(CGB_A14, 14 - CGB_A14) break;
     case 15: KHO(7, 8) break;
     default: KHO(8, 8) break;
   }
@@ -3981,7 +3987,7 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     }
     // two-pass row-tile order: entry blk*M + i (i = 2^sp + g) = pair 2^(a+sp) + blk 2^sp + g
     if (logN >= 12) {
-      const int a = logN / 2, b = logN - a, M = 1 << b;
+      const int a = split_a(logN), b = logN - a, M = 1 << b;
       for (int blk = 0; blk < (1 << a); blk++)
         for (int ii = 0; ii < M; ii++) {
           size_t dst = (size_t)blk * M + ii, src = 0;
@@ -4004,7 +4010,7 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
         memcpy(&tab[8ull * N + (size_t)o * 2 * N + 2 * k + 1], &wq, 8);
       }
     if (logN >= 12) {
-      const int M = 1 << (logN - logN / 2);
+      const int M = 1 << (logN - split_a(logN));
       for (int o = 0; o < 2; o++)
         for (int row = 0; row < N / M; row++)
           for (int ii = 0; ii < M; ii++) {
@@ -4228,7 +4234,7 @@ static bool tensor_intt_fused(cgb_ring *r, int n, u64 *ten, const TensorLoad &tl
   if (!(g_tensor_fuse && r->fp_ntt && (g_fp_regio & 3) == 3 && r->logN >= 13 && r->logN <= 16)) return false;
   switch (r->logN) {
     case 13: tensor_intt_t<6, 7>(r, n, ten, tl, mod_of_limb); break;
-    case 14: tensor_intt_t<7, 7>(r, n, ten, tl, mod_of_limb); break;
+    case 14: tensor_intt_t<CGB_A14, 14 - CGB_A14>(r, n, ten, tl, mod_of_limb); break;
     case 15: tensor_intt_t<7, 8>(r, n, ten, tl, mod_of_limb); break;
     default: tensor_intt_t<8, 8>(r, n, ten, tl, mod_of_limb); break;
   }
@@ -4290,7 +4296,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
     switch (log_n) {
       case 12: ntt2_attrs<6, 6>(); break;
       case 13: ntt2_attrs<6, 7>(); break;
-      case 14: ntt2_attrs<7, 7>(); break;
+      case 14: ntt2_attrs<CGB_A14, 14 - CGB_A14>(); break;
       case 15: ntt2_attrs<7, 8>(); break;
       case 16: ntt2_attrs<8, 8>(); break;
       default: break;

@@ -5,7 +5,7 @@ recompute from profiles/ within 5 %).
     python scripts/roofline_recompute.py [bench.json] [launches.csv]
 
 Key-switch unit time from ncu: every five-kernel group ks_digit_rows ->
-col_fused -> ks_row<..,1> -> col_fused -> ks_row<..,2> that is NOT a
+col_fused -> ks_row<..,1> -> col_fused -> ks_row<..,2> (or k_ks_row2) that is NOT a
 relinearisation (a relinearisation's digit-rows pass directly follows the
 forward NTT row pass of mult_cipher's scale-and-round output), summed.
 Bytes: the bench line's own 8(d) bytes per step (launches_per_step x
@@ -26,11 +26,12 @@ roof = line["roofline"]
 rows = [r for r in csv.reader(open(launches)) if len(r) > 10 and r[0].isdigit()]
 names = [r[6].split("(")[0].replace("void ", "").replace("cgb::", "") for r in rows]
 ns = [float(r[-1]) for r in rows]
-seq = ("k_ntt2_fpr<7, 7, 0, 1", "k_col_fused", "k_ks_row<7, 7, 3, 1>", "k_col_fused", "k_ks_row<7, 7, 3, 2>")
+seq = (("k_ntt2_fpr<7, 7, 0, 1",), ("k_col_fused",), ("k_ks_row<7, 7, 3, 1>", "k_ks_row2<7, 7, 3, 0>"), ("k_col_fused",),
+       ("k_ks_row<7, 7, 3, 2>", "k_ks_row2<7, 7, 3, 1>"))
 ks_ns, relin_ns, groups, relin = 0.0, 0.0, 0, 0
 i = 0
 while i + 5 <= len(names):
-    if all(names[i + k].startswith(seq[k]) for k in range(5)):
+    if all(names[i + k].startswith(seq[k]) for k in range(5)):  # str.startswith takes a tuple of alternatives
         t = sum(ns[i:i + 5])
         if i > 0 and names[i - 1].startswith("k_ntt2_fpr<7, 7, 1, 1"):
             relin_ns += t
