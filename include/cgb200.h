@@ -193,6 +193,13 @@ int cgb_rotate(cgb_ring *ring, int count, const uint32_t *a, const int64_t *step
  * (arcc.py:90-93), tile_token (encodings.py:212-215) and fold_sum
  * (linear_kernels.py:37-41), fused into one pass */
 int cgb_rotate_add(cgb_ring *ring, int count, const uint32_t *a, const int64_t *steps, const uint32_t *out);
+/* The rotate-and-add chain of a fold / broadcast (reference linear_kernels.py:37-41,
+ * arcc.py:90-93): x <- add(x, rotate(x, steps[k])) for k = 0 .. nsteps-1 on each of the
+ * count ciphertexts, out = the last x.  The same words as nsteps cgb_rotate_add calls;
+ * the intermediate ciphertexts live in device scratch (no arena slots).  Every step must
+ * be non-zero modulo the slot count. */
+int cgb_rotate_add_chain(cgb_ring *ring, int count, const uint32_t *a, int nsteps, const int64_t *steps,
+                         const uint32_t *out);
 /* out = sum of count ciphertexts a[0..count) (exact mod q: order-free) */
 int cgb_sum(cgb_ring *ring, int count, const uint32_t *a, uint32_t out);
 /* generate (and cache) evaluation keys for Galois elements ahead of use */

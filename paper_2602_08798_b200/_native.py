@@ -105,6 +105,7 @@ SIGNATURES = {
     "cgb_galois": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _u64p, _u32p]),
     "cgb_rotate": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _i64p, _u32p]),
     "cgb_rotate_add": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, _i64p, _u32p]),
+    "cgb_rotate_add_chain": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, ctypes.c_int, _i64p, _u32p]),
     "cgb_sum": (ctypes.c_int, [_vp, ctypes.c_int, _u32p, ctypes.c_uint32]),
     "cgb_prepare_galois": (ctypes.c_int, [_vp, ctypes.c_int, _u64p]),
 }

@@ -96,10 +96,15 @@ def broadcast_wave(wave, js, width: int):
     if js.size and (js.min() < 0 or js.max() >= n) or not 1 <= width <= n:
         raise ParameterError(f"slot / width {width} out of range for {n} slots")
     out = C.w_rotate(C.w_mult_plain(wave, _onehots(n, js)), js)
+    steps = []
     filled = 1
     while filled < width:
-        out = C.w_rotate(out, -filled, add_input=True)
+        steps.append(-filled)
         filled *= 2
+    if hasattr(C, "w_rotate_add_chain"):
+        return C.w_rotate_add_chain(out, steps)
+    for st in steps:
+        out = C.w_rotate(out, st, add_input=True)
     return out
 
 

@@ -348,6 +348,7 @@ SlotCiphertext = GpuCiphertext
 EXT_B = os.environ.get("CGB_EXT_B", "1") != "0"  # resident base-B extensions of KV cache parts
 EXT_A = os.environ.get("CGB_EXT_A", "1") != "0"  # ... and of an a-operand repeated across a mult_cipher wave
 _ROT_DEDUP = os.environ.get("CGB_ROT_DEDUP", "1") != "0"  # one key switch per (content class, step)
+_ROT_CHAIN = os.environ.get("CGB_ROT_CHAIN", "1") != "0"  # fold / doubling chains as one library call
 
 
 _class_counter = itertools.count(1)
@@ -883,6 +884,47 @@ class GpuContext:
         else:
             cids = GpuContext._charge(wave, "rotate")
         return Wave(wave.ctxs, wave.owner, ids, b, [blk], cids, klass)
+
+    @staticmethod
+    def w_rotate_add_chain(wave: Wave, steps) -> Wave:
+        """``wave <- w_rotate(wave, s, add_input=True)`` for s in steps, as ONE library
+        call (cgb_rotate_add_chain): the same words, budgets, counters and ciphertext
+        ids as the loop -- the intermediate ciphertexts never get arena slots and the
+        per-wave host work is paid once (small fold waves are host-bound).  Falls back
+        to the loop whenever the closed forms below would not describe it: repeated
+        handles (content classes), the two-row layout, a step that is a multiple of
+        the slot count, or a budget the chain would exhaust (the loop then raises at
+        the exact step)."""
+        steps = [int(s) for s in steps]
+        if not steps:
+            return wave
+        c0 = wave.ctxs[0]
+        costs = c0.params.noise_costs
+        per = costs.rotate + costs.add
+        n = c0.params.n_slots
+        if (not _ROT_CHAIN or len(steps) < 2 or wave.klass is not None or not c0._ring.one_row
+                or any(s % n == 0 for s in steps)
+                or (len(wave) and int(wave.budgets.min()) - per * len(steps) < 0)):
+            for s in steps:
+                wave = GpuContext.w_rotate(wave, s, add_input=True)
+            return wave
+        K = len(steps)
+        blk, ids = c0._new(len(wave))
+        c0._ring.rotate_add_chain(wave.aids, steps, ids)
+        # K rotates and K adds per item; each step emits two ids per item (the rotation's,
+        # then the sum's, which the item keeps), item order within each owner
+        counts = np.bincount(wave.owner, minlength=len(wave.ctxs))
+        cids = np.empty(len(wave), np.int64)
+        for o, c in enumerate(wave.ctxs):
+            k = int(counts[o])
+            if not k:
+                continue
+            c.counter.rotate += K * k
+            c.counter.add += K * k
+            sel = np.nonzero(wave.owner == o)[0]
+            cids[sel] = c._next_id + (K - 1) * 2 * k + 2 * np.arange(k) + 1
+            c._next_id += K * 2 * k
+        return Wave(wave.ctxs, wave.owner, ids, wave.budgets - per * K, [blk], cids)
 
     @staticmethod
     def w_sum(wave: Wave, groups) -> Wave:

@@ -3756,48 +3756,23 @@ static size_t chunk_for(cgb_ring *r, size_t words_per_item) {
 }
 
 // galois (+ optional add of the input) on a batch
-static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, const u32 *out, bool add_input) {
+// key switch of `total` ciphertexts given by pointer (arena slots or scratch), Galois elements != 1
+static void galois_ptrs(cgb_ring *r, int total, u64 *const *srcs, u64 *const *dsts, const u64 *gs, bool add_input) {
   const int L = r->L, N = r->N;
-  const u64 twoN = 2ull * N, ctw = r->ct_words;
-  std::vector<int> idx;  // items with g != 1
-  for (int i = 0; i < count; i++) {
-    u64 g = gs[i] % twoN;
-    if (!(g & 1)) FAIL(CGB_ERR_PARAM, "Galois element %llu is even", (unsigned long long)gs[i]);
-    if (g == 1) {
-      Scratch S(r);
-      std::vector<u64 *> src = ct_ptrs(r, 1, &a[i]), dst = ct_ptrs(r, 1, &out[i]);
-      u64 **d_src = S.up(src.data(), 1), **d_dst = S.up(dst.data(), 1);
-      launch_begin(r);
-      if (add_input) {
-        k_add<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
-                                                                 (const u64 *const *)d_src, r->d_mods, L, r->logN, ctw);
-      } else {
-        k_copy<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
-      }
-      launch_end(r, add_input ? "add" : "copy", (add_input ? 24.0 : 16.0) * ctw);
-    } else {
-      idx.push_back(i);
-    }
-  }
+  const u64 ctw = r->ct_words;
   size_t per_item = ctw * 2 + (size_t)L * N * (1 + L * (L + 1) + 2 * (L + 1) + 2 * L);
   size_t CH = chunk_for(r, per_item);
   if (g_ks_chunk > 0) {  // at most g_ks_chunk items per batched key switch; equal-sized chunks
-    const size_t nch = (idx.size() + (size_t)g_ks_chunk - 1) / (size_t)g_ks_chunk;
-    CH = std::min(CH, std::max<size_t>(1, (idx.size() + nch - 1) / std::max<size_t>(nch, 1)));
+    const size_t nch = ((size_t)total + (size_t)g_ks_chunk - 1) / (size_t)g_ks_chunk;
+    CH = std::min(CH, std::max<size_t>(1, ((size_t)total + nch - 1) / std::max<size_t>(nch, 1)));
   }
-  for (size_t c0 = 0; c0 < idx.size(); c0 += CH) {
-    int n = (int)std::min(CH, idx.size() - c0);
+  for (size_t c0 = 0; c0 < (size_t)total; c0 += CH) {
+    int n = (int)std::min(CH, (size_t)total - c0);
     Scratch S(r);
-    std::vector<u32> ia(n), io(n);
-    std::vector<u64> g(n);
+    std::vector<u64> g(gs + c0, gs + c0 + n);
     std::vector<u64 *> keys(n);
-    for (int k = 0; k < n; k++) {
-      ia[k] = a[idx[c0 + k]];
-      io[k] = out[idx[c0 + k]];
-      g[k] = gs[idx[c0 + k]] % twoN;
-      keys[k] = get_key(r, g[k]);
-    }
-    std::vector<u64 *> src = ct_ptrs(r, n, ia.data()), dst = ct_ptrs(r, n, io.data());
+    for (int k = 0; k < n; k++) keys[k] = get_key(r, g[k]);
+    std::vector<u64 *> src(srcs + c0, srcs + c0 + n), dst(dsts + c0, dsts + c0 + n);
     // sources shared by several items (one activation rotated by many steps): one ModUp each
     std::vector<u64> usrc;
     std::vector<u32> sidx(n);
@@ -3848,6 +3823,41 @@ static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, co
     group_end(r, hoisted ? "keyswitch_hoisted" : "keyswitch",
               8.0 * (double)ctw * ((hoisted ? nu : n) + n) + key_bytes);
   }
+}
+
+static void galois_batch(cgb_ring *r, int count, const u32 *a, const u64 *gs, const u32 *out, bool add_input) {
+  const int L = r->L, N = r->N;
+  const u64 twoN = 2ull * N, ctw = r->ct_words;
+  std::vector<int> idx;  // items with g != 1
+  for (int i = 0; i < count; i++) {
+    u64 g = gs[i] % twoN;
+    if (!(g & 1)) FAIL(CGB_ERR_PARAM, "Galois element %llu is even", (unsigned long long)gs[i]);
+    if (g == 1) {
+      Scratch S(r);
+      std::vector<u64 *> src = ct_ptrs(r, 1, &a[i]), dst = ct_ptrs(r, 1, &out[i]);
+      u64 **d_src = S.up(src.data(), 1), **d_dst = S.up(dst.data(), 1);
+      launch_begin(r);
+      if (add_input) {
+        k_add<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src,
+                                                                 (const u64 *const *)d_src, r->d_mods, L, r->logN, ctw);
+      } else {
+        k_copy<<<dim3(GRID1(ctw / 2, TPB).x, 1), TPB, 0, r->stream>>>(d_dst, (const u64 *const *)d_src, ctw);
+      }
+      launch_end(r, add_input ? "add" : "copy", (add_input ? 24.0 : 16.0) * ctw);
+    } else {
+      idx.push_back(i);
+    }
+  }
+  if (idx.empty()) return;
+  std::vector<u32> ia(idx.size()), io(idx.size());
+  std::vector<u64> g(idx.size());
+  for (size_t k = 0; k < idx.size(); k++) {
+    ia[k] = a[idx[k]];
+    io[k] = out[idx[k]];
+    g[k] = gs[idx[k]] % twoN;
+  }
+  std::vector<u64 *> src = ct_ptrs(r, (int)idx.size(), ia.data()), dst = ct_ptrs(r, (int)idx.size(), io.data());
+  galois_ptrs(r, (int)idx.size(), src.data(), dst.data(), g.data(), add_input);
 }
 
 // ============================================================================
@@ -5078,6 +5088,40 @@ int cgb_rotate_add(cgb_ring *r, int count, const uint32_t *a, const int64_t *ste
   if (count <= 0) return CGB_OK;
   auto g = steps_to_g(r, count, steps);
   galois_batch(r, count, a, g.data(), out, true);
+  API_END
+}
+// The fold / doubling chain x <- x + rotate(x, steps[k]), k = 0 .. nsteps - 1, as one call:
+// the same key switches as nsteps cgb_rotate_add calls (same words), the intermediate
+// ciphertexts in stream-ordered scratch instead of arena slots.  Small waves are
+// host-bound (one call per step costs more host time than its five launches take on
+// the device); a chain pays the per-call host work once.
+int cgb_rotate_add_chain(cgb_ring *r, int count, const uint32_t *a, int nsteps, const int64_t *steps,
+                         const uint32_t *out) {
+  API_BEGIN
+  RING_LOCK(r);
+  if (count <= 0) return CGB_OK;
+  if (nsteps <= 0) FAIL(CGB_ERR_PARAM, "empty rotation chain");
+  if (!r->one_row) FAIL(CGB_ERR_PARAM, "cgb_rotate_add_chain needs the one-row layout");
+  const u64 twoN = 2ull * r->N, ctw = r->ct_words;
+  std::vector<u64> gk(nsteps);
+  for (int k = 0; k < nsteps; k++) {
+    int64_t kk = steps[k] % r->n_slots;
+    if (kk < 0) kk += r->n_slots;
+    if (kk == 0) FAIL(CGB_ERR_PARAM, "chain step %d is a multiple of the slot count", k);
+    gk[k] = h_powmod(5, (u64)kk, twoN);
+  }
+  std::vector<u64 *> src = ct_ptrs(r, count, a), last = ct_ptrs(r, count, out), dst(count);
+  Scratch S(r);
+  u64 *tmp[2] = {nullptr, nullptr};
+  if (nsteps > 1) tmp[0] = S.alloc<u64>((size_t)count * ctw);
+  if (nsteps > 2) tmp[1] = S.alloc<u64>((size_t)count * ctw);
+  std::vector<u64> g(count);
+  for (int k = 0; k < nsteps; k++) {
+    for (int i = 0; i < count; i++) dst[i] = k == nsteps - 1 ? last[i] : tmp[k & 1] + (size_t)i * ctw;
+    std::fill(g.begin(), g.end(), gk[k]);
+    galois_ptrs(r, count, src.data(), dst.data(), g.data(), true);
+    src = dst;
+  }
   API_END
 }
 int cgb_prepare_galois(cgb_ring *r, int count, const uint64_t *g) {

@@ -31,10 +31,15 @@ def fold_wave(wave, block: int, first_step: int = 1):
     log2(block) batched rotate-and-add steps 1, 2, 4, ...  (:27-42)."""
     C = type(wave.ctxs[0])
     _fold_checks(block, wave.ctxs[0].params.n_slots)
+    steps = []
     step = first_step
     while step < block * first_step:
-        wave = C.w_rotate(wave, step, add_input=True)
+        steps.append(step)
         step *= 2
+    if hasattr(C, "w_rotate_add_chain"):  # one library call for the whole chain (same words and ledger)
+        return C.w_rotate_add_chain(wave, steps)
+    for step in steps:
+        wave = C.w_rotate(wave, step, add_input=True)
     return wave
 
 

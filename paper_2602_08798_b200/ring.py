@@ -292,6 +292,13 @@ class Ring:
         fn = nat.lib().cgb_rotate_add if add_input else nat.lib().cgb_rotate
         nat.check(fn(self._h, a.size, nat.u32ptr(a), nat.i64ptr(st), nat.u32ptr(out)), "cgb_rotate")
 
+    def rotate_add_chain(self, a, steps, out):
+        """x <- x + rotate(x, s) for s in steps, in one call (intermediates in scratch)."""
+        a, out = _ids(a), _ids(out)
+        st = np.ascontiguousarray(np.asarray(steps, dtype=np.int64).reshape(-1))
+        nat.check(nat.lib().cgb_rotate_add_chain(self._h, a.size, nat.u32ptr(a), st.size, nat.i64ptr(st),
+                                                 nat.u32ptr(out)), "cgb_rotate_add_chain")
+
     def sum(self, a, out: int):
         a = _ids(a)
         nat.check(nat.lib().cgb_sum(self._h, a.size, nat.u32ptr(a), int(out)), "cgb_sum")

@@ -14,7 +14,7 @@ def declared():
 def test_header_declares_entry_points():
     names = declared()
     for need in ("cgb_ring_create", "cgb_encrypt", "cgb_decrypt", "cgb_add", "cgb_add_plain", "cgb_mult_plain",
-                 "cgb_mult_cipher", "cgb_rotate", "cgb_galois", "cgb_rotate_add"):
+                 "cgb_mult_cipher", "cgb_rotate", "cgb_galois", "cgb_rotate_add", "cgb_rotate_add_chain"):
         assert need in names
 
 

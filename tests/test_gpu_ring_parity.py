@@ -97,6 +97,68 @@ def test_batched_rotate_bitexact(bench, add):
     assert not bad, f"{len(bad)} items differ, first {bad[:8]}"
 
 
+def test_rotate_add_chain_bitexact(bench):
+    """cgb_rotate_add_chain (a fold's doubling steps in one call, intermediates in
+    scratch) against the oracle's step-by-step rotate + add, every word; also equal to
+    the same steps issued one cgb_rotate_add at a time, including in-place output."""
+    g, pool, vals, ids, words = bench
+    cnt = 12
+    steps = [1, 2, 4, -64, 8191]
+    out = g.alloc(cnt)
+    g.rotate_add_chain(ids[:cnt], steps, out)
+    got = g.store(out)
+
+    def ref(o, w):
+        for k in steps:
+            w = o.add(o.rotate(w, int(k)), w)
+        return w
+
+    want = pool.map(ref, words[:cnt])
+    for i in range(cnt):
+        assert np.array_equal(got[i], want[i]), i
+    # step by step through the arena, and a one-step chain
+    cur = ids[:cnt]
+    tmp = []
+    for k in steps:
+        nxt = g.alloc(cnt)
+        g.rotate(cur, np.full(cnt, k, np.int64), nxt, add_input=True)
+        tmp.append(nxt)
+        cur = nxt
+    assert np.array_equal(g.store(cur), got)
+    one = g.alloc(cnt)
+    g.rotate_add_chain(ids[:cnt], steps[:1], one)
+    assert np.array_equal(g.store(one), g.store(tmp[0]))
+    for t in tmp + [one, out]:
+        g.free(t)
+
+
+def test_wave_chain_equals_step_loop():
+    """GpuContext.w_rotate_add_chain charges counters, ids and budgets exactly as the
+    loop of w_rotate(add_input=True) does, and yields the same words."""
+    import paper_2602_08798_b200 as cg
+    from paper_2602_08798_b200 import backend
+
+    def run(chain):
+        backend._ROT_CHAIN = chain
+        ctxs = [cg.new_context(cg.BackendParams(n_slots=8192, plain_modulus=536903681), seed=s) for s in (1, 2)]
+        rng = np.random.default_rng(5)
+        C = type(ctxs[0])
+        owners = [ctxs[0], ctxs[1], ctxs[0], ctxs[1], ctxs[1]]
+        w = C.w_encrypt(owners, rng.integers(0, 536903681, (5, 8192)))
+        w = C.w_rotate_add_chain(w, [1, 2, 4, 8])
+        words = ctxs[0]._ring.store(w.aids)
+        # ciphertext ids carry a per-context base (a multiple of 10^9): compare the sequence numbers
+        return (words, w.budgets.copy(), w.cids % 10**9,
+                [(c.counter.rotate, c.counter.add, c._next_id % 10**9) for c in ctxs])
+
+    try:
+        a, b = run(True), run(False)
+    finally:
+        backend._ROT_CHAIN = True
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
+
+
 def test_batched_rotate_decrypts(bench):
     g, pool, vals, ids, words = bench
     steps = np.array([1, 2, 4095, 4096, 8191, 100], np.int64)
