@@ -214,6 +214,13 @@ struct cgb_ring {
   size_t pin_cap = 0, pin_off = 0;
   int pin_half = 0;
   cudaEvent_t pin_left[2] = {nullptr, nullptr};
+  // device mirror of the pinned halves, filled on a side stream: a call's pointer tables
+  // are copied while the previous call's kernels still run, so the copy is not a bubble
+  // between two calls on the compute stream (which only waits for the copy's event)
+  char *dev_stage = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_ev;
+  size_t copy_ev_next = 0;
   u64 launches = 0;
   std::mutex mu;
   // every entry point taking the ring holds this while it enqueues: the reference runs
@@ -246,15 +253,19 @@ struct cgb_ring {
 // ---------------------------------------------------------------------------
 // pinned staging + device scratch
 // ---------------------------------------------------------------------------
+static bool g_side_copy = true;  // CGB_SIDE_COPY: pointer tables uploaded on a side stream into a device mirror
 template <class T>
 static T *stage_to_device(cgb_ring *r, const T *host, size_t n, std::vector<void *> &frees) {
   size_t bytes = sizeof(T) * n;
   if (bytes == 0) return nullptr;
   bytes = (bytes + 255) & ~(size_t)255;
-  T *dev;
-  CK(cudaMallocAsync((void **)&dev, bytes, r->stream));
-  frees.push_back(dev);
+  T *dev = nullptr;
   const size_t half = r->pin_cap / 2;
+  const bool side = g_side_copy && r->dev_stage && bytes <= half;
+  if (!side) {
+    CK(cudaMallocAsync((void **)&dev, bytes, r->stream));
+    frees.push_back(dev);
+  }
   if (bytes > half) {  // large payload: straight from the caller's buffer
     CK(cudaMemcpyAsync(dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
     // A pageable source is staged by the driver before the call returns.  A
@@ -282,6 +293,21 @@ static T *stage_to_device(cgb_ring *r, const T *host, size_t n, std::vector<void
   }
   char *dst = r->pin + (size_t)r->pin_half * half + r->pin_off;
   memcpy(dst, host, sizeof(T) * n);
+  if (g_side_copy && r->dev_stage) {
+    // the mirror slot is free: entering this half waited for every kernel that read it
+    T *mirror = reinterpret_cast<T *>(r->dev_stage + (size_t)r->pin_half * half + r->pin_off);
+    CK(cudaMemcpyAsync(mirror, dst, sizeof(T) * n, cudaMemcpyHostToDevice, r->copy_stream));
+    if (r->copy_ev.size() < 64) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      r->copy_ev.push_back(e);
+    }
+    cudaEvent_t e = r->copy_ev[r->copy_ev_next++ % r->copy_ev.size()];
+    CK(cudaEventRecord(e, r->copy_stream));
+    CK(cudaStreamWaitEvent(r->stream, e, 0));
+    r->pin_off += bytes;
+    return mirror;
+  }
   CK(cudaMemcpyAsync(dev, dst, sizeof(T) * n, cudaMemcpyHostToDevice, r->stream));
   r->pin_off += bytes;
   return dev;
@@ -4331,6 +4357,11 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   fused_attrs_for(log_n, n_limbs);
   r->pin_cap = (log_n >= 13 ? 128ull : 8ull) << 20;
   CK(cudaMallocHost((void **)&r->pin, r->pin_cap));
+  if (const char *e = getenv("CGB_SIDE_COPY")) g_side_copy = atoi(e) != 0;
+  if (g_side_copy) {
+    CK(cudaMalloc((void **)&r->dev_stage, r->pin_cap));
+    CK(cudaStreamCreateWithFlags(&r->copy_stream, cudaStreamNonBlocking));
+  }
   build_ring(r, key_seed);
   r->ct_words = 2ull * r->L * r->N;
   r->arena_cap = (size_t)std::max<int64_t>(arena_cts, 1);
@@ -4357,6 +4388,9 @@ void cgb_ring_destroy(cgb_ring *r) {
   cudaFree(r->d_s);
   cudaFree(r->d_c);
   cudaFreeHost(r->pin);
+  cudaFree(r->dev_stage);
+  if (r->copy_stream) cudaStreamDestroy(r->copy_stream);
+  for (auto e : r->copy_ev) cudaEventDestroy(e);
   for (auto &b : r->dec_pool) cudaFreeHost(b.second);
   for (auto e : r->pin_left)
     if (e) cudaEventDestroy(e);
