@@ -2689,6 +2689,51 @@ __global__ void k_tensor(u64 *ten, const u64 *in /*[item][4][nt][N]*/, const u64
   o[P + i] = add_mod(mul_mod(a0, b1, M), mul_mod(a1, b0, M), M.q);
   o[2 * P + i] = mul_mod(a1, b1, M);
 }
+// k_tensor on the FP64 pipe (rings of < 2^49 primes): 4 consecutive words per thread, every
+// operand and result a full 32-byte sector access, the four modular products error-free
+// FP64 products (5 FP64 instructions against ~14 integer ones, several of them the
+// quarter-rate IMAD.HI) -- the same canonical residues.
+__global__ void k_tensor_fp(u64 *ten, const u64 *in, const u64 *const *pa, const u64 *const *pb,
+                            const u64 *const *pbx, const ModTab *mods, int L, int nt, int iB0, int logN,
+                            const u64 *const *pax) {
+  const int item = blockIdx.y;
+  const u64 N = 1ull << logN, P = (u64)nt * N, LN = (u64)L * N;
+  const u64 i = 4 * ((u64)blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= P) return;
+  const int l = (int)(i >> logN);
+  const ModTab &M = mods[l < L ? l : iB0 + (l - L)];
+  const double q = M.qd, qi = M.qinv;
+  const u64 *x = in + (u64)item * 4 * P;
+  const u64 *p0, *p1, *p2, *p3;
+  if (l < L) {
+    p0 = pa[item] + i, p1 = pa[item] + LN + i, p2 = pb[item] + i, p3 = pb[item] + LN + i;
+  } else if (pax) {
+    p0 = pax[2 * item] + (i - LN), p1 = pax[2 * item + 1] + (i - LN), p2 = pbx[2 * item] + (i - LN),
+    p3 = pbx[2 * item + 1] + (i - LN);
+  } else if (pbx) {
+    p0 = x + i, p1 = x + P + i, p2 = pbx[2 * item] + (i - LN), p3 = pbx[2 * item + 1] + (i - LN);
+  } else {
+    p0 = x + i, p1 = x + P + i, p2 = x + 2 * P + i, p3 = x + 3 * P + i;
+  }
+  u64 a0[4], a1[4], b0[4], b1[4], o0[4], o1[4], o2[4];
+  ld256(p0, a0);
+  ld256(p1, a1);
+  ld256(p2, b0);
+  ld256(p3, b1);
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    const double A0 = u2d(a0[e]), A1 = u2d(a1[e]), B0 = u2d(b0[e]), B1 = u2d(b1[e]);
+    const double B0q = B0 * qi, B1q = B1 * qi;
+    o0[e] = fp_canon(fp_mulmod(A0, B0, B0q, q), q, qi);
+    o1[e] = fp_canon(fp_mulmod(A0, B1, B1q, q) + fp_mulmod(A1, B0, B0q, q), q, qi);
+    o2[e] = fp_canon(fp_mulmod(A1, B1, B1q, q), q, qi);
+  }
+  u64 *o = ten + (u64)item * 3 * P + i;
+  st256(o, o0[0], o0[1], o0[2], o0[3]);
+  st256(o + P, o1[0], o1[1], o1[2], o1[3]);
+  st256(o + 2 * P, o2[0], o2[1], o2[2], o2[3]);
+}
+static bool g_tensor_fp = true;  // CGB_TENSOR_FP
 // The tensor product fed straight into the first (row) pass of its inverse NTT:
 // unit (k, l) of item i is d_k in limb l of Q u B -- (a0 b0, a0 b1 + a1 b0, a1 b1)
 // mod q_l, from the operands' NTT words (the same residues k_tensor writes).  The
@@ -4351,6 +4396,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
   if (const char *e = getenv("CGB_KSROW8")) g_ksrow8 = atoi(e) != 0;
   if (const char *e = getenv("CGB_KSROW2")) g_ksrow2 = atoi(e);
+  if (const char *e = getenv("CGB_TENSOR_FP")) g_tensor_fp = atoi(e) != 0;
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
   if (const char *e = getenv("CGB_FP_BCONV")) g_fp_bconv = atoi(e) != 0;
@@ -5329,7 +5375,11 @@ static void mult_cipher_impl(cgb_ring *r, int count, const uint32_t *a, const ui
     u64 *ten = S.alloc<u64>((size_t)n * 3 * nt * N);
     const TensorLoad tl{dpa, dpb, in, dpx, dpax, r->d_mods, L, nt, r->iB0, logN};
     if (!tensor_intt_fused(r, n, ten, tl, tm.data())) {
-      LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
+      if (fpbc && g_tensor_fp && N >= 4) {
+        LAUNCH("tensor", BYTES_tensor, k_tensor_fp<<<dim3(GRID1((u64)nt * N / 4, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
+      } else {
+        LAUNCH("tensor", BYTES_tensor, k_tensor<<<dim3(GRID1((u64)nt * N, TPB).x, n), TPB, 0, r->stream>>>(ten, in, dpa, dpb, dpx, r->d_mods, L, nt, r->iB0, logN, dpax));
+      }
       ntt_items(r, false, ten, nullptr, 3ull * nt * N, n, 3, nt, tm.data());
     }
     u64 *d = S.alloc<u64>((size_t)n * 3 * L * N);
