@@ -1156,7 +1156,10 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
   issue_tile(0);
   auto load_tile = [&](double *x) {
 #pragma unroll
-    for (int k = 0; k < PA::K; k++) x[k] = (raw & 1) ? r2d(nv[k]) : u2d(nv[k]);
+    for (int k = 0; k < PA::K; k++) {
+      x[k] = (raw & 1) ? r2d(nv[k]) : u2d(nv[k]);
+      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
+    }
     issue_tile(tcur + 1);
     if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
@@ -1190,6 +1193,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     for (int k = 0; k < PA::K; k++) {
       const u64 v = src[PA::idx(tl, 0, k)];
       x[k] = (raw & 1) ? r2d(v) : u2d(v);
+      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
     }
     __syncwarp();  // every lane has read the staged tile
     issue_tile(tcur + 1);
@@ -1203,6 +1207,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     for (int k = 0; k < PA::K; k++) {
       const u64 v = (CGB_ABLATE & 4) ? (u64)(tid * 977 + k + tcur) : __ldcs(src + PA::idx(tl, 0, k));
       x[k] = ((raw & 1) && !(CGB_ABLATE & 4)) ? r2d(v) : u2d(v);
+      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
     }
     if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
@@ -1532,6 +1537,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 8, CGB_KSROW8_MINB)
       for (int k = 0; k < PA::K; k++) {
         const u64 v = __ldcs(src + PA::idx(tl, u, k));
         x[u * PA::K + k] = (raw & 1) ? r2d(v) : u2d(v);
+        if (raw & 4) x[u * PA::K + k] = fp_reduce(x[u * PA::K + k], qd, qinv);
       }
     if (t == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous pass's reads of the tile are done
     phase_regs_fp<LM, 0, 1, true, E, false>(x, tw, tl, qd, qinv);
@@ -1800,6 +1806,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     for (int k = 0; k < PA::K; k++) {
       const u64 v = b[PA::idx(tl, 0, k)];
       x[k] = (raw & 1) ? r2d(v) : u2d(v);
+      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);  // the column kernel stored its output unreduced
     }
     release();
     phase_regs_fp<LM, 0, RA, true, E, false, false, true>(x, tw, tl, qd, qinv);
@@ -1953,6 +1960,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     }
   }
 }
+static bool g_col_unred = true;  // CGB_COL_UNRED: the column kernels (FP64-bound) store D / W unreduced and the
+                                  // row kernels (L1-bound, FP64 to spare) reduce on load
 static int g_ksrow2 = 1;  // CGB_KSROW2: 1 = the Q-limb kernel (ks_row_md), 2 = the P-limb kernel too, 0 = k_ks_row
 
 
@@ -2024,14 +2033,23 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PF::K; k++) x[k] = fp_reduce(sd[spad(PF::idx(tl, 0, k))], qs, qsi);
-  phase_regs_fp<LM, 0, RA, false, E>(x, tws, tl, qs, qsi);
+  // ... its last stage (stage 0: pairs (k, k + 8), one twiddle) run here with N^-1 folded in:
+  // X' = (X + Y) N^-1, Y' = (X - Y) (w N^-1) -- 16 products instead of 8 + 16 and no
+  // reduction before them (|X +- Y| <= 8 q after three unreduced stages)
+  phase_regs_fp<LM, 0, RA, false, E, false, false, false, true>(x, tws, tl, qs, qsi);
+#pragma unroll
+  for (int k = 0; k < E / 2; k++) {
+    const double sm_ = x[k] + x[k + E / 2], df_ = x[k] - x[k + E / 2];
+    x[k] = fp_mulmod(sm_, Ms.ninv_fp, Ms.ninv_fpq, qs);
+    x[k + E / 2] = fp_mulmod(df_, Ms.itw0n_fp, Ms.itw0n_fpq, qs);
+  }
   // the centred lift of each coefficient: fp_reduce's residue in [-q_src/2, q_src/2]
   // IS the centred representative (q_src odd), and since every modulus of Q u P has
   // the same bit length (|r| <= q_src / 2 < q_t, col_fusable) it is a valid input of
   // each target's forward pass as it stands -- no canonical form, no integer lift
   double c[E];
 #pragma unroll
-  for (int k = 0; k < E; k++) c[k] = fp_reduce(fp_mulmod(fp_reduce(x[k], qs, qsi), Ms.ninv_fp, Ms.ninv_fpq, qs), qs, qsi);
+  for (int k = 0; k < E; k++) c[k] = fp_reduce(x[k], qs, qsi);
 #pragma unroll 1
   for (int t = 0; t < NT; t++) {
     const ModTab &Mt = job.mods[job.dst_mod[s][t]];
@@ -2055,7 +2073,9 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
 #pragma unroll
       for (int k = 0; k < PS::K; k++)
         dst[gaddr(PS::idx(tl, u, k))] =
-            job.out_raw ? fp_raw(x[u * PS::K + k], qt, qti) : fp_canon(x[u * PS::K + k], qt, qti);
+            job.out_raw == 2 ? (u64)__double_as_longlong(x[u * PS::K + k])  // unreduced: the row kernel reduces on load
+            : job.out_raw    ? fp_raw(x[u * PS::K + k], qt, qti)
+                             : fp_canon(x[u * PS::K + k], qt, qti);
   }
 }
 template <int LA, int LB>
@@ -3225,6 +3245,8 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   u64 *acc = D + nD;
   u64 *W = acc + nacc;
   const dim3 rows_grid1((unsigned)((size_t)count * L * ((1 << LA) / G1)));
+  const bool unred = g_col_unred && g_ks_md;
+  const int rawf = unred ? 7 : 3;
   {  // 1
     NttJob job{};
     job.base = xr;
@@ -3254,7 +3276,8 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     cj.dst = D;
     cj.dst_stride = (u64)L * LP * N;
     cj.nsrc = L;
-    cj.in_raw = cj.out_raw = 1;
+    cj.in_raw = 1;
+    cj.out_raw = unred ? 2 : 1;  // unreduced: the row kernels reduce on load
     for (int j = 0; j < L; j++) {
       cj.src_off[j] = (unsigned short)j;
       cj.src_mod[j] = (unsigned char)j;
@@ -3285,17 +3308,17 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     if (g_ksrow2 >= 2)
       launch_pdl(r, k_ks_row2<LA, LB, L, false>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
-                 (const u64 *)nullptr, epi, 3);
+                 (const u64 *)nullptr, epi, rawf);
     else
     launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, 3);
+               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
     launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
                (double)count * ((N / 2) * LB * (L + 2.0) + 2.0 * L * N));
   } else {  // 3
     const dim3 g1((unsigned)((size_t)count * LP * TILES));
     launch_begin(r);
     launch_pdl(r, k_ks_row<LA, LB, L, 0>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
-               r->iP, count, (const u64 *)nullptr, epi, 3);
+               r->iP, count, (const u64 *)nullptr, epi, rawf);
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
@@ -3306,7 +3329,8 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     cj.dst = W;
     cj.dst_stride = 2ull * L * N;
     cj.nsrc = 2;
-    cj.in_raw = cj.out_raw = 1;
+    cj.in_raw = 1;
+    cj.out_raw = unred ? 2 : 1;  // unreduced: the row kernels reduce on load
     for (int pp = 0; pp < 2; pp++) {
       cj.src_off[pp] = (unsigned short)(pp * LP + L);
       cj.src_mod[pp] = (unsigned char)r->iP;
@@ -3322,7 +3346,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     if (g_ksrow2) {
       launch_pdl(r, k_ks_row2<LA, LB, L, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
-                 epi, 3);
+                 epi, rawf);
     } else
     if constexpr (LB == 7) {
       if (g_ksrow8) {
@@ -3332,14 +3356,14 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
                                   (int)ks_row_smem<LA, LB>()));
         });
         launch_pdl(r, k_ks_row8<LA, LB, L>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 8,
-                   ks_row_smem<LA, LB>(), (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, (const u64 *)W, epi, 3);
+                   ks_row_smem<LA, LB>(), (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, (const u64 *)W, epi, rawf);
       } else {
         launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-                   ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
+                   ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, rawf);
       }
     } else {
       launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, 3);
+                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, rawf);
     }
     // D (L-1 digits) + own digit + W (2) + out (2) per limb, c0 / add1 when present; keys once
     launch_end(r, "ks_row_md",
@@ -4118,6 +4142,11 @@ static void build_ring(cgb_ring *r, const u32 key_seed[8]) {
     M.r64 = (u64)((((u128)1) << 64) % q);
     M.ninv = h_inv((u64)N % q, q);
     M.ninv_sh = h_shoup(M.ninv, q);
+    {  // the inverse transform's stage-0 twiddle (pair index 1) times N^-1
+      const u64 w0n = h_mulmod(tab[2ull * N + 2], M.ninv, q);
+      M.itw0n_fp = (double)w0n;
+      M.itw0n_fpq = (double)w0n / (double)q;
+    }
     M.tw = dt;
     M.tw_sh = nullptr;
     M.itw = dt + 2 * N;
@@ -4396,6 +4425,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KS_CHUNK")) g_ks_chunk = atoi(e);
   if (const char *e = getenv("CGB_KSROW8")) g_ksrow8 = atoi(e) != 0;
   if (const char *e = getenv("CGB_KSROW2")) g_ksrow2 = atoi(e);
+  if (const char *e = getenv("CGB_COL_UNRED")) g_col_unred = atoi(e) != 0;
   if (const char *e = getenv("CGB_TENSOR_FP")) g_tensor_fp = atoi(e) != 0;
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;

@@ -31,6 +31,7 @@ struct ModTab {
   const u64 *ftw1tw, *fitw1tw;           // the w halves of ftw1t / fitw1t alone (w / q is one DMUL on use)
   double qd, qinv;                       // q and 1/q as doubles (FP64 NTT)
   double ninv_fp, ninv_fpq;              // N^-1 and N^-1 / q as doubles
+  double itw0n_fp, itw0n_fpq;            // (last inverse stage's twiddle) * N^-1 mod q, and that / q
   int bits;
   int pad_;
 };
@@ -717,7 +718,10 @@ struct PhaseShape {
 // blocks read consecutive entries.
 // GTW: tws is a global table (read through the read-only path) instead of shared memory
 // WQ: tws holds the twiddles' w only (doubles); w/q is formed by one DMUL per use
-template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false, bool WQ = false>
+// SKIPLAST: leave out the last executed stage (an inverse phase ending at stage 0, whose
+// single butterfly layer the caller runs itself with N^-1 folded into both outputs)
+template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false, bool WQ = false,
+          bool SKIPLAST = false>
 __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, int tl, double q, double qinv) {
   using PS = PhaseShape<LM, S0, RP, E>;
   constexpr int K = PS::K, R = PS::R;
@@ -726,6 +730,7 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
     const int blk = PS::row(tl, u) / PS::ST;
 #pragma unroll
     for (int ll = 0; ll < RP; ll++) {
+      if (SKIPLAST && ll == RP - 1) continue;
       const int l = FWD ? ll : RP - 1 - ll;
       const int half = K >> (l + 1);
       double2 W;
