@@ -1072,7 +1072,7 @@ __host__ __device__ constexpr size_t ksr_pf_bytes(int LB) {
 // MODE 0: every limb of Q u P; 1: the P limb only; 2: the Q limbs, followed by
 // ModDown's forward row pass of W (the column-pass output of lift(INTT(acc_P)))
 // with the combine as its epilogue -- the Q limbs' accumulators never reach memory.
-template <int LA, int LB, int L, int MODE = 0>
+template <int LA, int LB, int L, int MODE = 0, bool UNRED = false>
 __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
                                                            const u64 *const *keys, const ModTab *mods, int iP,
                                                            int count, const u64 *W, MdEpi epi, int raw) {
@@ -1158,7 +1158,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
 #pragma unroll
     for (int k = 0; k < PA::K; k++) {
       x[k] = (raw & 1) ? r2d(nv[k]) : u2d(nv[k]);
-      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
+      if constexpr (UNRED) x[k] = fp_reduce(x[k], qd, qinv);
     }
     issue_tile(tcur + 1);
     if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
@@ -1193,7 +1193,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     for (int k = 0; k < PA::K; k++) {
       const u64 v = src[PA::idx(tl, 0, k)];
       x[k] = (raw & 1) ? r2d(v) : u2d(v);
-      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
+      if constexpr (UNRED) x[k] = fp_reduce(x[k], qd, qinv);
     }
     __syncwarp();  // every lane has read the staged tile
     issue_tile(tcur + 1);
@@ -1207,7 +1207,7 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
     for (int k = 0; k < PA::K; k++) {
       const u64 v = (CGB_ABLATE & 4) ? (u64)(tid * 977 + k + tcur) : __ldcs(src + PA::idx(tl, 0, k));
       x[k] = ((raw & 1) && !(CGB_ABLATE & 4)) ? r2d(v) : u2d(v);
-      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);
+      if constexpr (UNRED) x[k] = fp_reduce(x[k], qd, qinv);
     }
     if (tcur == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous tile's phase-B reads are done
     tcur++;
@@ -1537,7 +1537,6 @@ __global__ void __launch_bounds__(NTT2_TILE / 8, CGB_KSROW8_MINB)
       for (int k = 0; k < PA::K; k++) {
         const u64 v = __ldcs(src + PA::idx(tl, u, k));
         x[u * PA::K + k] = (raw & 1) ? r2d(v) : u2d(v);
-        if (raw & 4) x[u * PA::K + k] = fp_reduce(x[u * PA::K + k], qd, qinv);
       }
     if (t == 0) __syncthreads(); else ROW_SYNC();  // twiddles staged; the previous pass's reads of the tile are done
     phase_regs_fp<LM, 0, 1, true, E, false>(x, tw, tl, qd, qinv);
@@ -1662,7 +1661,7 @@ __host__ __device__ constexpr size_t ks_row2_smem() {
 #ifndef CGB_R2_ADD1
 #define CGB_R2_ADD1 1  // the rotate_add input through the ring (0: direct 256-bit loads in the epilogue)
 #endif
-template <int LA, int LB, int L, bool MD>
+template <int LA, int LB, int L, bool MD, bool UNRED = false>
 __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     k_ks_row2(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *keys, const ModTab *mods, int iP, const u64 *W,
               MdEpi epi, int raw) {
@@ -1806,7 +1805,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     for (int k = 0; k < PA::K; k++) {
       const u64 v = b[PA::idx(tl, 0, k)];
       x[k] = (raw & 1) ? r2d(v) : u2d(v);
-      if (raw & 4) x[k] = fp_reduce(x[k], qd, qinv);  // the column kernel stored its output unreduced
+      if constexpr (UNRED) x[k] = fp_reduce(x[k], qd, qinv);  // the column kernel stored its output unreduced
     }
     release();
     phase_regs_fp<LM, 0, RA, true, E, false, false, true>(x, tw, tl, qd, qinv);
@@ -1960,8 +1959,9 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     }
   }
 }
-static bool g_col_unred = true;  // CGB_COL_UNRED: the column kernels (FP64-bound) store D / W unreduced and the
-                                  // row kernels (L1-bound, FP64 to spare) reduce on load
+static bool g_col_unred = false;  // CGB_COL_UNRED: the column kernels (FP64-bound) store D / W unreduced and the
+                                   // row kernels reduce on load.  Measured: the column kernels gain 0.02 ms per
+                                   // 768 key switches, the row kernels lose 0.03 -- off
 static int g_ksrow2 = 1;  // CGB_KSROW2: 1 = the Q-limb kernel (ks_row_md), 2 = the P-limb kernel too, 0 = k_ks_row
 
 
@@ -2145,6 +2145,7 @@ static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 #ifdef CGB_KSROW_CARVE
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
@@ -3245,8 +3246,9 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   u64 *acc = D + nD;
   u64 *W = acc + nacc;
   const dim3 rows_grid1((unsigned)((size_t)count * L * ((1 << LA) / G1)));
-  const bool unred = g_col_unred && g_ks_md;
-  const int rawf = unred ? 7 : 3;
+  // unreduced D / W only with the kernels that take the flag as a template parameter
+  const bool unred = g_col_unred && g_ks_md && g_ksrow2 >= 1;
+  const int rawf = 3;
   {  // 1
     NttJob job{};
     job.base = xr;
@@ -3301,17 +3303,28 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
                               (int)ks_row2_smem<LB>()));
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
     });
   }
   if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
-    if (g_ksrow2 >= 2)
+    if (g_ksrow2 >= 2 && unred)
+      launch_pdl(r, k_ks_row2<LA, LB, L, false, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
+                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
+                 (const u64 *)nullptr, epi, rawf);
+    else if (g_ksrow2 >= 2)
       launch_pdl(r, k_ks_row2<LA, LB, L, false>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
                  (const u64 *)nullptr, epi, rawf);
+    else if (unred)
+      launch_pdl(r, k_ks_row<LA, LB, L, 1, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
+                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
     else
-    launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-               ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
+      launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
+                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
     launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
                (double)count * ((N / 2) * LB * (L + 2.0) + 2.0 * L * N));
   } else {  // 3
@@ -3343,7 +3356,11 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   }
   if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
     launch_begin(r);
-    if (g_ksrow2) {
+    if (g_ksrow2 && unred) {
+      launch_pdl(r, k_ks_row2<LA, LB, L, true, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
+                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
+                 epi, rawf);
+    } else if (g_ksrow2) {
       launch_pdl(r, k_ks_row2<LA, LB, L, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
                  epi, rawf);
