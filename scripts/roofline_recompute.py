@@ -26,8 +26,8 @@ roof = line["roofline"]
 rows = [r for r in csv.reader(open(launches)) if len(r) > 10 and r[0].isdigit()]
 names = [r[6].split("(")[0].replace("void ", "").replace("cgb::", "") for r in rows]
 ns = [float(r[-1]) for r in rows]
-seq = (("k_ntt2_fpr<7, 7, 0, 1",), ("k_col_fused",), ("k_ks_row<7, 7, 3, 1>", "k_ks_row2<7, 7, 3, 0>"), ("k_col_fused",),
-       ("k_ks_row<7, 7, 3, 2>", "k_ks_row2<7, 7, 3, 1>"))
+seq = (("k_ntt2_fpr<7, 7, 0, 1",), ("k_col_fused",), ("k_ks_row<7, 7, 3, 1", "k_ks_row2<7, 7, 3, 0"), ("k_col_fused",),
+       ("k_ks_row<7, 7, 3, 2", "k_ks_row2<7, 7, 3, 1"))
 ks_ns, relin_ns, groups, relin = 0.0, 0.0, 0, 0
 i = 0
 while i + 5 <= len(names):
