@@ -1654,6 +1654,9 @@ __host__ __device__ constexpr size_t ks_row2_smem() {
 #ifndef CGB_KSROW2_MINB
 #define CGB_KSROW2_MINB 3
 #endif
+#ifndef CGB_R2_RAWCONST
+#define CGB_R2_RAWCONST 1  // k_ks_row2 is only launched on reduced-double tiles (raw = 3): no predicated conversions
+#endif
 #ifndef CGB_R2_OWN
 #define CGB_R2_OWN 0   // own limb / c0 through the ring (0: direct gathered loads, c0 in the epilogue): the
                        // scattered shared-memory reads cost more than the gathers (ks_row_md 0.88 -> 0.95 ms)
@@ -1661,7 +1664,10 @@ __host__ __device__ constexpr size_t ks_row2_smem() {
 #ifndef CGB_R2_ADD1
 #define CGB_R2_ADD1 1  // the rotate_add input through the ring (0: direct 256-bit loads in the epilogue)
 #endif
-template <int LA, int LB, int L, bool MD, bool UNRED = false>
+// FLAGS >= 0: which epilogue operands exist is known at compile time (bit 0: c0 o sigma,
+// bit 1: the rotate_add / relinearisation input) -- the rotate and rotate_add waves of the
+// hot path; -1: decided from the arguments at run time
+template <int LA, int LB, int L, bool MD, bool UNRED = false, int FLAGS = -1>
 __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
     k_ks_row2(u64 *acc, const u64 *D, KsSrc xin, const u64 *const *keys, const ModTab *mods, int iP, const u64 *W,
               MdEpi epi, int raw) {
@@ -1698,8 +1704,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
   };
   stage_tw(Md.ftw1tw);
   const double2 *tw = reinterpret_cast<const double2 *>(twd + g * (M + 1));
-  const bool any_c0 = MD && (epi.add0.items || epi.add0.base);
-  const bool any_add1 = MD && epi.add1 != nullptr;
+  const bool any_c0 = MD && (FLAGS >= 0 ? (FLAGS & 1) != 0 : (epi.add0.items || epi.add0.base));
+  const bool any_add1 = MD && (FLAGS >= 0 ? (FLAGS & 2) != 0 : epi.add1 != nullptr);
   const bool has_c0 = CGB_R2_OWN == 1 && any_c0;      // ... as ring entries
   const bool has_add1 = CGB_R2_ADD1 && any_add1;
   const int c0n = has_c0 ? 1 : 0;
@@ -1804,7 +1810,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
 #pragma unroll
     for (int k = 0; k < PA::K; k++) {
       const u64 v = b[PA::idx(tl, 0, k)];
-      x[k] = (raw & 1) ? r2d(v) : u2d(v);
+      x[k] = (CGB_R2_RAWCONST || (raw & 1)) ? r2d(v) : u2d(v);
       if constexpr (UNRED) x[k] = fp_reduce(x[k], qd, qinv);  // the column kernel stored its output unreduced
     }
     release();
@@ -1955,10 +1961,14 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
       phase_regs_fp<LM, 0, RA, false, E, false, false, true>(y, tw, tl, qd, qinv);
       u64 *o = pp ? o1 : o0;
 #pragma unroll
-      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (raw & 2) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
+      for (int k = 0; k < PA::K; k++) o[PA::idx(tl, 0, k)] = (CGB_R2_RAWCONST || (raw & 2)) ? fp_raw(y[k], qd, qinv) : fp_canon(y[k], qd, qinv);
     }
   }
 }
+#ifndef CGB_COL_UNRED_BUILD
+#define CGB_COL_UNRED_BUILD 0  // instantiate the reduce-on-load row kernels (measured a net loss; not built by default)
+#endif
+static bool g_ksrow2_spec = true;  // CGB_KSROW2_SPEC: epilogue operands known at compile time for rotate / rotate_add
 static bool g_col_unred = false;  // CGB_COL_UNRED: the column kernels (FP64-bound) store D / W unreduced and the
                                    // row kernels reduce on load.  Measured: the column kernels gain 0.02 ms per
                                    // 768 key switches, the row kernels lose 0.03 -- off
@@ -2145,7 +2155,9 @@ static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+#if CGB_COL_UNRED_BUILD
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+#endif
 #ifdef CGB_KSROW_CARVE
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
@@ -3247,7 +3259,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   u64 *W = acc + nacc;
   const dim3 rows_grid1((unsigned)((size_t)count * L * ((1 << LA) / G1)));
   // unreduced D / W only with the kernels that take the flag as a template parameter
-  const bool unred = g_col_unred && g_ks_md && g_ksrow2 >= 1;
+  const bool unred = CGB_COL_UNRED_BUILD && g_col_unred && g_ks_md && g_ksrow2 >= 1;
   const int rawf = 3;
   {  // 1
     NttJob job{};
@@ -3303,25 +3315,36 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
                               (int)ks_row2_smem<LB>()));
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
+      CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)ks_row2_smem<LB>()));
+#if CGB_COL_UNRED_BUILD
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
+#endif
     });
   }
   if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
+#if CGB_COL_UNRED_BUILD
     if (g_ksrow2 >= 2 && unred)
       launch_pdl(r, k_ks_row2<LA, LB, L, false, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
                  (const u64 *)nullptr, epi, rawf);
-    else if (g_ksrow2 >= 2)
+    else
+#endif
+    if (g_ksrow2 >= 2)
       launch_pdl(r, k_ks_row2<LA, LB, L, false>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
                  (const u64 *)nullptr, epi, rawf);
+#if CGB_COL_UNRED_BUILD
     else if (unred)
       launch_pdl(r, k_ks_row<LA, LB, L, 1, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
+#endif
     else
       launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
                  ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
@@ -3356,14 +3379,20 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   }
   if (g_ks_md) {  // 5: Q limbs' inner product + ModDown row pass of W + combine -> out
     launch_begin(r);
-    if (g_ksrow2 && unred) {
-      launch_pdl(r, k_ks_row2<LA, LB, L, true, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
-                 epi, rawf);
-    } else if (g_ksrow2) {
-      launch_pdl(r, k_ks_row2<LA, LB, L, true>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
-                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W,
-                 epi, rawf);
+    if (g_ksrow2) {
+      const bool c0 = add0.items || add0.base, a1 = d_add1 != nullptr;
+      const dim3 gmd((unsigned)((size_t)count * L * TILES));
+#define KSR2(U, F)                                                                                              \
+  launch_pdl(r, k_ks_row2<LA, LB, L, true, U, F>, gmd, NTT2_TILE / 16, ks_row2_smem<LB>(), acc, (const u64 *)D, x, \
+             d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)W, epi, rawf)
+#if CGB_COL_UNRED_BUILD
+      if (unred) KSR2(true, -1);
+      else
+#endif
+      if (g_ksrow2_spec && c0 && a1) KSR2(false, 3);
+      else if (g_ksrow2_spec && c0) KSR2(false, 1);
+      else KSR2(false, -1);
+#undef KSR2
     } else
     if constexpr (LB == 7) {
       if (g_ksrow8) {
@@ -4443,6 +4472,7 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KSROW8")) g_ksrow8 = atoi(e) != 0;
   if (const char *e = getenv("CGB_KSROW2")) g_ksrow2 = atoi(e);
   if (const char *e = getenv("CGB_COL_UNRED")) g_col_unred = atoi(e) != 0;
+  if (const char *e = getenv("CGB_KSROW2_SPEC")) g_ksrow2_spec = atoi(e) != 0;
   if (const char *e = getenv("CGB_TENSOR_FP")) g_tensor_fp = atoi(e) != 0;
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
