@@ -1980,6 +1980,9 @@ static int g_ksrow2 = 1;  // CGB_KSROW2: 1 = the Q-limb kernel (ks_row_md), 2 = 
 // target's forward column pass.  The inverse's last phase and the forward's first
 // phase share one register shape, so the coefficients never leave registers; the
 // coefficient-domain polynomial is neither written nor re-read.
+#ifndef CGB_COLF_RAWCONST
+#define CGB_COLF_RAWCONST 1  // k_col_fused's callers all pass reduced-double words in and out: no per-word flag tests
+#endif
 struct ColJob {
   const u64 *src;     // source items (row-pass output of the inverse NTT)
   u64 src_stride;
@@ -2028,7 +2031,7 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
 #pragma unroll
     for (int k = 0; k < PS::K; k++) {
       const u64 v = __ldcs(src + gaddr(PS::idx(tl, u, k)));
-      x[u * PS::K + k] = job.in_raw ? r2d(v) : u2d(v);
+      x[u * PS::K + k] = (CGB_COLF_RAWCONST || job.in_raw) ? r2d(v) : u2d(v);
       if (RB == 4) x[u * PS::K + k] = fp_reduce(x[u * PS::K + k], Ms.qd, Ms.qinv);  // 4-stage inverse phase
     }
   double *sd = data + g * PADM;
@@ -2083,8 +2086,8 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_COLF_MINB) k_col_fused(Col
 #pragma unroll
       for (int k = 0; k < PS::K; k++)
         dst[gaddr(PS::idx(tl, u, k))] =
-            job.out_raw == 2 ? (u64)__double_as_longlong(x[u * PS::K + k])  // unreduced: the row kernel reduces on load
-            : job.out_raw    ? fp_raw(x[u * PS::K + k], qt, qti)
+            (CGB_COL_UNRED_BUILD && job.out_raw == 2) ? (u64)__double_as_longlong(x[u * PS::K + k])  // unreduced
+            : (CGB_COLF_RAWCONST || job.out_raw) ? fp_raw(x[u * PS::K + k], qt, qti)
                              : fp_canon(x[u * PS::K + k], qt, qti);
   }
 }
