@@ -30,6 +30,12 @@ typedef unsigned __int128 u128;
 // ============================================================================
 // two-pass split of the 2^14-point transform: 2^A14 strided column sub-transforms x 2^(14 - A14)
 // contiguous row sub-transforms (the other sizes split evenly: 6+7, 7+8, 8+8)
+// Superseded kernel variants kept for A/B runs (k_ks_row MODE 0 / 2, k_ks_row8, the P-limb k_ks_row2):
+// built only with -DCGB_BUILD_FALLBACKS=1 (they are ~100 heavy instantiations, half the compile time);
+// without them CGB_KS_MD / CGB_KSROW2 / CGB_KSROW8 keep their defaults.
+#ifndef CGB_BUILD_FALLBACKS
+#define CGB_BUILD_FALLBACKS 0
+#endif
 #ifndef CGB_A14
 #define CGB_A14 7
 #endif
@@ -2155,16 +2161,16 @@ static void ks_row_attrs() {  // > 48 KB of dynamic shared memory needs the opt-
   static std::once_flag once;
   std::call_once(once, [] {
     const int sm = (int)ks_row_smem<LA, LB>();
-    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+#if CGB_BUILD_FALLBACKS
+    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+#endif
 #if CGB_COL_UNRED_BUILD
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 #endif
 #ifdef CGB_KSROW_CARVE
-    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
     cudaFuncSetAttribute(k_ks_row<LA, LB, L, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
-    cudaFuncSetAttribute(k_ks_row<LA, LB, L, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, CGB_KSROW_CARVE);
 #endif
   });
 }
@@ -2178,8 +2184,13 @@ static void modup_ks_row_t(cgb_ring *r, const NttJob &job, int count, u64 *acc, 
   launch_pdl(r, k_ntt2_fpr<LA, LB, true, 0>, g0, NTT2_TILE / 16, fpr_smem_bytes<LA, LB>(0), job, NoEpi{});
   const dim3 g1((unsigned)((size_t)count * (L + 1) * ((1 << LA) / G1)));
   ks_row_attrs<LA, LB, L>();
+#if CGB_BUILD_FALLBACKS
   launch_pdl(r, k_ks_row<LA, LB, L>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
              r->iP, count, (const u64 *)nullptr, MdEpi{}, 0);
+#else
+  (void)g1, (void)acc, (void)D, (void)x, (void)d_keys;
+  FAIL(CGB_ERR_STATE, "the unfused ModUp row kernel is not built (CGB_BUILD_FALLBACKS)");
+#endif
 }
 static bool ks_row_fusable(const cgb_ring *r) {
   // the FP64 inner-product sum is reduced after every 4 digits (|sum| < 11.3 q < 2^53), so
@@ -3314,8 +3325,10 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   if (g_ks_md && g_ksrow2) {
     static std::once_flag once2;
     std::call_once(once2, [] {
+#if CGB_BUILD_FALLBACKS
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
+#endif
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3323,8 +3336,10 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
 #if CGB_COL_UNRED_BUILD
+#if CGB_BUILD_FALLBACKS
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
+#endif
       CK(cudaFuncSetAttribute(k_ks_row2<LA, LB, L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)ks_row2_smem<LB>()));
 #endif
@@ -3332,28 +3347,37 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
   }
   if (g_ks_md) {  // 3: the P limb only (its accumulators feed ModDown's INTT)
     launch_begin(r);
-#if CGB_COL_UNRED_BUILD
-    if (g_ksrow2 >= 2 && unred)
-      launch_pdl(r, k_ks_row2<LA, LB, L, false, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
-                 (const u64 *)nullptr, epi, rawf);
-    else
+    const dim3 gP((unsigned)((size_t)count * TILES));
+    bool done = false;
+#if CGB_COL_UNRED_BUILD && CGB_BUILD_FALLBACKS
+    if (!done && g_ksrow2 >= 2 && unred) {
+      launch_pdl(r, k_ks_row2<LA, LB, L, false, true>, gP, NTT2_TILE / 16, ks_row2_smem<LB>(), acc, (const u64 *)D, x,
+                 d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)nullptr, epi, rawf);
+      done = true;
+    }
 #endif
-    if (g_ksrow2 >= 2)
-      launch_pdl(r, k_ks_row2<LA, LB, L, false>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-                 ks_row2_smem<LB>(), acc, (const u64 *)D, x, d_keys, (const ModTab *)r->d_mods, r->iP,
-                 (const u64 *)nullptr, epi, rawf);
-#if CGB_COL_UNRED_BUILD
-    else if (unred)
-      launch_pdl(r, k_ks_row<LA, LB, L, 1, true>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
+#if CGB_BUILD_FALLBACKS
+    if (!done && g_ksrow2 >= 2) {
+      launch_pdl(r, k_ks_row2<LA, LB, L, false>, gP, NTT2_TILE / 16, ks_row2_smem<LB>(), acc, (const u64 *)D, x,
+                 d_keys, (const ModTab *)r->d_mods, r->iP, (const u64 *)nullptr, epi, rawf);
+      done = true;
+    }
 #endif
-    else
-      launch_pdl(r, k_ks_row<LA, LB, L, 1>, dim3((unsigned)((size_t)count * TILES)), NTT2_TILE / 16,
-                 ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
+#if CGB_COL_UNRED_BUILD
+    if (!done && unred) {
+      launch_pdl(r, k_ks_row<LA, LB, L, 1, true>, gP, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys,
+                 r->d_mods, r->iP, count, (const u64 *)nullptr, epi, rawf);
+      done = true;
+    }
+#endif
+    if (!done)
+      launch_pdl(r, k_ks_row<LA, LB, L, 1>, gP, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
+                 r->iP, count, (const u64 *)nullptr, epi, rawf);
     launch_end(r, "ks_row_P", 8.0 * (double)count * N * (L + 2.0) + 16.0 * L * N,
                (double)count * ((N / 2) * LB * (L + 2.0) + 2.0 * L * N));
-  } else {  // 3
+  }
+#if CGB_BUILD_FALLBACKS
+  else {  // 3
     const dim3 g1((unsigned)((size_t)count * LP * TILES));
     launch_begin(r);
     launch_pdl(r, k_ks_row<LA, LB, L, 0>, g1, NTT2_TILE / 16, ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods,
@@ -3361,6 +3385,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
     launch_end(r, "ks_row", 8.0 * (double)count * N * (L * L + 2.0 * LP + 4.0) + 16.0 * L * (double)LP * N,
                (double)count * ((N / 2) * LB * (L * L + 2.0) + 2.0 * LP * L * N));
   }
+#endif
   {  // 4
     ColJob cj{};
     cj.src = acc;
@@ -3396,7 +3421,9 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
       else if (g_ksrow2_spec && c0) KSR2(false, 1);
       else KSR2(false, -1);
 #undef KSR2
-    } else
+    }
+#if CGB_BUILD_FALLBACKS
+    else
     if constexpr (LB == 7) {
       if (g_ksrow8) {
         static std::once_flag once8;
@@ -3414,6 +3441,7 @@ static void keyswitch_fp_t(cgb_ring *r, Scratch &S, const KsSrc &x, int count, u
       launch_pdl(r, k_ks_row<LA, LB, L, 2>, dim3((unsigned)((size_t)count * L * TILES)), NTT2_TILE / 16,
                  ks_row_smem<LA, LB>(), acc, D, x, d_keys, r->d_mods, r->iP, count, (const u64 *)W, epi, rawf);
     }
+#endif
     // D (L-1 digits) + own digit + W (2) + out (2) per limb, c0 / add1 when present; keys once
     launch_end(r, "ks_row_md",
                8.0 * (double)count * N * L * (L + 4.0 + (add0.items || add0.base ? 1 : 0) + (d_add1 ? 2 : 0)) +
@@ -4476,6 +4504,11 @@ int cgb_ring_create_ex(int log_n, uint64_t plain_modulus, int n_limbs, int q_bit
   if (const char *e = getenv("CGB_KSROW2")) g_ksrow2 = atoi(e);
   if (const char *e = getenv("CGB_COL_UNRED")) g_col_unred = atoi(e) != 0;
   if (const char *e = getenv("CGB_KSROW2_SPEC")) g_ksrow2_spec = atoi(e) != 0;
+#if !CGB_BUILD_FALLBACKS  // the superseded variants are not in this build
+  g_ks_md = true;
+  g_ksrow2 = 1;
+  g_ksrow8 = false;
+#endif
   if (const char *e = getenv("CGB_TENSOR_FP")) g_tensor_fp = atoi(e) != 0;
   if (const char *e = getenv("CGB_WS_GIB")) g_ws_bytes = (size_t)(atof(e) * (double)(1ull << 30));
   if (const char *e = getenv("CGB_HOIST_FUSE")) g_hoist_fuse = atoi(e) != 0;
