@@ -877,6 +877,9 @@ __global__ void k_moddown_combine(u64 *const *out, const u64 *acc, const u64 *W,
 // ModDown combine as the store epilogue of the forward row pass that produces
 // W = NTT_l(lift_P(INTT_P(acc_P))): out = (acc_l - W) P^-1 (+ add0 on poly 0)
 // (+ add1), the same words as k_moddown_combine without W's round trip.
+#ifndef CGB_KEYPROD_Q
+#define CGB_KEYPROD_Q 1  // key products estimate the quotient from the rounded product (no k * (1/q) DMUL)
+#endif
 #ifndef CGB_ABLATE
 #define CGB_ABLATE 0  // timing experiments only (wrong results): which loads / phases bound k_ks_row
 #endif
@@ -1373,8 +1376,13 @@ __global__ void KSROW_BOUNDS k_ks_row(u64 *acc, const u64 *D, KsSrc xin,
         for (int e = 0; e < 4; e++) {
           const double xv = x[u * PB::K + k + e];
           const double d0 = r2d(w0[e]), d1 = r2d(w1[e]);
+#if CGB_KEYPROD_Q
+          a0[u * PB::K + k + e] += fp_mulmod_q(xv, d0, qd, qinv);
+          a1[u * PB::K + k + e] += fp_mulmod_q(xv, d1, qd, qinv);
+#else
           a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
           a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+#endif
         }
       }
     }
@@ -1892,8 +1900,13 @@ __global__ void __launch_bounds__(NTT2_TILE / 16, CGB_KSROW2_MINB)
           for (int e = 0; e < 4; e++) {
             const double xv = x[u * PB::K + k + e];
             const double d0 = r2d(w0[e]), d1 = r2d(w1[e]);
+#if CGB_KEYPROD_Q
+            a0[u * PB::K + k + e] += fp_mulmod_q(xv, d0, qd, qinv);
+            a1[u * PB::K + k + e] += fp_mulmod_q(xv, d1, qd, qinv);
+#else
             a0[u * PB::K + k + e] += fp_mulmod(xv, d0, d0 * qinv, qd);
             a1[u * PB::K + k + e] += fp_mulmod(xv, d1, d1 * qinv, qd);
+#endif
           }
         }
     }

@@ -524,6 +524,17 @@ __device__ __forceinline__ double fp_mulmod(double a, double w, double wq, doubl
   return fma(-rint(a * wq), q, hi) + lo;
 }
 
+// the same product with the quotient estimated from the rounded product itself:
+// rint(fl(a w) / q) instead of rint(a fl(w / q)) -- no w / q operand.  Three roundings
+// (1 / q, the product, the scaling), exactly as many as fp_mulmod(a, w, w * qinv, q)
+// spends when w / q has to be formed on the fly, so the same bound: |a w / q - qe| <=
+// 0.5 + 3 |a w / q| 2^-53, the result an exact integer in (-2.8 q, 2.8 q) for |a| < 12 q.
+__device__ __forceinline__ double fp_mulmod_q(double a, double w, double q, double qinv) {
+  const double hi = a * w;
+  const double lo = fma(a, w, -hi);
+  return fma(-rint(hi * qinv), q, hi) + lo;
+}
+
 template <int LM, int S0, int RP, bool FWD, int E>
 __device__ __forceinline__ void ntt2_phase_fp(double *sub, const double2 *tws, int tl, double q, double qinv) {
   constexpr int K = 1 << RP, R = E / K;
