@@ -729,6 +729,9 @@ struct PhaseShape {
 // blocks read consecutive entries.
 // GTW: tws is a global table (read through the read-only path) instead of shared memory
 // WQ: tws holds the twiddles' w only (doubles); w/q is formed by one DMUL per use
+#ifndef CGB_WQ_MULMODQ
+#define CGB_WQ_MULMODQ 1  // w-only twiddles: quotient from the rounded product instead of a w * (1/q) DMUL per twiddle
+#endif
 // SKIPLAST: leave out the last executed stage (an inverse phase ending at stage 0, whose
 // single butterfly layer the caller runs itself with N^-1 folded into both outputs)
 template <int LM, int S0, int RP, bool FWD, int E, bool TRANS = false, bool GTW = false, bool WQ = false,
@@ -753,20 +756,24 @@ __device__ __forceinline__ void phase_regs_fp(double x[E], const double2 *tws, i
                                : (1 << (S0 + l)) + (blk << l) + (k >> (RP - l));
           if constexpr (WQ) {
             const double w = GTW ? __ldg(reinterpret_cast<const double *>(tws) + ti) : reinterpret_cast<const double *>(tws)[ti];
-            W = make_double2(w, w * qinv);
+            W = make_double2(w, (CGB_WQ_MULMODQ && !GTW) ? 0.0 : w * qinv);
           } else {
             W = GTW ? __ldg(tws + ti) : tws[ti];
           }
         }
         double &X = x[u * K + k], &Y = x[u * K + k + half];
+        // staged w-only twiddles (the key switch's row kernels): the quotient comes from the rounded
+        // product (fp_mulmod_q) -- the three roundings that forming w / q on the fly spends, without
+        // the DMUL per twiddle.  (The register-I/O transform's row pass, twiddles through L1, measured
+        // slower this way -- the longer dependent chain -- and keeps w * (1/q).)
         if (FWD) {
-          const double t = fp_mulmod(Y, W.x, W.y, q);
+          const double t = (WQ && !GTW && CGB_WQ_MULMODQ) ? fp_mulmod_q(Y, W.x, q, qinv) : fp_mulmod(Y, W.x, W.y, q);
           Y = X - t;
           X = X + t;
         } else {  // X + Y left unreduced: scripts/sim/fp_bounds.py bounds a phase by 8q < 2^53
           const double d = X - Y;
           X = X + Y;
-          Y = fp_mulmod(d, W.x, W.y, q);
+          Y = (WQ && !GTW && CGB_WQ_MULMODQ) ? fp_mulmod_q(d, W.x, q, qinv) : fp_mulmod(d, W.x, W.y, q);
         }
       }
     }
