@@ -42,3 +42,48 @@ def test_threads_on_forked_contexts_equal_serial(n, p):
     for (d1, w1), (d6, w6) in zip(outs[1], outs[6]):
         assert np.array_equal(d1, d6)
         assert np.array_equal(w1, w6)
+
+
+@pytest.mark.parametrize("spec,n_items,rounds", [((14, 536903681, 3, 8192, True, 49), 24, 40),
+                                                 ((7, 67109633, 4, 64, True, 60), 512, 1200)],
+                         ids=["bench_ring", "toy_ring_wraps_staging"])
+def test_stream_switches_between_calls_keep_results(spec, n_items, rounds):
+    """The pointer tables of a call are uploaded on a side stream into a device mirror of
+    the pinned staging area and the compute stream waits for the upload's event.  Many
+    small calls, the ring's stream switched between them (cgb_set_stream), wrap the
+    staging halves several times; every output must equal the single-stream run."""
+    import torch
+
+    from paper_2602_08798_b200._native import build
+    from paper_2602_08798_b200.ring import Ring
+
+    build()
+    key = np.arange(8, dtype=np.uint32) * 3 + 1
+    enc = np.arange(8, dtype=np.uint32) + 77
+    log_n, t, L, n, one_row, qb = spec
+
+    def run(streams):
+        # (the toy ring's staging area is 8 MB: 1200 uploads of 16 KB wrap its halves twice)
+        g = Ring(log_n, t, L, n, one_row, key, arena_cts=4 * n_items + 8, arena_pts=8, q_bits=qb)
+        rng = np.random.default_rng(9)
+        src = g.alloc(n_items)
+        g.encrypt(rng.integers(0, t, (n_items, n)), enc, 0, src)
+        a, b = src, g.alloc(n_items)
+        for r in range(rounds):
+            s = streams[r % len(streams)]
+            if s is not None:
+                # hand over: the next stream waits for everything queued so far
+                prev = streams[(r - 1) % len(streams)]
+                if prev is not None and prev is not s:
+                    s.wait_stream(prev)
+                g.set_stream(s.cuda_stream)
+            steps = (np.arange(1, n_items + 1, dtype=np.int64) * (r + 1)) % n
+            steps[steps == 0] = 1
+            g.rotate(a, steps, b, add_input=bool(r & 1))
+            a, b = b, (g.alloc(n_items) if a is src else a)
+        torch.cuda.synchronize()
+        return g.store(a)
+
+    one = run([None])
+    two = run([torch.cuda.Stream(), torch.cuda.Stream()])
+    assert np.array_equal(one, two)
